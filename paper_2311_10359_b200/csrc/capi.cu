@@ -1,0 +1,395 @@
+// C-ABI entry points of libfikit.so (declared in include/fikit.h).
+// Argument checks on the host, then stream-ordered launches; no allocation.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "fikit_internal.cuh"
+
+namespace fikit {
+// kernels (measure.cu, finalize.cu, replay.cu)
+__global__ void k_reset_status(fikit_status_t*);
+__global__ void k_strtab_hash(fikit_strtab_t, uint64_t*, int, fikit_status_t*);
+__global__ void k_identify(const uint4*, uint64_t, const uint64_t*, const uint64_t*, uint32_t, uint32_t, uint64_t*,
+                           fikit_status_t*);
+__global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint32_t,
+                         uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*, uint32_t*);
+__global__ void k_hot_select(const fikit_status_t*, const uint32_t*, const Tuple*, uint32_t, Tuple*, uint32_t*);
+__global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
+                          uint32_t, uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*,
+                          const Tuple*, const uint32_t*, uint32_t*);
+size_t measure_smem_bytes();
+int measure_threads();
+struct FinRow;
+__global__ void k_fin_prep(const fikit_status_t*, fikit_table_t, FinRow*, uint32_t*);
+__global__ void k_fin_rank(const fikit_table_t, const uint32_t*, uint32_t*);
+__global__ void k_fin_scatter(fikit_table_t, const FinRow*, const uint32_t*, const uint32_t*);
+__global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
+__global__ void k_means(fikit_table_t);
+__global__ void k_lookup(fikit_table_t, const uint64_t*, const uint32_t*, uint64_t, uint32_t*);
+__global__ void k_resolve(const uint4*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*, uint32_t,
+                          uint32_t, fikit_table_t, uint32_t*, uint64_t*, uint64_t*, fikit_status_t*);
+__global__ void k_union_flags(const uint64_t*, const uint32_t*, const uint32_t*, uint32_t, uint32_t, uint32_t*);
+__global__ void k_union_scan(const uint32_t*, uint32_t, uint32_t*);
+__global__ void k_union_place(const uint64_t*, const uint32_t*, const uint32_t*, uint32_t, uint32_t, uint32_t,
+                              const uint32_t*, const uint32_t*, uint64_t*, uint32_t*, uint32_t, uint32_t*, uint32_t*,
+                              fikit_status_t*);
+__global__ void k_table_remap(fikit_table_t, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*,
+                              fikit_table_t);
+__global__ void k_fill(fikit_table_t, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
+                       const uint8_t*, const uint32_t*, const uint32_t*, uint32_t, fikit_fill_params_t, uint32_t*,
+                       const uint32_t*, uint32_t*, uint64_t*, uint64_t*, fikit_status_t*);
+__global__ void k_simulate(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
+                           const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
+                           fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
+}  // namespace fikit
+
+using namespace fikit;
+
+static std::atomic<uint64_t> g_launches{0};
+void fikit_note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+inline int launched() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libfikit: launch failed: %s\n", cudaGetErrorString(e));
+    return FIKIT_E_CUDA;
+  }
+  fikit_note_launch();
+  return FIKIT_OK;
+}
+
+struct Ws {
+  unsigned char* base;
+  WsLayout L;
+  fikit_status_t* st() const { return reinterpret_cast<fikit_status_t*>(base + L.status); }
+  uint32_t* misc() const { return reinterpret_cast<uint32_t*>(base + L.misc); }
+  uint64_t* name_hash() const { return reinterpret_cast<uint64_t*>(base + L.name_hash); }
+  uint64_t* sig_hash() const { return reinterpret_cast<uint64_t*>(base + L.sig_hash); }
+  IndexEntry* index() const { return reinterpret_cast<IndexEntry*>(base + L.index); }
+  Tuple* row_tuple() const { return reinterpret_cast<Tuple*>(base + L.row_tuple); }
+  uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
+  uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }
+  Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 16); }
+  unsigned char* fin() const { return base + L.fin; }
+};
+
+// workspace check for a capacity and string-table sizes
+int get_ws(void* ws, size_t ws_bytes, uint32_t cap, uint32_t nn, uint32_t ns, Ws* out) {
+  if (!ws || !aligned(ws, 256)) return FIKIT_E_ARG;
+  out->base = static_cast<unsigned char*>(ws);
+  out->L = ws_layout(cap, nn, ns);
+  if (ws_bytes < out->L.total) return FIKIT_E_ARG;
+  return FIKIT_OK;
+}
+
+inline int reset_status(const Ws& w, cudaStream_t s) {
+  k_reset_status<<<1, 32, 0, s>>>(w.st());  // a kernel, so the call stays graph-capturable
+  return launched();
+}
+
+inline bool strtab_ok(const fikit_strtab_t& t) { return t.offsets != nullptr && (t.count == 0 || t.bytes != nullptr); }
+
+inline bool table_ok(const fikit_table_t* t) {
+  return t && t->kernel_id && t->task_id && t->sums && t->hist && t->ext && t->mean && t->n_rows && t->capacity > 0 &&
+         t->capacity <= (1u << 24);
+}
+
+int hash_strtabs(const Ws& w, const fikit_strtab_t& names, const fikit_strtab_t& sigs, cudaStream_t s) {
+  if (names.count) {
+    k_strtab_hash<<<(names.count + 255) / 256, 256, 0, s>>>(names, w.name_hash(), 1, w.st());
+    if (int r = launched()) return r;
+  }
+  if (sigs.count) {
+    k_strtab_hash<<<(sigs.count + 255) / 256, 256, 0, s>>>(sigs, w.sig_hash(), 0, w.st());
+    if (int r = launched()) return r;
+  }
+  return FIKIT_OK;
+}
+
+unsigned grid_for(uint64_t work, unsigned per_block, unsigned max_blocks) {
+  uint64_t b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fikit_ws_bytes(uint32_t capacity, uint32_t n_names, uint32_t n_sigs) {
+  return ws_layout(capacity ? capacity : 1, n_names, n_sigs).total;
+}
+
+size_t fikit_table_bytes(uint32_t cap) {
+  size_t o = 0;
+  o = align256(o + 8ull * cap);   // kernel_id
+  o = align256(o + 4ull * cap);   // task_id
+  o = align256(o + 32ull * cap);  // sums
+  o = align256(o + 256ull * cap); // hist
+  o = align256(o + 32ull * cap);  // ext
+  o = align256(o + 16ull * cap);  // mean
+  o = align256(o + 4);            // n_rows
+  return o;
+}
+
+int fikit_table_carve(void* block, uint32_t cap, fikit_table_t* t) {
+  if (!block || !t || !aligned(block, 256) || cap == 0) return FIKIT_E_ARG;
+  unsigned char* b = static_cast<unsigned char*>(block);
+  size_t o = 0;
+  t->kernel_id = reinterpret_cast<uint64_t*>(b + o);
+  o = align256(o + 8ull * cap);
+  t->task_id = reinterpret_cast<uint32_t*>(b + o);
+  o = align256(o + 4ull * cap);
+  t->sums = reinterpret_cast<uint64_t*>(b + o);
+  o = align256(o + 32ull * cap);
+  t->hist = reinterpret_cast<uint32_t*>(b + o);
+  o = align256(o + 256ull * cap);
+  t->ext = reinterpret_cast<uint64_t*>(b + o);
+  o = align256(o + 32ull * cap);
+  t->mean = reinterpret_cast<uint64_t*>(b + o);
+  o = align256(o + 16ull * cap);
+  t->n_rows = reinterpret_cast<uint32_t*>(b + o);
+  t->capacity = cap;
+  return FIKIT_OK;
+}
+
+int fikit_identify(const fikit_record_t* recs, uint64_t n, fikit_strtab_t names, fikit_strtab_t sigs, uint64_t* out,
+                   void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Ws w;
+  if (n >= (1ull << 32) || (n && (!recs || !out || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs))
+    return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, 1, names.count, sigs.count, &w)) return r;
+  if (int r = reset_status(w, s)) return r;
+  if (int r = hash_strtabs(w, names, sigs, s)) return r;
+  if (n == 0) return FIKIT_OK;
+  k_identify<<<grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(recs), n, w.name_hash(), w.sig_hash(), names.count, sigs.count, out, w.st());
+  return launched();
+}
+
+int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes,
+                  void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Ws w;
+  if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs) ||
+      !table_ok(tab))
+    return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w)) return r;
+  const fikit_table_t t = *tab;
+  const uint32_t cap = t.capacity;
+  if (int r = reset_status(w, s)) return r;
+  // zero the table (an all-zero row is the identity of every statistic) and the index
+  cudaMemsetAsync(t.kernel_id, 0, 8ull * cap, s);
+  cudaMemsetAsync(t.task_id, 0, 4ull * cap, s);
+  cudaMemsetAsync(t.sums, 0, 32ull * cap, s);
+  cudaMemsetAsync(t.hist, 0, 256ull * cap, s);
+  cudaMemsetAsync(t.ext, 0, 32ull * cap, s);
+  cudaMemsetAsync(t.mean, 0, 16ull * cap, s);
+  cudaMemsetAsync(t.n_rows, 0, 4, s);
+  cudaMemsetAsync(w.index(), 0, sizeof(IndexEntry) * (size_t)w.L.slots, s);
+  cudaMemsetAsync(w.samp_cnt(), 0, 4ull * cap, s);
+  cudaMemsetAsync(w.hot_n(), 0, 16, s);
+  if (cudaGetLastError() != cudaSuccess) return FIKIT_E_CUDA;
+  if (int r = hash_strtabs(w, names, sigs, s)) return r;
+  if (n == 0) return FIKIT_OK;
+  // sample ~64k launches (all of them for small traces) to choose the hot rows
+  const uint64_t target = 65536;
+  uint64_t stride = n > target ? n / target : 1;
+  uint64_t ns = (n + stride - 1) / stride;
+  k_sample<<<grid_for(ns, 256, num_sms() * 4), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(recs), n, stride, ns, w.name_hash(), w.sig_hash(), names.count, sigs.count,
+      w.index(), w.L.slots, w.st(), t, w.row_tuple(), w.samp_cnt());
+  if (int r = launched()) return r;
+  k_hot_select<<<1, 1024, 0, s>>>(w.st(), w.samp_cnt(), w.row_tuple(), cap, w.hot(), w.hot_n());
+  if (int r = launched()) return r;
+  static bool attr_set = false;
+  size_t smem = measure_smem_bytes();
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_measure, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return FIKIT_E_CUDA;
+    attr_set = true;
+  }
+  uint64_t tiles = (n + 255) / 256;
+  unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
+  k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
+                                                  sigs.count, w.index(), w.L.slots, w.st(), t, w.row_tuple(),
+                                                  w.hot(), w.hot_n(), out_row);
+  return launched();
+}
+
+int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n, void* ws, size_t ws_bytes,
+                         void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!table_ok(tab) || (n && !out_row) || n >= (1ull << 32)) return FIKIT_E_ARG;
+  Ws w;
+  if (int r = get_ws(ws, ws_bytes, tab->capacity, 0, 0, &w)) return r;
+  const fikit_table_t t = *tab;
+  const uint32_t cap = t.capacity;
+  FinRow* fin = reinterpret_cast<FinRow*>(w.fin());
+  uint32_t* rank = reinterpret_cast<uint32_t*>(w.fin() + 336ull * cap);
+  uint32_t* kptr = w.misc() + kMiscNRec;
+  unsigned g = (cap + 255) / 256;
+  k_fin_prep<<<g, 256, 0, s>>>(w.st(), t, fin, kptr);
+  if (int r = launched()) return r;
+  k_fin_rank<<<g, 256, 0, s>>>(t, kptr, rank);
+  if (int r = launched()) return r;
+  k_fin_scatter<<<g, 256, 0, s>>>(t, fin, rank, kptr);
+  if (int r = launched()) return r;
+  if (out_row && n) {
+    k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, kptr);
+    if (int r = launched()) return r;
+  }
+  return FIKIT_OK;
+}
+
+int fikit_table_means(const fikit_table_t* tab, void* stream) {
+  if (!table_ok(tab)) return FIKIT_E_ARG;
+  k_means<<<(tab->capacity + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*tab);
+  return launched();
+}
+
+int fikit_resolve(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
+                  uint64_t* out_gap, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Ws w;
+  if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16) || !out_row || !out_dur || !out_gap)) ||
+      !strtab_ok(names) || !strtab_ok(sigs) || !table_ok(tab))
+    return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, 1, names.count, sigs.count, &w)) return r;
+  if (int r = reset_status(w, s)) return r;
+  if (int r = hash_strtabs(w, names, sigs, s)) return r;
+  if (n == 0) return FIKIT_OK;
+  k_resolve<<<grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(recs), n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, *tab,
+      out_row, out_dur, out_gap, w.st());
+  return launched();
+}
+
+int fikit_lookup(const fikit_table_t* tab, const uint64_t* kid, const uint32_t* task, uint64_t n, uint32_t* out_row,
+                 void* stream) {
+  if (!table_ok(tab) || (n && (!kid || !task || !out_row))) return FIKIT_E_ARG;
+  if (n == 0) return FIKIT_OK;
+  k_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, (cudaStream_t)stream>>>(*tab, kid, task, n, out_row);
+  return launched();
+}
+
+int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* deadline, const uint32_t* pool_row,
+               const uint64_t* pool_dur, const uint8_t* pool_level, const uint32_t* pool_off,
+               const uint32_t* pool_len, uint32_t G, fikit_fill_params_t prm, uint32_t* picks,
+               const uint32_t* picks_off, uint32_t* n_picks, uint64_t* R_left, uint64_t* t_used, void* ws,
+               size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Ws w;
+  if (!table_ok(tab) || (G && (!R0 || !deadline || !pool_off || !pool_len || !picks_off || !n_picks || !R_left ||
+                               !t_used)))
+    return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, 1, 0, 0, &w)) return r;
+  if (int r = reset_status(w, s)) return r;
+  if (G == 0) return FIKIT_OK;
+  k_fill<<<grid_for(G, 4, num_sms() * 16), 128, 0, s>>>(*tab, R0, deadline, pool_row, pool_dur, pool_level, pool_off,
+                                                         pool_len, G, prm, picks, picks_off, n_picks, R_left, t_used,
+                                                         w.st());
+  return launched();
+}
+
+int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
+                         const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
+                         const uint8_t* lp_level, const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t prm,
+                         fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off,
+                         void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Ws w;
+  if (!table_ok(tab) || (S && (!sc || !out))) return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, 1, 0, 0, &w)) return r;
+  if (int r = reset_status(w, s)) return r;
+  if (S == 0) return FIKIT_OK;
+  k_simulate<<<grid_for(S, 4, num_sms() * 16), 128, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
+                                                             sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
+  return launched();
+}
+
+int fikit_dict_union(const uint64_t* all_kid, const uint32_t* all_task, const uint32_t* n_list, uint32_t P,
+                     uint32_t Kmax, uint32_t self_rank, uint64_t* out_kid, uint32_t* out_task, uint32_t cap_out,
+                     uint32_t* out_n, uint32_t* local_to_union, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!all_kid || !all_task || !n_list || P == 0 || P > 1024 || Kmax == 0 || self_rank >= P || !out_kid ||
+      !out_task || !out_n || !local_to_union || cap_out == 0)
+    return FIKIT_E_ARG;
+  Ws w;
+  if (int r = get_ws(ws, ws_bytes, 1, 0, 0, &w)) return r;
+  // scratch: canon [P][Kmax] + cpre [P][Kmax+1]
+  size_t need = w.L.fin + 4ull * P * Kmax + 4ull * P * (Kmax + 1);
+  if (ws_bytes < need) return FIKIT_E_ARG;
+  uint32_t* canon = reinterpret_cast<uint32_t*>(w.fin());
+  uint32_t* cpre = canon + (size_t)P * Kmax;
+  if (int r = reset_status(w, s)) return r;
+  dim3 g((Kmax + 255) / 256, P);
+  k_union_flags<<<g, 256, 0, s>>>(all_kid, all_task, n_list, P, Kmax, canon);
+  if (int r = launched()) return r;
+  k_union_scan<<<P, 1024, 0, s>>>(canon, Kmax, cpre);
+  if (int r = launched()) return r;
+  k_union_place<<<g, 256, 0, s>>>(all_kid, all_task, n_list, P, Kmax, self_rank, canon, cpre, out_kid, out_task,
+                                  cap_out, out_n, local_to_union, w.st());
+  return launched();
+}
+
+int fikit_table_remap(const fikit_table_t* local, const uint32_t* l2u, const uint64_t* ukid, const uint32_t* utask,
+                      const uint32_t* un, const fikit_table_t* dense, void* stream) {
+  if (!table_ok(local) || !table_ok(dense) || !l2u || !ukid || !utask || !un) return FIKIT_E_ARG;
+  uint32_t m = local->capacity > dense->capacity ? local->capacity : dense->capacity;
+  k_table_remap<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*local, l2u, ukid, utask, un, *dense);
+  return launched();
+}
+
+int fikit_get_status(const void* ws, fikit_status_t* out, void* stream) {
+  if (!ws || !out) return FIKIT_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(out, ws, sizeof(fikit_status_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return FIKIT_E_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return FIKIT_E_CUDA;
+  uint32_t f = out->flags;
+  out->code = (f & kStatusArg)        ? FIKIT_E_ARG
+              : (f & kStatusName)     ? FIKIT_E_NAME
+              : (f & kStatusRecord)   ? FIKIT_E_RECORD
+              : (f & kStatusCapacity) ? FIKIT_E_CAPACITY
+                                      : FIKIT_OK;
+  return out->code;
+}
+
+const char* fikit_strerror(int code) {
+  switch (code) {
+    case FIKIT_OK: return "ok";
+    case FIKIT_E_ARG: return "invalid argument";
+    case FIKIT_E_RECORD: return "invalid launch record";
+    case FIKIT_E_CAPACITY: return "statistic table capacity exceeded";
+    case FIKIT_E_CUDA: return "CUDA launch failure";
+    case FIKIT_E_NAME: return "empty kernel name";
+    default: return "unknown";
+  }
+}
+
+uint64_t fikit_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+// Internal device helpers of libfikit.so (sm_100a).  Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fikit.h"
+
+namespace fikit {
+
+constexpr uint32_t kStatusArg = 1u, kStatusName = 2u, kStatusRecord = 4u, kStatusCapacity = 8u;
+constexpr int kBins = FIKIT_NBINS;
+
+// ---- workspace layout ------------------------------------------------------
+struct IndexEntry {  // global open-addressing index (task, kernel ID) -> row
+  unsigned long long kid;
+  uint32_t task;
+  uint32_t state;  // 0 empty, kBusy being written, else row + 1
+};
+constexpr uint32_t kBusy = 0xFFFFFFFFu;
+
+struct alignas(16) Tuple {  // a launch identity as raw record words (the hot dictionary key) + slot/row
+  uint32_t w[7];  // name_id, sig_id, grid_x, grid_y|grid_z<<16, block_x|block_y<<16, block_z, task_id
+  uint32_t row;
+};
+
+struct WsLayout {
+  size_t status, misc, name_hash, sig_hash, index, row_tuple, samp_cnt, hot, fin, total;
+  uint32_t slots;
+};
+
+constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (measure kernel)
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline uint32_t index_slots(uint32_t cap) {
+  uint32_t s = 1024;
+  while (s < 2ull * cap) s <<= 1;
+  return s;
+}
+
+inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs) {
+  WsLayout L;
+  size_t o = 0;
+  L.status = o;
+  o += 256;
+  L.misc = o;
+  o += 256;
+  L.name_hash = o;
+  o = align256(o + 8ull * (n_names ? n_names : 1));
+  L.sig_hash = o;
+  o = align256(o + 8ull * (n_sigs ? n_sigs : 1));
+  L.slots = index_slots(cap);
+  L.index = o;
+  o = align256(o + sizeof(IndexEntry) * (size_t)L.slots);
+  L.row_tuple = o;
+  o = align256(o + sizeof(Tuple) * (size_t)cap);
+  L.samp_cnt = o;
+  o = align256(o + 4ull * cap);
+  L.hot = o;
+  o = align256(o + 16 + sizeof(Tuple) * (size_t)kHotMax);
+  L.fin = o;
+  o = align256(o + 340ull * cap + 1024);
+  L.total = o;
+  return L;
+}
+
+// misc counters (u32 words at ws + misc)
+enum MiscWord { kMiscNames = 0, kMiscSigs = 1, kMiscHotN = 2, kMiscNRec = 3 };
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ---- hashing (R2) ------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t kernel_id_from(uint64_t h_name, uint64_t h_sig, uint32_t gx, uint32_t gyz,
+                                                   uint32_t bxy, uint32_t bz) {
+  // w1 = grid_x | grid_y<<32 | grid_z<<48 ; w2 = block_x | block_y<<16 | block_z<<32
+  uint64_t w1 = (uint64_t)gx | ((uint64_t)(gyz & 0xFFFFu) << 32) | ((uint64_t)(gyz >> 16) << 48);
+  uint64_t w2 = (uint64_t)bxy | ((uint64_t)(bz & 0xFFFFu) << 32);
+  uint64_t h = mix64(h_name ^ h_sig);
+  h = mix64(h ^ w1);
+  h = mix64(h ^ w2);
+  return h == 0 ? 1 : h;
+}
+
+__device__ __forceinline__ uint32_t key_hash(uint64_t kid, uint32_t task) {
+  uint64_t x = kid ^ (0x9e3779b97f4a7c15ULL * (uint64_t)(task + 1));
+  x ^= x >> 29;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  return (uint32_t)(x >> 32);
+}
+
+// cheap 32-bit hash of the raw identity words (hot-dictionary probe)
+__device__ __forceinline__ uint32_t tuple_hash(const uint32_t* w) {
+  uint32_t h = w[0] * 0x9E3779B1u;
+  h = (h ^ w[1]) * 0x85EBCA77u;
+  h = (h ^ w[2]) * 0xC2B2AE3Du;
+  h = (h ^ w[3]) * 0x27D4EB2Fu;
+  h = (h ^ w[4]) * 0x165667B1u;
+  h = (h ^ w[5]) * 0x9E3779B1u;
+  h = (h ^ w[6]) * 0x85EBCA77u;
+  return h ^ (h >> 15);
+}
+
+__device__ __forceinline__ int bin_of(uint64_t v) {
+  int b = 64 - __clzll((long long)v);  // bit_length
+  return b < 31 ? b : 31;
+}
+
+// ---- records as 12 u32 words --------------------------------------------------
+// w0,w1 start; w2,w3 end; w4 name; w5 sig; w6 grid_x; w7 grid_y|grid_z<<16;
+// w8 block_x|block_y<<16; w9 block_z|flags<<16; w10 run; w11 task
+__device__ __forceinline__ bool record_valid(const uint32_t* w, uint32_t n_names, uint32_t n_sigs) {
+  uint64_t s = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+  uint64_t e = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+  bool ok = (w[6] != 0) & ((w[7] & 0xFFFFu) != 0) & ((w[7] >> 16) != 0) & ((w[8] & 0xFFFFu) != 0) &
+            ((w[8] >> 16) != 0) & ((w[9] & 0xFFFFu) != 0) & ((w[9] >> 16) == 0) & (w[4] < n_names) &
+            (w[5] < n_sigs) & (e >= s);
+  return ok;
+}
+
+// ---- status ---------------------------------------------------------------------
+__device__ __forceinline__ void flag_record(fikit_status_t* st, uint64_t idx) {
+  atomicOr(&st->flags, kStatusRecord);
+  atomicMin((unsigned long long*)&st->first_bad_index, (unsigned long long)idx);
+}
+
+// ---- global index (task, kid) -> row --------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Find-or-insert; returns the row (possibly >= capacity, then nothing is materialised)
+// or FIKIT_NO_ROW if the index is full.  The inserting thread also records the
+// identity's raw tuple (hot-dictionary candidate) and the table key.
+__device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32_t slots, uint64_t kid, uint32_t task,
+                                                         const uint32_t* tuple_w, fikit_status_t* st,
+                                                         uint64_t* tab_kid, uint32_t* tab_task, Tuple* row_tuple,
+                                                         uint32_t cap) {
+  uint32_t h = key_hash(kid, task) & (slots - 1);
+  for (uint32_t probe = 0; probe < slots; probe++) {
+    IndexEntry* e = &idx[h];
+    uint32_t s = ld_acquire_u32(&e->state);
+    if (s == 0) {
+      uint32_t old = atomicCAS(&e->state, 0u, kBusy);
+      if (old == 0) {
+        e->kid = kid;
+        e->task = task;
+        uint32_t row = (uint32_t)atomicAdd((unsigned long long*)&st->n_rows_needed, 1ull);
+        if (row < cap) {
+          tab_kid[row] = kid;
+          tab_task[row] = task;
+          Tuple t;
+#pragma unroll
+          for (int j = 0; j < 7; j++) t.w[j] = tuple_w[j];
+          t.row = row;
+          row_tuple[row] = t;
+        } else {
+          atomicOr(&st->flags, kStatusCapacity);
+        }
+        __threadfence();
+        atomicExch(&e->state, row + 1);
+        return row;
+      }
+      s = old;
+    }
+    while (s == kBusy) s = ld_acquire_u32(&e->state);
+    volatile IndexEntry* ve = e;
+    if (ve->kid == kid && ve->task == task) return s - 1;
+    h = (h + 1) & (slots - 1);
+  }
+  atomicOr(&st->flags, kStatusCapacity);
+  return FIKIT_NO_ROW;
+}
+
+// ---- mbarrier / bulk copy (sm_90+ PTX) --------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA: global -> shared, completion counted on the mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void lds128(const void* p, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(smem_u32(p)));
+}
+
+// shared-memory 64-bit min/max (no native ATOMS.MIN.64: CAS loop; rare after warm-up)
+__device__ __forceinline__ void smem_min64(unsigned long long* p, unsigned long long v) {
+  unsigned long long cur = *(volatile unsigned long long*)p;
+  while (v < cur) {
+    unsigned long long prev = atomicCAS(p, cur, v);
+    if (prev == cur) break;
+    cur = prev;
+  }
+}
+__device__ __forceinline__ void smem_max64(unsigned long long* p, unsigned long long v) {
+  unsigned long long cur = *(volatile unsigned long long*)p;
+  while (v > cur) {
+    unsigned long long prev = atomicCAS(p, cur, v);
+    if (prev == cur) break;
+    cur = prev;
+  }
+}
+
+}  // namespace fikit
+
+// launch bookkeeping (host)
+void fikit_note_launch(int n = 1);

@@ -1,0 +1,327 @@
+// finalize / means / lookup / resolve / multi-GPU dictionary kernels.
+#include <cuda_runtime.h>
+
+#include "fikit_internal.cuh"
+
+namespace fikit {
+
+struct FinRow {  // scratch copy of one measured row
+  unsigned long long kid;
+  uint32_t task, pad;
+  unsigned long long sums[4];
+  unsigned long long ext[4];
+  uint32_t hist[64];
+};
+static_assert(sizeof(FinRow) == 336, "FinRow");
+
+__device__ __forceinline__ bool key_less(uint32_t ta, uint64_t ka, uint32_t tb, uint64_t kb) {
+  return ta < tb || (ta == tb && ka < kb);
+}
+
+// R8: floor(sum/cnt) + [2 (sum mod cnt) >= cnt]; cnt = 0 -> 0
+__device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
+  if (cnt == 0) return 0;
+  uint64_t q = sum / cnt, r = sum - q * cnt;
+  return q + ((2 * r >= cnt) ? 1 : 0);
+}
+
+// rows -> scratch; counts = histogram totals (SK/SG denominators)
+__global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* fin, uint32_t* n_out) {
+  uint32_t K = (uint32_t)umin64(st->n_rows_needed, tab.capacity);
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *n_out = K;
+  if (r >= K) return;
+  FinRow f;
+  f.kid = tab.kernel_id[r];
+  f.task = tab.task_id[r];
+  f.pad = 0;
+  uint64_t dc = 0, gc = 0;
+  for (int b = 0; b < 32; b++) {
+    f.hist[b] = tab.hist[(size_t)r * 64 + b];
+    f.hist[32 + b] = tab.hist[(size_t)r * 64 + 32 + b];
+    dc += f.hist[b];
+    gc += f.hist[32 + b];
+  }
+  f.sums[0] = dc;
+  f.sums[1] = tab.sums[(size_t)r * 4 + 1];
+  f.sums[2] = gc;
+  f.sums[3] = tab.sums[(size_t)r * 4 + 3];
+  for (int j = 0; j < 4; j++) f.ext[j] = tab.ext[(size_t)r * 4 + j];
+  fin[r] = f;
+}
+
+// rank of every key among the K distinct keys = its canonical row (R11)
+__global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const uint32_t* n_ptr,
+                                                  uint32_t* __restrict__ rank) {
+  __shared__ unsigned long long sk[2048];
+  __shared__ uint32_t st[2048];
+  uint32_t K = *n_ptr;
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x * blockDim.x >= K) return;
+  uint64_t mk = r < K ? tab.kernel_id[r] : 0;
+  uint32_t mt = r < K ? tab.task_id[r] : 0;
+  uint32_t cnt = 0;
+  for (uint32_t base = 0; base < K; base += 2048) {
+    uint32_t m = min(2048u, K - base);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      sk[i] = tab.kernel_id[base + i];
+      st[i] = tab.task_id[base + i];
+    }
+    __syncthreads();
+    for (uint32_t i = 0; i < m; i++) cnt += key_less(st[i], sk[i], mt, mk) ? 1u : 0u;
+  }
+  if (r < K) rank[r] = cnt;
+}
+
+__global__ void k_fin_scatter(fikit_table_t tab, const FinRow* __restrict__ fin, const uint32_t* __restrict__ rank,
+                              const uint32_t* n_ptr) {
+  uint32_t K = *n_ptr;
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *tab.n_rows = K;
+  if (r >= K) return;
+  const FinRow& f = fin[r];
+  uint32_t d = rank[r];
+  tab.kernel_id[d] = f.kid;
+  tab.task_id[d] = f.task;
+  for (int j = 0; j < 4; j++) tab.sums[(size_t)d * 4 + j] = f.sums[j];
+  for (int j = 0; j < 4; j++) tab.ext[(size_t)d * 4 + j] = f.ext[j];
+  for (int b = 0; b < 64; b++) tab.hist[(size_t)d * 64 + b] = f.hist[b];
+  tab.mean[(size_t)d * 2 + 0] = mean_half_up(f.sums[1], f.sums[0]);  // SK_j
+  tab.mean[(size_t)d * 2 + 1] = mean_half_up(f.sums[3], f.sums[2]);  // SG_j
+}
+
+__global__ void k_remap_rows(uint32_t* rows, uint64_t n, const uint32_t* __restrict__ rank, const uint32_t* n_ptr) {
+  uint32_t K = *n_ptr;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t r = rows[i];
+    rows[i] = (r < K) ? rank[r] : FIKIT_NO_ROW;
+  }
+}
+
+// counts from histograms + means of an already canonical table
+__global__ void k_means(fikit_table_t tab) {
+  uint32_t K = min(*tab.n_rows, tab.capacity);
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= K) return;
+  uint64_t dc = 0, gc = 0;
+  for (int b = 0; b < 32; b++) {
+    dc += tab.hist[(size_t)r * 64 + b];
+    gc += tab.hist[(size_t)r * 64 + 32 + b];
+  }
+  tab.sums[(size_t)r * 4 + 0] = dc;
+  tab.sums[(size_t)r * 4 + 2] = gc;
+  tab.mean[(size_t)r * 2 + 0] = mean_half_up(tab.sums[(size_t)r * 4 + 1], dc);
+  tab.mean[(size_t)r * 2 + 1] = mean_half_up(tab.sums[(size_t)r * 4 + 3], gc);
+}
+
+// binary search of (task, kid) in the canonical table
+__device__ __forceinline__ uint32_t find_row(const uint64_t* __restrict__ kid, const uint32_t* __restrict__ task,
+                                             uint32_t K, uint32_t t, uint64_t k) {
+  uint32_t lo = 0, hi = K;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    uint32_t tm = __ldg(task + mid);
+    uint64_t km = __ldg(kid + mid);
+    if (key_less(tm, km, t, k))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < K && __ldg(task + lo) == t && __ldg(kid + lo) == k) ? lo : FIKIT_NO_ROW;
+}
+
+__global__ void k_lookup(fikit_table_t tab, const uint64_t* __restrict__ kid, const uint32_t* __restrict__ task,
+                         uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t K = min(*tab.n_rows, tab.capacity);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = find_row(tab.kernel_id, tab.task_id, K, task[i], kid[i]);
+}
+
+// profile lookup + duration + following gap of fresh launches (Alg. 1 lines 3-5)
+__global__ void __launch_bounds__(256) k_resolve(const uint4* __restrict__ recs, uint64_t n,
+                                                 const fikit_record_t* __restrict__ halo,
+                                                 const uint64_t* __restrict__ name_hash,
+                                                 const uint64_t* __restrict__ sig_hash, uint32_t n_names,
+                                                 uint32_t n_sigs, fikit_table_t tab, uint32_t* __restrict__ out_row,
+                                                 uint64_t* __restrict__ out_dur, uint64_t* __restrict__ out_gap,
+                                                 fikit_status_t* st) {
+  __shared__ uint4 sbuf[8][99];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t K = min(*tab.n_rows, tab.capacity);
+  uint64_t nchunks = (n + 31) / 32;
+  uint32_t ov = 0;
+  for (uint64_t c = (uint64_t)blockIdx.x * 8 + wid; c < nchunks; c += (uint64_t)gridDim.x * 8) {
+    uint64_t first = c * 32;
+    uint32_t cnt = (uint32_t)umin64(33, n - first);  // +1: the next launch
+    __syncwarp();
+    const uint4* src = recs + first * 3;
+    for (uint32_t q = lane; q < cnt * 3; q += 32) sbuf[wid][q] = __ldcs(src + q);
+    __syncwarp();
+    if (lane < (int)umin64(32, n - first)) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&sbuf[wid][lane * 3]);
+      uint64_t gi = first + lane;
+      if (record_valid(w, n_names, n_sigs)) {
+        uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+        uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+        uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+        bool has_next = false;
+        uint64_t nstart = 0;
+        uint32_t nrun = 0, ntask = 0;
+        if (gi + 1 < n) {
+          const uint32_t* nx = reinterpret_cast<const uint32_t*>(&sbuf[wid][(lane + 1) * 3]);
+          nstart = (uint64_t)nx[0] | ((uint64_t)nx[1] << 32);
+          nrun = nx[10];
+          ntask = nx[11];
+          has_next = true;
+        } else if (halo) {
+          nstart = halo->start_ns;
+          nrun = halo->run_id;
+          ntask = halo->task_id;
+          has_next = true;
+        }
+        bool gap = has_next && ntask == w[11] && nrun == w[10];
+        bool o = gap && nstart < end;
+        ov += o;
+        out_row[gi] = find_row(tab.kernel_id, tab.task_id, K, w[11], kid);
+        out_dur[gi] = end - start;
+        out_gap[gi] = (gap && !o) ? nstart - end : 0;
+      } else {
+        flag_record(st, gi);
+      }
+    }
+  }
+  ov = __reduce_add_sync(0xffffffffu, ov);
+  if (lane == 0 && ov) atomicAdd((unsigned long long*)&st->n_overlap_gaps, (unsigned long long)ov);
+}
+
+// ---- multi-GPU dictionary union ----------------------------------------------
+// P sorted unique key lists (stride Kmax).  Element (r, j) is canonical iff no
+// list r' < r holds the same key; the union position of key x is
+//   sum_r' #{canonical y in list r' : y < x} = sum_r' cpre_r'[lower_bound_r'(x)].
+__device__ __forceinline__ uint32_t lower_bound_list(const uint64_t* kid, const uint32_t* task, uint32_t len,
+                                                     uint32_t t, uint64_t k) {
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (key_less(task[mid], kid[mid], t, k))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_union_flags(const uint64_t* __restrict__ all_kid, const uint32_t* __restrict__ all_task,
+                              const uint32_t* __restrict__ n_list, uint32_t P, uint32_t Kmax, uint32_t* canon) {
+  uint32_t r = blockIdx.y;
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Kmax) return;
+  uint32_t len = n_list[r];
+  if (j >= len) {
+    canon[(size_t)r * Kmax + j] = 0;
+    return;
+  }
+  uint64_t k = all_kid[(size_t)r * Kmax + j];
+  uint32_t t = all_task[(size_t)r * Kmax + j];
+  uint32_t c = 1;
+  for (uint32_t q = 0; q < r && c; q++) {
+    const uint64_t* kq = all_kid + (size_t)q * Kmax;
+    const uint32_t* tq = all_task + (size_t)q * Kmax;
+    uint32_t lb = lower_bound_list(kq, tq, n_list[q], t, k);
+    if (lb < n_list[q] && kq[lb] == k && tq[lb] == t) c = 0;
+  }
+  canon[(size_t)r * Kmax + j] = c;
+}
+
+// exclusive prefix of canon per list (one CTA per list); cpre has Kmax + 1 entries per list
+__global__ void __launch_bounds__(1024) k_union_scan(const uint32_t* __restrict__ canon, uint32_t Kmax,
+                                                     uint32_t* cpre) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  uint32_t r = blockIdx.x;
+  const uint32_t* c = canon + (size_t)r * Kmax;
+  uint32_t* o = cpre + (size_t)r * (Kmax + 1);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < Kmax; base += 1024) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < Kmax ? c[i] : 0;
+    uint32_t x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = warp_tot[lane];
+      for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+        if (lane >= d) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
+    if (i < Kmax) o[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) o[Kmax] = carry;
+}
+
+__global__ void k_union_place(const uint64_t* __restrict__ all_kid, const uint32_t* __restrict__ all_task,
+                              const uint32_t* __restrict__ n_list, uint32_t P, uint32_t Kmax, uint32_t self_rank,
+                              const uint32_t* __restrict__ canon, const uint32_t* __restrict__ cpre,
+                              uint64_t* out_kid, uint32_t* out_task, uint32_t cap_out, uint32_t* out_n,
+                              uint32_t* local_to_union, fikit_status_t* st) {
+  uint32_t r = blockIdx.y;
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0 && j == 0) {
+    uint32_t tot = 0;
+    for (uint32_t q = 0; q < P; q++) tot += cpre[(size_t)q * (Kmax + 1) + Kmax];
+    *out_n = min(tot, cap_out);
+    if (tot > cap_out) {
+      atomicOr(&st->flags, kStatusCapacity);
+      atomicMax((unsigned long long*)&st->n_rows_needed, (unsigned long long)tot);
+    }
+  }
+  if (j >= n_list[r]) return;
+  uint64_t k = all_kid[(size_t)r * Kmax + j];
+  uint32_t t = all_task[(size_t)r * Kmax + j];
+  uint32_t pos = 0;
+  for (uint32_t q = 0; q < P; q++) {
+    uint32_t lb = lower_bound_list(all_kid + (size_t)q * Kmax, all_task + (size_t)q * Kmax, n_list[q], t, k);
+    pos += cpre[(size_t)q * (Kmax + 1) + lb];
+  }
+  if (canon[(size_t)r * Kmax + j] && pos < cap_out) {
+    out_kid[pos] = k;
+    out_task[pos] = t;
+  }
+  if (r == self_rank) local_to_union[j] = pos < cap_out ? pos : FIKIT_NO_ROW;
+}
+
+// local canonical rows -> dense union rows (dense table zero-initialised by the caller)
+__global__ void k_table_remap(fikit_table_t local, const uint32_t* __restrict__ l2u,
+                              const uint64_t* __restrict__ ukid, const uint32_t* __restrict__ utask,
+                              const uint32_t* __restrict__ un, fikit_table_t dense) {
+  uint32_t U = min(*un, dense.capacity);
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *dense.n_rows = U;
+  if (i < U) {
+    dense.kernel_id[i] = ukid[i];
+    dense.task_id[i] = utask[i];
+  }
+  uint32_t K = min(*local.n_rows, local.capacity);
+  if (i >= K) return;
+  uint32_t d = l2u[i];
+  if (d >= U) return;
+  for (int j = 0; j < 4; j++) dense.sums[(size_t)d * 4 + j] = local.sums[(size_t)i * 4 + j];
+  for (int j = 0; j < 4; j++) dense.ext[(size_t)d * 4 + j] = local.ext[(size_t)i * 4 + j];
+  for (int b = 0; b < 64; b++) dense.hist[(size_t)d * 64 + b] = local.hist[(size_t)i * 64 + b];
+}
+
+}  // namespace fikit

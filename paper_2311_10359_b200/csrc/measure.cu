@@ -1,0 +1,402 @@
+// identify + measure kernels for sm_100a.
+//
+// Data path of fikit_measure:
+//   k_strtab_hash    FNV-1a-64 of every name / signature once (not per launch)
+//   k_sample         a strided sample of launches -> (task, KID) rows in the global
+//                    index, with sample counts (picks the rows worth caching)
+//   k_hot_select     the <= kHotMax most-sampled rows -> hot dictionary (raw tuple -> row)
+//   k_measure        persistent, one CTA per SM: a producer warp streams 256-record
+//                    tiles global->shared with 1-D TMA (cp.async.bulk) into a 6-stage
+//                    mbarrier ring; 16 consumer warps validate each launch, look its raw
+//                    identity up in the shared hot dictionary, and accumulate duration
+//                    and following-gap statistics into shared memory (packed 16-bit
+//                    histograms flushed every epoch, 32-bit split sums, 64-bit min/max);
+//                    launches of cold rows take the global path (KID hash, global index,
+//                    L2 reductions).  Shared rows are reduced into the table at the end.
+#include <cuda_runtime.h>
+
+#include "fikit_internal.cuh"
+
+namespace fikit {
+
+// ------------------------------------------------------------------------------------
+__global__ void k_reset_status(fikit_status_t* st) {
+  if (threadIdx.x == 0) {
+    st->code = 0;
+    st->flags = 0;
+    st->first_bad_index = ~0ull;
+    st->n_rows_needed = 0;
+    st->n_overlap_gaps = 0;
+  }
+}
+
+__global__ void k_strtab_hash(fikit_strtab_t t, uint64_t* __restrict__ out, int is_name, fikit_status_t* st) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= t.count) return;
+  uint32_t a = t.offsets[j], b = t.offsets[j + 1];
+  if (b < a) {
+    atomicOr(&st->flags, kStatusArg);
+    out[j] = 0;
+    return;
+  }
+  if (is_name && a == b) atomicOr(&st->flags, kStatusName);
+  uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a 64 (R2)
+  for (uint32_t i = a; i < b; i++) {
+    h ^= (uint64_t)__ldg(t.bytes + i);
+    h *= 0x100000001b3ULL;
+  }
+  out[j] = h;
+}
+
+// warp-cooperative coalesced load of up to 32 records (1536 B) into a per-warp
+// shared buffer; lane l then reads record l with three 16-B shared loads
+__device__ __forceinline__ void warp_stage_records(const uint4* __restrict__ g, uint64_t first, uint32_t cnt,
+                                                   uint4* sbuf, int lane) {
+  const uint4* src = g + first * 3;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    uint32_t c = lane + 32 * k;
+    if (c < cnt * 3) sbuf[c] = __ldcs(src + c);  // streaming: read once
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void read_rec_words(const uint4* sbuf, int j, uint32_t* w) {
+  uint4 a = sbuf[j * 3 + 0], b = sbuf[j * 3 + 1], c = sbuf[j * 3 + 2];
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+  w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+}
+
+// ---- identify: 48 B in, 8 B out per launch (HBM-bound streaming) ---------------------
+__global__ void __launch_bounds__(256) k_identify(const uint4* __restrict__ recs, uint64_t n,
+                                                  const uint64_t* __restrict__ name_hash,
+                                                  const uint64_t* __restrict__ sig_hash, uint32_t n_names,
+                                                  uint32_t n_sigs, uint64_t* __restrict__ out, fikit_status_t* st) {
+  __shared__ uint4 sbuf[8][96];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t nchunks = (n + 31) / 32;
+  for (uint64_t c = (uint64_t)blockIdx.x * 8 + wid; c < nchunks; c += (uint64_t)gridDim.x * 8) {
+    uint64_t first = c * 32;
+    uint32_t cnt = (uint32_t)umin64(32, n - first);
+    __syncwarp();
+    warp_stage_records(recs, first, cnt, sbuf[wid], lane);
+    if (lane < (int)cnt) {
+      uint32_t w[12];
+      read_rec_words(sbuf[wid], lane, w);
+      uint64_t kid = 0;
+      if (record_valid(w, n_names, n_sigs)) {
+        kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+      } else {
+        flag_record(st, first + lane);
+      }
+      __stcs(out + first + lane, kid);
+    }
+  }
+}
+
+// ---- sample: which rows are hot -------------------------------------------------------
+__global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t stride, uint64_t n_samples,
+                         const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash,
+                         uint32_t n_names, uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st,
+                         fikit_table_t tab, Tuple* row_tuple, uint32_t* samp_cnt) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_samples;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t i = j * stride;
+    if (i >= n) break;
+    uint4 a = __ldg(recs + i * 3), b = __ldg(recs + i * 3 + 1), c = __ldg(recs + i * 3 + 2);
+    uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    if (!record_valid(w, n_names, n_sigs)) continue;  // reported by k_measure
+    uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+    uint32_t tw[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
+    uint32_t row =
+        index_find_or_insert(idx, slots, kid, w[11], tw, st, tab.kernel_id, tab.task_id, row_tuple, tab.capacity);
+    if (row < tab.capacity) atomicAdd(samp_cnt + row, 1u);
+  }
+}
+
+// ---- hot select: the most-sampled rows (one CTA) ----------------------------------------
+__global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, const uint32_t* __restrict__ samp_cnt,
+                                                     const Tuple* __restrict__ row_tuple, uint32_t cap,
+                                                     Tuple* hot, uint32_t* hot_n_out) {
+  constexpr int NB = 4096;
+  __shared__ uint32_t h[NB];
+  __shared__ uint32_t s_T, s_n;
+  uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
+    uint32_t c = samp_cnt[r];
+    if (c) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0, T = 1;
+    for (int c = NB - 1; c >= 1; c--) {
+      if (acc + h[c] > kHotMax) {
+        T = c + 1;
+        break;
+      }
+      acc += h[c];
+    }
+    s_T = T;
+    s_n = 0;
+  }
+  __syncthreads();
+  uint32_t T = s_T;
+  for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
+    if (samp_cnt[r] >= T) {
+      uint32_t e = atomicAdd(&s_n, 1u);
+      if (e < kHotMax) hot[e] = row_tuple[r];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *hot_n_out = min(s_n, kHotMax);
+}
+
+// ---- the fused identify + measure kernel ----------------------------------------------------
+namespace mk {
+constexpr int TILE = 256;                 // launches per stage
+constexpr int NS = 6;                     // ring stages
+constexpr int GROUPS = 2;                 // consumer groups (one tile each in flight)
+constexpr int WPG = TILE / 32;            // warps per group
+constexpr int CONSUMERS = GROUPS * WPG * 32;
+constexpr int THREADS = CONSUMERS + 32;   // + producer warp
+constexpr int HOT_IDX = 1024;             // shared hash slots (load <= 0.625)
+constexpr int STAGE_BYTES = (TILE + 1) * 48;
+constexpr int EPOCH_ROUNDS = 65535 / (TILE * GROUPS);  // packed 16-bit bins never overflow
+
+struct Smem {
+  uint4 ring[NS][STAGE_BYTES / 16];
+  uint64_t full[NS], empty[NS];
+  Tuple idx[HOT_IDX];                   // raw identity -> slot + 1 (in .row)
+  uint32_t hist[kHotMax][kBins];         // 64 bins as packed u16 pairs
+  uint32_t sum[kHotMax][4];              // dur lo, dur hi, gap lo, gap hi
+  unsigned long long ext[kHotMax][4];    // dur min, dur max, gap min, gap max
+  uint32_t grow[kHotMax];                // slot -> global row
+  uint32_t hot_n;
+  unsigned long long overlap;
+};
+}  // namespace mk
+
+__device__ __forceinline__ void hot_add(mk::Smem& S, int e, int j, uint64_t v) {
+  int b = bin_of(v) + 32 * j;
+  atomicAdd(&S.hist[e][b >> 1], 1u << (16 * (b & 1)));
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  uint32_t old = atomicAdd(&S.sum[e][2 * j], lo);
+  hi += (old + lo < old) ? 1u : 0u;
+  if (hi) atomicAdd(&S.sum[e][2 * j + 1], hi);
+  unsigned long long mn = S.ext[e][2 * j], mx = S.ext[e][2 * j + 1];
+  if (v < mn) smem_min64(&S.ext[e][2 * j], v);
+  if (v > mx) smem_max64(&S.ext[e][2 * j + 1], v);
+}
+
+__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row, int j, uint64_t v) {
+  red_add_u32(tab.hist + (size_t)row * 64 + 32 * j + bin_of(v), 1u);
+  red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
+  uint64_t* ex = tab.ext + (size_t)row * 4 + 2 * j;
+  ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(ex));  // may be stale: only skips no-op REDs
+  if (v > cur.x) red_max_u64(ex, v);
+  if (~v > cur.y) red_max_u64(ex + 1, ~v);
+}
+
+// flush packed 16-bit bins of my slots to the table and zero them (consumers only)
+__device__ __forceinline__ void flush_hist(mk::Smem& S, const fikit_table_t& tab, int ctid) {
+  for (uint32_t e = ctid; e < S.hot_n; e += mk::CONSUMERS) {
+    uint32_t* gh = tab.hist + (size_t)S.grow[e] * 64;
+#pragma unroll 4
+    for (int w = 0; w < kBins; w++) {
+      uint32_t x = S.hist[e][w];
+      if (x) {
+        if (x & 0xFFFFu) red_add_u32(gh + 2 * w, x & 0xFFFFu);
+        if (x >> 16) red_add_u32(gh + 2 * w + 1, x >> 16);
+        S.hist[e][w] = 0;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(mk::CONSUMERS) : "memory"); }
+
+__global__ void __launch_bounds__(mk::THREADS, 1)
+    k_measure(const fikit_record_t* __restrict__ recs, uint64_t n, const fikit_record_t* __restrict__ halo,
+              const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
+              uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st, fikit_table_t tab,
+              Tuple* row_tuple, const Tuple* __restrict__ hot, const uint32_t* __restrict__ hot_n_ptr,
+              uint32_t* __restrict__ out_row) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
+
+  // ---- setup: hot dictionary into shared memory, zero stats ----
+  if (tid == 0) {
+    S.hot_n = min(*hot_n_ptr, kHotMax);
+    S.overlap = 0;
+    for (int s = 0; s < mk::NS; s++) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], mk::WPG);
+    }
+    fence_mbar_init();
+  }
+  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.idx[i].row = 0;
+  for (int i = tid; i < kHotMax * kBins; i += mk::THREADS) (&S.hist[0][0])[i] = 0;
+  for (int i = tid; i < kHotMax * 4; i += mk::THREADS) {
+    (&S.sum[0][0])[i] = 0;
+    (&S.ext[0][0])[i] = (i & 1) ? 0ull : ~0ull;
+  }
+  __syncthreads();
+  const uint32_t hot_n = S.hot_n;
+  for (uint32_t e = tid; e < hot_n; e += mk::THREADS) {
+    Tuple t = hot[e];
+    S.grow[e] = t.row;
+    uint32_t h = tuple_hash(t.w) & (mk::HOT_IDX - 1);
+    while (atomicCAS(&S.idx[h].row, 0u, e + 1) != 0u) h = (h + 1) & (mk::HOT_IDX - 1);
+#pragma unroll
+    for (int j = 0; j < 7; j++) S.idx[h].w[j] = t.w[j];
+  }
+  __syncthreads();
+
+  const uint64_t my_tiles = (ntiles > blockIdx.x) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == mk::CONSUMERS / 32) {
+    // ---------------- producer warp: 1-D TMA of each tile (+ the next launch) ----------------
+    if (lane == 0) {
+      for (uint64_t it = 0; it < my_tiles; it++) {
+        uint64_t tile = blockIdx.x + it * gridDim.x;
+        int s = (int)(it % mk::NS);
+        if (it >= mk::NS) mbar_wait(&S.empty[s], (uint32_t)((it / mk::NS) - 1) & 1u);
+        uint64_t first = tile * mk::TILE;
+        uint32_t cnt = (uint32_t)umin64(mk::TILE + 1, n - first);  // +1: next launch for the last gap
+        uint32_t bytes = cnt * 48;
+        mbar_arrive_expect_tx(&S.full[s], bytes);
+        bulk_g2s(S.ring[s], recs + first, bytes, &S.full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int group = warp / mk::WPG, wig = warp % mk::WPG;
+  const uint64_t rounds = (my_tiles + mk::GROUPS - 1) / mk::GROUPS;
+  uint32_t overlap_cnt = 0;
+  for (uint64_t r = 0; r < rounds; r++) {
+    uint64_t it = r * mk::GROUPS + group;
+    if (it < my_tiles) {
+      uint64_t tile = blockIdx.x + it * gridDim.x;
+      int s = (int)(it % mk::NS);
+      mbar_wait(&S.full[s], (uint32_t)(it / mk::NS) & 1u);
+      uint64_t first = tile * mk::TILE;
+      uint32_t cnt = (uint32_t)umin64(mk::TILE, n - first);
+      uint32_t j = wig * 32 + lane;
+      if (j < cnt) {
+        const unsigned char* base = reinterpret_cast<const unsigned char*>(S.ring[s]);
+        uint32_t w[12];
+        lds128(base + j * 48, w[0], w[1], w[2], w[3]);
+        lds128(base + j * 48 + 16, w[4], w[5], w[6], w[7]);
+        lds128(base + j * 48 + 32, w[8], w[9], w[10], w[11]);
+        uint64_t gi = first + j;
+        // next launch: in the tile (or the extra record), else the halo
+        bool has_next = false;
+        uint64_t nstart = 0;
+        uint32_t nrun = 0, ntask = 0;
+        if (gi + 1 < n) {
+          const uint32_t* nx = reinterpret_cast<const uint32_t*>(base + (j + 1) * 48);
+          nstart = (uint64_t)nx[0] | ((uint64_t)nx[1] << 32);
+          nrun = nx[10];
+          ntask = nx[11];
+          has_next = true;
+        } else if (halo != nullptr) {
+          nstart = halo->start_ns;
+          nrun = halo->run_id;
+          ntask = halo->task_id;
+          has_next = true;
+        }
+        if (record_valid(w, n_names, n_sigs)) {
+          uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+          uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+          uint64_t d = end - start;  // K = end - start
+          bool gap = has_next && ntask == w[11] && nrun == w[10];  // R5
+          bool ov = gap && nstart < end;
+          uint64_t g = ov ? 0 : nstart - end;  // G = next start - end, clamped
+          overlap_cnt += ov;
+          uint32_t key[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
+          uint32_t h = tuple_hash(key) & (mk::HOT_IDX - 1);
+          int slot = -1;
+          for (;;) {
+            uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+            lds128(&S.idx[h].w[0], a0, a1, a2, a3);
+            lds128(&S.idx[h].w[4], b0, b1, b2, b3);
+            if (b3 == 0) break;
+            if (a0 == key[0] && a1 == key[1] && a2 == key[2] && a3 == key[3] && b0 == key[4] && b1 == key[5] &&
+                b2 == key[6]) {
+              slot = (int)b3 - 1;
+              break;
+            }
+            h = (h + 1) & (mk::HOT_IDX - 1);
+          }
+          uint32_t row;
+          if (slot >= 0) {
+            row = S.grow[slot];
+            hot_add(S, slot, 0, d);
+            if (gap) hot_add(S, slot, 1, g);
+          } else {
+            uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+            row = index_find_or_insert(idx, slots, kid, w[11], key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                       tab.capacity);
+            if (row < tab.capacity) {
+              cold_add(tab, row, 0, d);
+              if (gap) cold_add(tab, row, 1, g);
+            }
+          }
+          if (out_row) out_row[gi] = row;
+        } else {
+          flag_record(st, gi);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
+    }
+    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit bins: flush before overflow
+      consumer_sync();
+      flush_hist(S, tab, tid);
+      consumer_sync();
+    }
+  }
+  // warp-aggregate the overlap count
+  uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
+  if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);
+  consumer_sync();
+  // ---- final reduction of the shared rows into the table ----
+  flush_hist(S, tab, tid);
+  for (uint32_t e = tid; e < hot_n; e += mk::CONSUMERS) {
+    uint32_t row = S.grow[e];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      uint64_t sum = (uint64_t)S.sum[e][2 * j] | ((uint64_t)S.sum[e][2 * j + 1] << 32);
+      unsigned long long mn = S.ext[e][2 * j], mx = S.ext[e][2 * j + 1];
+      if (mn != ~0ull || mx != 0ull) {  // touched
+        if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
+        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, mx);
+        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~mn);
+      }
+    }
+  }
+  if (tid == 0 && S.overlap) atomicAdd((unsigned long long*)&st->n_overlap_gaps, S.overlap);
+}
+
+size_t measure_smem_bytes() { return sizeof(mk::Smem); }
+int measure_threads() { return mk::THREADS; }
+
+}  // namespace fikit

@@ -1,0 +1,112 @@
+"""Device-resident end-to-end hot path: measure -> finalize -> resolve -> simulate.
+
+Holds the device buffers of one configuration (a trace, optionally a replay
+batch) and calls the C-ABI in order.  Marshalling only; the computation is
+in libfikit.so.  Input arrays use the 48-byte record layout of
+include/fikit.h and the scenario layout fikit_scenario_t.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve,
+               simulate_batch, strtab_to_device, table_finalize)
+
+
+class Pipeline:
+    def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
+                 want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None):
+        torch = _torch()
+        self.device = device
+        self.n = int(records.shape[0])
+        self.capacity = int(capacity if capacity is not None else max(1, min(self.n, 1 << 16)))
+        self.recs = records_to_device(records, device) if self.n else torch.zeros(48, dtype=torch.uint8,
+                                                                                    device=device)
+        self.halo = records_to_device(halo.reshape(1), device) if halo is not None else None
+        self.names: DevStrTab = strtab_to_device(names, device)
+        self.sigs: DevStrTab = strtab_to_device(sigs, device)
+        self.table = Table(self.capacity, device)
+        self.ws = Workspace(self.capacity, max(1, names.count), max(1, sigs.count), device)
+        self.out_row = torch.empty(max(1, self.n), dtype=torch.int32, device=device) if want_rows else None
+        self.replay = None
+        if replay is not None:
+            self._setup_replay(replay, want_schedule)
+
+    def _setup_replay(self, rp, want_schedule):
+        torch = _torch()
+        dev = self.device
+        nh, nl = int(rp.hp_records.shape[0]), int(rp.lp_records.shape[0])
+        S = int(rp.scenarios.shape[0])
+        r = {
+            "nh": nh, "nl": nl, "S": S, "threshold_ns": int(rp.threshold_ns), "feedback": int(rp.feedback),
+            "hp_recs": records_to_device(rp.hp_records, dev) if nh else torch.zeros(48, dtype=torch.uint8,
+                                                                                     device=dev),
+            "lp_recs": records_to_device(rp.lp_records, dev) if nl else torch.zeros(48, dtype=torch.uint8,
+                                                                                     device=dev),
+            "lp_level": torch.from_numpy(np.ascontiguousarray(rp.lp_level, dtype=np.uint8)).to(dev)
+            if nl else torch.zeros(1, dtype=torch.uint8, device=dev),
+            "sc": torch.from_numpy(np.ascontiguousarray(rp.scenarios).view(np.uint8).reshape(-1)).to(dev)
+            if S else torch.zeros(24, dtype=torch.uint8, device=dev),
+            "hp_row": torch.empty(max(1, nh), dtype=torch.int32, device=dev),
+            "hp_dur": torch.empty(max(1, nh), dtype=torch.int64, device=dev),
+            "hp_gap": torch.empty(max(1, nh), dtype=torch.int64, device=dev),
+            "lp_row": torch.empty(max(1, nl), dtype=torch.int32, device=dev),
+            "lp_dur": torch.empty(max(1, nl), dtype=torch.int64, device=dev),
+            "lp_gap": torch.empty(max(1, nl), dtype=torch.int64, device=dev),
+            "out": torch.empty(max(1, S) * 48, dtype=torch.uint8, device=dev),
+        }
+        if want_schedule and S:
+            m = rp.scenarios["lp_len"].astype(np.uint64)
+            so = np.zeros(S, dtype=np.uint64)
+            so[1:] = np.cumsum(m[:-1])
+            tot = max(1, int(m.sum()))
+            r["sched_off"] = torch.from_numpy(so.view(np.int64)).to(dev)
+            r["fill_gap"] = torch.empty(tot, dtype=torch.int32, device=dev)
+            r["lp_start"] = torch.empty(tot, dtype=torch.int64, device=dev)
+        self.replay = r
+
+    # -- a1..a6: identify + measure + finalize --------------------------------------------
+    def run_measure(self, stream=None):
+        measure(self.recs, self.n, self.names, self.sigs, self.table, self.ws, halo=self.halo, out_row=self.out_row,
+                stream=stream)
+        table_finalize(self.table, self.ws, out_row=self.out_row, n=self.n if self.out_row is not None else 0,
+                       stream=stream)
+
+    # -- a8..a10: resolve the replay's launches, then the batch replay ------------------------
+    def run_replay(self, stream=None):
+        r = self.replay
+        resolve(r["hp_recs"], r["nh"], self.names, self.sigs, self.table, r["hp_row"], r["hp_dur"], r["hp_gap"],
+                self.ws, stream=stream)
+        resolve(r["lp_recs"], r["nl"], self.names, self.sigs, self.table, r["lp_row"], r["lp_dur"], r["lp_gap"],
+                self.ws, stream=stream)
+        simulate_batch(self.table, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
+                       r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],
+                       fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off"),
+                       stream=stream)
+
+    def step(self, stream=None):
+        self.run_measure(stream)
+        if self.replay is not None:
+            self.run_replay(stream)
+
+    def check(self, what="pipeline", stream=None):
+        return check(self.ws, what, stream)
+
+    # -- host views ------------------------------------------------------------------------------
+    def results(self) -> np.ndarray:
+        r = self.replay
+        return r["out"].cpu().numpy()[: r["S"] * 48].view(RESULT_DTYPE)
+
+    def schedule(self):
+        r = self.replay
+        return r["fill_gap"].cpu().numpy(), r["lp_start"].cpu().numpy().view(np.uint64)
+
+    def resolved(self):
+        r = self.replay
+        u = lambda t, n, dt: t.cpu().numpy().view(dt)[:n]
+        return ((u(r["hp_row"], r["nh"], np.uint32), u(r["hp_dur"], r["nh"], np.uint64),
+                 u(r["hp_gap"], r["nh"], np.uint64)),
+                (u(r["lp_row"], r["nl"], np.uint32), u(r["lp_dur"], r["nl"], np.uint64)))
+
+    def rows(self) -> np.ndarray:
+        return self.out_row.cpu().numpy().view(np.uint32)[: self.n]

@@ -1,0 +1,236 @@
+"""GPU <-> oracle parity through the C-ABI (bit-exact: all work is integer).
+
+Every test runs the CUDA path (libfikit.so via the thin binding) and the CPU
+oracle on the same seeded inputs and compares element by element."""
+import numpy as np
+import pytest
+
+import fikit_synth as F
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+TABLE_FIELDS = ("kernel_id", "task_id", "dur_cnt", "dur_sum", "dur_min", "dur_max", "gap_cnt", "gap_sum", "gap_min",
+                "gap_max", "dur_hist", "gap_hist", "dur_mean", "gap_mean")
+
+
+@pytest.fixture(scope="module")
+def fk():
+    import paper_2311_10359_b200 as fk
+
+    from paper_2311_10359_b200 import _build
+
+    _build.build()
+    return fk
+
+
+def assert_tables_equal(got: dict, ref_tab, ctx=""):
+    ref = ref_tab.head()
+    assert got["kernel_id"].shape[0] == ref_tab.n_rows, f"{ctx}: n_rows {got['kernel_id'].shape[0]} vs {ref_tab.n_rows}"
+    for k in TABLE_FIELDS:
+        a, b = np.asarray(got[k]), np.asarray(ref[k])
+        if not np.array_equal(a, b):
+            bad = np.argwhere(a != b)[:5]
+            raise AssertionError(f"{ctx}: field {k} differs at {bad.tolist()}: gpu {a[tuple(bad[0])]} "
+                                 f"oracle {b[tuple(bad[0])]}")
+
+
+def run_measure(fk, tr, capacity=None, halo=None, want_rows=False):
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=capacity, want_rows=want_rows, halo=halo)
+    p.run_measure()
+    return p
+
+
+def test_toy_end_to_end(fk, orc):
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.toy()
+    for fb in (1, 0):
+        cfg.replay.feedback = fb
+        ref = orc.pipeline(cfg, capacity=64)
+        p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=64, replay=cfg.replay,
+                     want_schedule=True)
+        p.step()
+        st = p.check()
+        assert st["n_overlap_gaps"] == ref["status"]["n_overlap_gaps"]
+        assert_tables_equal(p.table.to_numpy(), ref["table"], "toy")
+        (hr, hd, hg), (lr, ld) = p.resolved()
+        assert np.array_equal(hr, ref["hp"][0]) and np.array_equal(hd, ref["hp"][1]) and np.array_equal(hg, ref["hp"][2])
+        assert np.array_equal(lr, ref["lp"][0]) and np.array_equal(ld, ref["lp"][1])
+        assert p.results().tobytes() == ref["results"].tobytes()
+        fg, ls = p.schedule()
+        assert np.array_equal(fg, ref["fill_gap"]) and np.array_equal(ls, ref["lp_start"])
+
+
+@pytest.mark.parametrize("seed,n,kw", [
+    (1, 1, {}), (2, 31, {}), (3, 32, {}), (4, 33, {}), (5, 255, {}), (6, 256, {}), (7, 257, {}),
+    (8, 5000, {"overlap_frac": 0.2}), (9, 5000, {"zero_frac": 0.3}), (10, 5000, {"big_frac": 0.1}),
+    (11, 5000, {"run_len_max": 1}), (12, 5000, {"n_ids": 1, "n_tasks": 1}),
+    (13, 20000, {"n_ids": 900, "n_tasks": 4, "n_names": 300}),  # > kHotMax rows: cold path
+    (14, 70000, {"n_ids": 3000, "n_tasks": 7, "n_names": 800, "overlap_frac": 0.05}),
+])
+def test_measure_random(fk, orc, seed, n, kw):
+    tr = F.random_trace(seed, n, **kw)
+    ref, rst, rrows = orc.measure(tr.records, tr.names, tr.sigs, want_rows=True)
+    p = run_measure(fk, tr, capacity=max(16, 2 * ref.n_rows), want_rows=True)
+    st = p.check()
+    assert st["n_overlap_gaps"] == rst["n_overlap_gaps"]
+    assert st["n_rows_needed"] == ref.n_rows
+    assert_tables_equal(p.table.to_numpy(), ref, f"seed {seed}")
+    assert np.array_equal(p.rows(), rrows)
+
+
+def test_identify_random(fk, orc):
+    import torch
+
+    tr = F.random_trace(21, 10007, n_ids=500, n_names=200)
+    ref, _ = orc.identify(tr.records, tr.names, tr.sigs)
+    recs = fk.records_to_device(tr.records)
+    names, sigs = fk.strtab_to_device(tr.names), fk.strtab_to_device(tr.sigs)
+    out = torch.empty(tr.records.shape[0], dtype=torch.int64, device="cuda")
+    ws = fk.Workspace(1, tr.names.count, tr.sigs.count)
+    fk.identify(recs, tr.records.shape[0], names, sigs, out, ws)
+    fk.check(ws)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), ref)
+
+
+@pytest.mark.parametrize("field,val", [("grid_x", 0), ("block_z", 0), ("name_id", 10**6), ("sig_id", 10**6),
+                                       ("flags", 3), ("end_ns", 0)])
+def test_invalid_record_index(fk, orc, field, val):
+    tr = F.random_trace(22, 3000)
+    rec = tr.records.copy()
+    for i in (1777, 2900, 2001):
+        rec[field][i] = val
+        if field == "end_ns":
+            rec["start_ns"][i] = 5
+    _, rst, _ = orc.measure(rec, tr.names, tr.sigs)
+    assert rst["code"] == orc.E_RECORD and rst["first_bad_index"] == 1777
+    bad = F.Trace(rec, tr.names, tr.sigs)
+    p = run_measure(fk, bad, capacity=256)
+    st = fk.get_status(p.ws)
+    assert st["code"] == fk.E_RECORD and st["first_bad_index"] == 1777
+
+
+def test_capacity_and_empty_name(fk, orc):
+    tr = F.random_trace(23, 4000, n_ids=60, n_tasks=3)
+    ref, _, _ = orc.measure(tr.records, tr.names, tr.sigs)
+    _, rst, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=10)
+    p = run_measure(fk, tr, capacity=10)
+    st = fk.get_status(p.ws)
+    assert st["code"] == fk.E_CAPACITY == rst["code"] and st["n_rows_needed"] == rst["n_rows_needed"] == ref.n_rows
+    names = F.StrTab.from_list([tr.names.get(i) for i in range(tr.names.count)] + [b""])
+    p = run_measure(fk, F.Trace(tr.records, names, tr.sigs), capacity=512)
+    assert fk.get_status(p.ws)["code"] == fk.E_NAME
+
+
+def test_halo(fk, orc):
+    tr = F.random_trace(24, 3001, run_len_max=80)
+    for cut in (1, 1000, 2048, 3000):
+        a = F.Trace(tr.records[:cut], tr.names, tr.sigs)
+        ref, rst, _ = orc.measure(a.records, a.names, a.sigs, halo=tr.records[cut])
+        p = run_measure(fk, a, capacity=512, halo=tr.records[cut])
+        st = p.check()
+        assert_tables_equal(p.table.to_numpy(), ref, f"halo cut {cut}")
+        assert st["n_overlap_gaps"] == rst["n_overlap_gaps"]
+
+
+def test_resnet_full(fk, orc):
+    cfg = F.resnet_trace()
+    ref, rst, _ = orc.measure(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=4096)
+    p = run_measure(fk, cfg.trace, capacity=4096)
+    p.check()
+    assert ref.n_rows == 96
+    assert_tables_equal(p.table.to_numpy(), ref, "resnet")
+
+
+def _replay_parity(fk, orc, cfg, capacity, check_schedule=True):
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    ref = orc.pipeline(cfg, capacity=capacity)
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=capacity, replay=cfg.replay,
+                 want_schedule=check_schedule)
+    p.step()
+    p.check()
+    assert_tables_equal(p.table.to_numpy(), ref["table"], cfg.name)
+    (hr, hd, hg), (lr, ld) = p.resolved()
+    assert np.array_equal(hr, ref["hp"][0]) and np.array_equal(hg, ref["hp"][2]) and np.array_equal(lr, ref["lp"][0])
+    got = p.results()
+    if got.tobytes() != ref["results"].tobytes():
+        bad = np.flatnonzero(got != ref["results"])[:5]
+        raise AssertionError(f"{cfg.name}: scenarios {bad.tolist()} differ: {got[bad]} vs {ref['results'][bad]}")
+    if check_schedule:
+        fg, ls = p.schedule()
+        assert np.array_equal(fg, ref["fill_gap"]) and np.array_equal(ls, ref["lp_start"])
+    return ref
+
+
+def test_random_replay(fk, orc):
+    tr = F.random_trace(31, 4000, n_ids=40)
+    for seed in range(4):
+        rp = F.random_replay(40 + seed, tr, 300, m_max=70, n_h_max=50, levels=9,
+                             gap_scale=(1 << 14, 1 << 16, 1 << 19))
+        _replay_parity(fk, orc, F.Config("random", tr, rp), 256)
+
+
+def test_bert_vgg_full(fk, orc):
+    cfg = F.bert_vgg()
+    ref = _replay_parity(fk, orc, cfg, 1024, check_schedule=True)
+    assert ref["results"]["n_fills"].sum() > 0
+
+
+def test_sweep_sample(fk, orc):
+    cfg = F.sweep(S=4000)
+    _replay_parity(fk, orc, cfg, 1024, check_schedule=True)
+
+
+def test_zipf_small_full(fk, orc):
+    cfg = F.zipf_trace(n_runs=8000)  # 2.05 M records, all 8,192-row structure, hot + cold paths
+    ref, rst, _ = orc.measure(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=8192)
+    p = run_measure(fk, cfg.trace, capacity=8192)
+    st = p.check()
+    assert ref.n_rows > 640  # more rows than the shared-memory hot cache
+    assert_tables_equal(p.table.to_numpy(), ref, "zipf-2M")
+    assert st["n_overlap_gaps"] == rst["n_overlap_gaps"]
+
+
+def test_fill_batch(fk, orc):
+    import torch
+
+    tr = F.random_trace(51, 3000, n_ids=30)
+    ref_tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs)
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=128)
+    p.run_measure()
+    rng = np.random.default_rng(52)
+    G = 3000
+    pool_len = rng.integers(0, 80, size=G).astype(np.uint32)
+    pool_off = np.zeros(G, np.uint32)
+    pool_off[1:] = np.cumsum(pool_len[:-1])
+    tot = int(pool_len.sum())
+    pool_row = rng.integers(0, ref_tab.n_rows + 3, size=tot).astype(np.uint32)  # some absent rows
+    pool_dur = rng.integers(1, 3 * F.MS, size=tot).astype(np.uint64)
+    pool_level = rng.integers(1, 10, size=tot).astype(np.uint8)
+    R0 = rng.integers(0, 10 * F.MS, size=G).astype(np.uint64)
+    dl = np.where(rng.random(G) < 0.5, rng.integers(0, 5 * F.MS, size=G), 2**64 - 1).astype(np.uint64)
+    for fb in (0, 1):
+        picks, poff, npk, Rl, tu, st = orc.fill_batch(R0, dl, pool_row, pool_dur, pool_level, pool_off, pool_len,
+                                                      ref_tab, feedback=fb)
+        d = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).cuda()
+        g_picks = torch.zeros(max(1, tot), dtype=torch.int32, device="cuda")
+        g_np = torch.zeros(G, dtype=torch.int32, device="cuda")
+        g_R = torch.zeros(G, dtype=torch.int64, device="cuda")
+        g_t = torch.zeros(G, dtype=torch.int64, device="cuda")
+        fk.fill(p.table, d(R0, np.int64), d(dl, np.int64), d(pool_row, np.int32), d(pool_dur, np.int64),
+                d(pool_level, np.uint8), d(pool_off, np.int32), d(pool_len, np.int32), G, g_picks,
+                d(poff, np.int32), g_np, g_R, g_t, p.ws, feedback=fb)
+        fk.check(p.ws)
+        assert np.array_equal(g_np.cpu().numpy().view(np.uint32), npk)
+        assert np.array_equal(g_R.cpu().numpy().view(np.uint64), Rl)
+        assert np.array_equal(g_t.cpu().numpy().view(np.uint64), tu)
+        gp = g_picks.cpu().numpy().view(np.uint32)
+        for g in range(G):
+            o = int(poff[g])
+            assert np.array_equal(gp[o:o + npk[g]], picks[o:o + npk[g]]), g
