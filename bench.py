@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py -- FIKIT hot path on B200: launch-records/s (identify+measure) and
+fill-scenarios/s, with the HBM roofline of the measure kernel.
+
+A step = one pass of the whole hot path over one batch (SURVEY §8a rows
+a1-a10): fikit_measure (stream + validate + identify + per-ID statistics) ->
+fikit_table_finalize -> [P > 1: dictionary union + NCCL merge] ->
+fikit_resolve (HP and LP launches) -> fikit_simulate_batch.
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload zipf|resnet|bert_vgg|sweep]
+  python bench.py --impl reference ...   # the CPU oracle, timed on host cores
+
+Default workload (N=1): configs[3], the 100M-launch Zipf trace (4.8 GB, the
+largest single-GPU configuration and the one the >= 60 % HBM target is quoted
+on) + a 100k-scenario replay batch over its table.  Multi-GPU: records shard
+contiguously with a one-record halo (strong scaling: the 100M total is fixed),
+scenarios shard s mod N.  Inputs are synthetic (fikit_synth, seeded).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "launch-records/s (identify+measure) and fill-scenarios/s at 1/2/4/8 B200; % HBM peak"
+UNIT = "launch-records/s"
+REC_BYTES = 48  # algorithmic bytes per launch record
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
+    ap.add_argument("--workload", default="zipf", choices=["zipf", "resnet", "bert_vgg", "sweep"])
+    ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
+    ap.add_argument("--scenarios", type=int, default=100_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+def make_workload(args, rank, world):
+    """This rank's inputs: (records, halo, names, sigs, replay subset, meta)."""
+    import fikit_synth as F
+    from paper_2311_10359_b200.dist import scenario_shard, shard_range
+
+    if args.workload == "zipf":
+        runs = 390_625 if args.records is None else max(1, args.records // 256)
+        N = runs * 256
+        lo, hi = shard_range(N, rank, world)
+        cfg = F.zipf_trace(n_runs=runs, rec_lo=lo, rec_hi=min(N, hi + 1), threads=min(16, os.cpu_count() or 8))
+        recs = cfg.trace.records
+        halo = recs[hi - lo] if hi < N else None
+        recs = recs[: hi - lo]
+        replay = F.zipf_replay(cfg, S=args.scenarios)
+        cap = 8192
+        desc = f"zipf-{N // 1_000_000}M (configs[3]) + replay-{args.scenarios // 1000}k"
+    else:
+        cfg = {"resnet": F.resnet_trace, "bert_vgg": F.bert_vgg, "sweep": F.sweep}[args.workload]()
+        N = cfg.trace.records.shape[0]
+        lo, hi = shard_range(N, rank, world)
+        recs = cfg.trace.records[lo:hi]
+        halo = cfg.trace.records[hi] if hi < N else None
+        replay = cfg.replay
+        cap = 4096
+        desc = {"resnet": "resnet-3M (configs[1])", "bert_vgg": "bert_vgg-100k (configs[2])",
+                "sweep": "sweep-1M (configs[4])"}[args.workload]
+    if replay is not None and world > 1:
+        sel = scenario_shard(replay.scenarios.shape[0], rank, world)
+        replay = F.Replay(replay.hp_records, replay.lp_records, replay.lp_level, replay.scenarios[sel],
+                          replay.threshold_ns, replay.feedback)
+    return dict(records=recs, halo=halo, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=replay, N=N, cap=cap,
+                desc=desc, cfg=cfg)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50", "-i",
+                 str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy kernel)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per fikit_measure launch from the committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "measure_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_record"), d.get("source")
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_sample_time(wl, budget_s, seed=0):
+    """Time the CPU oracle (as it stands, single thread) on a bounded sample of
+    the workload and extrapolate the whole job.  Returns (job_seconds, sample_desc)."""
+    import oracle
+
+    oracle.build()
+    recs, names, sigs = wl["records"], wl["names"], wl["sigs"]
+    # calibrate on a small slice, then size the measure sample to ~60 % of the budget
+    n0 = min(recs.shape[0], 100_000)
+    t = time.perf_counter()
+    oracle.measure(recs[:n0], names, sigs, capacity=65536)
+    r0 = n0 / max(1e-9, time.perf_counter() - t)
+    n1 = int(min(recs.shape[0], max(n0, r0 * budget_s * 0.6)))
+    t = time.perf_counter()
+    tab, _, _ = oracle.measure(recs[:n1], names, sigs, capacity=65536)
+    t_meas = time.perf_counter() - t
+    job = t_meas * (wl["N"] / n1)
+    desc = f"oracle measure on the first {n1:,} of {wl['N']:,} records"
+    rp = wl["replay"]
+    if rp is not None:
+        S = rp.scenarios.shape[0]
+        # a bounded set of scenarios, resolving only the launches they reference
+        s_n = max(1, min(S, 200))
+        sc = rp.scenarios[:s_n].copy()
+        hp_idx = np.concatenate([np.arange(c["hp_off"], c["hp_off"] + c["hp_len"]) for c in sc]).astype(np.int64)
+        lp_idx = np.concatenate([np.arange(c["lp_off"], c["lp_off"] + c["lp_len"]) for c in sc]).astype(np.int64)
+        t = time.perf_counter()
+        hr, hd, hg, _ = oracle.resolve(rp.hp_records[hp_idx], names, sigs, tab)
+        lr, ld, _, _ = oracle.resolve(rp.lp_records[lp_idx], names, sigs, tab)
+        off_h = np.concatenate([[0], np.cumsum(sc["hp_len"][:-1])]).astype(np.uint32)
+        off_l = np.concatenate([[0], np.cumsum(sc["lp_len"][:-1])]).astype(np.uint32)
+        sc["hp_off"], sc["lp_off"] = off_h, off_l
+        oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
+        t_rep = time.perf_counter() - t
+        job += t_rep * (S / s_n)
+        desc += f" + resolve/replay of {s_n} of {S:,} scenarios"
+    return job, desc + "; whole-job time extrapolated linearly"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the tier's reference arm), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = make_workload(args, 0, 1)
+    per_step = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        job, desc = oracle_sample_time(wl, per_step)
+        if i >= args.warmup:
+            times.append(job)
+    job = float(np.median(times))
+    value = wl["N"] / job
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": job * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "records": wl["N"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2311_10359_b200 import _build
+
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2311_10359_b200 as fk
+    from paper_2311_10359_b200.dist import LibOps, merge_tables
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    t_gen = time.perf_counter()
+    wl = make_workload(args, rank, world)
+    t_gen = time.perf_counter() - t_gen
+    stream = torch.cuda.current_stream()
+    p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"])
+    n_local = p.n
+    dense = fk.Table(wl["cap"]) if world > 1 else None
+    ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None
+    S_local = p.replay["S"] if p.replay else 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    stage_ms = np.zeros(4)
+
+    def step(timed):
+        if timed:
+            ev[0].record(stream)
+        fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo)
+        if timed:
+            ev[1].record(stream)
+        fk.table_finalize(p.table, p.ws)
+        tab = p.table
+        if world > 1:
+            merge_tables(p.table, dense, ops)
+            tab = dense
+        if timed:
+            ev[2].record(stream)
+        if p.replay:
+            p.run_replay(table=tab)
+        if timed:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    st = fk.check(p.ws, "bench warm-up")  # the path ran clean (status of the last call)
+    # per-stage breakdown on separately timed steps (events between launches)
+    n_stage = min(20, args.steps)
+    for _ in range(n_stage):
+        step(True)
+        torch.cuda.synchronize()
+        stage_ms += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]), 0]
+    stage_ms /= n_stage
+
+    # ---- timed region: K back-to-back steps, barrier + sync on both sides ----
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = fk.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(False)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = fk.launch_count() - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    N = wl["N"]
+    S_total = wl["replay"].scenarios.shape[0] * (world if world > 1 else 1) if wl["replay"] is not None else 0
+    if wl["replay"] is not None and world > 1:
+        S_total = int(torch.tensor([S_local], device="cuda").sum().item())
+        t = torch.tensor([S_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        S_total = int(t.item())
+    value = N / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (fikit_measure: 48 algorithmic bytes per launch) ----
+    peak, peak_src = peaks()
+    meas_ms = stage_ms[0]
+    achieved = REC_BYTES * n_local / (meas_ms * 1e-3) / 1e9
+    trf, trf_src = ncu_traffic()
+    roof = {"bound": "hbm", "kernel": "fikit_measure (k_sample + k_hot_select + k_measure)", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": REC_BYTES * n_local,
+            "traffic": (trf * n_local if trf is not None else None), "traffic_source": trf_src,
+            "measure_ms": meas_ms}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (fikit_synth, seeded)",
+            "config": {"workload": wl["desc"], "records": N, "records_per_gpu": n_local, "scenarios": S_total,
+                       "table_rows": p.table.n_rows() if world == 1 else dense.n_rows(),
+                       "l2": "inputs (4.8 GB trace) larger than the 126 MB L2; no flush",
+                       "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},
+            "scenarios_per_s": (S_total / (ms * 1e-3)) if S_total else None,
+            "stages_ms": {"measure": stage_ms[0], "finalize+merge": stage_ms[1], "resolve+replay": stage_ms[2]},
+            "measure_records_per_s": n_local / (stage_ms[0] * 1e-3),
+            "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "status": {"code": st["code"], "n_rows_needed": st["n_rows_needed"]},
+            "gen_s": round(t_gen, 2)}
+
+    # ---- end to end through the C-ABI with host buffers (H2D + step + D2H inside the region) ----
+    if not args.no_e2e:
+        pin = torch.from_numpy(np.ascontiguousarray(wl["records"]).view(np.uint8).reshape(-1)).pin_memory()
+        host_out = torch.empty(p.table.block.numel(), dtype=torch.uint8).pin_memory()
+        rep_out = torch.empty(p.replay["out"].numel(), dtype=torch.uint8).pin_memory() if p.replay else None
+        h2d = pin.numel()
+        d2h = host_out.numel() + (rep_out.numel() if rep_out is not None else 0)
+        if p.replay:
+            rp_pins = [p.replay[k].cpu().pin_memory() for k in ("hp_recs", "lp_recs", "lp_level", "sc")]
+            h2d += sum(x.numel() * x.element_size() for x in rp_pins)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            p.recs.copy_(pin, non_blocking=True)
+            if p.replay:
+                for k, x in zip(("hp_recs", "lp_recs", "lp_level", "sc"), rp_pins):
+                    p.replay[k].copy_(x, non_blocking=True)
+            step(False)
+            (dense if world > 1 else p.table).block.numel()
+            host_out.copy_((dense if world > 1 else p.table).block, non_blocking=True)
+            if rep_out is not None:
+                rep_out.copy_(p.replay["out"], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        line["e2e"] = {"value": N / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "steps": args.e2e_steps,
+                       "path": "pinned host -> device copies + fikit_* C-ABI calls + result copies back"}
+
+    # ---- CPU baseline: the oracle on the host cores, rank 0, N=1 only ----
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        job, desc = oracle_sample_time(wl, args.cpu_budget_s)
+        line["cpu_baseline"] = {"value": N / job, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                "host_cores_available": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -418,12 +418,18 @@ def _zipf_p(n: int, s: float = ZIPF_S) -> np.ndarray:
 
 
 def zipf_trace(seed: int = 4, n_runs: int = 390_625, run_len: int = 256, n_tasks: int = 32, vocab_per_task: int = 256,
-               chunk_runs: int = 16384) -> Config:
+               chunk_runs: int = 8192, rec_lo: int = 0, rec_hi: int | None = None, threads: int = 8) -> Config:
     """configs[3]: multi-model trace with Zipf(1.1) kernel-ID skew: 32 tasks x a
     256-kernel vocabulary each (<= 8,192 rows); runs of 256 launches; each
     run's task ~ Zipf(1.1) over 32 tasks; each launch's kernel ~ Zipf(1.1)
     over its task's vocabulary.  390,625 runs -> 100,000,000 records (4.8 GB).
-    Durations log-U[2 us, 2 ms] per row x U[0.9, 1.1]; gaps as config R."""
+    Durations log-U[2 us, 2 ms] per row x U[0.9, 1.1]; gaps as config R.
+
+    Runs are generated in chunks of `chunk_runs`, each from its own seeded
+    stream and time origin (chunk * 2^42 ns), so any record range
+    [rec_lo, rec_hi) -- a rank's shard plus its halo -- is reproducible alone."""
+    from concurrent.futures import ThreadPoolExecutor
+
     rng = np.random.default_rng(seed)
     n_names = 2048
     names = _mangled_names(rng, n_names)
@@ -442,19 +448,24 @@ def zipf_trace(seed: int = 4, n_runs: int = 390_625, run_len: int = 256, n_tasks
     p_task = _zipf_p(n_tasks)
     p_k = _zipf_p(vocab_per_task)
     N = n_runs * run_len
-    rec = np.zeros(N, dtype=REC_DTYPE)
+    rec_hi = N if rec_hi is None else min(rec_hi, N)
+    rec_lo = max(0, min(rec_lo, rec_hi))
+    rec = np.zeros(rec_hi - rec_lo, dtype=REC_DTYPE)
     all_name = np.stack([v.name_id for v in vocabs])
     all_sig = np.stack([v.sig_id for v in vocabs])
     all_grid = np.stack([v.grid for v in vocabs])
     all_block = np.stack([v.block for v in vocabs])
-    t0 = 0
-    for r0 in range(0, n_runs, chunk_runs):
+    CR = chunk_runs * run_len
+
+    def gen(c):
+        r0 = c * chunk_runs
         nr = min(chunk_runs, n_runs - r0)
         n = nr * run_len
-        sl = rec[r0 * run_len : r0 * run_len + n]
-        task = rng.choice(n_tasks, size=nr, p=p_task)
+        crng = np.random.default_rng([seed, c])
+        sl = np.zeros(n, dtype=REC_DTYPE)
+        task = crng.choice(n_tasks, size=nr, p=p_task)
         task_r = np.repeat(task, run_len)
-        kk = perm[task_r, rng.choice(vocab_per_task, size=n, p=p_k)]
+        kk = perm[task_r, crng.choice(vocab_per_task, size=n, p=p_k)]
         sl["name_id"] = all_name[task_r, kk]
         sl["sig_id"] = all_sig[task_r, kk]
         sl["grid_x"] = all_grid[task_r, kk, 0]
@@ -463,14 +474,21 @@ def zipf_trace(seed: int = 4, n_runs: int = 390_625, run_len: int = 256, n_tasks
         sl["block_x"] = all_block[task_r, kk, 0]
         sl["block_y"] = all_block[task_r, kk, 1]
         sl["block_z"] = all_block[task_r, kk, 2]
-        dur = np.maximum(np.rint(base_dur[task_r, kk] * rng.uniform(0.9, 1.1, n)), 1).astype(np.uint64)
-        gap = np.clip(np.rint(_gap_mixture(rng, n) * rng.uniform(0.8, 1.2, n)), 1 * US, 20 * MS).astype(np.uint64)
-        t0 = _timestamps(sl, dur, gap, run_len, t0)
+        dur = np.maximum(np.rint(base_dur[task_r, kk] * crng.uniform(0.9, 1.1, n)), 1).astype(np.uint64)
+        gap = np.clip(np.rint(_gap_mixture(crng, n) * crng.uniform(0.8, 1.2, n)), 1 * US, 20 * MS).astype(np.uint64)
+        _timestamps(sl, dur, gap, run_len, c << 42)
         sl["run_id"] = r0 + np.repeat(np.arange(nr, dtype=np.uint32), run_len)
         sl["task_id"] = task_r.astype(np.uint32)
+        a, b = max(rec_lo, c * CR), min(rec_hi, c * CR + n)
+        rec[a - rec_lo : b - rec_lo] = sl[a - c * CR : b - c * CR]
+
+    chunks = range(rec_lo // CR, (rec_hi - 1) // CR + 1) if rec_hi > rec_lo else range(0)
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(gen, chunks))
     return Config("zipf", Trace(rec, StrTab.from_list(names), StrTab.from_list(sigs)), None,
                   {"seed": seed, "runs": n_runs, "run_len": run_len, "tasks": n_tasks, "vocab": vocab_per_task,
-                   "p_task": p_task, "p_k": p_k, "perm": perm, "vocabs": vocabs})
+                   "p_task": p_task, "p_k": p_k, "perm": perm, "vocabs": vocabs, "N": N, "rec_lo": rec_lo,
+                   "rec_hi": rec_hi})
 
 
 def zipf_replay(cfg: Config, seed: int = 44, n_hp_runs: int = 1000, pop: int = 1 << 20, S: int = 100_000,

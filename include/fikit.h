@@ -235,6 +235,13 @@ int fikit_table_remap(const fikit_table_t* local, const uint32_t* local_to_union
                       const uint32_t* union_task, const uint32_t* union_n, const fikit_table_t* dense,
                       void* stream);
 
+/* XOR 2^63 into every ext word of rows [0, capacity): maps the unsigned order of
+ * the MAX block onto the signed order, so a signed 64-bit MAX all-reduce
+ * (what NCCL / gloo offer through torch) reduces it correctly; an all-zero row
+ * becomes INT64_MIN, the identity of signed MAX.  An involution: apply it
+ * before and after the reduction. */
+int fikit_table_bias(const fikit_table_t* tab, void* stream);
+
 /* ---- status --------------------------------------------------------------- */
 /* Synchronises `stream`, copies the workspace status to *out (host) and
  * derives out->code from the flags by precedence.  Returns out->code. */

@@ -24,7 +24,7 @@ NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
            "fikit_table_finalize", "fikit_table_means", "fikit_resolve", "fikit_lookup", "fikit_fill",
-           "fikit_simulate_batch", "fikit_dict_union", "fikit_table_remap", "fikit_get_status", "fikit_strerror",
+           "fikit_simulate_batch", "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
 
 
@@ -82,6 +82,7 @@ def lib():
                                            sz, p]
         L.fikit_dict_union.argtypes = [p, p, p, u32, u32, u32, p, p, u32, p, p, p, sz, p]
         L.fikit_table_remap.argtypes = [C.POINTER(TableC), p, p, p, p, C.POINTER(TableC), p]
+        L.fikit_table_bias.argtypes = [C.POINTER(TableC), p]
         L.fikit_get_status.argtypes = [p, C.POINTER(StatusC), p]
         L.fikit_strerror.restype = C.c_char_p
         L.fikit_strerror.argtypes = [C.c_int]
@@ -287,3 +288,7 @@ def dict_union(all_kid, all_task, n_list, P: int, Kmax: int, self_rank: int, out
 def table_remap(local: Table, local_to_union, union_kid, union_task, union_n, dense: Table, stream=None):
     _chk(lib().fikit_table_remap(C.byref(local.c), _ptr(local_to_union), _ptr(union_kid), _ptr(union_task),
                                  _ptr(union_n), C.byref(dense.c), _stream(stream)), "table_remap")
+
+
+def table_bias(table: Table, stream=None):
+    _chk(lib().fikit_table_bias(C.byref(table.c), _stream(stream)), "table_bias")

@@ -37,6 +37,7 @@ __global__ void k_union_place(const uint64_t*, const uint32_t*, const uint32_t*,
                               fikit_status_t*);
 __global__ void k_table_remap(fikit_table_t, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*,
                               fikit_table_t);
+__global__ void k_table_bias(fikit_table_t);
 __global__ void k_fill(fikit_table_t, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
                        const uint8_t*, const uint32_t*, const uint32_t*, uint32_t, fikit_fill_params_t, uint32_t*,
                        const uint32_t*, uint32_t*, uint64_t*, uint64_t*, fikit_status_t*);
@@ -360,6 +361,12 @@ int fikit_table_remap(const fikit_table_t* local, const uint32_t* l2u, const uin
   if (!table_ok(local) || !table_ok(dense) || !l2u || !ukid || !utask || !un) return FIKIT_E_ARG;
   uint32_t m = local->capacity > dense->capacity ? local->capacity : dense->capacity;
   k_table_remap<<<(m + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*local, l2u, ukid, utask, un, *dense);
+  return launched();
+}
+
+int fikit_table_bias(const fikit_table_t* tab, void* stream) {
+  if (!table_ok(tab)) return FIKIT_E_ARG;
+  k_table_bias<<<grid_for(4ull * tab->capacity, 256, num_sms() * 4), 256, 0, (cudaStream_t)stream>>>(*tab);
   return launched();
 }
 

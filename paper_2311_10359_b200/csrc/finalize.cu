@@ -324,4 +324,10 @@ __global__ void k_table_remap(fikit_table_t local, const uint32_t* __restrict__ 
   for (int b = 0; b < 64; b++) dense.hist[(size_t)d * 64 + b] = local.hist[(size_t)i * 64 + b];
 }
 
+__global__ void k_table_bias(fikit_table_t tab) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 4ull * tab.capacity;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    tab.ext[i] ^= 0x8000000000000000ULL;
+}
+
 }  // namespace fikit

@@ -15,8 +15,12 @@ from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure
 
 class Pipeline:
     def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
-                 want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None):
+                 want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None,
+                 checked: bool = False):
+        """checked: verify the workspace status after every call (tests); the
+        bench leaves it off and checks once after warm-up."""
         torch = _torch()
+        self.checked = checked
         self.device = device
         self.n = int(records.shape[0])
         self.capacity = int(capacity if capacity is not None else max(1, min(self.n, 1 << 16)))
@@ -69,20 +73,30 @@ class Pipeline:
     def run_measure(self, stream=None):
         measure(self.recs, self.n, self.names, self.sigs, self.table, self.ws, halo=self.halo, out_row=self.out_row,
                 stream=stream)
+        self._chk("measure", stream)
         table_finalize(self.table, self.ws, out_row=self.out_row, n=self.n if self.out_row is not None else 0,
                        stream=stream)
 
     # -- a8..a10: resolve the replay's launches, then the batch replay ------------------------
-    def run_replay(self, stream=None):
+    def run_replay(self, stream=None, table: Table | None = None):
+        """table: the profile to replay against (default: this pipeline's; the merged one for P > 1)."""
         r = self.replay
-        resolve(r["hp_recs"], r["nh"], self.names, self.sigs, self.table, r["hp_row"], r["hp_dur"], r["hp_gap"],
+        tab = self.table if table is None else table
+        resolve(r["hp_recs"], r["nh"], self.names, self.sigs, tab, r["hp_row"], r["hp_dur"], r["hp_gap"],
                 self.ws, stream=stream)
-        resolve(r["lp_recs"], r["nl"], self.names, self.sigs, self.table, r["lp_row"], r["lp_dur"], r["lp_gap"],
+        self._chk("resolve(hp)", stream)
+        resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
                 self.ws, stream=stream)
-        simulate_batch(self.table, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
+        self._chk("resolve(lp)", stream)
+        simulate_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
                        r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],
                        fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off"),
                        stream=stream)
+        self._chk("simulate_batch", stream)
+
+    def _chk(self, what, stream):
+        if self.checked:
+            self.last_status = check(self.ws, what, stream)
 
     def step(self, stream=None):
         self.run_measure(stream)

@@ -51,9 +51,10 @@ def test_toy_end_to_end(fk, orc):
         cfg.replay.feedback = fb
         ref = orc.pipeline(cfg, capacity=64)
         p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=64, replay=cfg.replay,
-                     want_schedule=True)
-        p.step()
+                     want_schedule=True, checked=True)
+        p.run_measure()
         st = p.check()
+        p.run_replay()
         assert st["n_overlap_gaps"] == ref["status"]["n_overlap_gaps"]
         assert_tables_equal(p.table.to_numpy(), ref["table"], "toy")
         (hr, hd, hg), (lr, ld) = p.resolved()
@@ -150,9 +151,8 @@ def _replay_parity(fk, orc, cfg, capacity, check_schedule=True):
 
     ref = orc.pipeline(cfg, capacity=capacity)
     p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=capacity, replay=cfg.replay,
-                 want_schedule=check_schedule)
+                 want_schedule=check_schedule, checked=True)
     p.step()
-    p.check()
     assert_tables_equal(p.table.to_numpy(), ref["table"], cfg.name)
     (hr, hd, hg), (lr, ld) = p.resolved()
     assert np.array_equal(hr, ref["hp"][0]) and np.array_equal(hg, ref["hp"][2]) and np.array_equal(lr, ref["lp"][0])
