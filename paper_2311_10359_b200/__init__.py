@@ -193,6 +193,9 @@ class Table:
         self.mean = view(self.c.mean, cap * 2, torch.int64, 8)
         self.n_rows_t = view(self.c.n_rows, 1, torch.int32, 4)
 
+    def zero(self):
+        self.block.zero_()
+
     def n_rows(self) -> int:
         return int(self.n_rows_t.item()) & 0xFFFFFFFF
 

@@ -75,7 +75,7 @@ def merge_tables(local, dense, ops, group=None):
     utask = torch.empty(dense.capacity, dtype=torch.int32, device=dev)
     un = torch.zeros(1, dtype=torch.int32, device=dev)
     l2u = torch.empty(cap, dtype=torch.int32, device=dev)
-    dense.block.zero_()
+    dense.zero()
     ops.dict_union(all_kid, all_task, n_all, P, cap, r, ukid, utask, dense.capacity, un, l2u)
     ops.table_remap(local, l2u, ukid, utask, un, dense)
     ops.table_bias(dense)

@@ -234,3 +234,51 @@ def test_fill_batch(fk, orc):
         for g in range(G):
             o = int(poff[g])
             assert np.array_equal(gp[o:o + npk[g]], picks[o:o + npk[g]]), g
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_sharded_merge_one_gpu(fk, orc, P):
+    """Multi-GPU merge kernels on one GPU: P record shards (+ halos) measured
+    separately, keys 'all-gathered' by stacking, fikit_dict_union +
+    fikit_table_remap + fikit_table_bias, the collectives replaced by torch
+    sum / max over the P dense tables, then fikit_table_means: equals the
+    unsharded oracle table."""
+    import torch
+
+    from paper_2311_10359_b200.dist import shard_range
+
+    cfg = F.zipf_trace(n_runs=3000)  # 768k records, > kHotMax rows
+    tr = cfg.trace
+    N = tr.records.shape[0]
+    ref, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=8192)
+    cap = 8192
+    locs = []
+    for r in range(P):
+        lo, hi = shard_range(N, r, P)
+        sub = F.Trace(tr.records[lo:hi], tr.names, tr.sigs)
+        p = run_measure(fk, sub, capacity=cap, halo=tr.records[hi] if hi < N else None)
+        p.check()
+        locs.append(p)
+    n_all = torch.cat([p.table.n_rows_t for p in locs])
+    all_kid = torch.stack([p.table.kernel_id for p in locs])
+    all_task = torch.stack([p.table.task_id for p in locs])
+    denses = []
+    for r, p in enumerate(locs):
+        ws = fk.Workspace(1, 1, 1, extra=64 * P * cap + (1 << 20))
+        d = fk.Table(cap)
+        ukid = torch.empty(cap, dtype=torch.int64, device="cuda")
+        utask = torch.empty(cap, dtype=torch.int32, device="cuda")
+        un = torch.zeros(1, dtype=torch.int32, device="cuda")
+        l2u = torch.empty(cap, dtype=torch.int32, device="cuda")
+        fk.dict_union(all_kid, all_task, n_all, P, cap, r, ukid, utask, cap, un, l2u, ws)
+        fk.check(ws)
+        fk.table_remap(p.table, l2u, ukid, utask, un, d)
+        fk.table_bias(d)
+        denses.append(d)
+    out = denses[0]
+    out.sums.copy_(torch.stack([d.sums for d in denses]).sum(0))
+    out.hist.copy_(torch.stack([d.hist for d in denses]).sum(0))
+    out.ext.copy_(torch.stack([d.ext for d in denses]).max(0).values)
+    fk.table_bias(out)
+    fk.table_means(out)
+    assert_tables_equal(out.to_numpy(), ref, f"merge P={P}")
