@@ -17,8 +17,8 @@ __global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint6
                          uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*, uint32_t*);
 __global__ void k_hot_select(const fikit_status_t*, const uint32_t*, const Tuple*, uint32_t, Tuple*, uint32_t*);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
-                          uint32_t, uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*,
-                          const Tuple*, const uint32_t*, uint32_t*);
+                          uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, fikit_table_t,
+                          Tuple*, const Tuple*, const uint32_t*, uint32_t*);
 size_t measure_smem_bytes();
 int measure_threads();
 struct FinRow;
@@ -86,6 +86,7 @@ struct Ws {
   uint64_t* sig_hash() const { return reinterpret_cast<uint64_t*>(base + L.sig_hash); }
   IndexEntry* index() const { return reinterpret_cast<IndexEntry*>(base + L.index); }
   Tuple* row_tuple() const { return reinterpret_cast<Tuple*>(base + L.row_tuple); }
+  Tuple* tindex() const { return reinterpret_cast<Tuple*>(base + L.tindex); }
   uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
   uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }
   Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 16); }
@@ -209,6 +210,7 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   cudaMemsetAsync(t.mean, 0, 16ull * cap, s);
   cudaMemsetAsync(t.n_rows, 0, 4, s);
   cudaMemsetAsync(w.index(), 0, sizeof(IndexEntry) * (size_t)w.L.slots, s);
+  cudaMemsetAsync(w.tindex(), 0, sizeof(Tuple) * (size_t)w.L.tslots, s);
   cudaMemsetAsync(w.samp_cnt(), 0, 4ull * cap, s);
   cudaMemsetAsync(w.hot_n(), 0, 16, s);
   if (cudaGetLastError() != cudaSuccess) return FIKIT_E_CUDA;
@@ -234,7 +236,8 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   uint64_t tiles = (n + 255) / 256;
   unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
   k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
-                                                  sigs.count, w.index(), w.L.slots, w.st(), t, w.row_tuple(),
+                                                  sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
+                                                  t, w.row_tuple(),
                                                   w.hot(), w.hot_n(), out_row);
   return launched();
 }
@@ -253,7 +256,8 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   unsigned g = (cap + 255) / 256;
   k_fin_prep<<<g, 256, 0, s>>>(w.st(), t, fin, kptr);
   if (int r = launched()) return r;
-  k_fin_rank<<<g, 256, 0, s>>>(t, kptr, rank);
+  cudaMemsetAsync(rank, 0, 4ull * cap, s);
+  k_fin_rank<<<dim3(g, (cap + 2047) / 2048), 256, 0, s>>>(t, kptr, rank);
   if (int r = launched()) return r;
   k_fin_scatter<<<g, 256, 0, s>>>(t, fin, rank, kptr);
   if (int r = launched()) return r;

@@ -24,8 +24,8 @@ struct alignas(16) Tuple {  // a launch identity as raw record words (the hot di
 };
 
 struct WsLayout {
-  size_t status, misc, name_hash, sig_hash, index, row_tuple, samp_cnt, hot, fin, total;
-  uint32_t slots;
+  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, fin, total;
+  uint32_t slots, tslots;
 };
 
 constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (measure kernel)
@@ -52,6 +52,9 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs) {
   L.slots = index_slots(cap);
   L.index = o;
   o = align256(o + sizeof(IndexEntry) * (size_t)L.slots);
+  L.tslots = index_slots(2 * cap);
+  L.tindex = o;
+  o = align256(o + sizeof(Tuple) * (size_t)L.tslots);
   L.row_tuple = o;
   o = align256(o + sizeof(Tuple) * (size_t)cap);
   L.samp_cnt = o;
@@ -97,7 +100,9 @@ __device__ __forceinline__ uint32_t key_hash(uint64_t kid, uint32_t task) {
   return (uint32_t)(x >> 32);
 }
 
-// cheap 32-bit hash of the raw identity words (hot-dictionary probe)
+// 32-bit hash of the raw identity words (hot dictionary / tuple index probe);
+// murmur3 fmix32 finaliser: grid/block dims are powers of two, so the low bits
+// of a plain multiplicative hash would cluster
 __device__ __forceinline__ uint32_t tuple_hash(const uint32_t* w) {
   uint32_t h = w[0] * 0x9E3779B1u;
   h = (h ^ w[1]) * 0x85EBCA77u;
@@ -106,7 +111,12 @@ __device__ __forceinline__ uint32_t tuple_hash(const uint32_t* w) {
   h = (h ^ w[4]) * 0x165667B1u;
   h = (h ^ w[5]) * 0x9E3779B1u;
   h = (h ^ w[6]) * 0x85EBCA77u;
-  return h ^ (h >> 15);
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
 }
 
 __device__ __forceinline__ int bin_of(uint64_t v) {
@@ -132,16 +142,20 @@ __device__ __forceinline__ void flag_record(fikit_status_t* st, uint64_t idx) {
   atomicMin((unsigned long long*)&st->first_bad_index, (unsigned long long)idx);
 }
 
-// ---- global index (task, kid) -> row --------------------------------------------
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+// ---- global indices -------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-// Find-or-insert; returns the row (possibly >= capacity, then nothing is materialised)
-// or FIKIT_NO_ROW if the index is full.  The inserting thread also records the
-// identity's raw tuple (hot-dictionary candidate) and the table key.
+// Entries are written once (key words, __threadfence, then the state word) and never
+// change after; a reader takes a 16-B / 32-B entry from L2 in one access (__ldcg), so a
+// published state implies the key words of the same sector are visible.
+
+// KID index: find-or-insert (task, kid); returns the row (possibly >= capacity: then
+// nothing is materialised and E_CAPACITY is flagged) or FIKIT_NO_ROW if the index is
+// full.  The inserting thread records the row's key and a representative raw tuple.
 __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32_t slots, uint64_t kid, uint32_t task,
                                                          const uint32_t* tuple_w, fikit_status_t* st,
                                                          uint64_t* tab_kid, uint32_t* tab_task, Tuple* row_tuple,
@@ -149,7 +163,8 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
   uint32_t h = key_hash(kid, task) & (slots - 1);
   for (uint32_t probe = 0; probe < slots; probe++) {
     IndexEntry* e = &idx[h];
-    uint32_t s = ld_acquire_u32(&e->state);
+    uint4 v = __ldcg(reinterpret_cast<const uint4*>(e));
+    uint32_t s = v.w;
     if (s == 0) {
       uint32_t old = atomicCAS(&e->state, 0u, kBusy);
       if (old == 0) {
@@ -173,13 +188,53 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
       }
       s = old;
     }
-    while (s == kBusy) s = ld_acquire_u32(&e->state);
-    volatile IndexEntry* ve = e;
-    if (ve->kid == kid && ve->task == task) return s - 1;
+    if (s == kBusy) {
+      while (s == kBusy) s = ld_relaxed_u32(&e->state);
+    }
+    v = __ldcg(reinterpret_cast<const uint4*>(e));
+    if ((((uint64_t)v.y << 32) | v.x) == kid && v.z == task) return v.w - 1;
     h = (h + 1) & (slots - 1);
   }
   atomicOr(&st->flags, kStatusCapacity);
   return FIKIT_NO_ROW;
+}
+
+// tuple index: raw identity words -> row.  Steady state: one 32-B L2 read per
+// launch of a cold row (no name-hash gather, no 64-bit ID mixing); a miss computes
+// the kernel ID and resolves it through the KID index (two names with identical
+// bytes are two tuples of one row).
+template <class Slow>
+__device__ __forceinline__ uint32_t tuple_find_or_insert(Tuple* tidx, uint32_t tslots, const uint32_t* key,
+                                                         Slow slow) {
+  uint32_t h = tuple_hash(key) & (tslots - 1);
+  for (uint32_t probe = 0; probe < tslots; probe++) {
+    Tuple* e = &tidx[h];
+    uint4 a = __ldcg(reinterpret_cast<const uint4*>(e));
+    uint4 b = __ldcg(reinterpret_cast<const uint4*>(e) + 1);
+    uint32_t s = b.w;
+    if (s == 0) {
+      uint32_t old = atomicCAS(&e->row, 0u, kBusy);
+      if (old == 0) {
+        uint32_t row = slow();
+#pragma unroll
+        for (int j = 0; j < 7; j++) e->w[j] = key[j];
+        __threadfence();
+        atomicExch(&e->row, (row < 0xFFFFFFFDu ? row : 0xFFFFFFFDu) + 1);
+        return row;
+      }
+      s = old;
+    }
+    if (s == kBusy || b.w == 0) {  // being written, or our CAS lost to a writer: re-read
+      while (s == kBusy) s = ld_relaxed_u32(&e->row);
+      a = __ldcg(reinterpret_cast<const uint4*>(e));
+      b = __ldcg(reinterpret_cast<const uint4*>(e) + 1);
+    }
+    if (a.x == key[0] && a.y == key[1] && a.z == key[2] && a.w == key[3] && b.x == key[4] && b.y == key[5] &&
+        b.z == key[6])
+      return b.w - 1;
+    h = (h + 1) & (tslots - 1);
+  }
+  return slow();
 }
 
 // ---- mbarrier / bulk copy (sm_90+ PTX) --------------------------------------------

@@ -50,28 +50,30 @@ __global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* 
   fin[r] = f;
 }
 
-// rank of every key among the K distinct keys = its canonical row (R11)
+// rank of every key among the K distinct keys = its canonical row (R11).
+// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a chunk of 2048 keys staged in
+// shared memory; partial counts are added into rank[] (zeroed by the caller).
 __global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const uint32_t* n_ptr,
                                                   uint32_t* __restrict__ rank) {
   __shared__ unsigned long long sk[2048];
   __shared__ uint32_t st[2048];
   uint32_t K = *n_ptr;
   uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.x * blockDim.x >= K) return;
-  uint64_t mk = r < K ? tab.kernel_id[r] : 0;
-  uint32_t mt = r < K ? tab.task_id[r] : 0;
-  uint32_t cnt = 0;
-  for (uint32_t base = 0; base < K; base += 2048) {
-    uint32_t m = min(2048u, K - base);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      sk[i] = tab.kernel_id[base + i];
-      st[i] = tab.task_id[base + i];
-    }
-    __syncthreads();
-    for (uint32_t i = 0; i < m; i++) cnt += key_less(st[i], sk[i], mt, mk) ? 1u : 0u;
+  uint32_t base = blockIdx.y * 2048;
+  if (blockIdx.x * blockDim.x >= K || base >= K) return;
+  uint32_t m = min(2048u, K - base);
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    sk[i] = tab.kernel_id[base + i];
+    st[i] = tab.task_id[base + i];
   }
-  if (r < K) rank[r] = cnt;
+  __syncthreads();
+  if (r >= K) return;
+  uint64_t mk = tab.kernel_id[r];
+  uint32_t mt = tab.task_id[r];
+  uint32_t cnt = 0;
+#pragma unroll 8
+  for (uint32_t i = 0; i < m; i++) cnt += key_less(st[i], sk[i], mt, mk) ? 1u : 0u;
+  if (cnt) atomicAdd(rank + r, cnt);
 }
 
 __global__ void k_fin_scatter(fikit_table_t tab, const FinRow* __restrict__ fin, const uint32_t* __restrict__ rank,

@@ -129,20 +129,43 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
     uint32_t c = samp_cnt[r];
     if (c) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
   }
+  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0, T = 1;
-    for (int c = NB - 1; c >= 1; c--) {
-      if (acc + h[c] > kHotMax) {
-        T = c + 1;
-        break;
-      }
-      acc += h[c];
+  // T = smallest count c >= 1 whose suffix S(c) = #rows with count >= c fits kHotMax:
+  // a block-wide suffix scan of the 4096-bin count histogram (4 bins per thread)
+  {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t s_Tmin;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    uint32_t loc[4], x = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      loc[j] = h[4 * t + j];
+      x += loc[j];
     }
-    s_T = T;
-    s_n = 0;
+    uint32_t mine = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_down_sync(0xffffffffu, x, d);
+      if (lane + d < 32) x += y;
+    }
+    if (lane == 0) wsum[wid] = x;
+    if (t == 0) s_Tmin = NB;
+    __syncthreads();
+    uint32_t later = 0;
+    for (int w2 = wid + 1; w2 < 32; w2++) later += wsum[w2];
+    uint32_t S = x + later;  // suffix from bin 4t
+    (void)mine;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      uint32_t c = 4 * t + j;
+      if (c >= 1 && S <= kHotMax) atomicMin(&s_Tmin, c);
+      S -= loc[j];
+    }
+    __syncthreads();
+    if (t == 0) s_T = s_Tmin;
+    __syncthreads();
   }
-  __syncthreads();
   uint32_t T = s_T;
   for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
     if (samp_cnt[r] >= T) {
@@ -202,12 +225,11 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
 }
 
 __device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row, int j, uint64_t v) {
+  // fire-and-forget L2 reductions (no read-back, no dependent latency)
   red_add_u32(tab.hist + (size_t)row * 64 + 32 * j + bin_of(v), 1u);
   red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
-  uint64_t* ex = tab.ext + (size_t)row * 4 + 2 * j;
-  ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(ex));  // may be stale: only skips no-op REDs
-  if (v > cur.x) red_max_u64(ex, v);
-  if (~v > cur.y) red_max_u64(ex + 1, ~v);
+  red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
+  red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
 }
 
 // flush packed 16-bit bins of my slots to the table and zero them (consumers only)
@@ -231,9 +253,9 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 __global__ void __launch_bounds__(mk::THREADS, 1)
     k_measure(const fikit_record_t* __restrict__ recs, uint64_t n, const fikit_record_t* __restrict__ halo,
               const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
-              uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st, fikit_table_t tab,
-              Tuple* row_tuple, const Tuple* __restrict__ hot, const uint32_t* __restrict__ hot_n_ptr,
-              uint32_t* __restrict__ out_row) {
+              uint32_t n_sigs, IndexEntry* idx, uint32_t slots, Tuple* tidx, uint32_t tslots, fikit_status_t* st,
+              fikit_table_t tab, Tuple* row_tuple, const Tuple* __restrict__ hot,
+              const uint32_t* __restrict__ hot_n_ptr, uint32_t* __restrict__ out_row) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -352,9 +374,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
             hot_add(S, slot, 0, d);
             if (gap) hot_add(S, slot, 1, g);
           } else {
-            uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
-            row = index_find_or_insert(idx, slots, kid, w[11], key, st, tab.kernel_id, tab.task_id, row_tuple,
-                                       tab.capacity);
+            row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+              uint64_t kid =
+                  kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+              return index_find_or_insert(idx, slots, kid, w[11], key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                          tab.capacity);
+            });
             if (row < tab.capacity) {
               cold_add(tab, row, 0, d);
               if (gap) cold_add(tab, row, 1, g);

@@ -77,6 +77,17 @@ __device__ __forceinline__ bool load_pool(const fikit_table_t& tab, uint32_t K, 
   return __all_sync(0xffffffffu, ok);
 }
 
+// smallest predicted duration among alive eligible requests (UINT64_MAX if none):
+// a gap with R < qmin has no candidate, so BestPrioFit's scan is skipped
+__device__ __forceinline__ uint64_t warp_min_q(const uint64_t* q, const uint8_t* meta, uint32_t m, int lane) {
+  uint64_t mn = ~0ull;
+  for (uint32_t k = lane; k < m; k += 32)
+    if ((meta[k] & (kAlive | kElig)) == (kAlive | kElig)) mn = min(mn, q[k]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+  return mn;
+}
+
 __device__ __forceinline__ uint64_t digest_term(uint32_t k, int32_t fg, uint64_t start) {
   return mix64((uint64_t)k ^ ((uint64_t)(uint32_t)(fg + 1) << 32) ^ mix64(start));
 }
@@ -106,8 +117,10 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint64_t R = R0[g], t = 0, dl = deadline[g];
     uint32_t np = 0, po = picks_off[g];
     if (R >= prm.threshold_ns) {  // Alg. 1 lines 6-8
+      uint64_t qmin = warp_min_q(q, meta, m, lane);
       for (;;) {                  // lines 9-16
         if (prm.feedback && t >= dl) break;  // early stop on the HP launch
+        if (R < qmin) break;                 // nothing can fit
         int k = warp_best_prio_fit(q, meta, m, R, lane);
         if (k < 0) break;
         if (lane == 0) {
@@ -117,7 +130,9 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
         __syncwarp();
         np++;
         t += __ldg(pool_dur + off + k);  // launched (line 14)
-        R -= q[k];                         // revised by the predicted duration (line 15, R17)
+        uint64_t qk = q[k];
+        R -= qk;                           // revised by the predicted duration (line 15, R17)
+        if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
       }
     }
     if (lane == 0) {
@@ -154,6 +169,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
     const uint64_t scale = c.gap_scale_q16;
+    uint64_t qmin = warp_min_q(q, meta, m, lane);
     uint64_t t = 0, hp_delay = 0, fill_work = 0, lp_end = 0, dig = 0;
     uint32_t n_fills = 0;
     for (uint32_t base = 0; base < nh; base += 32) {
@@ -179,6 +195,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
           uint64_t R = p;
           for (;;) {
             if (prm.feedback && t >= r) break;
+            if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
             int k = warp_best_prio_fit(q, meta, m, R, lane);
             if (k < 0) break;
             uint64_t e = __ldg(lp_dur + c.lp_off + k);
@@ -191,8 +208,10 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
               dig += digest_term((uint32_t)k, (int32_t)i, t);
             }
             __syncwarp();
-            R -= q[k];
+            uint64_t qk = q[k];
+            R -= qk;
             t += e;
+            if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
             fill_work += e;
             n_fills++;
             lp_end = max(lp_end, t);
