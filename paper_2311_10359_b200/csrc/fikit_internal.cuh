@@ -149,6 +149,17 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
+// coherent 16-B load at gpu scope; asm volatile so it is never merged with an
+// earlier load of the same entry (the CUDA __ldcg is non-volatile asm and can be CSE'd)
+__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
 // Entries are written once (key words, __threadfence, then the state word) and never
 // change after; a reader takes a 16-B / 32-B entry from L2 in one access (__ldcg), so a
 // published state implies the key words of the same sector are visible.
@@ -163,7 +174,7 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
   uint32_t h = key_hash(kid, task) & (slots - 1);
   for (uint32_t probe = 0; probe < slots; probe++) {
     IndexEntry* e = &idx[h];
-    uint4 v = __ldcg(reinterpret_cast<const uint4*>(e));
+    uint4 v = ld_relaxed_v4(e);
     uint32_t s = v.w;
     if (s == 0) {
       uint32_t old = atomicCAS(&e->state, 0u, kBusy);
@@ -191,7 +202,7 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
     if (s == kBusy) {
       while (s == kBusy) s = ld_relaxed_u32(&e->state);
     }
-    v = __ldcg(reinterpret_cast<const uint4*>(e));
+    v = ld_relaxed_v4(e);
     if ((((uint64_t)v.y << 32) | v.x) == kid && v.z == task) return v.w - 1;
     h = (h + 1) & (slots - 1);
   }
@@ -209,8 +220,8 @@ __device__ __forceinline__ uint32_t tuple_find_or_insert(Tuple* tidx, uint32_t t
   uint32_t h = tuple_hash(key) & (tslots - 1);
   for (uint32_t probe = 0; probe < tslots; probe++) {
     Tuple* e = &tidx[h];
-    uint4 a = __ldcg(reinterpret_cast<const uint4*>(e));
-    uint4 b = __ldcg(reinterpret_cast<const uint4*>(e) + 1);
+    uint4 a = ld_relaxed_v4(e);
+    uint4 b = ld_relaxed_v4(reinterpret_cast<const uint4*>(e) + 1);
     uint32_t s = b.w;
     if (s == 0) {
       uint32_t old = atomicCAS(&e->row, 0u, kBusy);
@@ -226,8 +237,8 @@ __device__ __forceinline__ uint32_t tuple_find_or_insert(Tuple* tidx, uint32_t t
     }
     if (s == kBusy || b.w == 0) {  // being written, or our CAS lost to a writer: re-read
       while (s == kBusy) s = ld_relaxed_u32(&e->row);
-      a = __ldcg(reinterpret_cast<const uint4*>(e));
-      b = __ldcg(reinterpret_cast<const uint4*>(e) + 1);
+      a = ld_relaxed_v4(e);
+      b = ld_relaxed_v4(reinterpret_cast<const uint4*>(e) + 1);
     }
     if (a.x == key[0] && a.y == key[1] && a.z == key[2] && a.w == key[3] && b.x == key[4] && b.y == key[5] &&
         b.z == key[6])
