@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
       loc[j] = h[4 * t + j];
       x += loc[j];
     }
-    uint32_t mine = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       uint32_t y = __shfl_down_sync(0xffffffffu, x, d);
@@ -155,7 +154,6 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
     uint32_t later = 0;
     for (int w2 = wid + 1; w2 < 32; w2++) later += wsum[w2];
     uint32_t S = x + later;  // suffix from bin 4t
-    (void)mine;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       uint32_t c = 4 * t + j;
@@ -179,20 +177,21 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 
 // ---- the fused identify + measure kernel ----------------------------------------------------
 namespace mk {
-constexpr int TILE = 256;                 // launches per stage
-constexpr int NS = 6;                     // ring stages
-constexpr int GROUPS = 2;                 // consumer groups (one tile each in flight)
+constexpr int TILE = 128;                 // launches per stage
+constexpr int NS = 12;                    // ring stages (GROUPS being consumed, the rest loading)
+constexpr int GROUPS = 6;                 // consumer groups (one tile each in flight)
 constexpr int WPG = TILE / 32;            // warps per group
 constexpr int CONSUMERS = GROUPS * WPG * 32;
 constexpr int THREADS = CONSUMERS + 32;   // + producer warp
-constexpr int HOT_IDX = 1024;             // shared hash slots (load <= 0.625)
+constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
 constexpr int EPOCH_ROUNDS = 65535 / (TILE * GROUPS);  // packed 16-bit bins never overflow
 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS], empty[NS];
-  Tuple idx[HOT_IDX];                   // raw identity -> slot + 1 (in .row)
+  uint2 tag[HOT_IDX];                    // (tuple hash, slot + 1); 0 = empty
+  uint4 tup[kHotMax][2];                 // slot -> raw identity words 0..6
   uint32_t hist[kHotMax][kBins];         // 64 bins as packed u16 pairs
   uint32_t sum[kHotMax][4];              // dur lo, dur hi, gap lo, gap hi
   unsigned long long ext[kHotMax][4];    // dur min, dur max, gap min, gap max
@@ -200,6 +199,7 @@ struct Smem {
   uint32_t hot_n;
   unsigned long long overlap;
 };
+static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
 }  // namespace mk
 
 __device__ __forceinline__ void hot_add(mk::Smem& S, int e, int j, uint64_t v) {
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     fence_mbar_init();
   }
-  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.idx[i].row = 0;
+  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
   for (int i = tid; i < kHotMax * kBins; i += mk::THREADS) (&S.hist[0][0])[i] = 0;
   for (int i = tid; i < kHotMax * 4; i += mk::THREADS) {
     (&S.sum[0][0])[i] = 0;
@@ -283,10 +283,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   for (uint32_t e = tid; e < hot_n; e += mk::THREADS) {
     Tuple t = hot[e];
     S.grow[e] = t.row;
-    uint32_t h = tuple_hash(t.w) & (mk::HOT_IDX - 1);
-    while (atomicCAS(&S.idx[h].row, 0u, e + 1) != 0u) h = (h + 1) & (mk::HOT_IDX - 1);
-#pragma unroll
-    for (int j = 0; j < 7; j++) S.idx[h].w[j] = t.w[j];
+    S.tup[e][0] = make_uint4(t.w[0], t.w[1], t.w[2], t.w[3]);
+    S.tup[e][1] = make_uint4(t.w[4], t.w[5], t.w[6], 0u);
+    uint32_t h = tuple_hash(t.w);
+    uint32_t pos = h & (mk::HOT_IDX - 1);
+    while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
+    S.tag[pos].x = h;
   }
   __syncthreads();
 
@@ -354,19 +356,23 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           uint64_t g = ov ? 0 : nstart - end;  // G = next start - end, clamped
           overlap_cnt += ov;
           uint32_t key[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
-          uint32_t h = tuple_hash(key) & (mk::HOT_IDX - 1);
+          const uint32_t hk = tuple_hash(key);
+          uint32_t pos = hk & (mk::HOT_IDX - 1);
           int slot = -1;
           for (;;) {
-            uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-            lds128(&S.idx[h].w[0], a0, a1, a2, a3);
-            lds128(&S.idx[h].w[4], b0, b1, b2, b3);
-            if (b3 == 0) break;
-            if (a0 == key[0] && a1 == key[1] && a2 == key[2] && a3 == key[3] && b0 == key[4] && b1 == key[5] &&
-                b2 == key[6]) {
-              slot = (int)b3 - 1;
-              break;
+            uint2 tg = S.tag[pos];
+            if (tg.y == 0) break;
+            if (tg.x == hk) {
+              uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+              lds128(&S.tup[tg.y - 1][0], a0, a1, a2, a3);
+              lds128(&S.tup[tg.y - 1][1], b0, b1, b2, b3);
+              if (a0 == key[0] && a1 == key[1] && a2 == key[2] && a3 == key[3] && b0 == key[4] && b1 == key[5] &&
+                  b2 == key[6]) {
+                slot = (int)tg.y - 1;
+                break;
+              }
             }
-            h = (h + 1) & (mk::HOT_IDX - 1);
+            pos = (pos + 1) & (mk::HOT_IDX - 1);
           }
           uint32_t row;
           if (slot >= 0) {
