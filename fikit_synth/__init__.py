@@ -528,7 +528,8 @@ def zipf_replay(cfg: Config, seed: int = 44, n_hp_runs: int = 1000, pop: int = 1
     sc["hp_len"] = L
     sc["lp_off"] = (s * m) % (lp.shape[0] - m + 1)
     sc["lp_len"] = m
-    sc["gap_scale_q16"] = 1 << 16
+    # the Z gap mixture averages ~47 us, under the 0.1 ms gate: replay at scales 1, 2, 4, 8 (R24)
+    sc["gap_scale_q16"] = (1 << 16) << (s % 4)
     return Replay(hp, lp, lvl, sc)
 
 

@@ -177,9 +177,9 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 
 // ---- the fused identify + measure kernel ----------------------------------------------------
 namespace mk {
-constexpr int TILE = 128;                 // launches per stage
-constexpr int NS = 12;                    // ring stages (GROUPS being consumed, the rest loading)
-constexpr int GROUPS = 6;                 // consumer groups (one tile each in flight)
+constexpr int TILE = 64;                  // launches per stage
+constexpr int NS = 24;                    // ring stages (GROUPS being consumed, the rest loading)
+constexpr int GROUPS = 16;                // consumer groups (one tile each in flight)
 constexpr int WPG = TILE / 32;            // warps per group
 constexpr int CONSUMERS = GROUPS * WPG * 32;
 constexpr int THREADS = CONSUMERS + 32;   // + producer warp
@@ -292,20 +292,26 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   }
   __syncthreads();
 
-  const uint64_t my_tiles = (ntiles > blockIdx.x) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping
+  const uint32_t n32 = (uint32_t)n;
+  const uint32_t ntiles32 = (uint32_t)ntiles;
+  const uint32_t my_tiles = (ntiles32 > blockIdx.x) ? (ntiles32 - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
   if (warp == mk::CONSUMERS / 32) {
     // ---------------- producer warp: 1-D TMA of each tile (+ the next launch) ----------------
     if (lane == 0) {
-      for (uint64_t it = 0; it < my_tiles; it++) {
-        uint64_t tile = blockIdx.x + it * gridDim.x;
-        int s = (int)(it % mk::NS);
-        if (it >= mk::NS) mbar_wait(&S.empty[s], (uint32_t)((it / mk::NS) - 1) & 1u);
-        uint64_t first = tile * mk::TILE;
-        uint32_t cnt = (uint32_t)umin64(mk::TILE + 1, n - first);  // +1: next launch for the last gap
-        uint32_t bytes = cnt * 48;
-        mbar_arrive_expect_tx(&S.full[s], bytes);
-        bulk_g2s(S.ring[s], recs + first, bytes, &S.full[s]);
+      uint32_t s = 0, k = 0;  // stage, use count of the stage
+      for (uint32_t it = 0; it < my_tiles; it++) {
+        const uint32_t tile = blockIdx.x + it * gridDim.x;
+        if (it >= (uint32_t)mk::NS) mbar_wait(&S.empty[s], (k - 1) & 1u);
+        const uint32_t first = tile * mk::TILE;
+        const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);  // +1: next launch for the last gap
+        mbar_arrive_expect_tx(&S.full[s], cnt * 48);
+        bulk_g2s(S.ring[s], recs + first, cnt * 48, &S.full[s]);
+        if (++s == (uint32_t)mk::NS) {
+          s = 0;
+          k++;
+        }
       }
     }
     return;
@@ -313,33 +319,63 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 
   // ---------------- consumers ----------------
   const int group = warp / mk::WPG, wig = warp % mk::WPG;
-  const uint64_t rounds = (my_tiles + mk::GROUPS - 1) / mk::GROUPS;
+  const uint32_t rounds = (my_tiles + mk::GROUPS - 1) / mk::GROUPS;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t overlap_cnt = 0;
-  for (uint64_t r = 0; r < rounds; r++) {
-    uint64_t it = r * mk::GROUPS + group;
+  // deferred cold launches, compacted into lanes [0, np): key words, d, g, record index
+  uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
+  uint64_t pd = 0, pg = 0;
+  uint32_t np = 0;
+  auto flush_cold = [&]() {
+    if (lane < (int)np) {
+      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
+      const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+        const uint32_t bxy = pk4, bz = pk5 & 0xFFFFu;
+        const uint64_t kid = kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, bxy, bz);
+        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                    tab.capacity);
+      });
+      if (row < tab.capacity) {
+        cold_add(tab, row, 0, pd);
+        if (pk5 >> 16) cold_add(tab, row, 1, pg);
+      }
+      if (out_row) out_row[pgi] = row;
+    }
+    np = 0;
+  };
+  uint32_t s = group, kuse = 0;  // stage of iteration it = r * GROUPS + group, and its use count
+  for (uint32_t r = 0; r < rounds; r++) {
+    const uint32_t it = r * mk::GROUPS + group;
+    bool cold = false;
+    uint32_t key[7];
+    uint64_t d = 0, g = 0;
+    bool gap = false;
+    uint32_t gi = 0;
     if (it < my_tiles) {
-      uint64_t tile = blockIdx.x + it * gridDim.x;
-      int s = (int)(it % mk::NS);
-      mbar_wait(&S.full[s], (uint32_t)(it / mk::NS) & 1u);
-      uint64_t first = tile * mk::TILE;
-      uint32_t cnt = (uint32_t)umin64(mk::TILE, n - first);
-      uint32_t j = wig * 32 + lane;
+      const uint32_t tile = blockIdx.x + it * gridDim.x;
+      mbar_wait(&S.full[s], kuse & 1u);
+      const uint32_t first = tile * mk::TILE;
+      const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
+      const uint32_t j = wig * 32 + lane;
       if (j < cnt) {
         const unsigned char* base = reinterpret_cast<const unsigned char*>(S.ring[s]);
         uint32_t w[12];
         lds128(base + j * 48, w[0], w[1], w[2], w[3]);
         lds128(base + j * 48 + 16, w[4], w[5], w[6], w[7]);
         lds128(base + j * 48 + 32, w[8], w[9], w[10], w[11]);
-        uint64_t gi = first + j;
-        // next launch: in the tile (or the extra record), else the halo
+        gi = first + j;
+        // next launch: in the tile (or the TMA'd extra record), else the halo
         bool has_next = false;
         uint64_t nstart = 0;
         uint32_t nrun = 0, ntask = 0;
-        if (gi + 1 < n) {
-          const uint32_t* nx = reinterpret_cast<const uint32_t*>(base + (j + 1) * 48);
-          nstart = (uint64_t)nx[0] | ((uint64_t)nx[1] << 32);
-          nrun = nx[10];
-          ntask = nx[11];
+        if (gi + 1 < n32) {
+          uint32_t x0, x1, x2, x3;
+          lds128(base + (j + 1) * 48, x0, x1, x2, x3);
+          uint32_t y0, y1, y2, y3;
+          lds128(base + (j + 1) * 48 + 32, y0, y1, y2, y3);
+          nstart = (uint64_t)x0 | ((uint64_t)x1 << 32);
+          nrun = y2;
+          ntask = y3;
           has_next = true;
         } else if (halo != nullptr) {
           nstart = halo->start_ns;
@@ -348,19 +384,20 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           has_next = true;
         }
         if (record_valid(w, n_names, n_sigs)) {
-          uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-          uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-          uint64_t d = end - start;  // K = end - start
-          bool gap = has_next && ntask == w[11] && nrun == w[10];  // R5
-          bool ov = gap && nstart < end;
-          uint64_t g = ov ? 0 : nstart - end;  // G = next start - end, clamped
+          const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+          const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+          d = end - start;                                   // K = end - start
+          gap = has_next && ntask == w[11] && nrun == w[10];  // R5
+          const bool ov = gap && nstart < end;
+          g = ov ? 0 : nstart - end;  // G = next start - end, clamped
           overlap_cnt += ov;
-          uint32_t key[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
+          key[0] = w[4]; key[1] = w[5]; key[2] = w[6]; key[3] = w[7]; key[4] = w[8]; key[5] = w[9] & 0xFFFFu;
+          key[6] = w[11];
           const uint32_t hk = tuple_hash(key);
           uint32_t pos = hk & (mk::HOT_IDX - 1);
           int slot = -1;
           for (;;) {
-            uint2 tg = S.tag[pos];
+            const uint2 tg = S.tag[pos];
             if (tg.y == 0) break;
             if (tg.x == hk) {
               uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
@@ -374,37 +411,69 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
             }
             pos = (pos + 1) & (mk::HOT_IDX - 1);
           }
-          uint32_t row;
           if (slot >= 0) {
-            row = S.grow[slot];
             hot_add(S, slot, 0, d);
             if (gap) hot_add(S, slot, 1, g);
+            if (out_row) out_row[gi] = S.grow[slot];
           } else {
-            row = tuple_find_or_insert(tidx, tslots, key, [&]() {
-              uint64_t kid =
-                  kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
-              return index_find_or_insert(idx, slots, kid, w[11], key, st, tab.kernel_id, tab.task_id, row_tuple,
-                                          tab.capacity);
-            });
-            if (row < tab.capacity) {
-              cold_add(tab, row, 0, d);
-              if (gap) cold_add(tab, row, 1, g);
-            }
+            cold = true;
           }
-          if (out_row) out_row[gi] = row;
         } else {
           flag_record(st, gi);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[s]);
+      s += mk::GROUPS;
+      if (s >= (uint32_t)mk::NS) {
+        s -= mk::NS;
+        kuse++;
+      }
     }
+    // ---- compact this tile's cold launches behind the pending ones; resolve when a batch is full ----
+    const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
+    if (cmask) {
+      const uint32_t nc = __popc(cmask);
+      if (np + nc > 32) flush_cold();
+      // lane np + t takes the t-th cold launch of this tile
+      const int t = lane - (int)np;
+      int src = 0;
+      if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
+        uint32_t m = cmask, q = (uint32_t)t, c;
+        c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
+        c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
+        c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
+        c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
+        c = m & 1u;              if (q >= c) { src += 1; }
+      }
+      const bool take = t >= 0 && t < (int)nc;
+      const uint32_t k5 = key[5] | (gap ? 0x10000u : 0u);
+      uint32_t v;
+      v = __shfl_sync(0xffffffffu, key[0], src); if (take) pk0 = v;
+      v = __shfl_sync(0xffffffffu, key[1], src); if (take) pk1 = v;
+      v = __shfl_sync(0xffffffffu, key[2], src); if (take) pk2 = v;
+      v = __shfl_sync(0xffffffffu, key[3], src); if (take) pk3 = v;
+      v = __shfl_sync(0xffffffffu, key[4], src); if (take) pk4 = v;
+      v = __shfl_sync(0xffffffffu, k5, src);     if (take) pk5 = v;
+      v = __shfl_sync(0xffffffffu, key[6], src); if (take) pk6 = v;
+      v = __shfl_sync(0xffffffffu, gi, src);     if (take) pgi = v;
+      const uint64_t dv = __shfl_sync(0xffffffffu, d, src);
+      const uint64_t gv = __shfl_sync(0xffffffffu, g, src);
+      if (take) {
+        pd = dv;
+        pg = gv;
+      }
+      np += nc;
+      if (np >= 24) flush_cold();
+    }
+    (void)lt_mask;
     if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit bins: flush before overflow
       consumer_sync();
       flush_hist(S, tab, tid);
       consumer_sync();
     }
   }
+  if (np) flush_cold();
   // warp-aggregate the overlap count
   uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);

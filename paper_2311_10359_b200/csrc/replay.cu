@@ -172,54 +172,70 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint64_t qmin = warp_min_q(q, meta, m, lane);
     uint64_t t = 0, hp_delay = 0, fill_work = 0, lp_end = 0, dig = 0;
     uint32_t n_fills = 0;
+    // t = start of the next HP kernel.  Without a fill, kernel i+1 starts at
+    // T_i + d_i + a'_i; only gaps whose gate can open (p >= tau, p >= qmin, and
+    // with feedback a' > 0) need the serial Alg. 1 loop, so each chunk of 32 HP
+    // kernels is advanced by a prefix sum and visits just its open gates.
     for (uint32_t base = 0; base < nh; base += 32) {
-      // 32 HP kernels at a time: lane j holds kernel base+j (d, a', p)
       uint32_t i_l = base + lane;
       uint64_t d_l = 0, a_l = 0, p_l = 0;
-      if (i_l < nh) {
+      bool valid = i_l < nh, last = i_l == nh - 1;
+      if (valid) {
         d_l = __ldg(hp_dur + c.hp_off + i_l);
-        a_l = (__ldg(hp_gap + c.hp_off + i_l) * scale) >> 16;  // R24
+        a_l = last ? 0 : (__ldg(hp_gap + c.hp_off + i_l) * scale) >> 16;  // R24; no gap after the last
         uint32_t r = __ldg(hp_row + c.hp_off + i_l);
         p_l = r < K ? ((__ldg(tab.mean + (size_t)r * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
       }
-      uint32_t cnt = min(32u, nh - base);
-      for (uint32_t j = 0; j < cnt; j++) {
-        uint32_t i = base + j;
-        uint64_t d = __shfl_sync(0xffffffffu, d_l, j);
-        t += d;  // HP kernel i runs [start, end); t = end
-        if (i == nh - 1) break;
-        uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
-        uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
-        uint64_t r = t + a;  // the HP client's next launch arrives (R20)
-        if (p >= prm.threshold_ns) {
-          uint64_t R = p;
-          for (;;) {
-            if (prm.feedback && t >= r) break;
-            if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
-            int k = warp_best_prio_fit(q, meta, m, R, lane);
-            if (k < 0) break;
-            uint64_t e = __ldg(lp_dur + c.lp_off + k);
-            if (lane == 0) {
-              meta[k] &= (uint8_t)~kAlive;
-              if (sched) {
-                fill_gap[so + k] = (int32_t)i;
-                lp_start[so + k] = t;
-              }
-              dig += digest_term((uint32_t)k, (int32_t)i, t);
-            }
-            __syncwarp();
-            uint64_t qk = q[k];
-            R -= qk;
-            t += e;
-            if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
-            fill_work += e;
-            n_fills++;
-            lp_end = max(lp_end, t);
-          }
-        }
-        if (t > r) hp_delay += t - r;  // overhead 2
-        t = max(t, r);                 // next HP kernel starts at max(t, r_{i+1})
+      const uint64_t x_l = d_l + a_l;
+      uint64_t X = x_l;  // inclusive prefix over the chunk
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
+        if (lane >= dd) X += y;
       }
+      const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= qmin && (!prm.feedback || a_l > 0);
+      uint32_t gmask = __ballot_sync(0xffffffffu, gate);
+      const uint64_t T0 = t;
+      uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
+      while (gmask) {
+        const int j = __ffs(gmask) - 1;
+        gmask &= gmask - 1;
+        const uint32_t i = base + j;
+        const uint64_t Xj = __shfl_sync(0xffffffffu, X, j);
+        const uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
+        const uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
+        t = T0 + shift + Xj - a;  // end of HP kernel i
+        const uint64_t r = t + a;   // the HP client's next launch arrives (R20)
+        uint64_t R = p;
+        for (;;) {
+          if (prm.feedback && t >= r) break;
+          if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
+          int k = warp_best_prio_fit(q, meta, m, R, lane);
+          if (k < 0) break;
+          uint64_t e = __ldg(lp_dur + c.lp_off + k);
+          if (lane == 0) {
+            meta[k] &= (uint8_t)~kAlive;
+            if (sched) {
+              fill_gap[so + k] = (int32_t)i;
+              lp_start[so + k] = t;
+            }
+            dig += digest_term((uint32_t)k, (int32_t)i, t);
+          }
+          __syncwarp();
+          uint64_t qk = q[k];
+          R -= qk;
+          t += e;
+          if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
+          fill_work += e;
+          n_fills++;
+          lp_end = max(lp_end, t);
+        }
+        if (t > r) {  // overhead 2: kernel i+1 starts at max(t, r_{i+1})
+          hp_delay += t - r;
+          shift += t - r;
+        }
+      }
+      t = T0 + shift + __shfl_sync(0xffffffffu, X, 31);  // next kernel's start (or the HP end)
     }
     const uint64_t hp_jct = t;
     // tail: remaining requests in Q1..Q9 order, FIFO within a queue (R22)
