@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 namespace mk {
 constexpr int TILE = 64;                  // launches per stage
 constexpr int NS = 24;                    // ring stages (GROUPS being consumed, the rest loading)
-constexpr int GROUPS = 16;                // consumer groups (one tile each in flight)
+constexpr int GROUPS = 15;                // consumer groups (one tile each in flight); 31 warps <= 1024 threads
 constexpr int WPG = TILE / 32;            // warps per group
 constexpr int CONSUMERS = GROUPS * WPG * 32;
 constexpr int THREADS = CONSUMERS + 32;   // + producer warp
@@ -200,6 +200,7 @@ struct Smem {
   unsigned long long overlap;
 };
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
+static_assert(THREADS <= 1024, "a CTA has at most 1024 threads");
 }  // namespace mk
 
 __device__ __forceinline__ void hot_add(mk::Smem& S, int e, int j, uint64_t v) {

@@ -56,7 +56,9 @@ def test_sm100a_sass(libpath):
     sass = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "-sass", libpath], text=True)
     assert "sm_100a" in subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "-lelf", libpath], text=True) or \
         "arch = sm_100a" in sass
-    m = sass[sass.index("k_measure"):]
+    blocks = [b for b in sass.split("Function : ") if b.startswith("_ZN5fikit9k_measure")]
+    assert blocks, "k_measure not found in the SASS"
+    m = blocks[0]
     assert "UBLKCP" in m and "SYNCS" in m
 
 
