@@ -69,7 +69,9 @@ typedef struct {
   uint32_t task_id; /* caller-interned Task Key */
 } fikit_record_t;
 
-/* count strings; string j = bytes[offsets[j] .. offsets[j+1]) (device arrays). */
+/* count strings; string j = bytes[offsets[j] .. offsets[j+1]) (device arrays).
+ * The kernels read `bytes` in whole aligned 16-byte blocks (any block holding a
+ * string byte), which device allocations (>= 256-byte granularity) always allow. */
 typedef struct {
   const uint8_t* bytes;
   const uint32_t* offsets; /* count + 1 entries, non-decreasing */

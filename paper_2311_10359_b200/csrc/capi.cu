@@ -116,11 +116,11 @@ inline bool table_ok(const fikit_table_t* t) {
 
 int hash_strtabs(const Ws& w, const fikit_strtab_t& names, const fikit_strtab_t& sigs, cudaStream_t s) {
   if (names.count) {
-    k_strtab_hash<<<(names.count + 255) / 256, 256, 0, s>>>(names, w.name_hash(), 1, w.st());
+    k_strtab_hash<<<(names.count + 127) / 128, 128, 0, s>>>(names, w.name_hash(), 1, w.st());
     if (int r = launched()) return r;
   }
   if (sigs.count) {
-    k_strtab_hash<<<(sigs.count + 255) / 256, 256, 0, s>>>(sigs, w.sig_hash(), 0, w.st());
+    k_strtab_hash<<<(sigs.count + 127) / 128, 128, 0, s>>>(sigs, w.sig_hash(), 0, w.st());
     if (int r = launched()) return r;
   }
   return FIKIT_OK;

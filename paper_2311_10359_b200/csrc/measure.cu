@@ -30,7 +30,8 @@ __global__ void k_reset_status(fikit_status_t* st) {
   }
 }
 
-__global__ void k_strtab_hash(fikit_strtab_t t, uint64_t* __restrict__ out, int is_name, fikit_status_t* st) {
+__global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t t, uint64_t* __restrict__ out, int is_name,
+                                                     fikit_status_t* st) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= t.count) return;
   uint32_t a = t.offsets[j], b = t.offsets[j + 1];
@@ -40,10 +41,22 @@ __global__ void k_strtab_hash(fikit_strtab_t t, uint64_t* __restrict__ out, int 
     return;
   }
   if (is_name && a == b) atomicOr(&st->flags, kStatusName);
-  uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a 64 (R2)
-  for (uint32_t i = a; i < b; i++) {
-    h ^= (uint64_t)__ldg(t.bytes + i);
-    h *= 0x100000001b3ULL;
+  uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a 64 (R2), bytes in order
+  // aligned 16-byte loads (independent, issued ahead), bytes consumed from registers
+  const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(t.bytes) & ~uintptr_t(15));
+  const uint32_t skew = (uint32_t)(reinterpret_cast<uintptr_t>(t.bytes) & 15);
+  const uint32_t lo = a + skew, hi = b + skew;  // byte range relative to base
+  for (uint32_t c = lo >> 4; c < (hi + 15) >> 4; c++) {
+    const uint4 v = __ldg(base + c);
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const uint32_t pos = c * 16 + q;
+      if (pos >= lo && pos < hi) {
+        h ^= (uint64_t)((wv[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+        h *= 0x100000001b3ULL;
+      }
+    }
   }
   out[j] = h;
 }
@@ -358,25 +371,24 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       const uint32_t first = tile * mk::TILE;
       const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
       const uint32_t j = wig * 32 + lane;
+      uint32_t w[12];
+      bool has_next = false;
+      uint64_t nstart = 0;
+      uint32_t nrun = 0, ntask = 0;
       if (j < cnt) {
-        const unsigned char* base = reinterpret_cast<const unsigned char*>(S.ring[s]);
-        uint32_t w[12];
-        lds128(base + j * 48, w[0], w[1], w[2], w[3]);
-        lds128(base + j * 48 + 16, w[4], w[5], w[6], w[7]);
-        lds128(base + j * 48 + 32, w[8], w[9], w[10], w[11]);
+        // record j and the start/run/task of the next launch (in the tile, the TMA'd
+        // extra record, else the halo) -> registers; then the stage is released
+        const uint4* rp = S.ring[s] + j * 3;
+        const uint4 r0 = rp[0], r1 = rp[1], r2 = rp[2];
+        w[0] = r0.x; w[1] = r0.y; w[2] = r0.z; w[3] = r0.w;
+        w[4] = r1.x; w[5] = r1.y; w[6] = r1.z; w[7] = r1.w;
+        w[8] = r2.x; w[9] = r2.y; w[10] = r2.z; w[11] = r2.w;
         gi = first + j;
-        // next launch: in the tile (or the TMA'd extra record), else the halo
-        bool has_next = false;
-        uint64_t nstart = 0;
-        uint32_t nrun = 0, ntask = 0;
         if (gi + 1 < n32) {
-          uint32_t x0, x1, x2, x3;
-          lds128(base + (j + 1) * 48, x0, x1, x2, x3);
-          uint32_t y0, y1, y2, y3;
-          lds128(base + (j + 1) * 48 + 32, y0, y1, y2, y3);
-          nstart = (uint64_t)x0 | ((uint64_t)x1 << 32);
-          nrun = y2;
-          ntask = y3;
+          const uint4 x = rp[3], y = rp[5];
+          nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
+          nrun = y.z;
+          ntask = y.w;
           has_next = true;
         } else if (halo != nullptr) {
           nstart = halo->start_ns;
@@ -384,6 +396,15 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           ntask = halo->task_id;
           has_next = true;
         }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);  // release early: keep the ring loading
+      s += mk::GROUPS;
+      if (s >= (uint32_t)mk::NS) {
+        s -= mk::NS;
+        kuse++;
+      }
+      if (j < cnt) {
         if (record_valid(w, n_names, n_sigs)) {
           const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
           const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
@@ -401,11 +422,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
             const uint2 tg = S.tag[pos];
             if (tg.y == 0) break;
             if (tg.x == hk) {
-              uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-              lds128(&S.tup[tg.y - 1][0], a0, a1, a2, a3);
-              lds128(&S.tup[tg.y - 1][1], b0, b1, b2, b3);
-              if (a0 == key[0] && a1 == key[1] && a2 == key[2] && a3 == key[3] && b0 == key[4] && b1 == key[5] &&
-                  b2 == key[6]) {
+              const uint4 ta = S.tup[tg.y - 1][0], tb = S.tup[tg.y - 1][1];
+              if (ta.x == key[0] && ta.y == key[1] && ta.z == key[2] && ta.w == key[3] && tb.x == key[4] &&
+                  tb.y == key[5] && tb.z == key[6]) {
                 slot = (int)tg.y - 1;
                 break;
               }
@@ -422,13 +441,6 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         } else {
           flag_record(st, gi);
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
-      s += mk::GROUPS;
-      if (s >= (uint32_t)mk::NS) {
-        s -= mk::NS;
-        kuse++;
       }
     }
     // ---- compact this tile's cold launches behind the pending ones; resolve when a batch is full ----
