@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 namespace mk {
 constexpr int TILE = 64;                  // launches per stage
 constexpr int NS = 24;                    // ring stages (GROUPS being consumed, the rest loading)
-constexpr int GROUPS = 15;                // consumer groups (one tile each in flight); 31 warps <= 1024 threads
+constexpr int GROUPS = 12;                // consumer groups (one tile each in flight)
 constexpr int WPG = TILE / 32;            // warps per group
 constexpr int CONSUMERS = GROUPS * WPG * 32;
 constexpr int THREADS = CONSUMERS + 32;   // + producer warp
@@ -214,6 +214,9 @@ struct Smem {
 };
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
 static_assert(THREADS <= 1024, "a CTA has at most 1024 threads");
+// Each stage must belong to one consumer group: with NS % GROUPS != 0 a fast group could
+// wait on a stage two uses ahead, and the mbarrier phase parity would alias (stale data).
+static_assert(NS % GROUPS == 0, "stage ownership: NS must be a multiple of GROUPS");
 }  // namespace mk
 
 __device__ __forceinline__ void hot_add(mk::Smem& S, int e, int j, uint64_t v) {

@@ -1,17 +1,22 @@
 #!/bin/bash
-# one gpurun call: GPU parity tests, the bench, an ncu launch list and one full capture of k_measure
+# one gpurun call: GPU parity tests, the bench, an ncu launch list and full captures of selected kernels
+#   NCU=1 CAPTURE="k_measure k_simulate" BENCH_ARGS="..." bash scripts/gpu_check.sh
 set -x
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-cat gpurun_out/pytest_gpu.log
+if [ -z "$NOTEST" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+  cat gpurun_out/pytest_gpu.log
+fi
 timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
      python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>gpurun_out/ncu1.err
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_measure -s 1 -c 1 \
-     -o gpurun_out/prof_measure -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>gpurun_out/ncu2.err
+  for k in ${CAPTURE:-k_measure}; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+       -o gpurun_out/prof_$k -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>gpurun_out/ncu_$k.err
+  done
   ls -la gpurun_out
 fi
