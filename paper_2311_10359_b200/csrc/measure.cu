@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   for (uint32_t r = 0; r < rounds; r++) {
     const uint32_t it = r * mk::GROUPS + group;
     bool cold = false;
-    uint32_t key[7];
+    uint32_t key[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
     uint64_t d = 0, g = 0;
     bool gap = false;
     uint32_t gi = 0;
@@ -400,25 +400,34 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           has_next = true;
         }
       }
+      bool valid = false;
+      if (j < cnt) {
+        valid = record_valid(w, n_names, n_sigs);
+        const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+        const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+        d = end - start;                                   // K = end - start
+        gap = has_next && ntask == w[11] && nrun == w[10];  // R5
+        const bool ov = gap && nstart < end;
+        g = ov ? 0 : nstart - end;  // G = next start - end, clamped
+        overlap_cnt += (valid && ov) ? 1u : 0u;
+        key[0] = w[4]; key[1] = w[5]; key[2] = w[6]; key[3] = w[7]; key[4] = w[8]; key[5] = w[9] & 0xFFFFu;
+        key[6] = w[11];
+      }
+      const uint32_t hk = tuple_hash(key);
+      // every loaded word has been consumed (the values below are materialised before
+      // this point, so their shared loads have completed); order the reads (generic
+      // proxy) before the TMA overwrite (async proxy), then release the stage early
+      asm volatile("" ::"r"(hk), "l"(d), "l"(g), "r"((uint32_t)gap), "r"((uint32_t)valid), "r"(gi));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);  // release early: keep the ring loading
+      if (lane == 0) mbar_arrive(&S.empty[s]);
       s += mk::GROUPS;
       if (s >= (uint32_t)mk::NS) {
         s -= mk::NS;
         kuse++;
       }
       if (j < cnt) {
-        if (record_valid(w, n_names, n_sigs)) {
-          const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-          const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-          d = end - start;                                   // K = end - start
-          gap = has_next && ntask == w[11] && nrun == w[10];  // R5
-          const bool ov = gap && nstart < end;
-          g = ov ? 0 : nstart - end;  // G = next start - end, clamped
-          overlap_cnt += ov;
-          key[0] = w[4]; key[1] = w[5]; key[2] = w[6]; key[3] = w[7]; key[4] = w[8]; key[5] = w[9] & 0xFFFFu;
-          key[6] = w[11];
-          const uint32_t hk = tuple_hash(key);
+        if (valid) {
           uint32_t pos = hk & (mk::HOT_IDX - 1);
           int slot = -1;
           for (;;) {
