@@ -198,17 +198,19 @@ constexpr int CONSUMERS = GROUPS * WPG * 32;
 constexpr int THREADS = CONSUMERS + 32;   // + producer warp
 constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
-constexpr int EPOCH_ROUNDS = 65535 / (TILE * GROUPS);  // packed 16-bit bins never overflow
+// per epoch a slot sees <= EPOCH_ROUNDS * TILE * GROUPS launches: packed 16-bit bins and the
+// 16-bit-split sum accumulators cannot overflow before the epoch flush
+constexpr int EPOCH_ROUNDS = 65535 / (TILE * GROUPS);
 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS], empty[NS];
-  uint2 tag[HOT_IDX];                    // (tuple hash, slot + 1); 0 = empty
-  uint4 tup[kHotMax][2];                 // slot -> raw identity words 0..6
-  uint32_t hist[kHotMax][kBins];         // 64 bins as packed u16 pairs
-  uint32_t sum[kHotMax][4];              // dur lo, dur hi, gap lo, gap hi
-  unsigned long long ext[kHotMax][4];    // dur min, dur max, gap min, gap max
-  uint32_t grow[kHotMax];                // slot -> global row
+  uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
+  uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6
+  uint32_t hist[kHotMax][kBins];  // 64 bins (32 duration, 32 gap) as packed u16 pairs
+  uint32_t acc[kHotMax][4];       // sum of (v & 0xFFFF), sum of (v >> 16): duration, gap (v < 2^32)
+  uint32_t mm[kHotMax][4];        // min, max (u32): duration, gap (values >= 2^32 go to the table)
+  uint32_t grow[kHotMax];         // slot -> global row
   uint32_t hot_n;
   unsigned long long overlap;
 };
@@ -219,18 +221,16 @@ static_assert(THREADS <= 1024, "a CTA has at most 1024 threads");
 static_assert(NS % GROUPS == 0, "stage ownership: NS must be a multiple of GROUPS");
 }  // namespace mk
 
-__device__ __forceinline__ void hot_add(mk::Smem& S, int e, int j, uint64_t v) {
-  int b = bin_of(v) + 32 * j;
-  atomicAdd(&S.hist[e][b >> 1], 1u << (16 * (b & 1)));
-  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-  uint32_t old = atomicAdd(&S.sum[e][2 * j], lo);
-  hi += (old + lo < old) ? 1u : 0u;
-  if (hi) atomicAdd(&S.sum[e][2 * j + 1], hi);
-  unsigned long long mn = S.ext[e][2 * j], mx = S.ext[e][2 * j + 1];
-  if (v < mn) smem_min64(&S.ext[e][2 * j], v);
-  if (v > mx) smem_max64(&S.ext[e][2 * j + 1], v);
+// fire-and-forget reductions (no return value, no dependent latency)
+__device__ __forceinline__ void red_shared_add(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
-
+__device__ __forceinline__ void red_shared_min(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_shared_max(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -241,6 +241,25 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// one duration (j = 0) or gap (j = 1) value of a hot row: 5 shared reductions, no branches
+// on the common path (values < 2^32); larger values go straight to the table
+__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t acc_e, uint32_t mm_e, const fikit_table_t& tab,
+                                        uint32_t row, int j, uint64_t v) {
+  const int b = bin_of(v) + 32 * j;
+  red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
+  if ((v >> 32) == 0) {
+    const uint32_t v32 = (uint32_t)v;
+    red_shared_add(acc_e + 8u * j, v32 & 0xFFFFu);
+    red_shared_add(acc_e + 8u * j + 4u, v32 >> 16);
+    red_shared_min(mm_e + 8u * j, v32);
+    red_shared_max(mm_e + 8u * j + 4u, v32);
+  } else {  // rare: a value >= 2^32 ns (4.3 s)
+    red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
+    red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
+    red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
+  }
+}
+
 __device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row, int j, uint64_t v) {
   // fire-and-forget L2 reductions (no read-back, no dependent latency)
   red_add_u32(tab.hist + (size_t)row * 64 + 32 * j + bin_of(v), 1u);
@@ -249,18 +268,26 @@ __device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row,
   red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
 }
 
-// flush packed 16-bit bins of my slots to the table and zero them (consumers only)
-__device__ __forceinline__ void flush_hist(mk::Smem& S, const fikit_table_t& tab, int ctid) {
+// epoch flush of my slots (consumers only): packed 16-bit bins and split sums -> table, zeroed
+__device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& tab, int ctid) {
   for (uint32_t e = ctid; e < S.hot_n; e += mk::CONSUMERS) {
-    uint32_t* gh = tab.hist + (size_t)S.grow[e] * 64;
+    const uint32_t row = S.grow[e];
+    uint32_t* gh = tab.hist + (size_t)row * 64;
 #pragma unroll 4
     for (int w = 0; w < kBins; w++) {
-      uint32_t x = S.hist[e][w];
+      const uint32_t x = S.hist[e][w];
       if (x) {
         if (x & 0xFFFFu) red_add_u32(gh + 2 * w, x & 0xFFFFu);
         if (x >> 16) red_add_u32(gh + 2 * w + 1, x >> 16);
         S.hist[e][w] = 0;
       }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const uint64_t sum = (uint64_t)S.acc[e][2 * j] + ((uint64_t)S.acc[e][2 * j + 1] << 16);
+      if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
+      S.acc[e][2 * j] = 0;
+      S.acc[e][2 * j + 1] = 0;
     }
   }
 }
@@ -275,6 +302,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
               const uint32_t* __restrict__ hot_n_ptr, uint32_t* __restrict__ out_row) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
+  const uint32_t sbase = smem_u32(smem_raw);
+  const uint32_t s_hist = sbase + (uint32_t)offsetof(mk::Smem, hist);
+  const uint32_t s_acc = sbase + (uint32_t)offsetof(mk::Smem, acc);
+  const uint32_t s_mm = sbase + (uint32_t)offsetof(mk::Smem, mm);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
@@ -283,17 +314,17 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   if (tid == 0) {
     S.hot_n = min(*hot_n_ptr, kHotMax);
     S.overlap = 0;
-    for (int s = 0; s < mk::NS; s++) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], mk::WPG);
+    for (int i = 0; i < mk::NS; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], mk::WPG);
     }
     fence_mbar_init();
   }
   for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
   for (int i = tid; i < kHotMax * kBins; i += mk::THREADS) (&S.hist[0][0])[i] = 0;
   for (int i = tid; i < kHotMax * 4; i += mk::THREADS) {
-    (&S.sum[0][0])[i] = 0;
-    (&S.ext[0][0])[i] = (i & 1) ? 0ull : ~0ull;
+    (&S.acc[0][0])[i] = 0;
+    (&S.mm[0][0])[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
   }
   __syncthreads();
   const uint32_t hot_n = S.hot_n;
@@ -337,7 +368,6 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // ---------------- consumers ----------------
   const int group = warp / mk::WPG, wig = warp % mk::WPG;
   const uint32_t rounds = (my_tiles + mk::GROUPS - 1) / mk::GROUPS;
-  const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t overlap_cnt = 0;
   // deferred cold launches, compacted into lanes [0, np): key words, d, g, record index
   uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
@@ -347,8 +377,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (lane < (int)np) {
       const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
       const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
-        const uint32_t bxy = pk4, bz = pk5 & 0xFFFFu;
-        const uint64_t kid = kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, bxy, bz);
+        const uint64_t kid =
+            kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
         return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
                                     tab.capacity);
       });
@@ -374,32 +404,35 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       const uint32_t first = tile * mk::TILE;
       const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
       const uint32_t j = wig * 32 + lane;
-      uint32_t w[12];
-      bool has_next = false;
-      uint64_t nstart = 0;
-      uint32_t nrun = 0, ntask = 0;
+      // record j (3 x 16-B shared loads); the next launch's start/run/task come from lane + 1
+      // by shuffle, lane 31 reads record j + 1 (the TMA'd extra record for the tile's last)
+      const uint4* rp = S.ring[s] + j * 3;
+      uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
       if (j < cnt) {
-        // record j and the start/run/task of the next launch (in the tile, the TMA'd
-        // extra record, else the halo) -> registers; then the stage is released
-        const uint4* rp = S.ring[s] + j * 3;
-        const uint4 r0 = rp[0], r1 = rp[1], r2 = rp[2];
-        w[0] = r0.x; w[1] = r0.y; w[2] = r0.z; w[3] = r0.w;
-        w[4] = r1.x; w[5] = r1.y; w[6] = r1.z; w[7] = r1.w;
-        w[8] = r2.x; w[9] = r2.y; w[10] = r2.z; w[11] = r2.w;
-        gi = first + j;
-        if (gi + 1 < n32) {
+        r0 = rp[0];
+        r1 = rp[1];
+        r2 = rp[2];
+      }
+      uint64_t nstart = __shfl_down_sync(0xffffffffu, (uint64_t)r0.x | ((uint64_t)r0.y << 32), 1);
+      uint32_t nrun = __shfl_down_sync(0xffffffffu, r2.z, 1);
+      uint32_t ntask = __shfl_down_sync(0xffffffffu, r2.w, 1);
+      gi = first + j;
+      bool has_next = gi + 1 < n32;
+      if (lane == 31 && j < cnt) {
+        if (has_next) {
           const uint4 x = rp[3], y = rp[5];
           nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
           nrun = y.z;
           ntask = y.w;
-          has_next = true;
-        } else if (halo != nullptr) {
-          nstart = halo->start_ns;
-          nrun = halo->run_id;
-          ntask = halo->task_id;
-          has_next = true;
         }
       }
+      if (!has_next && halo != nullptr && j < cnt) {
+        nstart = halo->start_ns;
+        nrun = halo->run_id;
+        ntask = halo->task_id;
+        has_next = true;
+      }
+      const uint32_t w[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
       bool valid = false;
       if (j < cnt) {
         valid = record_valid(w, n_names, n_sigs);
@@ -444,9 +477,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
             pos = (pos + 1) & (mk::HOT_IDX - 1);
           }
           if (slot >= 0) {
-            hot_add(S, slot, 0, d);
-            if (gap) hot_add(S, slot, 1, g);
-            if (out_row) out_row[gi] = S.grow[slot];
+            const uint32_t row = S.grow[slot];
+            const uint32_t hist_e = s_hist + (uint32_t)slot * (kBins * 4);
+            const uint32_t acc_e = s_acc + (uint32_t)slot * 16u, mm_e = s_mm + (uint32_t)slot * 16u;
+            hot_add(hist_e, acc_e, mm_e, tab, row, 0, d);
+            if (gap) hot_add(hist_e, acc_e, mm_e, tab, row, 1, g);
+            if (out_row) out_row[gi] = row;
           } else {
             cold = true;
           }
@@ -491,10 +527,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       np += nc;
       if (np >= 24) flush_cold();
     }
-    (void)lt_mask;
-    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit bins: flush before overflow
+    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit accumulators: flush before overflow
       consumer_sync();
-      flush_hist(S, tab, tid);
+      flush_epoch(S, tab, tid);
       consumer_sync();
     }
   }
@@ -504,17 +539,15 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);
   consumer_sync();
   // ---- final reduction of the shared rows into the table ----
-  flush_hist(S, tab, tid);
+  flush_epoch(S, tab, tid);
   for (uint32_t e = tid; e < hot_n; e += mk::CONSUMERS) {
-    uint32_t row = S.grow[e];
+    const uint32_t row = S.grow[e];
 #pragma unroll
     for (int j = 0; j < 2; j++) {
-      uint64_t sum = (uint64_t)S.sum[e][2 * j] | ((uint64_t)S.sum[e][2 * j + 1] << 32);
-      unsigned long long mn = S.ext[e][2 * j], mx = S.ext[e][2 * j + 1];
-      if (mn != ~0ull || mx != 0ull) {  // touched
-        if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
-        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, mx);
-        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~mn);
+      const uint32_t mn = S.mm[e][2 * j], mx = S.mm[e][2 * j + 1];
+      if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
+        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
+        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);
       }
     }
   }
