@@ -206,10 +206,11 @@ struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS], empty[NS];
   uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
-  uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6
-  uint32_t hist[kHotMax][kBins];  // 64 bins (32 duration, 32 gap) as packed u16 pairs
-  uint32_t acc[kHotMax][4];       // sum of (v & 0xFFFF), sum of (v >> 16): duration, gap (v < 2^32)
-  uint32_t mm[kHotMax][4];        // min, max (u32): duration, gap (values >= 2^32 go to the table)
+  uint32_t tupw[7][kHotMax];      // slot -> raw identity words 0..6 (SoA: conflict-free verify)
+  // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
+  uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
+  uint32_t st[kHotMax][9];        // 0-3: sum of (v & 0xFFFF), sum of (v >> 16) for duration, gap (v < 2^32)
+                                  // 4-7: min, max (u32) for duration, gap; 8: pad
   uint32_t grow[kHotMax];         // slot -> global row
   uint32_t hot_n;
   unsigned long long overlap;
@@ -243,16 +244,16 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
 
 // one duration (j = 0) or gap (j = 1) value of a hot row: 5 shared reductions, no branches
 // on the common path (values < 2^32); larger values go straight to the table
-__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t acc_e, uint32_t mm_e, const fikit_table_t& tab,
-                                        uint32_t row, int j, uint64_t v) {
+__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, const fikit_table_t& tab, uint32_t row,
+                                        int j, uint64_t v) {
   const int b = bin_of(v) + 32 * j;
   red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
-    red_shared_add(acc_e + 8u * j, v32 & 0xFFFFu);
-    red_shared_add(acc_e + 8u * j + 4u, v32 >> 16);
-    red_shared_min(mm_e + 8u * j, v32);
-    red_shared_max(mm_e + 8u * j + 4u, v32);
+    red_shared_add(st_e + 8u * j, v32 & 0xFFFFu);
+    red_shared_add(st_e + 8u * j + 4u, v32 >> 16);
+    red_shared_min(st_e + 16u + 8u * j, v32);
+    red_shared_max(st_e + 16u + 8u * j + 4u, v32);
   } else {  // rare: a value >= 2^32 ns (4.3 s)
     red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
@@ -284,10 +285,10 @@ __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& ta
     }
 #pragma unroll
     for (int j = 0; j < 2; j++) {
-      const uint64_t sum = (uint64_t)S.acc[e][2 * j] + ((uint64_t)S.acc[e][2 * j + 1] << 16);
+      const uint64_t sum = (uint64_t)S.st[e][2 * j] + ((uint64_t)S.st[e][2 * j + 1] << 16);
       if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
-      S.acc[e][2 * j] = 0;
-      S.acc[e][2 * j + 1] = 0;
+      S.st[e][2 * j] = 0;
+      S.st[e][2 * j + 1] = 0;
     }
   }
 }
@@ -304,8 +305,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
   const uint32_t s_hist = sbase + (uint32_t)offsetof(mk::Smem, hist);
-  const uint32_t s_acc = sbase + (uint32_t)offsetof(mk::Smem, acc);
-  const uint32_t s_mm = sbase + (uint32_t)offsetof(mk::Smem, mm);
+  const uint32_t s_st = sbase + (uint32_t)offsetof(mk::Smem, st);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
@@ -321,18 +321,18 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     fence_mbar_init();
   }
   for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
-  for (int i = tid; i < kHotMax * kBins; i += mk::THREADS) (&S.hist[0][0])[i] = 0;
-  for (int i = tid; i < kHotMax * 4; i += mk::THREADS) {
-    (&S.acc[0][0])[i] = 0;
-    (&S.mm[0][0])[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
+  for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
+  for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
+    const int w = i % 9;  // min words (4, 6) start at ~0
+    (&S.st[0][0])[i] = (w == 4 || w == 6) ? 0xFFFFFFFFu : 0u;
   }
   __syncthreads();
   const uint32_t hot_n = S.hot_n;
   for (uint32_t e = tid; e < hot_n; e += mk::THREADS) {
     Tuple t = hot[e];
     S.grow[e] = t.row;
-    S.tup[e][0] = make_uint4(t.w[0], t.w[1], t.w[2], t.w[3]);
-    S.tup[e][1] = make_uint4(t.w[4], t.w[5], t.w[6], 0u);
+#pragma unroll
+    for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
     uint32_t h = tuple_hash(t.w);
     uint32_t pos = h & (mk::HOT_IDX - 1);
     while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
@@ -467,9 +467,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
             const uint2 tg = S.tag[pos];
             if (tg.y == 0) break;
             if (tg.x == hk) {
-              const uint4 ta = S.tup[tg.y - 1][0], tb = S.tup[tg.y - 1][1];
-              if (ta.x == key[0] && ta.y == key[1] && ta.z == key[2] && ta.w == key[3] && tb.x == key[4] &&
-                  tb.y == key[5] && tb.z == key[6]) {
+              const uint32_t e = tg.y - 1;
+              if (S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
+                  S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] &&
+                  S.tupw[6][e] == key[6]) {
                 slot = (int)tg.y - 1;
                 break;
               }
@@ -478,10 +479,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           }
           if (slot >= 0) {
             const uint32_t row = S.grow[slot];
-            const uint32_t hist_e = s_hist + (uint32_t)slot * (kBins * 4);
-            const uint32_t acc_e = s_acc + (uint32_t)slot * 16u, mm_e = s_mm + (uint32_t)slot * 16u;
-            hot_add(hist_e, acc_e, mm_e, tab, row, 0, d);
-            if (gap) hot_add(hist_e, acc_e, mm_e, tab, row, 1, g);
+            const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
+            const uint32_t st_e = s_st + (uint32_t)slot * 36u;
+            hot_add(hist_e, st_e, tab, row, 0, d);
+            if (gap) hot_add(hist_e, st_e, tab, row, 1, g);
             if (out_row) out_row[gi] = row;
           } else {
             cold = true;
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     const uint32_t row = S.grow[e];
 #pragma unroll
     for (int j = 0; j < 2; j++) {
-      const uint32_t mn = S.mm[e][2 * j], mx = S.mm[e][2 * j + 1];
+      const uint32_t mn = S.st[e][4 + 2 * j], mx = S.st[e][5 + 2 * j];
       if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
         red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
         red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);

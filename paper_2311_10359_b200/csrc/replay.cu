@@ -88,6 +88,111 @@ __device__ __forceinline__ uint64_t warp_min_q(const uint64_t* q, const uint8_t*
   return mn;
 }
 
+// ---- sorted pool (fast path) --------------------------------------------------------------
+// When every eligible q < 2^50 and m <= 1024, the pool is sorted once per scenario by the
+// composite key  level << 60 | (2^50 - 1 - q) << 10 | index  (ineligible: ~0).  Sorted
+// order is exactly BestPrioFit's preference order (level asc, q desc, index asc), and since
+// the remaining idle time R only shrinks, BestPrioFit(R) = the first alive position whose
+// q <= R: a ballot per 32 positions instead of a full argmin.  Lane c holds the alive bits
+// of sorted positions [32c, 32c + 32).
+constexpr uint64_t kQ50 = (1ull << 50) - 1;
+
+__device__ __forceinline__ uint64_t key_q(uint64_t key) { return kQ50 - ((key >> 10) & kQ50); }
+
+__device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
+  for (uint32_t k = 2; k <= P; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < P / 2; t += 32) {
+        const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const uint32_t l = i + j;
+        const uint64_t a = K[i], b = K[l];
+        const bool asc = (i & k) == 0;
+        if ((a > b) == asc) {
+          K[i] = b;
+          K[l] = a;
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// Build the sorted pool in place of q (q[k] by index -> K[p] by sorted position).
+// Returns false (pool left by index) if the fast path does not apply.
+__device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* meta, uint32_t m, int lane,
+                                                 uint32_t& A, uint32_t& nch) {
+  bool ok = true;
+  for (uint32_t k = lane; k < m; k += 32)
+    if ((meta[k] & kElig) && q[k] > kQ50) ok = false;
+  if (!__all_sync(0xffffffffu, ok) || m > 1024u) return false;
+  uint32_t P = 32;
+  while (P < m) P <<= 1;
+  for (uint32_t k = lane; k < P; k += 32) {
+    uint64_t key = ~0ull;
+    if (k < m && (meta[k] & kElig)) key = ((uint64_t)(meta[k] & 0xF) << 60) | ((kQ50 - q[k]) << 10) | k;
+    q[k] = key;
+  }
+  __syncwarp();
+  warp_bitonic_sort(q, P, lane);
+  nch = (m + 31) / 32;
+  A = 0;
+  for (uint32_t c = 0; c < nch; c++) {
+    const uint32_t p = c * 32 + lane;
+    const uint32_t b = __ballot_sync(0xffffffffu, p < m && q[p] != ~0ull);
+    if (lane == (int)c) A = b;
+  }
+  return true;
+}
+
+// first alive sorted position with q <= R, or -1 (uniform)
+__device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint32_t nch, uint64_t R, int lane) {
+  for (uint32_t c = 0; c < nch; c++) {
+    const uint32_t word = __shfl_sync(0xffffffffu, A, c);
+    if (!word) continue;
+    const bool fit = ((word >> lane) & 1u) && key_q(K[c * 32 + lane]) <= R;
+    const uint32_t b = __ballot_sync(0xffffffffu, fit);
+    if (b) return (int)(c * 32 + __ffs(b) - 1);
+  }
+  return -1;
+}
+
+__device__ __forceinline__ uint64_t sorted_min_q(const uint64_t* K, uint32_t A, uint32_t nch, int lane) {
+  uint64_t mn = ~0ull;
+  for (uint32_t c = 0; c < nch; c++) {
+    const uint32_t word = __shfl_sync(0xffffffffu, A, c);
+    if ((word >> lane) & 1u) mn = min(mn, key_q(K[c * 32 + lane]));
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+  return mn;
+}
+
+// One BestPrioFit pick (Alg. 2) on either representation: returns the request index (or -1)
+// and its q; dequeues it (alive bit cleared in both views).
+__device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
+                                         uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
+  int k;
+  if (fast) {
+    const int p = sorted_best(q, A, nch, R, lane);
+    if (p < 0) return -1;
+    const uint64_t key = q[p];
+    k = (int)(key & 1023u);
+    qk = key_q(key);
+    if (lane == (p >> 5)) A &= ~(1u << (p & 31));
+  } else {
+    k = warp_best_prio_fit(q, meta, m, R, lane);
+    if (k < 0) return -1;
+    qk = q[k];
+  }
+  if (lane == 0) meta[k] &= (uint8_t)~kAlive;
+  __syncwarp();
+  return k;
+}
+
+__device__ __forceinline__ uint64_t pool_min_q(bool fast, const uint64_t* q, const uint8_t* meta, uint32_t m,
+                                               uint32_t A, uint32_t nch, int lane) {
+  return fast ? sorted_min_q(q, A, nch, lane) : warp_min_q(q, meta, m, lane);
+}
+
 __device__ __forceinline__ uint64_t digest_term(uint32_t k, int32_t fg, uint64_t start) {
   return mix64((uint64_t)k ^ ((uint64_t)(uint32_t)(fg + 1) << 32) ^ mix64(start));
 }
@@ -117,22 +222,20 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint64_t R = R0[g], t = 0, dl = deadline[g];
     uint32_t np = 0, po = picks_off[g];
     if (R >= prm.threshold_ns) {  // Alg. 1 lines 6-8
-      uint64_t qmin = warp_min_q(q, meta, m, lane);
-      for (;;) {                  // lines 9-16
+      uint32_t A = 0, nch = 0;
+      const bool fast = make_sorted_pool(q, meta, m, lane, A, nch);
+      uint64_t qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
+      for (;;) {                             // lines 9-16
         if (prm.feedback && t >= dl) break;  // early stop on the HP launch
         if (R < qmin) break;                 // nothing can fit
-        int k = warp_best_prio_fit(q, meta, m, R, lane);
+        uint64_t qk;
+        const int k = pool_pick(fast, q, meta, m, A, nch, R, lane, qk);  // Alg. 2
         if (k < 0) break;
-        if (lane == 0) {
-          meta[k] &= (uint8_t)~kAlive;  // dequeue (Alg. 2 lines 25-29)
-          picks[po + np] = (uint32_t)k;
-        }
-        __syncwarp();
+        if (lane == 0) picks[po + np] = (uint32_t)k;
         np++;
         t += __ldg(pool_dur + off + k);  // launched (line 14)
-        uint64_t qk = q[k];
         R -= qk;                           // revised by the predicted duration (line 15, R17)
-        if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
+        if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
       }
     }
     if (lane == 0) {
@@ -169,7 +272,9 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
     const uint64_t scale = c.gap_scale_q16;
-    uint64_t qmin = warp_min_q(q, meta, m, lane);
+    uint32_t A = 0, nch = 0;
+    const bool fast = make_sorted_pool(q, meta, m, lane, A, nch);
+    uint64_t qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
     uint64_t t = 0, hp_delay = 0, fill_work = 0, lp_end = 0, dig = 0;
     uint32_t n_fills = 0;
     // t = start of the next HP kernel.  Without a fill, kernel i+1 starts at
@@ -210,22 +315,20 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
         for (;;) {
           if (prm.feedback && t >= r) break;
           if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
-          int k = warp_best_prio_fit(q, meta, m, R, lane);
+          uint64_t qk;
+          const int k = pool_pick(fast, q, meta, m, A, nch, R, lane, qk);  // Alg. 2
           if (k < 0) break;
-          uint64_t e = __ldg(lp_dur + c.lp_off + k);
+          const uint64_t e = __ldg(lp_dur + c.lp_off + k);
           if (lane == 0) {
-            meta[k] &= (uint8_t)~kAlive;
             if (sched) {
               fill_gap[so + k] = (int32_t)i;
               lp_start[so + k] = t;
             }
             dig += digest_term((uint32_t)k, (int32_t)i, t);
           }
-          __syncwarp();
-          uint64_t qk = q[k];
           R -= qk;
           t += e;
-          if (qk == qmin) qmin = warp_min_q(q, meta, m, lane);
+          if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
           fill_work += e;
           n_fills++;
           lp_end = max(lp_end, t);

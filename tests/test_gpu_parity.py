@@ -282,3 +282,14 @@ def test_sharded_merge_one_gpu(fk, orc, P):
     fk.table_bias(out)
     fk.table_means(out)
     assert_tables_equal(out.to_numpy(), ref, f"merge P={P}")
+
+
+def test_replay_huge_durations_slow_path(fk, orc):
+    """Requests with SK >= 2^50 ns leave the sorted-pool fast path: the exact argmin path must agree too."""
+    tr = F.random_trace(61, 3000, n_ids=25)
+    rec = tr.records.copy()
+    big = rec["name_id"] == rec["name_id"][0]
+    rec["end_ns"][big] += np.uint64(1 << 52)
+    tr2 = F.Trace(rec, tr.names, tr.sigs)
+    rp = F.random_replay(62, tr2, 200, m_max=60, n_h_max=40, levels=4)
+    _replay_parity(fk, orc, F.Config("huge", tr2, rp), 256)
