@@ -242,19 +242,25 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// one duration (j = 0) or gap (j = 1) value of a hot row: 5 shared reductions, no branches
-// on the common path (values < 2^32); larger values go straight to the table
+// one duration (j = 0) or gap (j = 1) value of a hot row.  Histogram and split sums are
+// fire-and-forget shared reductions; min/max are read first (a broadcast when several lanes
+// hit the same row) and reduced only when the value improves them.  Values >= 2^32 ns
+// (4.3 s, rare) go straight to the table.
 __device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, const fikit_table_t& tab, uint32_t row,
                                         int j, uint64_t v) {
-  const int b = bin_of(v) + 32 * j;
-  red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
+    const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
+    red_shared_add(hist_e + 4u * (b >> 1), 1u << (16 * (b & 1)));
     red_shared_add(st_e + 8u * j, v32 & 0xFFFFu);
     red_shared_add(st_e + 8u * j + 4u, v32 >> 16);
-    red_shared_min(st_e + 16u + 8u * j, v32);
-    red_shared_max(st_e + 16u + 8u * j + 4u, v32);
-  } else {  // rare: a value >= 2^32 ns (4.3 s)
+    uint32_t mn, mx;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mn), "=r"(mx) : "r"(st_e + 16u + 8u * j));
+    if (v32 < mn) red_shared_min(st_e + 16u + 8u * j, v32);
+    if (v32 > mx) red_shared_max(st_e + 16u + 8u * j + 4u, v32);
+  } else {  // rare: a value >= 2^32 ns
+    const int b = bin_of(v) + 32 * j;
+    red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
     red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
@@ -306,6 +312,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   const uint32_t sbase = smem_u32(smem_raw);
   const uint32_t s_hist = sbase + (uint32_t)offsetof(mk::Smem, hist);
   const uint32_t s_st = sbase + (uint32_t)offsetof(mk::Smem, st);
+  const uint32_t s_full = sbase + (uint32_t)offsetof(mk::Smem, full);
+  const uint32_t s_empty = sbase + (uint32_t)offsetof(mk::Smem, empty);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       uint32_t s = 0, k = 0;  // stage, use count of the stage
       for (uint32_t it = 0; it < my_tiles; it++) {
         const uint32_t tile = blockIdx.x + it * gridDim.x;
-        if (it >= (uint32_t)mk::NS) mbar_wait(&S.empty[s], (k - 1) & 1u);
+        if (it >= (uint32_t)mk::NS) mbar_wait_s(s_empty + 8u * s, (k - 1) & 1u);
         const uint32_t first = tile * mk::TILE;
         const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);  // +1: next launch for the last gap
         mbar_arrive_expect_tx(&S.full[s], cnt * 48);
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     uint32_t gi = 0;
     if (it < my_tiles) {
       const uint32_t tile = blockIdx.x + it * gridDim.x;
-      mbar_wait(&S.full[s], kuse & 1u);
+      mbar_wait_s(s_full + 8u * s, kuse & 1u);
       const uint32_t first = tile * mk::TILE;
       const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
       const uint32_t j = wig * 32 + lane;
@@ -453,7 +461,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       asm volatile("" ::"r"(hk), "l"(d), "l"(g), "r"((uint32_t)gap), "r"((uint32_t)valid), "r"(gi));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
+      if (lane == 0) mbar_arrive_s(s_empty + 8u * s);
       s += mk::GROUPS;
       if (s >= (uint32_t)mk::NS) {
         s -= mk::NS;
