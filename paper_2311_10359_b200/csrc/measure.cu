@@ -255,7 +255,8 @@ __device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, const fi
     red_shared_add(st_e + 8u * j, v32 & 0xFFFFu);
     red_shared_add(st_e + 8u * j + 4u, v32 >> 16);
     uint32_t mn, mx;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mn), "=r"(mx) : "r"(st_e + 16u + 8u * j));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mn) : "r"(st_e + 16u + 8u * j));  // 9-word rows: 4-B aligned
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mx) : "r"(st_e + 20u + 8u * j));
     if (v32 < mn) red_shared_min(st_e + 16u + 8u * j, v32);
     if (v32 > mx) red_shared_max(st_e + 16u + 8u * j + 4u, v32);
   } else {  // rare: a value >= 2^32 ns
