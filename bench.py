@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --same-device: test the N>1 path on one GPU)")
+    ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (testing only)")
+    ap.add_argument("--verify-merge", action="store_true",
+                    help="N>1: rank 0 re-measures the whole trace on one GPU and checks the merged table bit-exactly")
     return ap.parse_args()
 
 
@@ -240,9 +245,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev_index = 0 if args.same_device else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2311_10359_b200 import _build
 
@@ -299,7 +308,7 @@ def main():
     # ---- timed region: K back-to-back steps, barrier + sync on both sides ----
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = fk.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -386,6 +395,17 @@ def main():
                        "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "steps": args.e2e_steps,
                        "path": "pinned host -> device copies + fikit_* C-ABI calls + result copies back"}
 
+    # ---- N>1: the merged table must equal a 1-GPU measure of the whole trace ----
+    if world > 1 and args.verify_merge and rank == 0:
+        full = make_workload(args, 0, 1)
+        q = Pipeline(full["records"], full["names"], full["sigs"], capacity=wl["cap"])
+        q.run_measure()
+        q.check("verify-merge")
+        a, b = dense.to_numpy(), q.table.to_numpy()
+        same = all(np.array_equal(a[k], b[k]) for k in a)
+        line["verify_merge"] = {"equal_to_1gpu": bool(same), "rows": int(a["kernel_id"].shape[0])}
+        if not same:
+            print("verify-merge: MISMATCH", file=sys.stderr)
     # ---- CPU baseline: the oracle on the host cores, rank 0, N=1 only ----
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         job, desc = oracle_sample_time(wl, args.cpu_budget_s)

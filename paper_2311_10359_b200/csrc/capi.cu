@@ -233,8 +233,9 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
       return FIKIT_E_CUDA;
     attr_set = true;
   }
-  uint64_t tiles = (n + 255) / 256;
-  unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : (uint64_t)num_sms());
+  // persistent: one CTA per SM, fewer if there are not enough 32-launch warp-tiles for all warps
+  uint64_t ctas = ((n + 31) / 32 + measure_threads() / 32 - 1) / (measure_threads() / 32);
+  unsigned grid = (unsigned)(ctas < (uint64_t)num_sms() ? ctas : (uint64_t)num_sms());
   k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
                                                   sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
                                                   t, w.row_tuple(),

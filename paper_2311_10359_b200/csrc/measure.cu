@@ -190,21 +190,21 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 
 // ---- the fused identify + measure kernel ----------------------------------------------------
 namespace mk {
-constexpr int TILE = 64;                  // launches per stage
-constexpr int NS = 24;                    // ring stages (GROUPS being consumed, the rest loading)
-constexpr int GROUPS = 12;                // consumer groups (one tile each in flight)
-constexpr int WPG = TILE / 32;            // warps per group
-constexpr int CONSUMERS = GROUPS * WPG * 32;
-constexpr int THREADS = CONSUMERS + 32;   // + producer warp
+constexpr int TILE = 32;                  // launches per warp-tile (one per lane)
+constexpr int WARPS = 24;                 // warps per CTA; every warp streams and consumes its own tiles
+constexpr int SPW = 2;                    // stages per warp: the tile being read + the next one in flight
+constexpr int NS = WARPS * SPW;           // ring stages
+constexpr int CONSUMERS = WARPS * 32;
+constexpr int THREADS = CONSUMERS;
 constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
-// per epoch a slot sees <= EPOCH_ROUNDS * TILE * GROUPS launches: packed 16-bit bins and the
+// per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
-constexpr int EPOCH_ROUNDS = 65535 / (TILE * GROUPS);
+constexpr int EPOCH_ROUNDS = 65535 / (TILE * WARPS);
 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
-  uint64_t full[NS], empty[NS];
+  uint64_t full[NS];
   uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
   uint32_t tupw[7][kHotMax];      // slot -> raw identity words 0..6 (SoA: conflict-free verify)
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
@@ -217,9 +217,9 @@ struct Smem {
 };
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
 static_assert(THREADS <= 1024, "a CTA has at most 1024 threads");
-// Each stage must belong to one consumer group: with NS % GROUPS != 0 a fast group could
-// wait on a stage two uses ahead, and the mbarrier phase parity would alias (stale data).
-static_assert(NS % GROUPS == 0, "stage ownership: NS must be a multiple of GROUPS");
+// Each warp owns its SPW stages and is their only producer and consumer, so a stage's
+// mbarrier phase can never be waited on two uses ahead (no parity aliasing) and no slow
+// warp can stall another warp's prefetch.
 }  // namespace mk
 
 // fire-and-forget reductions (no return value, no dependent latency)
@@ -314,7 +314,6 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   const uint32_t s_hist = sbase + (uint32_t)offsetof(mk::Smem, hist);
   const uint32_t s_st = sbase + (uint32_t)offsetof(mk::Smem, st);
   const uint32_t s_full = sbase + (uint32_t)offsetof(mk::Smem, full);
-  const uint32_t s_empty = sbase + (uint32_t)offsetof(mk::Smem, empty);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
@@ -323,10 +322,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   if (tid == 0) {
     S.hot_n = min(*hot_n_ptr, kHotMax);
     S.overlap = 0;
-    for (int i = 0; i < mk::NS; i++) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], mk::WPG);
-    }
+    for (int i = 0; i < mk::NS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
@@ -349,34 +345,27 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   }
   __syncthreads();
 
-  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping
+  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  Warp-tile k of warp w of
+  // CTA b is tile (b * WARPS + w) + k * (gridDim * WARPS).
   const uint32_t n32 = (uint32_t)n;
   const uint32_t ntiles32 = (uint32_t)ntiles;
-  const uint32_t my_tiles = (ntiles32 > blockIdx.x) ? (ntiles32 - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-
-  if (warp == mk::CONSUMERS / 32) {
-    // ---------------- producer warp: 1-D TMA of each tile (+ the next launch) ----------------
-    if (lane == 0) {
-      uint32_t s = 0, k = 0;  // stage, use count of the stage
-      for (uint32_t it = 0; it < my_tiles; it++) {
-        const uint32_t tile = blockIdx.x + it * gridDim.x;
-        if (it >= (uint32_t)mk::NS) mbar_wait_s(s_empty + 8u * s, (k - 1) & 1u);
-        const uint32_t first = tile * mk::TILE;
-        const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);  // +1: next launch for the last gap
-        mbar_arrive_expect_tx(&S.full[s], cnt * 48);
-        bulk_g2s(S.ring[s], recs + first, cnt * 48, &S.full[s]);
-        if (++s == (uint32_t)mk::NS) {
-          s = 0;
-          k++;
-        }
-      }
-    }
-    return;
-  }
+  const uint32_t stride = gridDim.x * mk::WARPS;
+  const uint32_t tile0 = blockIdx.x * mk::WARPS + warp;
+  const uint32_t tileW = blockIdx.x * mk::WARPS;  // warp 0: the most tiles in this CTA
+  const uint32_t my_tiles = ntiles32 > tile0 ? (ntiles32 - tile0 + stride - 1) / stride : 0;
+  const uint32_t rounds = ntiles32 > tileW ? (ntiles32 - tileW + stride - 1) / stride : 0;  // CTA-uniform
+  // 1-D TMA of warp-tile k (+ the next launch, for the tile's last gap) into stage k % SPW
+  auto issue = [&](uint32_t k) {
+    const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
+    const uint32_t first = (tile0 + k * stride) * mk::TILE;
+    const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);
+    mbar_arrive_expect_tx(&S.full[sg], cnt * 48);
+    bulk_g2s(S.ring[sg], recs + first, cnt * 48, &S.full[sg]);
+  };
+  if (lane == 0)
+    for (uint32_t k = 0; k < (uint32_t)mk::SPW && k < my_tiles; k++) issue(k);
 
   // ---------------- consumers ----------------
-  const int group = warp / mk::WPG, wig = warp % mk::WPG;
-  const uint32_t rounds = (my_tiles + mk::GROUPS - 1) / mk::GROUPS;
   uint32_t overlap_cnt = 0;
   // deferred cold launches, compacted into lanes [0, np): key words, d, g, record index
   uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
@@ -399,23 +388,21 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     np = 0;
   };
-  uint32_t s = group, kuse = 0;  // stage of iteration it = r * GROUPS + group, and its use count
   for (uint32_t r = 0; r < rounds; r++) {
-    const uint32_t it = r * mk::GROUPS + group;
     bool cold = false;
     uint32_t key[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
     uint64_t d = 0, g = 0;
     bool gap = false;
     uint32_t gi = 0;
-    if (it < my_tiles) {
-      const uint32_t tile = blockIdx.x + it * gridDim.x;
-      mbar_wait_s(s_full + 8u * s, kuse & 1u);
-      const uint32_t first = tile * mk::TILE;
+    if (r < my_tiles) {
+      const uint32_t sg = warp * mk::SPW + (r % mk::SPW);
+      mbar_wait_s(s_full + 8u * sg, (r / mk::SPW) & 1u);
+      const uint32_t first = (tile0 + r * stride) * mk::TILE;
       const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
-      const uint32_t j = wig * 32 + lane;
+      const uint32_t j = lane;
       // record j (3 x 16-B shared loads); the next launch's start/run/task come from lane + 1
       // by shuffle, lane 31 reads record j + 1 (the TMA'd extra record for the tile's last)
-      const uint4* rp = S.ring[s] + j * 3;
+      const uint4* rp = S.ring[sg] + j * 3;
       uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
       if (j < cnt) {
         r0 = rp[0];
@@ -462,12 +449,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       asm volatile("" ::"r"(hk), "l"(d), "l"(g), "r"((uint32_t)gap), "r"((uint32_t)valid), "r"(gi));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive_s(s_empty + 8u * s);
-      s += mk::GROUPS;
-      if (s >= (uint32_t)mk::NS) {
-        s -= mk::NS;
-        kuse++;
-      }
+      if (lane == 0 && r + mk::SPW < my_tiles) issue(r + mk::SPW);  // refill this stage early
       if (j < cnt) {
         if (valid) {
           uint32_t pos = hk & (mk::HOT_IDX - 1);

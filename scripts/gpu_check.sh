@@ -20,3 +20,10 @@ if [ -n "$NCU" ]; then
   done
   ls -la gpurun_out
 fi
+if [ -n "$MULTI" ]; then
+  # the N>1 bench path on one GPU: 2 ranks, gloo collectives, both ranks on cuda:0, merged table checked
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
+    bench.py --gpus 2 --steps 5 --warmup 2 --backend gloo --same-device --verify-merge --records 4000000 \
+    --scenarios 20000 --no-e2e --no-cpu-baseline > gpurun_out/bench_multi.json 2> gpurun_out/bench_multi.err
+  cat gpurun_out/bench_multi.json; tail -5 gpurun_out/bench_multi.err
+fi
