@@ -192,7 +192,7 @@ def oracle_sample_time(wl, budget_s, seed=0):
     if rp is not None:
         S = rp.scenarios.shape[0]
         # a bounded set of scenarios, resolving only the launches they reference
-        s_n = max(1, min(S, 200))
+        s_n = max(1, min(S, 200, int(budget_s * 40)))  # ~2.5 ms of oracle work per scenario
         sc = rp.scenarios[:s_n].copy()
         hp_idx = np.concatenate([np.arange(c["hp_off"], c["hp_off"] + c["hp_len"]) for c in sc]).astype(np.int64)
         lp_idx = np.concatenate([np.arange(c["lp_off"], c["lp_off"] + c["lp_len"]) for c in sc]).astype(np.int64)
