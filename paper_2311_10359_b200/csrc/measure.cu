@@ -200,7 +200,7 @@ constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: sho
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
 // per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
-constexpr int EPOCH_ROUNDS = 65535 / (TILE * WARPS);
+constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);  // a round consumes SPW tiles per warp
 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
@@ -388,138 +388,153 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     np = 0;
   };
-  for (uint32_t r = 0; r < rounds; r++) {
-    bool cold = false;
-    uint32_t key[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    uint64_t d = 0, g = 0;
-    bool gap = false;
-    uint32_t gi = 0;
-    if (r < my_tiles) {
-      const uint32_t sg = warp * mk::SPW + (r % mk::SPW);
-      mbar_wait_s(s_full + 8u * sg, (r / mk::SPW) & 1u);
-      const uint32_t first = (tile0 + r * stride) * mk::TILE;
-      const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
-      const uint32_t j = lane;
-      // record j (3 x 16-B shared loads); the next launch's start/run/task come from lane + 1
-      // by shuffle, lane 31 reads record j + 1 (the TMA'd extra record for the tile's last)
-      const uint4* rp = S.ring[sg] + j * 3;
-      uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
-      if (j < cnt) {
-        r0 = rp[0];
-        r1 = rp[1];
-        r2 = rp[2];
-      }
-      uint64_t nstart = __shfl_down_sync(0xffffffffu, (uint64_t)r0.x | ((uint64_t)r0.y << 32), 1);
-      uint32_t nrun = __shfl_down_sync(0xffffffffu, r2.z, 1);
-      uint32_t ntask = __shfl_down_sync(0xffffffffu, r2.w, 1);
-      gi = first + j;
-      bool has_next = gi + 1 < n32;
-      if (lane == 31 && j < cnt) {
-        if (has_next) {
-          const uint4 x = rp[3], y = rp[5];
-          nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
-          nrun = y.z;
-          ntask = y.w;
-        }
-      }
-      if (!has_next && halo != nullptr && j < cnt) {
-        nstart = halo->start_ns;
-        nrun = halo->run_id;
-        ntask = halo->task_id;
-        has_next = true;
-      }
-      const uint32_t w[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      bool valid = false;
-      if (j < cnt) {
-        valid = record_valid(w, n_names, n_sigs);
-        const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-        const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-        d = end - start;                                   // K = end - start
-        gap = has_next && ntask == w[11] && nrun == w[10];  // R5
-        const bool ov = gap && nstart < end;
-        g = ov ? 0 : nstart - end;  // G = next start - end, clamped
-        overlap_cnt += (valid && ov) ? 1u : 0u;
-        key[0] = w[4]; key[1] = w[5]; key[2] = w[6]; key[3] = w[7]; key[4] = w[8]; key[5] = w[9] & 0xFFFFu;
-        key[6] = w[11];
-      }
-      const uint32_t hk = tuple_hash(key);
-      // every loaded word has been consumed (the values below are materialised before
-      // this point, so their shared loads have completed); order the reads (generic
-      // proxy) before the TMA overwrite (async proxy), then release the stage early
-      asm volatile("" ::"r"(hk), "l"(d), "l"(g), "r"((uint32_t)gap), "r"((uint32_t)valid), "r"(gi));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0 && r + mk::SPW < my_tiles) issue(r + mk::SPW);  // refill this stage early
-      if (j < cnt) {
-        if (valid) {
-          uint32_t pos = hk & (mk::HOT_IDX - 1);
-          int slot = -1;
-          for (;;) {
-            const uint2 tg = S.tag[pos];
-            if (tg.y == 0) break;
-            if (tg.x == hk) {
-              const uint32_t e = tg.y - 1;
-              if (S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
-                  S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] &&
-                  S.tupw[6][e] == key[6]) {
-                slot = (int)tg.y - 1;
-                break;
-              }
-            }
-            pos = (pos + 1) & (mk::HOT_IDX - 1);
-          }
-          if (slot >= 0) {
-            const uint32_t row = S.grow[slot];
-            const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
-            const uint32_t st_e = s_st + (uint32_t)slot * 36u;
-            hot_add(hist_e, st_e, tab, row, 0, d);
-            if (gap) hot_add(hist_e, st_e, tab, row, 1, g);
-            if (out_row) out_row[gi] = row;
-          } else {
-            cold = true;
-          }
-        } else {
-          flag_record(st, gi);
-        }
-      }
+  // One warp-tile in registers: identity key, K, G and flags of this lane's launch.
+  struct Rec {
+    uint32_t key[7];
+    uint32_t hk, gi;
+    uint64_t d, g;
+    bool valid, gap, live;
+  };
+  // wait for warp-tile k (stage k % SPW), read this lane's launch and the next launch's
+  // start/run/task (lane + 1 by shuffle; lane 31 from the stage's extra record; the halo
+  // after the last launch), validate, and compute K, G and the identity hash
+  auto load_tile = [&](uint32_t k, Rec& R) {
+    const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
+    mbar_wait_s(s_full + 8u * sg, (k / mk::SPW) & 1u);
+    const uint32_t first = (tile0 + k * stride) * mk::TILE;
+    const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
+    const uint4* rp = S.ring[sg] + lane * 3;
+    R.live = (uint32_t)lane < cnt;
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
+    if (R.live) {
+      r0 = rp[0];
+      r1 = rp[1];
+      r2 = rp[2];
     }
-    // ---- compact this tile's cold launches behind the pending ones; resolve when a batch is full ----
+    uint64_t nstart = __shfl_down_sync(0xffffffffu, (uint64_t)r0.x | ((uint64_t)r0.y << 32), 1);
+    uint32_t nrun = __shfl_down_sync(0xffffffffu, r2.z, 1);
+    uint32_t ntask = __shfl_down_sync(0xffffffffu, r2.w, 1);
+    R.gi = first + lane;
+    bool has_next = R.gi + 1 < n32;
+    if (lane == 31 && R.live && has_next) {
+      const uint4 x = rp[3], y = rp[5];
+      nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
+      nrun = y.z;
+      ntask = y.w;
+    }
+    if (!has_next && halo != nullptr && R.live) {
+      nstart = halo->start_ns;
+      nrun = halo->run_id;
+      ntask = halo->task_id;
+      has_next = true;
+    }
+    const uint32_t w[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+    R.valid = R.live && record_valid(w, n_names, n_sigs);
+    const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+    const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+    R.d = end - start;                                       // K = end - start
+    R.gap = R.live && has_next && ntask == w[11] && nrun == w[10];  // R5
+    const bool ov = R.gap && nstart < end;
+    R.g = ov ? 0 : nstart - end;  // G = next start - end, clamped
+    overlap_cnt += (R.valid && ov) ? 1u : 0u;
+    R.key[0] = w[4]; R.key[1] = w[5]; R.key[2] = w[6]; R.key[3] = w[7]; R.key[4] = w[8];
+    R.key[5] = w[9] & 0xFFFFu; R.key[6] = w[11];
+    R.hk = tuple_hash(R.key);
+    // every loaded word is consumed here, so the shared loads have completed
+    asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
+  };
+  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {
+    return S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
+           S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] && S.tupw[6][e] == key[6];
+  };
+  // rest of a probe chain after a first tag that did not verify
+  auto probe_rest = [&](uint32_t pos, const Rec& R) -> int {
+    for (;;) {
+      pos = (pos + 1) & (mk::HOT_IDX - 1);
+      const uint2 tg = S.tag[pos];
+      if (tg.y == 0) return -1;
+      if (tg.x == R.hk && verify(tg.y - 1, R.key)) return (int)tg.y - 1;
+    }
+  };
+  auto update = [&](const Rec& R, int slot) {
+    const uint32_t row = S.grow[slot];
+    const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
+    const uint32_t st_e = s_st + (uint32_t)slot * 36u;
+    hot_add(hist_e, st_e, tab, row, 0, R.d);
+    if (R.gap) hot_add(hist_e, st_e, tab, row, 1, R.g);
+    if (out_row) out_row[R.gi] = row;
+  };
+  // compact this tile's cold launches behind the pending ones; resolve when a batch is full
+  auto compact = [&](const Rec& R, bool cold) {
     const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
-    if (cmask) {
-      const uint32_t nc = __popc(cmask);
-      if (np + nc > 32) flush_cold();
-      // lane np + t takes the t-th cold launch of this tile
-      const int t = lane - (int)np;
-      int src = 0;
-      if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
-        uint32_t m = cmask, q = (uint32_t)t, c;
-        c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
-        c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
-        c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
-        c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
-        c = m & 1u;              if (q >= c) { src += 1; }
-      }
-      const bool take = t >= 0 && t < (int)nc;
-      const uint32_t k5 = key[5] | (gap ? 0x10000u : 0u);
-      uint32_t v;
-      v = __shfl_sync(0xffffffffu, key[0], src); if (take) pk0 = v;
-      v = __shfl_sync(0xffffffffu, key[1], src); if (take) pk1 = v;
-      v = __shfl_sync(0xffffffffu, key[2], src); if (take) pk2 = v;
-      v = __shfl_sync(0xffffffffu, key[3], src); if (take) pk3 = v;
-      v = __shfl_sync(0xffffffffu, key[4], src); if (take) pk4 = v;
-      v = __shfl_sync(0xffffffffu, k5, src);     if (take) pk5 = v;
-      v = __shfl_sync(0xffffffffu, key[6], src); if (take) pk6 = v;
-      v = __shfl_sync(0xffffffffu, gi, src);     if (take) pgi = v;
-      const uint64_t dv = __shfl_sync(0xffffffffu, d, src);
-      const uint64_t gv = __shfl_sync(0xffffffffu, g, src);
-      if (take) {
-        pd = dv;
-        pg = gv;
-      }
-      np += nc;
-      if (np >= 24) flush_cold();
+    if (!cmask) return;
+    const uint32_t nc = __popc(cmask);
+    if (np + nc > 32) flush_cold();
+    const int t = lane - (int)np;  // lane np + t takes the t-th cold launch of this tile
+    int src = 0;
+    if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
+      uint32_t m = cmask, q = (uint32_t)t, c;
+      c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
+      c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
+      c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
+      c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
+      c = m & 1u;              if (q >= c) { src += 1; }
     }
-    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit accumulators: flush before overflow
+    const bool take = t >= 0 && t < (int)nc;
+    const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u);
+    uint32_t v;
+    v = __shfl_sync(0xffffffffu, R.key[0], src); if (take) pk0 = v;
+    v = __shfl_sync(0xffffffffu, R.key[1], src); if (take) pk1 = v;
+    v = __shfl_sync(0xffffffffu, R.key[2], src); if (take) pk2 = v;
+    v = __shfl_sync(0xffffffffu, R.key[3], src); if (take) pk3 = v;
+    v = __shfl_sync(0xffffffffu, R.key[4], src); if (take) pk4 = v;
+    v = __shfl_sync(0xffffffffu, k5, src);       if (take) pk5 = v;
+    v = __shfl_sync(0xffffffffu, R.key[6], src); if (take) pk6 = v;
+    v = __shfl_sync(0xffffffffu, R.gi, src);     if (take) pgi = v;
+    const uint64_t dv = __shfl_sync(0xffffffffu, R.d, src);
+    const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+    if (take) {
+      pd = dv;
+      pg = gv;
+    }
+    np += nc;
+    if (np >= 24) flush_cold();
+  };
+
+  // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
+  // and both stages refilled before either is processed, and the two identity probes are
+  // interleaved (two independent dependency chains per lane).
+  const uint32_t rounds2 = (rounds + mk::SPW - 1) / mk::SPW;
+  for (uint32_t r = 0; r < rounds2; r++) {
+    const uint32_t kA = r * mk::SPW, kB = kA + 1;
+    Rec A, B;
+    A.live = B.live = A.valid = B.valid = false;
+    if (kA < my_tiles) load_tile(kA, A);
+    if (kB < my_tiles) load_tile(kB, B);
+    // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      if (kA + mk::SPW < my_tiles) issue(kA + mk::SPW);
+      if (kB + mk::SPW < my_tiles) issue(kB + mk::SPW);
+    }
+    // first probe step of both launches together (tags, then speculative verification of the
+    // slots they name); the rare longer chains continue in probe_rest
+    const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
+    const uint2 tA = S.tag[pA], tB = S.tag[pB];
+    const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
+    const bool vA = tA.x == A.hk && verify(eA, A.key);
+    const bool vB = tB.x == B.hk && verify(eB, B.key);
+    int sA = -1, sB = -1;
+    if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
+    if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
+    if (sA >= 0) update(A, sA);
+    if (sB >= 0) update(B, sB);
+    if (A.live && !A.valid) flag_record(st, A.gi);
+    if (B.live && !B.valid) flag_record(st, B.gi);
+    compact(A, A.valid && sA < 0);
+    compact(B, B.valid && sB < 0);
+    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
       consumer_sync();
       flush_epoch(S, tab, tid);
       consumer_sync();
