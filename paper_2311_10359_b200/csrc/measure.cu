@@ -196,7 +196,7 @@ constexpr int SPW = 2;                    // stages per warp: the tile being rea
 constexpr int NS = WARPS * SPW;           // ring stages
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
-constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
+constexpr int NBKT = 512;                 // shared dictionary buckets x 4 entries (load <= 0.31)
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
 // per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
@@ -205,7 +205,7 @@ constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);  // a round consumes 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS];
-  uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
+  uint4 bkt[NBKT];                // 4 entries (hash >> 16) << 16 | (slot + 1); 0 = empty
   uint32_t tupw[7][kHotMax];      // slot -> raw identity words 0..6 (SoA: conflict-free verify)
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     for (int i = 0; i < mk::NS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
+  for (int i = tid; i < mk::NBKT; i += mk::THREADS) S.bkt[i] = make_uint4(0u, 0u, 0u, 0u);
   for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
   for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
     const int w = i % 9;  // min words (4, 6) start at ~0
@@ -339,9 +339,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 #pragma unroll
     for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
     uint32_t h = tuple_hash(t.w);
-    uint32_t pos = h & (mk::HOT_IDX - 1);
-    while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
-    S.tag[pos].x = h;
+    const uint32_t ent = (h & 0xFFFF0000u) | (e + 1);
+    for (uint32_t b = h & (mk::NBKT - 1);; b = (b + 1) & (mk::NBKT - 1)) {
+      uint32_t* wv = reinterpret_cast<uint32_t*>(&S.bkt[b]);
+      int q = 0;
+      while (q < 4 && atomicCAS(&wv[q], 0u, ent) != 0u) q++;
+      if (q < 4) break;
+    }
   }
   __syncthreads();
 
@@ -370,16 +374,23 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // deferred cold launches, compacted into lanes [0, np): key words, d, g, record index
   uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
   uint64_t pd = 0, pg = 0;
+  uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;  // prefetched first tuple-index entry of the pending launch
   uint32_t np = 0;
   auto flush_cold = [&]() {
     if (lane < (int)np) {
       const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
-      const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
-        const uint64_t kid =
-            kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
-        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
-                                    tab.capacity);
-      });
+      uint32_t row;
+      if (pb.w != 0 && pb.w != kBusy && pa.x == key[0] && pa.y == key[1] && pa.z == key[2] && pa.w == key[3] &&
+          pb.x == key[4] && pb.y == key[5] && pb.z == key[6]) {
+        row = pb.w - 1;  // entries never change once published: a prefetched hit is final
+      } else {
+        row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+          const uint64_t kid =
+              kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
+          return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                      tab.capacity);
+        });
+      }
       if (row < tab.capacity) {
         cold_add(tab, row, 0, pd);
         if (pk5 >> 16) cold_add(tab, row, 1, pg);
@@ -447,14 +458,46 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     return S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
            S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] && S.tupw[6][e] == key[6];
   };
-  // rest of a probe chain after a first tag that did not verify
-  auto probe_rest = [&](uint32_t pos, const Rec& R) -> int {
+  // complete, exact probe from bucket b: a bucket with an empty entry ends the chain
+  auto probe_full = [&](uint32_t b, const Rec& R) -> int {
+    const uint32_t t16 = R.hk >> 16;
     for (;;) {
-      pos = (pos + 1) & (mk::HOT_IDX - 1);
-      const uint2 tg = S.tag[pos];
-      if (tg.y == 0) return -1;
-      if (tg.x == R.hk && verify(tg.y - 1, R.key)) return (int)tg.y - 1;
+      const uint4 v = S.bkt[b];
+      const uint32_t e4[4] = {v.x, v.y, v.z, v.w};
+      bool empty = false;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t x = e4[q];
+        if (x == 0) {
+          empty = true;
+        } else if ((x >> 16) == t16 && verify((x & 0xFFFFu) - 1, R.key)) {
+          return (int)(x & 0xFFFFu) - 1;
+        }
+      }
+      if (empty) return -1;
+      b = (b + 1) & (mk::NBKT - 1);
     }
+  };
+  // first bucket of a probe: the slot of the first tag match (or 0), whether any tag
+  // matched, whether the bucket has an empty entry
+  struct First {
+    uint32_t e;
+    bool match, empty;
+  };
+  auto first_bucket = [&](const uint4 v, uint32_t hk) -> First {
+    const uint32_t t16 = hk >> 16;
+    const uint32_t e4[4] = {v.x, v.y, v.z, v.w};
+    First f{0u, false, false};
+#pragma unroll
+    for (int q = 3; q >= 0; q--) {
+      const uint32_t x = e4[q];
+      if (x == 0) f.empty = true;
+      if (x != 0 && (x >> 16) == t16) {
+        f.match = true;
+        f.e = (x & 0xFFFFu) - 1;
+      }
+    }
+    return f;
   };
   auto update = [&](const Rec& R, int slot) {
     const uint32_t row = S.grow[slot];
@@ -493,9 +536,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     v = __shfl_sync(0xffffffffu, R.gi, src);     if (take) pgi = v;
     const uint64_t dv = __shfl_sync(0xffffffffu, R.d, src);
     const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+    const uint32_t hv = __shfl_sync(0xffffffffu, R.hk, src);
     if (take) {
       pd = dv;
       pg = gv;
+      // prefetch the first tuple-index entry now; the batch flush finds it in registers
+      const Tuple* te = tidx + (hv & (tslots - 1));
+      pa = ld_relaxed_v4(te);
+      pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
     }
     np += nc;
     if (np >= 24) flush_cold();
@@ -519,15 +567,15 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       if (kB + mk::SPW < my_tiles) issue(kB + mk::SPW);
     }
     // first probe step of both launches together (tags, then speculative verification of the
-    // slots they name); the rare longer chains continue in probe_rest
-    const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
-    const uint2 tA = S.tag[pA], tB = S.tag[pB];
-    const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
-    const bool vA = tA.x == A.hk && verify(eA, A.key);
-    const bool vB = tB.x == B.hk && verify(eB, B.key);
+    // slots they name); the rare longer chains continue in probe_full
+    const uint32_t bA = A.hk & (mk::NBKT - 1), bB = B.hk & (mk::NBKT - 1);
+    const uint4 wA = S.bkt[bA], wB = S.bkt[bB];
+    const First fA = first_bucket(wA, A.hk), fB = first_bucket(wB, B.hk);
+    const bool vA = fA.match && verify(fA.e, A.key);
+    const bool vB = fB.match && verify(fB.e, B.key);
     int sA = -1, sB = -1;
-    if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
-    if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
+    if (A.valid) sA = vA ? (int)fA.e : ((!fA.match && fA.empty) ? -1 : probe_full(bA, A));
+    if (B.valid) sB = vB ? (int)fB.e : ((!fB.match && fB.empty) ? -1 : probe_full(bB, B));
     if (sA >= 0) update(A, sA);
     if (sB >= 0) update(B, sB);
     if (A.live && !A.valid) flag_record(st, A.gi);
