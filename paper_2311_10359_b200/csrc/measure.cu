@@ -376,29 +376,6 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   uint64_t pd = 0, pg = 0;
   uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;  // prefetched first tuple-index entry of the pending launch
   uint32_t np = 0;
-  auto flush_cold = [&]() {
-    if (lane < (int)np) {
-      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
-      uint32_t row;
-      if (pb.w != 0 && pb.w != kBusy && pa.x == key[0] && pa.y == key[1] && pa.z == key[2] && pa.w == key[3] &&
-          pb.x == key[4] && pb.y == key[5] && pb.z == key[6]) {
-        row = pb.w - 1;  // entries never change once published: a prefetched hit is final
-      } else {
-        row = tuple_find_or_insert(tidx, tslots, key, [&]() {
-          const uint64_t kid =
-              kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
-          return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
-                                      tab.capacity);
-        });
-      }
-      if (row < tab.capacity) {
-        cold_add(tab, row, 0, pd);
-        if (pk5 >> 16) cold_add(tab, row, 1, pg);
-      }
-      if (out_row) out_row[pgi] = row;
-    }
-    np = 0;
-  };
   // One warp-tile in registers: identity key, K, G and flags of this lane's launch.
   struct Rec {
     uint32_t key[7];
@@ -507,8 +484,48 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (R.gap) hot_add(hist_e, st_e, tab, row, 1, R.g);
     if (out_row) out_row[R.gi] = row;
   };
+  auto flush_cold = [&]() {
+    if (lane < (int)np) {
+      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
+      int slot = -1;
+      if (pk5 & 0x20000u) {  // ambiguous shared probe: run it to the end
+        Rec R;
+#pragma unroll
+        for (int q = 0; q < 7; q++) R.key[q] = key[q];
+        R.hk = tuple_hash(key);
+        slot = probe_full(R.hk & (mk::NBKT - 1), R);
+      }
+      if (slot >= 0) {
+        const uint32_t row = S.grow[slot];
+        const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
+        const uint32_t st_e = s_st + (uint32_t)slot * 36u;
+        hot_add(hist_e, st_e, tab, row, 0, pd);
+        if (pk5 & 0x10000u) hot_add(hist_e, st_e, tab, row, 1, pg);
+        if (out_row) out_row[pgi] = row;
+      } else {
+      uint32_t row;
+      if (pb.w != 0 && pb.w != kBusy && pa.x == key[0] && pa.y == key[1] && pa.z == key[2] && pa.w == key[3] &&
+          pb.x == key[4] && pb.y == key[5] && pb.z == key[6]) {
+        row = pb.w - 1;  // entries never change once published: a prefetched hit is final
+      } else {
+        row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+          const uint64_t kid =
+              kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
+          return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                      tab.capacity);
+        });
+      }
+      if (row < tab.capacity) {
+        cold_add(tab, row, 0, pd);
+        if (pk5 & 0x10000u) cold_add(tab, row, 1, pg);
+      }
+      if (out_row) out_row[pgi] = row;
+      }
+    }
+    np = 0;
+  };
   // compact this tile's cold launches behind the pending ones; resolve when a batch is full
-  auto compact = [&](const Rec& R, bool cold) {
+  auto compact = [&](const Rec& R, bool cold, bool recheck) {
     const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
     if (!cmask) return;
     const uint32_t nc = __popc(cmask);
@@ -524,7 +541,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       c = m & 1u;              if (q >= c) { src += 1; }
     }
     const bool take = t >= 0 && t < (int)nc;
-    const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u);
+    const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u) | (recheck ? 0x20000u : 0u);
     uint32_t v;
     v = __shfl_sync(0xffffffffu, R.key[0], src); if (take) pk0 = v;
     v = __shfl_sync(0xffffffffu, R.key[1], src); if (take) pk1 = v;
@@ -573,15 +590,18 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     const First fA = first_bucket(wA, A.hk), fB = first_bucket(wB, B.hk);
     const bool vA = fA.match && verify(fA.e, A.key);
     const bool vB = fB.match && verify(fB.e, B.key);
+    // hit -> slot; certain miss (no tag match, bucket not full) -> -1; ambiguous (tag match
+    // that did not verify, or a full bucket) -> -2: deferred with the cold launches, where the
+    // full probe runs with all lanes active instead of stalling this warp on one lane
     int sA = -1, sB = -1;
-    if (A.valid) sA = vA ? (int)fA.e : ((!fA.match && fA.empty) ? -1 : probe_full(bA, A));
-    if (B.valid) sB = vB ? (int)fB.e : ((!fB.match && fB.empty) ? -1 : probe_full(bB, B));
+    if (A.valid) sA = vA ? (int)fA.e : ((!fA.match && fA.empty) ? -1 : -2);
+    if (B.valid) sB = vB ? (int)fB.e : ((!fB.match && fB.empty) ? -1 : -2);
     if (sA >= 0) update(A, sA);
     if (sB >= 0) update(B, sB);
     if (A.live && !A.valid) flag_record(st, A.gi);
     if (B.live && !B.valid) flag_record(st, B.gi);
-    compact(A, A.valid && sA < 0);
-    compact(B, B.valid && sB < 0);
+    compact(A, A.valid && sA < 0, sA == -2);
+    compact(B, B.valid && sB < 0, sB == -2);
     if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
       consumer_sync();
       flush_epoch(S, tab, tid);
