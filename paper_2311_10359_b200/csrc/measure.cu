@@ -524,46 +524,51 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     np = 0;
   };
-  // compact this tile's cold launches behind the pending ones; resolve when a batch is full
-  auto compact = [&](const Rec& R, bool cold, bool recheck) {
+  // Compact this tile's cold launches behind the pending ones (lanes [0, np)) and resolve the
+  // batch when it is full.  One flush site (pass 0: room for the new launches, pass 1: batch
+  // full or `final`), so the large flush code is emitted once.
+  auto compact = [&](const Rec& R, bool cold, bool recheck, bool final) {
     const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
-    if (!cmask) return;
     const uint32_t nc = __popc(cmask);
-    if (np + nc > 32) flush_cold();
-    const int t = lane - (int)np;  // lane np + t takes the t-th cold launch of this tile
-    int src = 0;
-    if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
-      uint32_t m = cmask, q = (uint32_t)t, c;
-      c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
-      c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
-      c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
-      c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
-      c = m & 1u;              if (q >= c) { src += 1; }
+    if (!cmask && !(final && np)) return;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+      if (pass == 0 ? (np + nc > 32) : (np >= 24 || (final && np))) flush_cold();
+      if (pass == 1 || !nc) continue;
+      const int t = lane - (int)np;  // lane np + t takes the t-th cold launch of this tile
+      int src = 0;
+      if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
+        uint32_t m = cmask, q = (uint32_t)t, c;
+        c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
+        c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
+        c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
+        c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
+        c = m & 1u;              if (q >= c) { src += 1; }
+      }
+      const bool take = t >= 0 && t < (int)nc;
+      const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u) | (recheck ? 0x20000u : 0u);
+      uint32_t v;
+      v = __shfl_sync(0xffffffffu, R.key[0], src); if (take) pk0 = v;
+      v = __shfl_sync(0xffffffffu, R.key[1], src); if (take) pk1 = v;
+      v = __shfl_sync(0xffffffffu, R.key[2], src); if (take) pk2 = v;
+      v = __shfl_sync(0xffffffffu, R.key[3], src); if (take) pk3 = v;
+      v = __shfl_sync(0xffffffffu, R.key[4], src); if (take) pk4 = v;
+      v = __shfl_sync(0xffffffffu, k5, src);       if (take) pk5 = v;
+      v = __shfl_sync(0xffffffffu, R.key[6], src); if (take) pk6 = v;
+      v = __shfl_sync(0xffffffffu, R.gi, src);     if (take) pgi = v;
+      const uint64_t dv = __shfl_sync(0xffffffffu, R.d, src);
+      const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+      const uint32_t hv = __shfl_sync(0xffffffffu, R.hk, src);
+      if (take) {
+        pd = dv;
+        pg = gv;
+        // prefetch the first tuple-index entry now; the batch flush finds it in registers
+        const Tuple* te = tidx + (hv & (tslots - 1));
+        pa = ld_relaxed_v4(te);
+        pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
+      }
+      np += nc;
     }
-    const bool take = t >= 0 && t < (int)nc;
-    const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u) | (recheck ? 0x20000u : 0u);
-    uint32_t v;
-    v = __shfl_sync(0xffffffffu, R.key[0], src); if (take) pk0 = v;
-    v = __shfl_sync(0xffffffffu, R.key[1], src); if (take) pk1 = v;
-    v = __shfl_sync(0xffffffffu, R.key[2], src); if (take) pk2 = v;
-    v = __shfl_sync(0xffffffffu, R.key[3], src); if (take) pk3 = v;
-    v = __shfl_sync(0xffffffffu, R.key[4], src); if (take) pk4 = v;
-    v = __shfl_sync(0xffffffffu, k5, src);       if (take) pk5 = v;
-    v = __shfl_sync(0xffffffffu, R.key[6], src); if (take) pk6 = v;
-    v = __shfl_sync(0xffffffffu, R.gi, src);     if (take) pgi = v;
-    const uint64_t dv = __shfl_sync(0xffffffffu, R.d, src);
-    const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
-    const uint32_t hv = __shfl_sync(0xffffffffu, R.hk, src);
-    if (take) {
-      pd = dv;
-      pg = gv;
-      // prefetch the first tuple-index entry now; the batch flush finds it in registers
-      const Tuple* te = tidx + (hv & (tslots - 1));
-      pa = ld_relaxed_v4(te);
-      pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
-    }
-    np += nc;
-    if (np >= 24) flush_cold();
   };
 
   // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
@@ -596,19 +601,26 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     int sA = -1, sB = -1;
     if (A.valid) sA = vA ? (int)fA.e : ((!fA.match && fA.empty) ? -1 : -2);
     if (B.valid) sB = vB ? (int)fB.e : ((!fB.match && fB.empty) ? -1 : -2);
-    if (sA >= 0) update(A, sA);
-    if (sB >= 0) update(B, sB);
-    if (A.live && !A.valid) flag_record(st, A.gi);
-    if (B.live && !B.valid) flag_record(st, B.gi);
-    compact(A, A.valid && sA < 0, sA == -2);
-    compact(B, B.valid && sB < 0, sB == -2);
+    // the two launches share one copy of the update / compaction code
+#pragma unroll 1
+    for (int x = 0; x < 2; x++) {
+      const Rec R = x ? B : A;
+      const int sl = x ? sB : sA;
+      if (sl >= 0) update(R, sl);
+      if (R.live && !R.valid) flag_record(st, R.gi);
+      compact(R, R.valid && sl < 0, sl == -2, false);
+    }
     if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
       consumer_sync();
       flush_epoch(S, tab, tid);
       consumer_sync();
     }
   }
-  if (np) flush_cold();
+  {
+    Rec none;
+    none.live = none.valid = none.gap = false;
+    compact(none, false, false, true);  // the last pending batch
+  }
   // warp-aggregate the overlap count
   uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);
