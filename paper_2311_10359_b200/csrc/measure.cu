@@ -196,7 +196,7 @@ constexpr int SPW = 2;                    // stages per warp: the tile being rea
 constexpr int NS = WARPS * SPW;           // ring stages
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
-constexpr int NBKT = 512;                 // shared dictionary buckets x 4 entries (load <= 0.31)
+constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
 // per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
@@ -205,7 +205,7 @@ constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);  // a round consumes 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS];
-  uint4 bkt[NBKT];                // 4 entries (hash >> 16) << 16 | (slot + 1); 0 = empty
+  uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
   uint32_t tupw[7][kHotMax];      // slot -> raw identity words 0..6 (SoA: conflict-free verify)
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     for (int i = 0; i < mk::NS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < mk::NBKT; i += mk::THREADS) S.bkt[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
   for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
   for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
     const int w = i % 9;  // min words (4, 6) start at ~0
@@ -339,13 +339,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 #pragma unroll
     for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
     uint32_t h = tuple_hash(t.w);
-    const uint32_t ent = (h & 0xFFFF0000u) | (e + 1);
-    for (uint32_t b = h & (mk::NBKT - 1);; b = (b + 1) & (mk::NBKT - 1)) {
-      uint32_t* wv = reinterpret_cast<uint32_t*>(&S.bkt[b]);
-      int q = 0;
-      while (q < 4 && atomicCAS(&wv[q], 0u, ent) != 0u) q++;
-      if (q < 4) break;
-    }
+    uint32_t pos = h & (mk::HOT_IDX - 1);
+    while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
+    S.tag[pos].x = h;
   }
   __syncthreads();
 
@@ -371,178 +367,37 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 
   // ---------------- consumers ----------------
   uint32_t overlap_cnt = 0;
-  // Deferred launches (cold, or an ambiguous shared probe), compacted into lanes [0, np).
-  // Only the record index travels; the flush re-reads the record from L2, where it still is.
-  uint32_t pgi = 0, pfl = 0;                    // pfl bit 0: re-probe the shared dictionary
-  uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;  // prefetched first tuple-index entry
+  // deferred cold launches, compacted into lanes [0, np): key words, d, g, record index
+  uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
+  uint64_t pd = 0, pg = 0;
   uint32_t np = 0;
-
-  // decode a launch (12 words) given the next launch's start / run / task
-  struct Dec {
-    uint32_t key[7];
-    uint64_t d, g;
-    bool valid, gap, ov;
-  };
-  auto decode = [&](const uint32_t* w, bool has_next, uint64_t nstart, uint32_t nrun, uint32_t ntask, Dec& D) {
-    D.valid = record_valid(w, n_names, n_sigs);
-    const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-    const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-    D.d = end - start;                                   // K = end - start
-    D.gap = has_next && ntask == w[11] && nrun == w[10];  // R5
-    D.ov = D.gap && nstart < end;
-    D.g = D.ov ? 0 : nstart - end;  // G = next start - end, clamped
-    D.key[0] = w[4]; D.key[1] = w[5]; D.key[2] = w[6]; D.key[3] = w[7]; D.key[4] = w[8];
-    D.key[5] = w[9] & 0xFFFFu; D.key[6] = w[11];
-  };
-  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {
-    return S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
-           S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] && S.tupw[6][e] == key[6];
-  };
-  // complete, exact probe from bucket b: a bucket with an empty entry ends the chain
-  auto probe_full = [&](uint32_t b, uint32_t hk, const uint32_t* key) -> int {
-    const uint32_t t16 = hk >> 16;
-    for (;;) {
-      const uint4 v = S.bkt[b];
-      const uint32_t e4[4] = {v.x, v.y, v.z, v.w};
-      bool empty = false;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint32_t x = e4[q];
-        if (x == 0) {
-          empty = true;
-        } else if ((x >> 16) == t16 && verify((x & 0xFFFFu) - 1, key)) {
-          return (int)(x & 0xFFFFu) - 1;
-        }
-      }
-      if (empty) return -1;
-      b = (b + 1) & (mk::NBKT - 1);
-    }
-  };
-  // first bucket of a probe: slot of the first tag match (or 0), any tag match, any empty entry
-  struct First {
-    uint32_t e;
-    bool match, empty;
-  };
-  auto first_bucket = [&](const uint4 v, uint32_t hk) -> First {
-    const uint32_t t16 = hk >> 16;
-    const uint32_t e4[4] = {v.x, v.y, v.z, v.w};
-    First f{0u, false, false};
-#pragma unroll
-    for (int q = 3; q >= 0; q--) {
-      const uint32_t x = e4[q];
-      if (x == 0) f.empty = true;
-      if (x != 0 && (x >> 16) == t16) {
-        f.match = true;
-        f.e = (x & 0xFFFFu) - 1;
-      }
-    }
-    return f;
-  };
-  auto update = [&](int slot, uint64_t d, uint64_t g, bool gap, uint32_t gi) {
-    const uint32_t row = S.grow[slot];
-    const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
-    const uint32_t st_e = s_st + (uint32_t)slot * 36u;
-    hot_add(hist_e, st_e, tab, row, 0, d);
-    if (gap) hot_add(hist_e, st_e, tab, row, 1, g);
-    if (out_row) out_row[gi] = row;
-  };
-  // resolve the pending batch with all lanes: re-read each record, re-probe the shared
-  // dictionary if ambiguous, else the tuple index / KID index and L2 reductions
   auto flush_cold = [&]() {
     if (lane < (int)np) {
-      const uint4* rp = reinterpret_cast<const uint4*>(recs) + (size_t)pgi * 3;
-      const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2);
-      bool has_next = pgi + 1 < n32;
-      uint64_t nstart = 0;
-      uint32_t nrun = 0, ntask = 0;
-      if (has_next) {
-        const uint4 x = __ldg(rp + 3), y = __ldg(rp + 5);
-        nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
-        nrun = y.z;
-        ntask = y.w;
-      } else if (halo != nullptr) {
-        nstart = halo->start_ns;
-        nrun = halo->run_id;
-        ntask = halo->task_id;
-        has_next = true;
+      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
+      const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+        const uint64_t kid =
+            kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
+        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                    tab.capacity);
+      });
+      if (row < tab.capacity) {
+        cold_add(tab, row, 0, pd);
+        if (pk5 >> 16) cold_add(tab, row, 1, pg);
       }
-      const uint32_t w[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      Dec D;
-      decode(w, has_next, nstart, nrun, ntask, D);
-      int slot = -1;
-      if (pfl & 1u) {  // ambiguous shared probe: run it to the end
-        const uint32_t hk = tuple_hash(D.key);
-        slot = probe_full(hk & (mk::NBKT - 1), hk, D.key);
-      }
-      if (slot >= 0) {
-        update(slot, D.d, D.g, D.gap, pgi);
-      } else {
-        uint32_t row;
-        if (pb.w != 0 && pb.w != kBusy && pa.x == D.key[0] && pa.y == D.key[1] && pa.z == D.key[2] &&
-            pa.w == D.key[3] && pb.x == D.key[4] && pb.y == D.key[5] && pb.z == D.key[6]) {
-          row = pb.w - 1;  // entries never change once published: a prefetched hit is final
-        } else {
-          row = tuple_find_or_insert(tidx, tslots, D.key, [&]() {
-            const uint64_t kid = kernel_id_from(__ldg(name_hash + D.key[0]), __ldg(sig_hash + D.key[1]),
-                                                D.key[2], D.key[3], D.key[4], D.key[5]);
-            return index_find_or_insert(idx, slots, kid, D.key[6], D.key, st, tab.kernel_id, tab.task_id,
-                                        row_tuple, tab.capacity);
-          });
-        }
-        if (row < tab.capacity) {
-          cold_add(tab, row, 0, D.d);
-          if (D.gap) cold_add(tab, row, 1, D.g);
-        }
-        if (out_row) out_row[pgi] = row;
-      }
+      if (out_row) out_row[pgi] = row;
     }
     np = 0;
   };
-  // Compact this tile's deferred launches behind the pending ones and resolve the batch when
-  // it is full.  One flush site (pass 0: room for the new launches, pass 1: batch full or
-  // `final`), so the flush code is emitted once.
-  auto compact = [&](bool cold, bool recheck, uint32_t gi, uint32_t hk, bool final) {
-    const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
-    const uint32_t rmask = __ballot_sync(0xffffffffu, recheck);
-    const uint32_t nc = __popc(cmask);
-    if (!cmask && !(final && np)) return;
-#pragma unroll 1
-    for (int pass = 0; pass < 2; pass++) {
-      if (pass == 0 ? (np + nc > 32) : (np >= 24 || (final && np))) flush_cold();
-      if (pass == 1 || !nc) continue;
-      const int t = lane - (int)np;  // lane np + t takes the t-th deferred launch of this tile
-      int src = 0;
-      if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
-        uint32_t m = cmask, q = (uint32_t)t, c;
-        c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
-        c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
-        c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
-        c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
-        c = m & 1u;              if (q >= c) { src += 1; }
-      }
-      const uint32_t vgi = __shfl_sync(0xffffffffu, gi, src);
-      const uint32_t vhk = __shfl_sync(0xffffffffu, hk, src);
-      if (t >= 0 && t < (int)nc) {
-        pgi = vgi;
-        pfl = (rmask >> src) & 1u;
-        // prefetch the first tuple-index entry now; the batch flush finds it in registers
-        const Tuple* te = tidx + (vhk & (tslots - 1));
-        pa = ld_relaxed_v4(te);
-        pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
-      }
-      np += nc;
-    }
-  };
-
-  // One warp-tile in registers: this lane's launch decoded.
+  // One warp-tile in registers: identity key, K, G and flags of this lane's launch.
   struct Rec {
-    Dec D;
+    uint32_t key[7];
     uint32_t hk, gi;
-    bool live;
+    uint64_t d, g;
+    bool valid, gap, live;
   };
   // wait for warp-tile k (stage k % SPW), read this lane's launch and the next launch's
   // start/run/task (lane + 1 by shuffle; lane 31 from the stage's extra record; the halo
-  // after the last launch) and decode it
+  // after the last launch), validate, and compute K, G and the identity hash
   auto load_tile = [&](uint32_t k, Rec& R) {
     const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
     mbar_wait_s(s_full + 8u * sg, (k / mk::SPW) & 1u);
@@ -574,24 +429,86 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       has_next = true;
     }
     const uint32_t w[12] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-    decode(w, has_next && R.live, nstart, nrun, ntask, R.D);
-    R.D.valid = R.D.valid && R.live;
-    overlap_cnt += (R.D.valid && R.D.ov) ? 1u : 0u;
-    R.hk = tuple_hash(R.D.key);
+    R.valid = R.live && record_valid(w, n_names, n_sigs);
+    const uint64_t start = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+    const uint64_t end = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+    R.d = end - start;                                       // K = end - start
+    R.gap = R.live && has_next && ntask == w[11] && nrun == w[10];  // R5
+    const bool ov = R.gap && nstart < end;
+    R.g = ov ? 0 : nstart - end;  // G = next start - end, clamped
+    overlap_cnt += (R.valid && ov) ? 1u : 0u;
+    R.key[0] = w[4]; R.key[1] = w[5]; R.key[2] = w[6]; R.key[3] = w[7]; R.key[4] = w[8];
+    R.key[5] = w[9] & 0xFFFFu; R.key[6] = w[11];
+    R.hk = tuple_hash(R.key);
     // every loaded word is consumed here, so the shared loads have completed
-    asm volatile("" ::"r"(R.hk), "l"(R.D.d), "l"(R.D.g), "r"((uint32_t)R.D.gap), "r"((uint32_t)R.D.valid),
-                 "r"(R.gi));
+    asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
+  };
+  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {
+    return S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
+           S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] && S.tupw[6][e] == key[6];
+  };
+  // rest of a probe chain after a first tag that did not verify
+  auto probe_rest = [&](uint32_t pos, const Rec& R) -> int {
+    for (;;) {
+      pos = (pos + 1) & (mk::HOT_IDX - 1);
+      const uint2 tg = S.tag[pos];
+      if (tg.y == 0) return -1;
+      if (tg.x == R.hk && verify(tg.y - 1, R.key)) return (int)tg.y - 1;
+    }
+  };
+  auto update = [&](const Rec& R, int slot) {
+    const uint32_t row = S.grow[slot];
+    const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
+    const uint32_t st_e = s_st + (uint32_t)slot * 36u;
+    hot_add(hist_e, st_e, tab, row, 0, R.d);
+    if (R.gap) hot_add(hist_e, st_e, tab, row, 1, R.g);
+    if (out_row) out_row[R.gi] = row;
+  };
+  // compact this tile's cold launches behind the pending ones; resolve when a batch is full
+  auto compact = [&](const Rec& R, bool cold) {
+    const uint32_t cmask = __ballot_sync(0xffffffffu, cold);
+    if (!cmask) return;
+    const uint32_t nc = __popc(cmask);
+    if (np + nc > 32) flush_cold();
+    const int t = lane - (int)np;  // lane np + t takes the t-th cold launch of this tile
+    int src = 0;
+    if (t >= 0 && t < (int)nc) {  // position of the t-th set bit of cmask
+      uint32_t m = cmask, q = (uint32_t)t, c;
+      c = __popc(m & 0xFFFFu); if (q >= c) { q -= c; src += 16; m >>= 16; }
+      c = __popc(m & 0xFFu);   if (q >= c) { q -= c; src += 8;  m >>= 8; }
+      c = __popc(m & 0xFu);    if (q >= c) { q -= c; src += 4;  m >>= 4; }
+      c = __popc(m & 0x3u);    if (q >= c) { q -= c; src += 2;  m >>= 2; }
+      c = m & 1u;              if (q >= c) { src += 1; }
+    }
+    const bool take = t >= 0 && t < (int)nc;
+    const uint32_t k5 = R.key[5] | (R.gap ? 0x10000u : 0u);
+    uint32_t v;
+    v = __shfl_sync(0xffffffffu, R.key[0], src); if (take) pk0 = v;
+    v = __shfl_sync(0xffffffffu, R.key[1], src); if (take) pk1 = v;
+    v = __shfl_sync(0xffffffffu, R.key[2], src); if (take) pk2 = v;
+    v = __shfl_sync(0xffffffffu, R.key[3], src); if (take) pk3 = v;
+    v = __shfl_sync(0xffffffffu, R.key[4], src); if (take) pk4 = v;
+    v = __shfl_sync(0xffffffffu, k5, src);       if (take) pk5 = v;
+    v = __shfl_sync(0xffffffffu, R.key[6], src); if (take) pk6 = v;
+    v = __shfl_sync(0xffffffffu, R.gi, src);     if (take) pgi = v;
+    const uint64_t dv = __shfl_sync(0xffffffffu, R.d, src);
+    const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+    if (take) {
+      pd = dv;
+      pg = gv;
+    }
+    np += nc;
+    if (np >= 24) flush_cold();
   };
 
   // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
-  // and both stages refilled before either is processed; the two first probe steps overlap.
+  // and both stages refilled before either is processed, and the two identity probes are
+  // interleaved (two independent dependency chains per lane).
   const uint32_t rounds2 = (rounds + mk::SPW - 1) / mk::SPW;
   for (uint32_t r = 0; r < rounds2; r++) {
     const uint32_t kA = r * mk::SPW, kB = kA + 1;
     Rec A, B;
-    A.live = B.live = A.D.valid = B.D.valid = false;
-    A.hk = B.hk = 0;
-    A.gi = B.gi = 0;
+    A.live = B.live = A.valid = B.valid = false;
     if (kA < my_tiles) load_tile(kA, A);
     if (kB < my_tiles) load_tile(kB, B);
     // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
@@ -601,33 +518,29 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       if (kA + mk::SPW < my_tiles) issue(kA + mk::SPW);
       if (kB + mk::SPW < my_tiles) issue(kB + mk::SPW);
     }
-    const uint32_t bA = A.hk & (mk::NBKT - 1), bB = B.hk & (mk::NBKT - 1);
-    const uint4 wA = S.bkt[bA], wB = S.bkt[bB];
-    const First fA = first_bucket(wA, A.hk), fB = first_bucket(wB, B.hk);
-    const bool vA = fA.match && verify(fA.e, A.D.key);
-    const bool vB = fB.match && verify(fB.e, B.D.key);
-    // hit -> slot; certain miss (no tag match, bucket not full) -> -1; ambiguous (a tag match
-    // that did not verify, or a full bucket) -> -2: deferred, re-probed in the batch flush
+    // first probe step of both launches together (tags, then speculative verification of the
+    // slots they name); the rare longer chains continue in probe_rest
+    const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
+    const uint2 tA = S.tag[pA], tB = S.tag[pB];
+    const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
+    const bool vA = tA.x == A.hk && verify(eA, A.key);
+    const bool vB = tB.x == B.hk && verify(eB, B.key);
     int sA = -1, sB = -1;
-    if (A.D.valid) sA = vA ? (int)fA.e : ((!fA.match && fA.empty) ? -1 : -2);
-    if (B.D.valid) sB = vB ? (int)fB.e : ((!fB.match && fB.empty) ? -1 : -2);
-    // the two launches share one copy of the update / compaction code
-#pragma unroll 1
-    for (int x = 0; x < 2; x++) {
-      const int sl = x ? sB : sA;
-      const bool valid = x ? B.D.valid : A.D.valid, live = x ? B.live : A.live;
-      const uint32_t gi = x ? B.gi : A.gi;
-      if (sl >= 0) update(sl, x ? B.D.d : A.D.d, x ? B.D.g : A.D.g, x ? B.D.gap : A.D.gap, gi);
-      if (live && !valid) flag_record(st, gi);
-      compact(valid && sl < 0, sl == -2, gi, x ? B.hk : A.hk, false);
-    }
+    if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
+    if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
+    if (sA >= 0) update(A, sA);
+    if (sB >= 0) update(B, sB);
+    if (A.live && !A.valid) flag_record(st, A.gi);
+    if (B.live && !B.valid) flag_record(st, B.gi);
+    compact(A, A.valid && sA < 0);
+    compact(B, B.valid && sB < 0);
     if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
       consumer_sync();
       flush_epoch(S, tab, tid);
       consumer_sync();
     }
   }
-  compact(false, false, 0u, 0u, true);  // the last pending batch
+  if (np) flush_cold();
   // warp-aggregate the overlap count
   uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);

@@ -1,0 +1,103 @@
+"""A/B timing of fikit_measure across library variants in ONE process on one GPU.
+
+  python scripts/ab_measure.py build <name>=<git-rev> ...   (here, CPU: builds build/ab/<name>/libfikit.so)
+  python scripts/ab_measure.py run [--records N]             (on the GPU: times every built variant)
+"""
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+AB = os.path.join(ROOT, "abtest")
+sys.path.insert(0, ROOT)
+
+
+def build(specs):
+    for spec in specs:
+        name, rev = spec.split("=")
+        d = os.path.join(AB, name)
+        src = os.path.join(d, "src")
+        os.makedirs(os.path.join(src, "paper_2311_10359_b200", "csrc"), exist_ok=True)
+        os.makedirs(os.path.join(src, "include"), exist_ok=True)
+        files = ["paper_2311_10359_b200/csrc/" + f for f in
+                 ("measure.cu", "finalize.cu", "replay.cu", "capi.cu", "fikit_internal.cuh")] + ["include/fikit.h"]
+        for f in files:
+            data = subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:{f}"])
+            open(os.path.join(src, f), "wb").write(data)
+        objs = []
+        for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
+            o = os.path.join(d, f + ".o")
+            subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                                   "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+                                   os.path.join(src, "paper_2311_10359_b200", "csrc", f), "-o", o])
+            objs.append(o)
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                               "-o", os.path.join(d, "libfikit.so"), *objs])
+        print("built", name, rev)
+
+
+def run(records):
+    import numpy as np
+    import torch
+
+    import fikit_synth as F
+    import paper_2311_10359_b200 as fk
+
+    cfg = F.zipf_trace(n_runs=max(1, records // 256))
+    tr = cfg.trace
+    n = tr.records.shape[0]
+    recs = fk.records_to_device(tr.records)
+    names, sigs = fk.strtab_to_device(tr.names), fk.strtab_to_device(tr.sigs)
+    out = {}
+    for name in sorted(os.listdir(AB)):
+        path = os.path.join(AB, name, "libfikit.so")
+        if not os.path.exists(path):
+            continue
+        L = C.CDLL(path)
+        L.fikit_ws_bytes.restype = C.c_size_t
+        L.fikit_ws_bytes.argtypes = [C.c_uint32] * 3
+        L.fikit_table_bytes.restype = C.c_size_t
+        L.fikit_table_bytes.argtypes = [C.c_uint32]
+        L.fikit_table_carve.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(fk.TableC)]
+        L.fikit_measure.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, fk.StrTabC, fk.StrTabC, C.POINTER(fk.TableC),
+                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.fikit_get_status.argtypes = [C.c_void_p, C.POINTER(fk.StatusC), C.c_void_p]
+        cap = 8192
+        wsb = L.fikit_ws_bytes(cap, names.count, sigs.count)
+        ws = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
+        wsp = ws.data_ptr() + (-ws.data_ptr()) % 256
+        tb = torch.zeros(L.fikit_table_bytes(cap) + 256, dtype=torch.uint8, device="cuda")
+        t = fk.TableC()
+        L.fikit_table_carve(C.c_void_p(tb.data_ptr() + (-tb.data_ptr()) % 256), cap, C.byref(t))
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        call = lambda: L.fikit_measure(C.c_void_p(recs.data_ptr()), n, None, names.c(), sigs.c(), C.byref(t), None,
+                                       C.c_void_p(wsp), wsb, stream)
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        st = fk.StatusC()
+        L.fikit_get_status(C.c_void_p(wsp), C.byref(st), stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = []
+        for rep in range(5):
+            e0.record()
+            for _ in range(10):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 10)
+        ms = min(times)
+        out[name] = {"ms": ms, "GBps": 48 * n / ms / 1e6, "status": st.code, "rows": st.n_rows_needed}
+        print(name, json.dumps(out[name]), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2:])
+    else:
+        rec = int(sys.argv[sys.argv.index("--records") + 1]) if "--records" in sys.argv else 100_000_000
+        run(rec)
