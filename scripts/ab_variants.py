@@ -1,0 +1,131 @@
+"""Build k_measure variants from the working tree (abtest/<name>/libfikit.so) for scripts/ab_measure.py run."""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+AB = os.path.join(ROOT, "abtest")
+CS = "paper_2311_10359_b200/csrc/"
+
+
+def sub(txt, old, new, count=1):
+    assert old in txt, old[:80]
+    return txt.replace(old, new, count)
+
+
+def t_base(m, h):
+    return m, h
+
+
+def t_hot(k):
+    def f(m, h):
+        return m, sub(h, "constexpr uint32_t kHotMax = 640;", f"constexpr uint32_t kHotMax = {k};")
+    return f
+
+
+def t_idx(n, k):
+    def f(m, h):
+        m = sub(m, "constexpr int HOT_IDX = 2048;", f"constexpr int HOT_IDX = {n};")
+        return m, sub(h, "constexpr uint32_t kHotMax = 640;", f"constexpr uint32_t kHotMax = {k};")
+    return f
+
+
+def t_warps(w, k):
+    def f(m, h):
+        m = sub(m, "constexpr int WARPS = 24;", f"constexpr int WARPS = {w};")
+        return m, sub(h, "constexpr uint32_t kHotMax = 640;", f"constexpr uint32_t kHotMax = {k};")
+    return f
+
+
+def t_prefetch(m, h):
+    m = sub(m, "  uint64_t pd = 0, pg = 0;\n  uint32_t np = 0;",
+            "  uint64_t pd = 0, pg = 0;\n  uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;\n  uint32_t np = 0;")
+    m = sub(m, """      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
+      const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {""",
+            """      const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
+      const bool pre = pb.w != 0 && pb.w != kBusy && pa.x == key[0] && pa.y == key[1] && pa.z == key[2] &&
+                       pa.w == key[3] && pb.x == key[4] && pb.y == key[5] && pb.z == key[6];
+      const uint32_t row = pre ? pb.w - 1 : tuple_find_or_insert(tidx, tslots, key, [&]() {""")
+    m = sub(m, """    const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+    if (take) {
+      pd = dv;
+      pg = gv;
+    }""", """    const uint64_t gv = __shfl_sync(0xffffffffu, R.g, src);
+    const uint32_t hv = __shfl_sync(0xffffffffu, R.hk, src);
+    if (take) {
+      pd = dv;
+      pg = gv;
+      const Tuple* te = tidx + (hv & (tslots - 1));
+      pa = ld_relaxed_v4(te);
+      pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
+    }""")
+    return m, h
+
+
+def t_nocold(m, h):  # diagnostic only: drop the L2 reductions of cold launches
+    return sub(m, "  // fire-and-forget L2 reductions (no read-back, no dependent latency)\n",
+               "  if (row != 0xFFFFFFFEu) return;  // DIAGNOSTIC\n"), h
+
+
+def t_nohot(m, h):  # diagnostic only: drop the shared reductions of hot launches
+    return sub(m, "  if ((v >> 32) == 0) {\n    const uint32_t v32 = (uint32_t)v;",
+               "  if (row != 0xFFFFFFFEu) return;  // DIAGNOSTIC\n  if ((v >> 32) == 0) {\n    const uint32_t v32 = (uint32_t)v;"), h
+
+
+def t_nocompact(m, h):  # diagnostic only: cold launches are dropped (no compaction, no flush)
+    return sub(m, "    compact(A, A.valid && sA < 0);\n    compact(B, B.valid && sB < 0);", ""), h
+
+
+VARIANTS = {
+    "x_nocold": [t_nocold],
+    "x_nohot": [t_nohot],
+    "x_nohot_nocold": [t_nohot, t_nocold],
+    "x_nocompact": [t_nocompact],
+    "x_nocompact_nohot": [t_nocompact, t_nohot],
+    "a_base": [t_base],
+    "b_prefetch": [t_prefetch],
+    "c_hot690": [t_hot(690)],
+    "d_idx4096": [t_idx(4096, 560)],
+    "e_warps32": [t_warps(32, 512)],
+    "f_warps28": [t_warps(28, 560)],
+}
+
+
+def build(names):
+    os.makedirs(AB, exist_ok=True)
+    for name in names:
+        d = os.path.join(AB, name)
+        src = os.path.join(d, "src")
+        os.makedirs(os.path.join(src, CS), exist_ok=True)
+        os.makedirs(os.path.join(src, "include"), exist_ok=True)
+        for f in ("finalize.cu", "replay.cu", "capi.cu"):
+            shutil.copy(os.path.join(ROOT, CS, f), os.path.join(src, CS, f))
+        shutil.copy(os.path.join(ROOT, "include/fikit.h"), os.path.join(src, "include/fikit.h"))
+        m = open(os.path.join(ROOT, CS, "measure.cu")).read()
+        h = open(os.path.join(ROOT, CS, "fikit_internal.cuh")).read()
+        for t in VARIANTS[name]:
+            m, h = t(m, h)
+        open(os.path.join(src, CS, "measure.cu"), "w").write(m)
+        open(os.path.join(src, CS, "fikit_internal.cuh"), "w").write(h)
+        objs = []
+        for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
+            o = os.path.join(d, f + ".o")
+            r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                                "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-c", os.path.join(src, CS, f),
+                                "-o", o], capture_output=True, text=True)
+            if r.returncode:
+                print(name, "FAILED", r.stderr[-2000:])
+                raise SystemExit(1)
+            if f == "measure.cu":
+                lines = r.stderr.splitlines()
+                i = [k for k, ln in enumerate(lines) if "k_measure" in ln and "Compiling" in ln][0]
+                info = [ln.strip() for ln in lines[i:i + 4] if "registers" in ln or "spill" in ln]
+                print(name, info)
+            objs.append(o)
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                               "-o", os.path.join(d, "libfikit.so"), *objs])
+
+
+if __name__ == "__main__":
+    build(sys.argv[1:] or list(VARIANTS))
