@@ -115,7 +115,10 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
                          fikit_table_t tab, Tuple* row_tuple, uint32_t* samp_cnt) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_samples;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t i = j * stride;
+    // jittered stride: a fixed stride aliases with periodic traces (a 300-kernel template
+    // sampled every 1525 launches sees only 12 of its positions); a hashed offset inside each
+    // stride window covers every position
+    uint64_t i = j * stride + (stride > 1 ? mix64(j + 0x9E3779B97F4A7C15ULL) % stride : 0);
     if (i >= n) break;
     uint4 a = __ldg(recs + i * 3), b = __ldg(recs + i * 3 + 1), c = __ldg(recs + i * 3 + 2);
     uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};

@@ -39,14 +39,17 @@ def build(specs):
         print("built", name, rev)
 
 
-def run(records):
+def run(records, workload="zipf"):
     import numpy as np
     import torch
 
     import fikit_synth as F
     import paper_2311_10359_b200 as fk
 
-    cfg = F.zipf_trace(n_runs=max(1, records // 256))
+    if workload == "resnet":
+        cfg = F.resnet_trace(n_runs=max(1, records // 300))
+    else:
+        cfg = F.zipf_trace(n_runs=max(1, records // 256))
     tr = cfg.trace
     n = tr.records.shape[0]
     recs = fk.records_to_device(tr.records)
@@ -100,4 +103,5 @@ if __name__ == "__main__":
         build(sys.argv[2:])
     else:
         rec = int(sys.argv[sys.argv.index("--records") + 1]) if "--records" in sys.argv else 100_000_000
-        run(rec)
+        wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "zipf"
+        run(rec, wl)

@@ -77,7 +77,75 @@ def t_nocompact(m, h):  # diagnostic only: cold launches are dropped (no compact
     return sub(m, "    compact(A, A.valid && sA < 0);\n    compact(B, B.valid && sB < 0);", ""), h
 
 
+def t_gionly(m, h):
+    """deferred cold launches carry only (index, tuple hash); flush re-reads the record from L2
+    and uses the tuple-index entry prefetched at compaction"""
+    m = sub(m, """  uint32_t pk0 = 0, pk1 = 0, pk2 = 0, pk3 = 0, pk4 = 0, pk5 = 0, pk6 = 0, pgi = 0;
+  uint64_t pd = 0, pg = 0;""", """  uint32_t pgi = 0;
+  uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;""")
+    a = m.index("  auto flush_cold = [&]() {")
+    b = m.index("    np = 0;\n  };", a)
+    m = m[:a] + """  auto flush_cold = [&]() {
+    if (lane < (int)np) {
+      const uint4* rp = reinterpret_cast<const uint4*>(recs) + (size_t)pgi * 3;
+      const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1), r2 = __ldg(rp + 2);
+      bool has_next = pgi + 1 < n32;
+      uint64_t nstart = 0;
+      uint32_t nrun = 0, ntask = 0;
+      if (has_next) {
+        const uint4 x = __ldg(rp + 3), y = __ldg(rp + 5);
+        nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
+        nrun = y.z;
+        ntask = y.w;
+      } else if (halo != nullptr) {
+        nstart = halo->start_ns;
+        nrun = halo->run_id;
+        ntask = halo->task_id;
+        has_next = true;
+      }
+      const uint64_t start = (uint64_t)r0.x | ((uint64_t)r0.y << 32);
+      const uint64_t end = (uint64_t)r0.z | ((uint64_t)r0.w << 32);
+      const uint64_t d = end - start;
+      const bool gap = has_next && ntask == r2.w && nrun == r2.z;
+      const uint64_t g = (gap && nstart >= end) ? nstart - end : 0;
+      const uint32_t key[7] = {r1.x, r1.y, r1.z, r1.w, r2.x, r2.y & 0xFFFFu, r2.w};
+      uint32_t row;
+      if (pb.w != 0 && pb.w != kBusy && pa.x == key[0] && pa.y == key[1] && pa.z == key[2] && pa.w == key[3] &&
+          pb.x == key[4] && pb.y == key[5] && pb.z == key[6]) {
+        row = pb.w - 1;
+      } else {
+        row = tuple_find_or_insert(tidx, tslots, key, [&]() {
+          const uint64_t kid = kernel_id_from(__ldg(name_hash + key[0]), __ldg(sig_hash + key[1]), key[2], key[3],
+                                              key[4], key[5]);
+          return index_find_or_insert(idx, slots, kid, key[6], key, st, tab.kernel_id, tab.task_id, row_tuple,
+                                      tab.capacity);
+        });
+      }
+      if (row < tab.capacity) {
+        cold_add(tab, row, 0, d);
+        if (gap) cold_add(tab, row, 1, g);
+      }
+      if (out_row) out_row[pgi] = row;
+    }
+""" + m[b:]
+    a = m.index("    const bool take = t >= 0 && t < (int)nc;")
+    b = m.index("    np += nc;", a)
+    m = m[:a] + """    const bool take = t >= 0 && t < (int)nc;
+    const uint32_t vgi = __shfl_sync(0xffffffffu, R.gi, src);
+    const uint32_t vhk = __shfl_sync(0xffffffffu, R.hk, src);
+    if (take) {
+      pgi = vgi;
+      const Tuple* te = tidx + (vhk & (tslots - 1));
+      pa = ld_relaxed_v4(te);
+      pb = ld_relaxed_v4(reinterpret_cast<const uint4*>(te) + 1);
+    }
+""" + m[b:]
+    return m, h
+
+
 VARIANTS = {
+    "g_gionly": [t_gionly],
+    "g_gionly_w28": [t_gionly, t_warps(28, 560)],
     "x_nocold": [t_nocold],
     "x_nohot": [t_nohot],
     "x_nohot_nocold": [t_nohot, t_nocold],
