@@ -106,6 +106,9 @@ typedef struct {
   uint64_t first_bad_index; /* E_RECORD: smallest invalid index (deterministic: atomicMin) */
   uint64_t n_rows_needed;   /* measure: number of distinct (task, kernel ID) rows seen */
   uint64_t n_overlap_gaps;  /* measure/resolve: gaps clamped from negative to 0 (R5) */
+  uint32_t schedule;        /* measure: 0 = address-order sweep with one global hot set,
+                               1 = warp-tiles sorted by task bucket, per-bucket hot sets */
+  uint32_t n_task_buckets;  /* measure, schedule 1: non-empty task buckets */
 } fikit_status_t;
 
 /* Scenario of the batch replay: HP template kernels [hp_off, hp_off+hp_len) and
@@ -130,9 +133,11 @@ typedef struct {
 } fikit_result_t;
 
 /* ---- sizes ---------------------------------------------------------------- */
-/* Workspace bytes for tables of `capacity` rows (<= 2^24) and string tables of
- * up to n_names / n_sigs entries; the same workspace serves every call. */
-size_t fikit_ws_bytes(uint32_t capacity, uint32_t n_names, uint32_t n_sigs);
+/* Workspace bytes for tables of `capacity` rows (<= 2^24), string tables of up to
+ * n_names / n_sigs entries, and fikit_measure calls of up to n_records launches
+ * (its task-partitioned tile schedule: ~5 bytes per 32 launches); the same workspace
+ * serves every call. */
+size_t fikit_ws_bytes(uint32_t capacity, uint32_t n_names, uint32_t n_sigs, uint64_t n_records);
 /* Device bytes of a table of `capacity` rows when allocated as one block
  * (layout of fikit_table_carve). */
 size_t fikit_table_bytes(uint32_t capacity);

@@ -45,7 +45,8 @@ class TableC(C.Structure):
 
 class StatusC(C.Structure):
     _fields_ = [("code", C.c_int32), ("flags", C.c_uint32), ("first_bad_index", C.c_uint64),
-                ("n_rows_needed", C.c_uint64), ("n_overlap_gaps", C.c_uint64)]
+                ("n_rows_needed", C.c_uint64), ("n_overlap_gaps", C.c_uint64), ("schedule", C.c_uint32),
+                ("n_task_buckets", C.c_uint32)]
 
 
 class FillParamsC(C.Structure):
@@ -67,7 +68,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         p, u32, u64, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_size_t
         L.fikit_ws_bytes.restype = sz
-        L.fikit_ws_bytes.argtypes = [u32, u32, u32]
+        L.fikit_ws_bytes.argtypes = [u32, u32, u32, u64]
         L.fikit_table_bytes.restype = sz
         L.fikit_table_bytes.argtypes = [u32]
         L.fikit_table_carve.argtypes = [p, u32, C.POINTER(TableC)]
@@ -154,10 +155,10 @@ def records_to_device(rec: np.ndarray, device="cuda", pinned_src=None):
 
 
 class Workspace:
-    def __init__(self, capacity: int, n_names: int, n_sigs: int, device="cuda", extra: int = 0):
+    def __init__(self, capacity: int, n_names: int, n_sigs: int, device="cuda", extra: int = 0, n_records: int = 0):
         torch = _torch()
         self.capacity, self.n_names, self.n_sigs = capacity, n_names, n_sigs
-        self.nbytes = int(lib().fikit_ws_bytes(capacity, n_names, n_sigs)) + int(extra)
+        self.nbytes = int(lib().fikit_ws_bytes(capacity, n_names, n_sigs, n_records)) + int(extra)
         self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8, device=device)
         off = (-self.buf.data_ptr()) % 256
         self.t = self.buf[off:off + self.nbytes]
@@ -222,7 +223,8 @@ def get_status(ws: Workspace, stream=None) -> dict:
     st = StatusC()
     lib().fikit_get_status(ws.ptr(), C.byref(st), _stream(stream))
     return {"code": st.code, "flags": st.flags, "first_bad_index": st.first_bad_index,
-            "n_rows_needed": st.n_rows_needed, "n_overlap_gaps": st.n_overlap_gaps}
+            "n_rows_needed": st.n_rows_needed, "n_overlap_gaps": st.n_overlap_gaps, "schedule": st.schedule,
+            "n_task_buckets": st.n_task_buckets}
 
 
 def check(ws: Workspace, what="", stream=None) -> dict:

@@ -16,9 +16,14 @@ __global__ void k_identify(const uint4*, uint64_t, const uint64_t*, const uint64
 __global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint32_t,
                          uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*, uint32_t*);
 __global__ void k_hot_select(const fikit_status_t*, const uint32_t*, const Tuple*, uint32_t, Tuple*, uint32_t*);
+__global__ void k_tile_bucket(const fikit_record_t*, uint32_t, const uint32_t*, uint8_t*, uint32_t*);
+__global__ void k_tile_plan(uint32_t*, uint32_t, uint32_t, uint32_t, const uint32_t*, uint32_t*, Phase*,
+                            fikit_status_t*);
+__global__ void k_tile_scatter(const uint8_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
                           uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, fikit_table_t,
-                          Tuple*, const Tuple*, const uint32_t*, uint32_t*);
+                          Tuple*, const Tuple*, const uint32_t*, const uint32_t*, const Phase*, const uint32_t*,
+                          uint32_t*);
 size_t measure_smem_bytes();
 int measure_threads();
 struct FinRow;
@@ -88,16 +93,28 @@ struct Ws {
   Tuple* row_tuple() const { return reinterpret_cast<Tuple*>(base + L.row_tuple); }
   Tuple* tindex() const { return reinterpret_cast<Tuple*>(base + L.tindex); }
   uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
-  uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }
-  Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 16); }
+  uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }  // header [kHotHdr]
+  Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 4ull * kHotHdr); }  // [kBuckets + 1][kHotMax]
+  uint32_t* bcount() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }
+  uint32_t* bcursor() const { return bcount() + kBuckets; }
+  uint32_t* nphase() const { return bcursor() + kBuckets; }
+  Phase* plan() const { return reinterpret_cast<Phase*>(nphase() + kMaxCTAs); }
+  uint32_t* blkoff() const {  // [kSortBlocks][kBuckets]
+    return reinterpret_cast<uint32_t*>(
+        base + align256(L.tiles + 8ull * kBuckets + 4ull * kMaxCTAs + sizeof(Phase) * (size_t)kMaxCTAs * kMaxPhases));
+  }
+  uint8_t* tile_bucket() const {
+    return reinterpret_cast<uint8_t*>(blkoff()) + align256(4ull * kSortBlocks * kBuckets);
+  }
+  uint32_t* order() const { return reinterpret_cast<uint32_t*>(tile_bucket() + align256(L.ntiles)); }
   unsigned char* fin() const { return base + L.fin; }
 };
 
 // workspace check for a capacity and string-table sizes
-int get_ws(void* ws, size_t ws_bytes, uint32_t cap, uint32_t nn, uint32_t ns, Ws* out) {
+int get_ws(void* ws, size_t ws_bytes, uint32_t cap, uint32_t nn, uint32_t ns, Ws* out, uint64_t n_records = 0) {
   if (!ws || !aligned(ws, 256)) return FIKIT_E_ARG;
   out->base = static_cast<unsigned char*>(ws);
-  out->L = ws_layout(cap, nn, ns);
+  out->L = ws_layout(cap, nn, ns, n_records);
   if (ws_bytes < out->L.total) return FIKIT_E_ARG;
   return FIKIT_OK;
 }
@@ -137,8 +154,8 @@ unsigned grid_for(uint64_t work, unsigned per_block, unsigned max_blocks) {
 
 extern "C" {
 
-size_t fikit_ws_bytes(uint32_t capacity, uint32_t n_names, uint32_t n_sigs) {
-  return ws_layout(capacity ? capacity : 1, n_names, n_sigs).total;
+size_t fikit_ws_bytes(uint32_t capacity, uint32_t n_names, uint32_t n_sigs, uint64_t n_records) {
+  return ws_layout(capacity ? capacity : 1, n_names, n_sigs, n_records).total;
 }
 
 size_t fikit_table_bytes(uint32_t cap) {
@@ -197,7 +214,7 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs) ||
       !table_ok(tab))
     return FIKIT_E_ARG;
-  if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w)) return r;
+  if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w, n)) return r;
   const fikit_table_t t = *tab;
   const uint32_t cap = t.capacity;
   if (int r = reset_status(w, s)) return r;
@@ -212,7 +229,7 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   cudaMemsetAsync(w.index(), 0, sizeof(IndexEntry) * (size_t)w.L.slots, s);
   cudaMemsetAsync(w.tindex(), 0, sizeof(Tuple) * (size_t)w.L.tslots, s);
   cudaMemsetAsync(w.samp_cnt(), 0, 4ull * cap, s);
-  cudaMemsetAsync(w.hot_n(), 0, 16, s);
+  cudaMemsetAsync(w.hot_n(), 0, 4ull * kHotHdr, s);
   if (cudaGetLastError() != cudaSuccess) return FIKIT_E_CUDA;
   if (int r = hash_strtabs(w, names, sigs, s)) return r;
   if (n == 0) return FIKIT_OK;
@@ -224,7 +241,8 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
       reinterpret_cast<const uint4*>(recs), n, stride, ns, w.name_hash(), w.sig_hash(), names.count, sigs.count,
       w.index(), w.L.slots, w.st(), t, w.row_tuple(), w.samp_cnt());
   if (int r = launched()) return r;
-  k_hot_select<<<1, 1024, 0, s>>>(w.st(), w.samp_cnt(), w.row_tuple(), cap, w.hot(), w.hot_n());
+  // hot set of every task bucket (blocks 0..kBuckets-1) and the global one (block kBuckets)
+  k_hot_select<<<kBuckets + 1, 1024, 0, s>>>(w.st(), w.samp_cnt(), w.row_tuple(), cap, w.hot(), w.hot_n());
   if (int r = launched()) return r;
   static bool attr_set = false;
   size_t smem = measure_smem_bytes();
@@ -234,12 +252,26 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
     attr_set = true;
   }
   // persistent: one CTA per SM, fewer if there are not enough 32-launch warp-tiles for all warps
-  uint64_t ctas = ((n + 31) / 32 + measure_threads() / 32 - 1) / (measure_threads() / 32);
+  const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
+  uint64_t ctas = (ntiles + measure_threads() / 32 - 1) / (measure_threads() / 32);
   unsigned grid = (unsigned)(ctas < (uint64_t)num_sms() ? ctas : (uint64_t)num_sms());
+  if (grid > kMaxCTAs) grid = kMaxCTAs;
+  // task-partitioned schedule: bucket every warp-tile by its first launch's task, stably
+  // counting-sort the tiles by bucket (sb blocks, each a contiguous chunk of tiles), and plan
+  // which CTAs sweep which bucket's sorted range
+  uint32_t sb = (ntiles + 4095) / 4096;
+  sb = sb < 1 ? 1 : sb > kSortBlocks ? kSortBlocks : sb;
+  if (sb > 2u * num_sms()) sb = 2u * num_sms();
+  k_tile_bucket<<<sb, 1024, 0, s>>>(recs, ntiles, w.hot_n(), w.tile_bucket(), w.blkoff());
+  if (int r = launched()) return r;
+  k_tile_plan<<<1, 1024, 0, s>>>(w.blkoff(), sb, ntiles, grid, w.hot_n(), w.nphase(), w.plan(), w.st());
+  if (int r = launched()) return r;
+  k_tile_scatter<<<sb, 1024, 0, s>>>(w.tile_bucket(), ntiles, w.hot_n(), w.blkoff(), w.order());
+  if (int r = launched()) return r;
   k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
                                                   sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
-                                                  t, w.row_tuple(),
-                                                  w.hot(), w.hot_n(), out_row);
+                                                  t, w.row_tuple(), w.hot(), w.hot_n(), w.order(), w.plan(),
+                                                  w.nphase(), out_row);
   return launched();
 }
 
@@ -374,6 +406,8 @@ int fikit_table_bias(const fikit_table_t* tab, void* stream) {
   k_table_bias<<<grid_for(4ull * tab->capacity, 256, num_sms() * 4), 256, 0, (cudaStream_t)stream>>>(*tab);
   return launched();
 }
+
+static_assert(sizeof(fikit_status_t) <= 64, "status lives in the first 64 workspace bytes");
 
 int fikit_get_status(const void* ws, fikit_status_t* out, void* stream) {
   if (!ws || !out) return FIKIT_E_ARG;

@@ -24,11 +24,30 @@ struct alignas(16) Tuple {  // a launch identity as raw record words (the hot di
 };
 
 struct WsLayout {
-  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, fin, total;
+  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, fin, tiles, total;
   uint32_t slots, tslots;
+  uint64_t ntiles;  // warp-tiles of 32 launches the workspace can schedule
 };
 
 constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (measure kernel)
+// Task-partitioned scheduling of fikit_measure: warp-tiles (32 launches) are bucketed by a
+// hash of their first launch's task_id; every bucket has its own hot set.
+constexpr uint32_t kBuckets = 64;
+constexpr uint32_t kMaxPhases = 8;  // bucket ranges a CTA may cover
+constexpr uint32_t kMaxCTAs = 1024;
+constexpr uint32_t kSortBlocks = 160;  // blocks of the tile counting sort (each a contiguous chunk)
+constexpr uint32_t kGlobalSet = kBuckets;  // hot-set index of the global (all-task) hot set
+// hot-set header words (u32): hot_n[kBuckets + 1], then the sample coverage counters
+constexpr uint32_t kCovTask = kBuckets + 1;  // samples whose row is in its task bucket's hot set
+constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the global hot set
+constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
+constexpr uint32_t kHotHdr = kBuckets + 8;
+constexpr uint32_t kTileLaunches = 32;
+struct Phase {
+  // sorted-tile range [p0, p1) (one bucket's tiles), swept by g CTAs of which this is number c:
+  // warp w of this CTA takes positions p0 + c * WARPS + w + j * g * WARPS
+  uint32_t bucket, p0, p1, cg;  // cg = c << 16 | g
+};
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -38,7 +57,7 @@ inline uint32_t index_slots(uint32_t cap) {
   return s;
 }
 
-inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs) {
+inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint64_t n_records) {
   WsLayout L;
   size_t o = 0;
   L.status = o;
@@ -59,12 +78,34 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs) {
   o = align256(o + sizeof(Tuple) * (size_t)cap);
   L.samp_cnt = o;
   o = align256(o + 4ull * cap);
-  L.hot = o;
-  o = align256(o + 16 + sizeof(Tuple) * (size_t)kHotMax);
+  L.hot = o;  // header[kHotHdr] (u32), then hot[kBuckets + 1][kHotMax] (Tuple)
+  o = align256(o + 4ull * kHotHdr + sizeof(Tuple) * (size_t)kHotMax * (kBuckets + 1));
   L.fin = o;
   o = align256(o + 340ull * cap + 1024);
+  // tiles: bcount[kBuckets], bcursor[kBuckets], nphase[kMaxCTAs], plan[kMaxCTAs][kMaxPhases],
+  //        blkoff[kSortBlocks][kBuckets], tile_bucket[ntiles] (u8), order[ntiles] (u32)
+  L.ntiles = (n_records + kTileLaunches - 1) / kTileLaunches;
+  L.tiles = o;
+  o = align256(o + 8ull * kBuckets + 4ull * kMaxCTAs + sizeof(Phase) * (size_t)kMaxCTAs * kMaxPhases);
+  o = align256(o + 4ull * kSortBlocks * kBuckets);
+  o = align256(o + L.ntiles);
+  o = align256(o + 4ull * L.ntiles);
   L.total = o;
   return L;
+}
+
+// task bucket: xor-fold of the task id's 6-bit digits -- one-to-one for ids < 64 (a node's
+// tasks are usually numbered densely), and multiples of 64 still spread
+__host__ __device__ __forceinline__ uint32_t bucket_of(uint32_t task) {
+  return (task ^ (task >> 6) ^ (task >> 12) ^ (task >> 18) ^ (task >> 24) ^ (task >> 30)) & (kBuckets - 1);
+}
+
+// Schedule mode, decided identically by every kernel from the sample coverage counters (hdr =
+// hot-set header): task-partitioned when the global hot set misses > 2% of the sampled launches
+// and the per-task hot sets cover > 2 points more; else one grid-stride sweep in address order.
+__host__ __device__ __forceinline__ bool use_task_buckets(const uint32_t* hdr) {
+  const uint64_t tot = hdr[kCovTotal], g = hdr[kCovGlobal], t = hdr[kCovTask];
+  return (tot - g) * 50 > tot && t > g && (t - g) * 50 > tot;
 }
 
 // misc counters (u32 words at ws + misc)

@@ -27,6 +27,8 @@ __global__ void k_reset_status(fikit_status_t* st) {
     st->first_bad_index = ~0ull;
     st->n_rows_needed = 0;
     st->n_overlap_gaps = 0;
+    st->schedule = 0;
+    st->n_task_buckets = 0;
   }
 }
 
@@ -131,19 +133,23 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
   }
 }
 
-// ---- hot select: the most-sampled rows (one CTA) ----------------------------------------
+// ---- hot sets: per task bucket, the most-sampled rows (one CTA per bucket; CTA kBuckets:
+// the global set over all tasks).  Each CTA also counts the samples its set covers. -------
 __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, const uint32_t* __restrict__ samp_cnt,
                                                      const Tuple* __restrict__ row_tuple, uint32_t cap,
-                                                     Tuple* hot, uint32_t* hot_n_out) {
+                                                     Tuple* hot_all, uint32_t* hot_n_all) {
   constexpr int NB = 4096;
   __shared__ uint32_t h[NB];
   __shared__ uint32_t s_T, s_n;
-  uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  const uint32_t bkt = blockIdx.x;  // kGlobalSet: every row
+  Tuple* hot = hot_all + (size_t)bkt * kHotMax;
+  auto mine = [&](uint32_t r) { return bkt == kGlobalSet || bucket_of(row_tuple[r].w[6]) == bkt; };
+  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
   for (int i = threadIdx.x; i < NB; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    uint32_t c = samp_cnt[r];
-    if (c) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
+    const uint32_t c = samp_cnt[r];
+    if (c && mine(r)) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
   }
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
@@ -180,15 +186,215 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
     if (t == 0) s_T = s_Tmin;
     __syncthreads();
   }
-  uint32_t T = s_T;
+  const uint32_t T = s_T;
+  uint32_t cov = 0, tot = 0;
   for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    if (samp_cnt[r] >= T) {
-      uint32_t e = atomicAdd(&s_n, 1u);
-      if (e < kHotMax) hot[e] = row_tuple[r];
+    const uint32_t c = samp_cnt[r];
+    if (c && mine(r)) {
+      tot += c;
+      if (c >= T) {
+        const uint32_t e = atomicAdd(&s_n, 1u);
+        if (e < kHotMax) {
+          hot[e] = row_tuple[r];
+          cov += c;
+        }
+      }
+    }
+  }
+  cov = __reduce_add_sync(0xffffffffu, cov);
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  if ((threadIdx.x & 31) == 0) {
+    if (cov) atomicAdd(&hot_n_all[bkt == kGlobalSet ? kCovGlobal : kCovTask], cov);
+    if (tot && bkt == kGlobalSet) atomicAdd(&hot_n_all[kCovTotal], tot);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) hot_n_all[bkt] = min(s_n, kHotMax);
+}
+
+// ---- task-partitioned schedule ---------------------------------------------------------------
+// bucket of every warp-tile = bucket_of(task of its first launch).  Block k owns the contiguous
+// chunk of tiles [k*C, (k+1)*C) and writes its per-bucket counts to blkcnt[k][*].
+__global__ void __launch_bounds__(1024) k_tile_bucket(const fikit_record_t* __restrict__ recs, uint32_t ntiles,
+                                                     const uint32_t* __restrict__ hot_hdr,
+                                                     uint8_t* __restrict__ tile_bucket, uint32_t* __restrict__ blkcnt) {
+  if (!use_task_buckets(hot_hdr)) return;  // address-order sweep: nothing to sort
+  __shared__ uint32_t h[kBuckets];
+  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t C = (ntiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * C, t1 = min(ntiles, t0 + C);
+  constexpr int U = 4;  // independent one-sector loads in flight per thread
+  for (uint32_t t = t0 + threadIdx.x; t < t1; t += U * blockDim.x) {
+    uint32_t task[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t tu = t + u * blockDim.x;
+      task[u] = tu < t1 ? __ldcs(&recs[(uint64_t)tu * kTileLaunches].task_id) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t tu = t + u * blockDim.x;
+      if (tu < t1) {
+        const uint32_t b = bucket_of(task[u]);
+        tile_bucket[tu] = (uint8_t)b;
+        atomicAdd(&h[b], 1u);
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *hot_n_out = min(s_n, kHotMax);
+  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) blkcnt[blockIdx.x * kBuckets + i] = h[i];
+}
+
+// One block of 1024 threads.  Address-order mode: CTA c sweeps all tiles with the global hot set
+// (c-th of G interleaved CTAs).  Task mode: blk[k][b] (block k's count of bucket-b tiles) becomes
+// block k's first sorted position for bucket b (column scans in shared memory), and thread 0
+// lays out each CTA's phases.  Every non-empty bucket gets g_b >= 1 CTAs in proportion to its
+// tiles (largest remainder); the g_b CTAs of a bucket sweep its sorted range together
+// (interleaved warp-tiles), so at most one moving window per bucket touches DRAM.  With more
+// non-empty buckets than CTAs, CTA c takes a group of consecutive buckets, one phase each (the
+// last phase also takes any further buckets: correct, those launches go cold).
+__global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, uint32_t nblk, uint32_t ntiles,
+                                                    uint32_t G, const uint32_t* __restrict__ hot_hdr,
+                                                    uint32_t* __restrict__ nphase, Phase* __restrict__ plan,
+                                                    fikit_status_t* st) {
+  __shared__ uint32_t m[kSortBlocks * kBuckets];
+  __shared__ uint32_t bcount[kBuckets], start[kBuckets + 1], s_g[kBuckets], s_need[2];
+  const uint32_t tid = threadIdx.x;
+  if (!use_task_buckets(hot_hdr)) {
+    for (uint32_t c = tid; c < G; c += blockDim.x) {
+      plan[c * kMaxPhases] = Phase{kGlobalSet, 0u, ntiles, (c << 16) | G};
+      nphase[c] = 1;
+    }
+    return;
+  }
+  for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) m[i] = blk[i];
+  __syncthreads();
+  if (tid < kBuckets) {
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < nblk; k++) {
+      const uint32_t c = m[k * kBuckets + tid];
+      m[k * kBuckets + tid] = run;
+      run += c;
+    }
+    bcount[tid] = run;
+  }
+  __syncthreads();
+  // smallest per-CTA load L with sum_b ceil(c_b / L) <= G (binary search, 64 threads; uniform loop)
+  {
+    uint32_t lo = (ntiles + G - 1) / G, hi = ntiles;  // f(hi) = #non-empty buckets <= G assumed
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      uint32_t need = 0;
+      if (tid < kBuckets) need = (bcount[tid] + mid - 1) / mid;
+      need = __reduce_add_sync(0xffffffffu, need);
+      if ((tid & 31) == 0 && tid < kBuckets) s_need[tid >> 5] = need;
+      __syncthreads();
+      const uint32_t tot = s_need[0] + s_need[1];
+      __syncthreads();
+      if (tot <= G) hi = mid; else lo = mid + 1;
+    }
+    if (tid < kBuckets) s_g[tid] = (bcount[tid] + lo - 1) / lo;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    start[0] = 0;
+    uint32_t nb = 0;
+    for (uint32_t b = 0; b < kBuckets; b++) {
+      start[b + 1] = start[b] + bcount[b];
+      nb += bcount[b] ? 1u : 0u;
+    }
+    st->schedule = 1;
+    st->n_task_buckets = nb;
+    for (uint32_t c = 0; c < G; c++) nphase[c] = 0;
+    if (nb > 0 && nb <= G) {
+      // g_b CTAs for bucket b: per-CTA load c_b / g_b balanced (see below); leftovers go to the
+      // buckets with the largest per-CTA load
+      uint32_t used = 0;
+      for (uint32_t b = 0; b < kBuckets; b++) used += s_g[b];
+      while (used < G) {
+        uint32_t best = 0;
+        uint64_t bn = 0, bd = 1;  // best ratio bn / bd
+        for (uint32_t b = 0; b < kBuckets; b++)
+          if (s_g[b] && (uint64_t)bcount[b] * bd > bn * s_g[b]) {
+            bn = bcount[b];
+            bd = s_g[b];
+            best = b;
+          }
+        s_g[best]++;
+        used++;
+      }
+      uint32_t c = 0;
+      for (uint32_t b = 0; b < kBuckets; b++)
+        for (uint32_t i = 0; i < s_g[b]; i++, c++) {
+          plan[c * kMaxPhases] = Phase{b, start[b], start[b + 1], (i << 16) | s_g[b]};
+          nphase[c] = 1;
+        }
+    } else if (nb > G) {  // more non-empty buckets than CTAs: consecutive buckets per CTA
+      uint32_t b = 0;
+      for (uint32_t c = 0; c < G; c++) {
+        const uint32_t want = (uint32_t)((uint64_t)(c + 1) * nb / G) - (uint32_t)((uint64_t)c * nb / G);
+        uint32_t np = 0;
+        for (uint32_t i = 0; i < want; i++) {
+          while (!bcount[b]) b++;
+          if (np < kMaxPhases) {
+            plan[c * kMaxPhases + np] = Phase{b, start[b], start[b + 1], 1u};
+            np++;
+          } else {
+            plan[c * kMaxPhases + kMaxPhases - 1].p1 = start[b + 1];  // contiguous in sorted order
+          }
+          b++;
+        }
+        nphase[c] = np;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) blk[i] = m[i] + start[i % kBuckets];
+}
+
+// stable counting-sort scatter: block k walks its chunk in address order, 256 tiles per step;
+// a tile's sorted position = its bucket's running cursor + same-bucket tiles of lower warps in
+// the step + same-bucket lanes below it (match_any).  Tiles of a bucket keep address order.
+__global__ void __launch_bounds__(1024) k_tile_scatter(const uint8_t* __restrict__ tile_bucket, uint32_t ntiles,
+                                                       const uint32_t* __restrict__ hot_hdr,
+                                                       const uint32_t* __restrict__ blkoff,
+                                                       uint32_t* __restrict__ order) {
+  if (!use_task_buckets(hot_hdr)) return;
+  constexpr int W = 32;
+  __shared__ uint32_t cur[kBuckets], wcnt[W][kBuckets];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) cur[i] = blkoff[blockIdx.x * kBuckets + i];
+  for (int i = threadIdx.x; i < W * (int)kBuckets; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t C = (ntiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * C, t1 = min(ntiles, t0 + C);
+  auto ldb = [&](uint32_t t) -> uint32_t { return t < t1 ? (uint32_t)tile_bucket[t] : kBuckets; };
+  uint32_t bnext = ldb(t0 + threadIdx.x);  // software-pipelined one step ahead
+  for (uint32_t base = t0; base < t1; base += blockDim.x) {
+    const uint32_t t = base + threadIdx.x;
+    const uint32_t b = bnext;  // kBuckets: no tile (tail)
+    bnext = ldb(t + blockDim.x);
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (b < kBuckets && rank == 0) wcnt[warp][b] = __popc(peers);
+    __syncthreads();
+    if (b < kBuckets) {
+      uint32_t pos = cur[b] + rank;
+      for (int v = 0; v < warp; v++) pos += wcnt[v][b];
+      order[pos] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < kBuckets) {
+      uint32_t add = 0;
+#pragma unroll
+      for (int v = 0; v < W; v++) {
+        add += wcnt[v][threadIdx.x];
+        wcnt[v][threadIdx.x] = 0;
+      }
+      cur[threadIdx.x] += add;
+    }
+    __syncthreads();
+  }
 }
 
 // ---- the fused identify + measure kernel ----------------------------------------------------
@@ -281,7 +487,8 @@ __device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row,
 
 // epoch flush of my slots (consumers only): packed 16-bit bins and split sums -> table, zeroed
 __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& tab, int ctid) {
-  for (uint32_t e = ctid; e < S.hot_n; e += mk::CONSUMERS) {
+  const uint32_t hn = min(S.hot_n, kHotMax);  // admission may overshoot the counter
+  for (uint32_t e = ctid; e < hn; e += mk::CONSUMERS) {
     const uint32_t row = S.grow[e];
     uint32_t* gh = tab.hist + (size_t)row * 64;
 #pragma unroll 4
@@ -309,8 +516,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     k_measure(const fikit_record_t* __restrict__ recs, uint64_t n, const fikit_record_t* __restrict__ halo,
               const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
               uint32_t n_sigs, IndexEntry* idx, uint32_t slots, Tuple* tidx, uint32_t tslots, fikit_status_t* st,
-              fikit_table_t tab, Tuple* row_tuple, const Tuple* __restrict__ hot,
-              const uint32_t* __restrict__ hot_n_ptr, uint32_t* __restrict__ out_row) {
+              fikit_table_t tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
+              const uint32_t* __restrict__ hot_n_all, const uint32_t* __restrict__ order,
+              const Phase* __restrict__ plan, const uint32_t* __restrict__ nphase, uint32_t* __restrict__ out_row) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
@@ -321,52 +529,91 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
 
-  // ---- setup: hot dictionary into shared memory, zero stats ----
   if (tid == 0) {
-    S.hot_n = min(*hot_n_ptr, kHotMax);
     S.overlap = 0;
     for (int i = 0; i < mk::NS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
-  for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
-  for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
-    const int w = i % 9;  // min words (4, 6) start at ~0
-    (&S.st[0][0])[i] = (w == 4 || w == 6) ? 0xFFFFFFFFu : 0u;
-  }
-  __syncthreads();
-  const uint32_t hot_n = S.hot_n;
-  for (uint32_t e = tid; e < hot_n; e += mk::THREADS) {
-    Tuple t = hot[e];
-    S.grow[e] = t.row;
+  // load the hot set of a task bucket into the shared dictionary, zero the statistics
+  auto load_hot_set = [&](uint32_t bkt) {
+    const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
+    if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
+    for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
+    for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
+    for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
+      const int w = i % 9;  // min words (4, 6) start at ~0
+      (&S.st[0][0])[i] = (w == 4 || w == 6) ? 0xFFFFFFFFu : 0u;
+    }
+    __syncthreads();
+    const uint32_t hn = S.hot_n;
+    for (uint32_t e = tid; e < hn; e += mk::THREADS) {
+      Tuple t = hot[e];
+      S.grow[e] = t.row;
 #pragma unroll
-    for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
-    uint32_t h = tuple_hash(t.w);
-    uint32_t pos = h & (mk::HOT_IDX - 1);
-    while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
-    S.tag[pos].x = h;
-  }
+      for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
+      uint32_t h = tuple_hash(t.w);
+      uint32_t pos = h & (mk::HOT_IDX - 1);
+      while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
+      S.tag[pos].x = h;
+    }
+    __syncthreads();
+  };
+  // reduce the shared rows into the table (end of a phase)
+  auto flush_hot_set = [&]() {
+    flush_epoch(S, tab, tid);
+    for (uint32_t e = tid, hn = min(S.hot_n, kHotMax); e < hn; e += mk::CONSUMERS) {
+      const uint32_t row = S.grow[e];
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const uint32_t mn = S.st[e][4 + 2 * j], mx = S.st[e][5 + 2 * j];
+        if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
+          red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
+          red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);
+        }
+      }
+    }
+  };
   __syncthreads();
 
-  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  Warp-tile k of warp w of
-  // CTA b is tile (b * WARPS + w) + k * (gridDim * WARPS).
+  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  In a phase, warp w takes sorted
+  // positions ph_p0 + w + j * ph_step; its j-th tile there is the (kk0 + j)-th tile it streams
+  // in this launch, in stage (kk0 + j) % SPW.
   const uint32_t n32 = (uint32_t)n;
-  const uint32_t ntiles32 = (uint32_t)ntiles;
-  const uint32_t stride = gridDim.x * mk::WARPS;
-  const uint32_t tile0 = blockIdx.x * mk::WARPS + warp;
-  const uint32_t tileW = blockIdx.x * mk::WARPS;  // warp 0: the most tiles in this CTA
-  const uint32_t my_tiles = ntiles32 > tile0 ? (ntiles32 - tile0 + stride - 1) / stride : 0;
-  const uint32_t rounds = ntiles32 > tileW ? (ntiles32 - tileW + stride - 1) / stride : 0;  // CTA-uniform
-  // 1-D TMA of warp-tile k (+ the next launch, for the tile's last gap) into stage k % SPW
-  auto issue = [&](uint32_t k) {
+  (void)ntiles;
+  uint32_t ph_p0 = 0, ph_step = mk::WARPS, kk0 = 0, my_tiles = 0;
+  uint32_t sfirst0 = 0, sfirst1 = 0;  // (all lanes) first launch of the tile in stage 0 / 1
+  // 1-D TMA of this warp's j-th tile of the phase (+ the next launch, for the tile's last gap)
+  // the warp's upcoming tiles: lane l holds the tile of phase position jbase + l
+  // (ordn: the window after it, loaded one window ahead so the refill never waits on L2)
+  uint32_t ord = 0, ordn = 0, jbase = 0;
+  const bool by_task = use_task_buckets(hot_n_all);  // else sorted position = tile
+  auto ld_ord = [&](uint32_t j) -> uint32_t {
+    const uint32_t p = ph_p0 + warp + j * ph_step;
+    return j < my_tiles ? (by_task ? __ldg(order + p) : p) : 0u;
+  };
+  auto load_window = [&](uint32_t jb) {
+    jbase = jb;
+    ord = ld_ord(jb + lane);
+    ordn = ld_ord(jb + 32 + lane);
+  };
+  auto next_window = [&]() {
+    jbase += 32;
+    ord = ordn;
+    ordn = ld_ord(jbase + 32 + lane);
+  };
+  auto tile_first = [&](uint32_t j) -> uint32_t {  // all lanes; task mode: j in [jbase, jbase + 32)
+    return (by_task ? __shfl_sync(0xffffffffu, ord, j - jbase) : ph_p0 + warp + j * ph_step) * mk::TILE;
+  };
+  auto issue = [&](uint32_t j, uint32_t first) {
+    const uint32_t k = kk0 + j;
     const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
-    const uint32_t first = (tile0 + k * stride) * mk::TILE;
     const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);
     mbar_arrive_expect_tx(&S.full[sg], cnt * 48);
     bulk_g2s(S.ring[sg], recs + first, cnt * 48, &S.full[sg]);
   };
-  if (lane == 0)
-    for (uint32_t k = 0; k < (uint32_t)mk::SPW && k < my_tiles; k++) issue(k);
+  auto set_first = [&](uint32_t j, uint32_t first) {
+    if ((kk0 + j) % mk::SPW) sfirst1 = first; else sfirst0 = first;
+  };
 
   // ---------------- consumers ----------------
   uint32_t overlap_cnt = 0;
@@ -375,6 +622,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   uint64_t pd = 0, pg = 0;
   uint32_t np = 0;
   auto flush_cold = [&]() {
+    const uint32_t pend = __ballot_sync(0xffffffffu, lane < (int)np);
     if (lane < (int)np) {
       const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
       const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
@@ -388,6 +636,24 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         if (pk5 >> 16) cold_add(tab, row, 1, pg);
       }
       if (out_row) out_row[pgi] = row;
+      // admit the row to the shared dictionary while it has room (one lane per distinct row):
+      // this CTA's later launches of it are hot.  Slot words first, then the tag: a reader that
+      // sees the tag half-written misses and takes the cold path, which is also correct; two
+      // CTA warps admitting the same row concurrently give two slots of one row (both flushed).
+      const uint32_t same = __match_any_sync(pend, row);
+      if (row < tab.capacity && (same & ((1u << lane) - 1u)) == 0 && *(volatile uint32_t*)&S.hot_n < kHotMax) {
+        const uint32_t e = atomicAdd(&S.hot_n, 1u);
+        if (e < kHotMax) {
+          S.grow[e] = row;
+#pragma unroll
+          for (int q = 0; q < 7; q++) S.tupw[q][e] = key[q];
+          const uint32_t h = tuple_hash(key);
+          __threadfence_block();
+          uint32_t pos = h & (mk::HOT_IDX - 1);
+          while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
+          S.tag[pos].x = h;
+        }
+      }
     }
     np = 0;
   };
@@ -401,10 +667,11 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // wait for warp-tile k (stage k % SPW), read this lane's launch and the next launch's
   // start/run/task (lane + 1 by shuffle; lane 31 from the stage's extra record; the halo
   // after the last launch), validate, and compute K, G and the identity hash
-  auto load_tile = [&](uint32_t k, Rec& R) {
+  auto load_tile = [&](uint32_t j, Rec& R) {
+    const uint32_t k = kk0 + j;
     const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
     mbar_wait_s(s_full + 8u * sg, (k / mk::SPW) & 1u);
-    const uint32_t first = (tile0 + k * stride) * mk::TILE;
+    const uint32_t first = (k % mk::SPW) ? sfirst1 : sfirst0;
     const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
     const uint4* rp = S.ring[sg] + lane * 3;
     R.live = (uint32_t)lane < cnt;
@@ -504,63 +771,80 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (np >= 24) flush_cold();
   };
 
-  // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
-  // and both stages refilled before either is processed, and the two identity probes are
-  // interleaved (two independent dependency chains per lane).
-  const uint32_t rounds2 = (rounds + mk::SPW - 1) / mk::SPW;
-  for (uint32_t r = 0; r < rounds2; r++) {
-    const uint32_t kA = r * mk::SPW, kB = kA + 1;
-    Rec A, B;
-    A.live = B.live = A.valid = B.valid = false;
-    if (kA < my_tiles) load_tile(kA, A);
-    if (kB < my_tiles) load_tile(kB, B);
-    // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      if (kA + mk::SPW < my_tiles) issue(kA + mk::SPW);
-      if (kB + mk::SPW < my_tiles) issue(kB + mk::SPW);
+  const uint32_t nph = nphase[blockIdx.x];
+  for (uint32_t ph = 0; ph < nph; ph++) {
+    const Phase P = plan[blockIdx.x * kMaxPhases + ph];
+    load_hot_set(P.bucket);
+    const uint32_t pc = P.cg >> 16, pg = P.cg & 0xFFFFu;
+    ph_p0 = P.p0 + pc * mk::WARPS;          // this CTA's first position; warp w adds w
+    ph_step = pg * mk::WARPS;               // positions between a warp's consecutive tiles
+    const uint32_t span = P.p1 > ph_p0 ? P.p1 - ph_p0 : 0;
+    my_tiles = span > (uint32_t)warp ? (span - warp + ph_step - 1) / ph_step : 0;
+    const uint32_t rounds = span ? (span + ph_step - 1) / ph_step : 0;  // warp 0 has the most
+    if (by_task) load_window(0);
+    {
+      const uint32_t f0 = tile_first(0), f1 = tile_first(1);
+      set_first(0, f0);
+      set_first(1, f1);
+      if (lane == 0) {
+        if (my_tiles > 0) issue(0, f0);
+        if (my_tiles > 1) issue(1, f1);
+      }
     }
-    // first probe step of both launches together (tags, then speculative verification of the
-    // slots they name); the rare longer chains continue in probe_rest
-    const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
-    const uint2 tA = S.tag[pA], tB = S.tag[pB];
-    const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
-    const bool vA = tA.x == A.hk && verify(eA, A.key);
-    const bool vB = tB.x == B.hk && verify(eB, B.key);
-    int sA = -1, sB = -1;
-    if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
-    if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
-    if (sA >= 0) update(A, sA);
-    if (sB >= 0) update(B, sB);
-    if (A.live && !A.valid) flag_record(st, A.gi);
-    if (B.live && !B.valid) flag_record(st, B.gi);
-    compact(A, A.valid && sA < 0);
-    compact(B, B.valid && sB < 0);
-    if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
-      consumer_sync();
-      flush_epoch(S, tab, tid);
-      consumer_sync();
+    // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
+    // and both stages refilled before either is processed, and the two identity probes are
+    // interleaved (two independent dependency chains per lane).
+    const uint32_t rounds2 = (rounds + mk::SPW - 1) / mk::SPW;  // CTA-uniform (warp 0 has the most tiles)
+    for (uint32_t r = 0; r < rounds2; r++) {
+      const uint32_t kA = r * mk::SPW, kB = kA + 1;
+      Rec A, B;
+      A.live = B.live = A.valid = B.valid = false;
+      if (kA < my_tiles) load_tile(kA, A);
+      if (kB < my_tiles) load_tile(kB, B);
+      // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      const uint32_t ja = kA + mk::SPW, jb = kB + mk::SPW;  // ja even: both in one 32-window
+      if (by_task && ja >= jbase + 32) next_window();
+      const uint32_t fa = tile_first(ja), fb = tile_first(jb);
+      set_first(ja, fa);
+      set_first(jb, fb);
+      if (lane == 0) {
+        if (ja < my_tiles) issue(ja, fa);
+        if (jb < my_tiles) issue(jb, fb);
+      }
+      // first probe step of both launches together (tags, then speculative verification of the
+      // slots they name); the rare longer chains continue in probe_rest
+      const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
+      const uint2 tA = S.tag[pA], tB = S.tag[pB];
+      const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
+      const bool vA = tA.x == A.hk && verify(eA, A.key);
+      const bool vB = tB.x == B.hk && verify(eB, B.key);
+      int sA = -1, sB = -1;
+      if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
+      if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
+      if (sA >= 0) update(A, sA);
+      if (sB >= 0) update(B, sB);
+      if (A.live && !A.valid) flag_record(st, A.gi);
+      if (B.live && !B.valid) flag_record(st, B.gi);
+      compact(A, A.valid && sA < 0);
+      compact(B, B.valid && sB < 0);
+      if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
+        consumer_sync();
+        flush_epoch(S, tab, tid);
+        consumer_sync();
+      }
     }
+    kk0 += my_tiles;
+    __syncthreads();  // every warp is done with this bucket's tiles
+    flush_hot_set();
+    __syncthreads();  // before the next phase reloads the shared rows
   }
   if (np) flush_cold();
   // warp-aggregate the overlap count
   uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);
-  consumer_sync();
-  // ---- final reduction of the shared rows into the table ----
-  flush_epoch(S, tab, tid);
-  for (uint32_t e = tid; e < hot_n; e += mk::CONSUMERS) {
-    const uint32_t row = S.grow[e];
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-      const uint32_t mn = S.st[e][4 + 2 * j], mx = S.st[e][5 + 2 * j];
-      if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
-        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
-        red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);
-      }
-    }
-  }
+  __syncthreads();
   if (tid == 0 && S.overlap) atomicAdd((unsigned long long*)&st->n_overlap_gaps, S.overlap);
 }
 

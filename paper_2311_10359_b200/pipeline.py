@@ -30,7 +30,7 @@ class Pipeline:
         self.names: DevStrTab = strtab_to_device(names, device)
         self.sigs: DevStrTab = strtab_to_device(sigs, device)
         self.table = Table(self.capacity, device)
-        self.ws = Workspace(self.capacity, max(1, names.count), max(1, sigs.count), device)
+        self.ws = Workspace(self.capacity, max(1, names.count), max(1, sigs.count), device, n_records=self.n)
         self.out_row = torch.empty(max(1, self.n), dtype=torch.int32, device=device) if want_rows else None
         self.replay = None
         if replay is not None:

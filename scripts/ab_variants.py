@@ -74,7 +74,7 @@ def t_nohot(m, h):  # diagnostic only: drop the shared reductions of hot launche
 
 
 def t_nocompact(m, h):  # diagnostic only: cold launches are dropped (no compaction, no flush)
-    return sub(m, "    compact(A, A.valid && sA < 0);\n    compact(B, B.valid && sB < 0);", ""), h
+    return sub(m, "      compact(A, A.valid && sA < 0);\n      compact(B, B.valid && sB < 0);", ""), h
 
 
 def t_gionly(m, h):
@@ -143,7 +143,12 @@ def t_gionly(m, h):
     return m, h
 
 
+def t_noepoch(m, h):  # diagnostic only: no epoch flushes (16-bit counters may wrap)
+    return sub(m, "constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);", "constexpr int EPOCH_ROUNDS = 1 << 20;"), h
+
+
 VARIANTS = {
+    "x_noepoch": [t_noepoch],
     "g_gionly": [t_gionly],
     "g_gionly_w28": [t_gionly, t_warps(28, 560)],
     "x_nocold": [t_nocold],

@@ -39,7 +39,7 @@ def test_library_loads_and_host_helpers(libpath):
     import paper_2311_10359_b200 as fk
 
     L = fk.lib()
-    assert L.fikit_ws_bytes(8192, 2048, 64) > 0
+    assert L.fikit_ws_bytes(8192, 2048, 64, 100_000_000) > 0
     assert L.fikit_table_bytes(96) >= 96 * (8 + 4 + 32 + 256 + 32 + 16)
     assert L.fikit_strerror(fk.E_CAPACITY).decode() == "statistic table capacity exceeded"
     # carving is host-only pointer arithmetic: check the SUM/MAX blocks are contiguous

@@ -71,6 +71,10 @@ def test_toy_end_to_end(fk, orc):
     (11, 5000, {"run_len_max": 1}), (12, 5000, {"n_ids": 1, "n_tasks": 1}),
     (13, 20000, {"n_ids": 900, "n_tasks": 4, "n_names": 300}),  # > kHotMax rows: cold path
     (14, 70000, {"n_ids": 3000, "n_tasks": 7, "n_names": 800, "overlap_frac": 0.05}),
+    # many tasks: more task buckets than CTAs (several phases per CTA, merged tail phase)
+    (15, 20000, {"n_ids": 500, "n_tasks": 100, "n_names": 300, "run_len_max": 200}),
+    (16, 2000, {"n_ids": 50, "n_tasks": 100, "run_len_max": 64}),
+    (17, 300000, {"n_ids": 400, "n_tasks": 40, "n_names": 300, "run_len_max": 400}),
 ])
 def test_measure_random(fk, orc, seed, n, kw):
     tr = F.random_trace(seed, n, **kw)
@@ -81,6 +85,8 @@ def test_measure_random(fk, orc, seed, n, kw):
     assert st["n_rows_needed"] == ref.n_rows
     assert_tables_equal(p.table.to_numpy(), ref, f"seed {seed}")
     assert np.array_equal(p.rows(), rrows)
+    if seed >= 13:  # far more rows than one hot set: the task-partitioned schedule runs
+        assert st["schedule"] == 1 and st["n_task_buckets"] > 1, st
 
 
 def test_identify_random(fk, orc):
@@ -144,6 +150,7 @@ def test_resnet_full(fk, orc):
     p.check()
     assert ref.n_rows == 96
     assert_tables_equal(p.table.to_numpy(), ref, "resnet")
+    assert p.check()["schedule"] == 0  # 96 rows: one global hot set, address-order sweep
 
 
 def _replay_parity(fk, orc, cfg, capacity, check_schedule=True):
@@ -193,6 +200,7 @@ def test_zipf_small_full(fk, orc):
     assert ref.n_rows > 640  # more rows than the shared-memory hot cache
     assert_tables_equal(p.table.to_numpy(), ref, "zipf-2M")
     assert st["n_overlap_gaps"] == rst["n_overlap_gaps"]
+    assert st["schedule"] == 1 and st["n_task_buckets"] == 32, st  # 32 tasks, one bucket each
 
 
 def test_fill_batch(fk, orc):
