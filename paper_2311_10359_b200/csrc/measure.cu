@@ -400,12 +400,14 @@ __global__ void __launch_bounds__(1024) k_tile_scatter(const uint8_t* __restrict
 // ---- the fused identify + measure kernel ----------------------------------------------------
 namespace mk {
 constexpr int TILE = 32;                  // launches per warp-tile (one per lane)
-constexpr int WARPS = 24;                 // warps per CTA; every warp streams and consumes its own tiles
+constexpr int WARPS = 20;                 // warps per CTA; every warp streams and consumes its own tiles (<= 102 registers)
 constexpr int SPW = 2;                    // stages per warp: the tile being read + the next one in flight
 constexpr int NS = WARPS * SPW;           // ring stages
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
-constexpr int HOT_IDX = 2048;             // shared tag slots (load <= 0.31: short probe chains)
+constexpr uint32_t TAG_Q = 1024;          // tag buckets of 4 one-word tags (4096 tags, load <= 0.16)
+constexpr uint32_t TAG_HB = 0xFFFFF800u;  // tag = hash bits 11..31 (bit 31 forced to 1) | (slot + 1)
+static_assert(kHotMax < 2048, "slot + 1 must fit the 11 tag bits");
 constexpr int STAGE_BYTES = (TILE + 1) * 48;
 // per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
@@ -414,8 +416,10 @@ constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);  // a round consumes 
 struct Smem {
   uint4 ring[NS][STAGE_BYTES / 16];
   uint64_t full[NS];
-  uint2 tag[HOT_IDX];             // (tuple hash, slot + 1); 0 = empty
-  uint32_t tupw[7][kHotMax];      // slot -> raw identity words 0..6 (SoA: conflict-free verify)
+  // Bucket q = hash % TAG_Q holds up to 4 tags, filled in order (the filled tags are a prefix);
+  // a full bucket continues in the next one.  0 = empty.
+  uint4 tagq[TAG_Q];
+  uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6 (+ 0): two 16-B loads verify
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
   uint32_t st[kHotMax][9];        // 0-3: sum of (v & 0xFFFF), sum of (v >> 16) for duration, gap (v < 2^32)
@@ -512,6 +516,29 @@ __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& ta
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(mk::CONSUMERS) : "memory"); }
 
+namespace mk {
+__device__ __forceinline__ uint32_t tag_bits(uint32_t h) { return (h & TAG_HB) | 0x80000000u; }
+// slot + 1 of the first tag of bucket t whose hash bits are hb's, 0 if none (an empty tag never
+// matches: hb has bit 31 set)
+__device__ __forceinline__ uint32_t bucket_match(const uint4 t, uint32_t hb) {
+  uint32_t c = 0;
+  if ((t.w ^ hb) < 0x800u) c = t.w;
+  if ((t.z ^ hb) < 0x800u) c = t.z;
+  if ((t.y ^ hb) < 0x800u) c = t.y;
+  if ((t.x ^ hb) < 0x800u) c = t.x;
+  return c & 0x7FFu;
+}
+// publish slot e under hash h (its tup words are written and fenced before)
+__device__ __forceinline__ void tag_insert(Smem& S, uint32_t h, uint32_t e) {
+  const uint32_t tg = tag_bits(h) | (e + 1);
+  uint32_t* w = reinterpret_cast<uint32_t*>(S.tagq);
+  for (uint32_t q = h & (TAG_Q - 1);; q = (q + 1) & (TAG_Q - 1))
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      if (atomicCAS(&w[q * 4 + i], 0u, tg) == 0u) return;
+}
+}  // namespace mk
+
 __global__ void __launch_bounds__(mk::THREADS, 1)
     k_measure(const fikit_record_t* __restrict__ recs, uint64_t n, const fikit_record_t* __restrict__ halo,
               const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
@@ -538,7 +565,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto load_hot_set = [&](uint32_t bkt) {
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
     if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
-    for (int i = tid; i < mk::HOT_IDX; i += mk::THREADS) S.tag[i] = make_uint2(0u, 0u);
+    for (int i = tid; i < (int)mk::TAG_Q; i += mk::THREADS) S.tagq[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
     for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
       const int w = i % 9;  // min words (4, 6) start at ~0
@@ -549,12 +576,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     for (uint32_t e = tid; e < hn; e += mk::THREADS) {
       Tuple t = hot[e];
       S.grow[e] = t.row;
-#pragma unroll
-      for (int q = 0; q < 7; q++) S.tupw[q][e] = t.w[q];
-      uint32_t h = tuple_hash(t.w);
-      uint32_t pos = h & (mk::HOT_IDX - 1);
-      while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
-      S.tag[pos].x = h;
+      S.tup[e][0] = make_uint4(t.w[0], t.w[1], t.w[2], t.w[3]);
+      S.tup[e][1] = make_uint4(t.w[4], t.w[5], t.w[6], 0u);
+      mk::tag_insert(S, tuple_hash(t.w), e);
     }
     __syncthreads();
   };
@@ -637,21 +661,18 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       }
       if (out_row) out_row[pgi] = row;
       // admit the row to the shared dictionary while it has room (one lane per distinct row):
-      // this CTA's later launches of it are hot.  Slot words first, then the tag: a reader that
-      // sees the tag half-written misses and takes the cold path, which is also correct; two
-      // CTA warps admitting the same row concurrently give two slots of one row (both flushed).
+      // this CTA's later launches of it are hot.  Slot words first, then the tag (one CAS): a
+      // reader that misses the new tag takes the cold path, which is also correct; two CTA warps
+      // admitting the same row concurrently give two slots of one row (both flushed).
       const uint32_t same = __match_any_sync(pend, row);
       if (row < tab.capacity && (same & ((1u << lane) - 1u)) == 0 && *(volatile uint32_t*)&S.hot_n < kHotMax) {
         const uint32_t e = atomicAdd(&S.hot_n, 1u);
         if (e < kHotMax) {
           S.grow[e] = row;
-#pragma unroll
-          for (int q = 0; q < 7; q++) S.tupw[q][e] = key[q];
-          const uint32_t h = tuple_hash(key);
+          S.tup[e][0] = make_uint4(key[0], key[1], key[2], key[3]);
+          S.tup[e][1] = make_uint4(key[4], key[5], key[6], 0u);
           __threadfence_block();
-          uint32_t pos = h & (mk::HOT_IDX - 1);
-          while (atomicCAS(&S.tag[pos].y, 0u, e + 1) != 0u) pos = (pos + 1) & (mk::HOT_IDX - 1);
-          S.tag[pos].x = h;
+          mk::tag_insert(S, tuple_hash(key), e);
         }
       }
     }
@@ -713,17 +734,22 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     // every loaded word is consumed here, so the shared loads have completed
     asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
   };
-  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {
-    return S.tupw[0][e] == key[0] && S.tupw[1][e] == key[1] && S.tupw[2][e] == key[2] &&
-           S.tupw[3][e] == key[3] && S.tupw[4][e] == key[4] && S.tupw[5][e] == key[5] && S.tupw[6][e] == key[6];
+  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {  // branch-free: both loads in flight
+    const uint4 a = S.tup[e][0], b = S.tup[e][1];
+    return ((a.x ^ key[0]) | (a.y ^ key[1]) | (a.z ^ key[2]) | (a.w ^ key[3]) | (b.x ^ key[4]) |
+            (b.y ^ key[5]) | (b.z ^ key[6])) == 0u;
   };
-  // rest of a probe chain after a first tag that did not verify
-  auto probe_rest = [&](uint32_t pos, const Rec& R) -> int {
-    for (;;) {
-      pos = (pos + 1) & (mk::HOT_IDX - 1);
-      const uint2 tg = S.tag[pos];
-      if (tg.y == 0) return -1;
-      if (tg.x == R.hk && verify(tg.y - 1, R.key)) return (int)tg.y - 1;
+  // full lookup (rare: a full home bucket without the key, or a 20-bit tag collision)
+  auto probe_slow = [&](const Rec& R) -> int {
+    const uint32_t hb = mk::tag_bits(R.hk);
+    for (uint32_t q = R.hk & (mk::TAG_Q - 1);; q = (q + 1) & (mk::TAG_Q - 1)) {
+      const uint4 t = S.tagq[q];
+      const uint32_t v[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        if (v[i] == 0u) return -1;  // end of the filled prefix: absent
+        if ((v[i] ^ hb) < 0x800u && verify((v[i] & 0x7FFu) - 1, R.key)) return (int)(v[i] & 0x7FFu) - 1;
+      }
     }
   };
   auto update = [&](const Rec& R, int slot) {
@@ -813,16 +839,16 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         if (ja < my_tiles) issue(ja, fa);
         if (jb < my_tiles) issue(jb, fb);
       }
-      // first probe step of both launches together (tags, then speculative verification of the
-      // slots they name); the rare longer chains continue in probe_rest
-      const uint32_t pA = A.hk & (mk::HOT_IDX - 1), pB = B.hk & (mk::HOT_IDX - 1);
-      const uint2 tA = S.tag[pA], tB = S.tag[pB];
-      const uint32_t eA = tA.y ? tA.y - 1 : 0, eB = tB.y ? tB.y - 1 : 0;
-      const bool vA = tA.x == A.hk && verify(eA, A.key);
-      const bool vB = tB.x == B.hk && verify(eB, B.key);
+      // home buckets of both launches together (one 16-B load each), then speculative
+      // verification of the slot whose tag matches; a miss is final unless the bucket is full
+      const uint4 tA = S.tagq[A.hk & (mk::TAG_Q - 1)], tB = S.tagq[B.hk & (mk::TAG_Q - 1)];
+      const uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
+      const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
+      const bool vA = verify(eA, A.key) & (cA != 0u);
+      const bool vB = verify(eB, B.key) & (cB != 0u);
       int sA = -1, sB = -1;
-      if (A.valid && tA.y) sA = vA ? (int)eA : probe_rest(pA, A);
-      if (B.valid && tB.y) sB = vB ? (int)eB : probe_rest(pB, B);
+      if (A.valid) sA = vA ? (int)eA : ((cA | tA.w) ? probe_slow(A) : -1);
+      if (B.valid) sB = vB ? (int)eB : ((cB | tB.w) ? probe_slow(B) : -1);
       if (sA >= 0) update(A, sA);
       if (sB >= 0) update(B, sB);
       if (A.live && !A.valid) flag_record(st, A.gi);

@@ -33,7 +33,7 @@ def t_idx(n, k):
 
 def t_warps(w, k):
     def f(m, h):
-        m = sub(m, "constexpr int WARPS = 24;", f"constexpr int WARPS = {w};")
+        m = sub(m, "constexpr int WARPS = 20;", f"constexpr int WARPS = {w};")
         return m, sub(h, "constexpr uint32_t kHotMax = 640;", f"constexpr uint32_t kHotMax = {k};")
     return f
 
@@ -148,6 +148,8 @@ def t_noepoch(m, h):  # diagnostic only: no epoch flushes (16-bit counters may w
 
 
 VARIANTS = {
+    "w24": [t_warps(24, 640)],
+    "w16": [t_warps(16, 640)],
     "x_noepoch": [t_noepoch],
     "g_gionly": [t_gionly],
     "g_gionly_w28": [t_gionly, t_warps(28, 560)],
@@ -184,7 +186,7 @@ def build(names):
         objs = []
         for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
             o = os.path.join(d, f + ".o")
-            r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+            r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
                                 "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-c", os.path.join(src, CS, f),
                                 "-o", o], capture_output=True, text=True)
             if r.returncode:
