@@ -251,7 +251,7 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
       return FIKIT_E_CUDA;
     attr_set = true;
   }
-  // persistent: one CTA per SM, fewer if there are not enough 32-launch warp-tiles for all warps
+  // persistent: one CTA per SM, fewer if there are not enough 64-launch warp-tiles for all warps
   const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
   uint64_t ctas = (ntiles + measure_threads() / 32 - 1) / (measure_threads() / 32);
   unsigned grid = (unsigned)(ctas < (uint64_t)num_sms() ? ctas : (uint64_t)num_sms());

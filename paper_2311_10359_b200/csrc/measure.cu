@@ -399,23 +399,23 @@ __global__ void __launch_bounds__(1024) k_tile_scatter(const uint8_t* __restrict
 
 // ---- the fused identify + measure kernel ----------------------------------------------------
 namespace mk {
-constexpr int TILE = 32;                  // launches per warp-tile (one per lane)
+constexpr int TILE = 32;                  // launches per half-tile (one per lane)
+constexpr int CH = 2 * TILE;              // launches per warp-tile: one TMA, one wait, two per lane
+static_assert(CH == (int)kTileLaunches, "the schedule's tile is the kernel's warp-tile");
 constexpr int WARPS = 20;                 // warps per CTA; every warp streams and consumes its own tiles (<= 102 registers)
-constexpr int SPW = 2;                    // stages per warp: the tile being read + the next one in flight
-constexpr int NS = WARPS * SPW;           // ring stages
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
 constexpr uint32_t TAG_Q = 1024;          // tag buckets of 4 one-word tags (4096 tags, load <= 0.16)
 constexpr uint32_t TAG_HB = 0xFFFFF800u;  // tag = hash bits 11..31 (bit 31 forced to 1) | (slot + 1)
 static_assert(kHotMax < 2048, "slot + 1 must fit the 11 tag bits");
-constexpr int STAGE_BYTES = (TILE + 1) * 48;
-// per epoch a slot sees <= EPOCH_ROUNDS * TILE * WARPS launches: packed 16-bit bins and the
+constexpr int STAGE_BYTES = (CH + 1) * 48;  // the tile + the next launch (the tile's last gap)
+// per epoch a slot sees <= EPOCH_ROUNDS * CH * WARPS launches: packed 16-bit bins and the
 // 16-bit-split sum accumulators cannot overflow before the epoch flush
-constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);  // a round consumes SPW tiles per warp
+constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);  // a round consumes one tile per warp
 
 struct Smem {
-  uint4 ring[NS][STAGE_BYTES / 16];
-  uint64_t full[NS];
+  uint4 ring[WARPS][STAGE_BYTES / 16];  // one stage per warp (refilled as soon as it is read)
+  uint64_t full[WARPS];
   // Bucket q = hash % TAG_Q holds up to 4 tags, filled in order (the filled tags are a prefix);
   // a full bucket continues in the next one.  0 = empty.
   uint4 tagq[TAG_Q];
@@ -430,9 +430,9 @@ struct Smem {
 };
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
 static_assert(THREADS <= 1024, "a CTA has at most 1024 threads");
-// Each warp owns its SPW stages and is their only producer and consumer, so a stage's
-// mbarrier phase can never be waited on two uses ahead (no parity aliasing) and no slow
-// warp can stall another warp's prefetch.
+// Each warp owns its stage and is its only producer and consumer, so the stage's mbarrier
+// phase can never be waited on two uses ahead (no parity aliasing) and no slow warp can
+// stall another warp's prefetch.
 }  // namespace mk
 
 // fire-and-forget reductions (no return value, no dependent latency)
@@ -554,11 +554,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   const uint32_t s_full = sbase + (uint32_t)offsetof(mk::Smem, full);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint64_t ntiles = (n + mk::TILE - 1) / mk::TILE;
-
   if (tid == 0) {
     S.overlap = 0;
-    for (int i = 0; i < mk::NS; i++) mbar_init(&S.full[i], 1);
+    for (int i = 0; i < mk::WARPS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
   }
   // load the hot set of a task bucket into the shared dictionary, zero the statistics
@@ -600,13 +598,11 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   __syncthreads();
 
   // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  In a phase, warp w takes sorted
-  // positions ph_p0 + w + j * ph_step; its j-th tile there is the (kk0 + j)-th tile it streams
-  // in this launch, in stage (kk0 + j) % SPW.
+  // positions ph_p0 + w + j * ph_step; its j-th tile there is the (kk0 + j)-th tile its stage
+  // holds in this launch (mbarrier parity (kk0 + j) & 1).
   const uint32_t n32 = (uint32_t)n;
-  (void)ntiles;
   uint32_t ph_p0 = 0, ph_step = mk::WARPS, kk0 = 0, my_tiles = 0;
-  uint32_t sfirst0 = 0, sfirst1 = 0;  // (all lanes) first launch of the tile in stage 0 / 1
-  // 1-D TMA of this warp's j-th tile of the phase (+ the next launch, for the tile's last gap)
+  uint32_t sfirst = 0;  // (all lanes) first launch of the tile in the stage
   // the warp's upcoming tiles: lane l holds the tile of phase position jbase + l
   // (ordn: the window after it, loaded one window ahead so the refill never waits on L2)
   uint32_t ord = 0, ordn = 0, jbase = 0;
@@ -626,17 +622,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     ordn = ld_ord(jbase + 32 + lane);
   };
   auto tile_first = [&](uint32_t j) -> uint32_t {  // all lanes; task mode: j in [jbase, jbase + 32)
-    return (by_task ? __shfl_sync(0xffffffffu, ord, j - jbase) : ph_p0 + warp + j * ph_step) * mk::TILE;
+    return (by_task ? __shfl_sync(0xffffffffu, ord, j - jbase) : ph_p0 + warp + j * ph_step) * mk::CH;
   };
-  auto issue = [&](uint32_t j, uint32_t first) {
-    const uint32_t k = kk0 + j;
-    const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
-    const uint32_t cnt = min((uint32_t)mk::TILE + 1, n32 - first);
-    mbar_arrive_expect_tx(&S.full[sg], cnt * 48);
-    bulk_g2s(S.ring[sg], recs + first, cnt * 48, &S.full[sg]);
-  };
-  auto set_first = [&](uint32_t j, uint32_t first) {
-    if ((kk0 + j) % mk::SPW) sfirst1 = first; else sfirst0 = first;
+  // 1-D TMA of a tile (+ the next launch) into the warp's stage (lane 0)
+  auto issue = [&](uint32_t first) {
+    const uint32_t cnt = min((uint32_t)mk::CH + 1, n32 - first);
+    mbar_arrive_expect_tx(&S.full[warp], cnt * 48);
+    bulk_g2s(S.ring[warp], recs + first, cnt * 48, &S.full[warp]);
   };
 
   // ---------------- consumers ----------------
@@ -685,16 +677,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     uint64_t d, g;
     bool valid, gap, live;
   };
-  // wait for warp-tile k (stage k % SPW), read this lane's launch and the next launch's
-  // start/run/task (lane + 1 by shuffle; lane 31 from the stage's extra record; the halo
-  // after the last launch), validate, and compute K, G and the identity hash
-  auto load_tile = [&](uint32_t j, Rec& R) {
-    const uint32_t k = kk0 + j;
-    const uint32_t sg = warp * mk::SPW + (k % mk::SPW);
-    mbar_wait_s(s_full + 8u * sg, (k / mk::SPW) & 1u);
-    const uint32_t first = (k % mk::SPW) ? sfirst1 : sfirst0;
-    const uint32_t cnt = min((uint32_t)mk::TILE, n32 - first);
-    const uint4* rp = S.ring[sg] + lane * 3;
+  // read this lane's launch of half h of the stage's tile and the next launch's start/run/task
+  // (lane + 1 by shuffle; lane 31 from the record after the half; the halo after the last
+  // launch), validate, and compute K, G and the identity hash
+  auto load_half = [&](int h, Rec& R) {
+    const uint32_t first = sfirst + h * mk::TILE;
+    const uint32_t cnt = n32 > first ? min((uint32_t)mk::TILE, n32 - first) : 0u;
+    const uint4* rp = S.ring[warp] + (h * mk::TILE + lane) * 3;
     R.live = (uint32_t)lane < cnt;
     uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
     if (R.live) {
@@ -806,38 +795,33 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     ph_step = pg * mk::WARPS;               // positions between a warp's consecutive tiles
     const uint32_t span = P.p1 > ph_p0 ? P.p1 - ph_p0 : 0;
     my_tiles = span > (uint32_t)warp ? (span - warp + ph_step - 1) / ph_step : 0;
-    const uint32_t rounds = span ? (span + ph_step - 1) / ph_step : 0;  // warp 0 has the most
+    const uint32_t rounds = span ? (span + ph_step - 1) / ph_step : 0;  // CTA-uniform: warp 0 has the most
     if (by_task) load_window(0);
     {
-      const uint32_t f0 = tile_first(0), f1 = tile_first(1);
-      set_first(0, f0);
-      set_first(1, f1);
-      if (lane == 0) {
-        if (my_tiles > 0) issue(0, f0);
-        if (my_tiles > 1) issue(1, f1);
-      }
+      const uint32_t f0 = tile_first(0);
+      sfirst = f0;
+      if (lane == 0 && my_tiles > 0) issue(f0);
     }
-    // Each round consumes the warp's two stages (warp-tiles 2r and 2r+1): both records are read
-    // and both stages refilled before either is processed, and the two identity probes are
-    // interleaved (two independent dependency chains per lane).
-    const uint32_t rounds2 = (rounds + mk::SPW - 1) / mk::SPW;  // CTA-uniform (warp 0 has the most tiles)
-    for (uint32_t r = 0; r < rounds2; r++) {
-      const uint32_t kA = r * mk::SPW, kB = kA + 1;
+    // Each round reads the warp's tile (both halves, A and B) into registers, refills the stage
+    // with the next tile, then processes A and B with their identity probes interleaved (two
+    // independent dependency chains per lane).
+    for (uint32_t r = 0; r < rounds; r++) {
       Rec A, B;
       A.live = B.live = A.valid = B.valid = false;
-      if (kA < my_tiles) load_tile(kA, A);
-      if (kB < my_tiles) load_tile(kB, B);
+      if (r < my_tiles) {
+        mbar_wait_s(s_full + 8u * warp, (kk0 + r) & 1u);
+        load_half(0, A);
+        load_half(1, B);
+      }
       // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      const uint32_t ja = kA + mk::SPW, jb = kB + mk::SPW;  // ja even: both in one 32-window
-      if (by_task && ja >= jbase + 32) next_window();
-      const uint32_t fa = tile_first(ja), fb = tile_first(jb);
-      set_first(ja, fa);
-      set_first(jb, fb);
-      if (lane == 0) {
-        if (ja < my_tiles) issue(ja, fa);
-        if (jb < my_tiles) issue(jb, fb);
+      const uint32_t jn = r + 1;
+      if (by_task && jn >= jbase + 32) next_window();
+      const uint32_t fn = tile_first(jn);
+      if (jn < my_tiles) {
+        sfirst = fn;
+        if (lane == 0) issue(fn);
       }
       // home buckets of both launches together (one 16-B load each), then speculative
       // verification of the slot whose tag matches; a miss is final unless the bucket is full
@@ -855,7 +839,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       if (B.live && !B.valid) flag_record(st, B.gi);
       compact(A, A.valid && sA < 0);
       compact(B, B.valid && sB < 0);
-      if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds2) {  // 16-bit accumulators: flush before overflow
+      if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit accumulators: flush before overflow
         consumer_sync();
         flush_epoch(S, tab, tid);
         consumer_sync();
