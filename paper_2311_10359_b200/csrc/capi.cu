@@ -49,6 +49,9 @@ __global__ void k_fill(fikit_table_t, const uint64_t*, const uint64_t*, const ui
 __global__ void k_simulate(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
                            const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
                            fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
+__global__ void k_simulate_reg(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
+                           const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
+                           fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
 }  // namespace fikit
 
 using namespace fikit;
@@ -352,6 +355,13 @@ int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* dea
   return launched();
 }
 
+// persistent grid: blocks of one full wave of the kernel at its occupancy
+static int one_wave(const void* kernel, int threads) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  return occ * num_sms();
+}
+
 int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
                          const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
                          const uint8_t* lp_level, const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t prm,
@@ -363,8 +373,22 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
   if (int r = get_ws(ws, ws_bytes, 1, 0, 0, &w)) return r;
   if (int r = reset_status(w, s)) return r;
   if (S == 0) return FIKIT_OK;
-  k_simulate<<<grid_for(S, 4, num_sms() * 16), 128, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
-                                                             sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
+  // pass 1: register-pool scenarios (m <= 64); pass 2: the ones it deferred (shared-memory pool).
+  // Both persistent: one wave of the kernel's occupancy.
+  static int g1 = 0, g2 = 0;
+  if (!g1) {
+    g1 = one_wave((const void*)k_simulate_reg, kRegThreads);
+    g2 = one_wave((const void*)k_simulate, kSimThreads);
+  }
+  const uint64_t n1 = ((uint64_t)S + kRegThreads / 32 - 1) / (kRegThreads / 32);
+  const uint64_t n2 = ((uint64_t)S + kSimThreads / 32 - 1) / (kSimThreads / 32);
+  const int b1 = (int)(n1 < (uint64_t)g1 ? n1 : (uint64_t)g1);
+  const int b2 = (int)(n2 < (uint64_t)g2 ? n2 : (uint64_t)g2);
+  k_simulate_reg<<<b1, kRegThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out, fill_gap,
+                                    lp_start, sched_off, w.st());
+  if (int r = launched()) return r;
+  k_simulate<<<b2, kSimThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out, fill_gap,
+                                lp_start, sched_off, w.st());
   return launched();
 }
 

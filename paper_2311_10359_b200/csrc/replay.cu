@@ -13,7 +13,7 @@
 
 namespace fikit {
 
-constexpr int kReplayWarps = 4;      // warps (scenarios) per CTA
+constexpr int kReplayWarps = kSimThreads / 32;  // warps (scenarios) per CTA
 constexpr uint32_t kPoolMax = 1024;  // LP requests per scenario held in shared memory
 constexpr uint8_t kAlive = 0x10, kElig = 0x20;
 
@@ -247,6 +247,340 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
 }
 
 // ---- fikit_simulate_batch: one warp per scenario ------------------------------------------------
+// Digest terms are batched: lane (n % 32) keeps the n-th fill's (k, gap, start) and every 32
+// fills the warp evaluates 32 terms in one SIMT pass (the digest is a sum: order-free).
+struct DigestBatch {
+  uint32_t n = 0, k = 0;
+  int32_t fg = 0;
+  uint64_t start = 0, sum = 0;
+  __device__ __forceinline__ void add(uint32_t kk, int32_t g, uint64_t t, int lane) {
+    if (lane == (int)(n & 31u)) {
+      k = kk;
+      fg = g;
+      start = t;
+    }
+    if ((++n & 31u) == 0) sum += digest_term(k, fg, start);
+  }
+  __device__ __forceinline__ void drain(int lane) {
+    if (lane < (int)(n & 31u)) sum += digest_term(k, fg, start);
+  }
+};
+
+// LP pool of at most 64 requests in registers: lane l holds sorted positions l and 32 + l
+// (key order = BestPrioFit's preference order, as in make_sorted_pool), and, by request index,
+// the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^50.
+struct RegPool {
+  uint64_t q0, q1;    // predicted duration at sorted positions lane, 32 + lane
+  uint32_t k0, k1;    // request index there
+  bool a0, a1;        // alive and eligible there
+  uint64_t dur0, dur1;  // LP duration of requests lane, 32 + lane
+  uint32_t lvl0, lvl1;  // level of requests lane, 32 + lane
+  uint64_t alive;     // alive requests by index (warp-uniform)
+
+  __device__ __forceinline__ uint64_t min_q() const {
+    uint64_t mn = min(a0 ? q0 : ~0ull, a1 ? q1 : ~0ull);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    return mn;
+  }
+  // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
+  __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
+    uint32_t b = __ballot_sync(0xffffffffu, a0 && q0 <= R);
+    const bool hi = b == 0;
+    if (hi) b = __ballot_sync(0xffffffffu, a1 && q1 <= R);
+    if (!b) return -1;
+    const int src = __ffs(b) - 1;
+    const int kk = (int)__shfl_sync(0xffffffffu, hi ? k1 : k0, src);
+    qk = __shfl_sync(0xffffffffu, hi ? q1 : q0, src);
+    if (lane == src) {
+      if (hi) a1 = false; else a0 = false;
+    }
+    alive &= ~(1ull << kk);
+    return kk;
+  }
+  __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const {
+    const uint64_t d0 = __shfl_sync(0xffffffffu, dur0, kk & 31u), d1 = __shfl_sync(0xffffffffu, dur1, kk & 31u);
+    return kk < 32 ? d0 : d1;
+  }
+};
+
+// register bitonic sort of 64 keys (lane holds positions lane (e0) and 32 + lane (e1)), ascending
+__device__ __forceinline__ void reg_bitonic64(uint64_t& e0, uint64_t& e1, int lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {  // partner in the same lane (k == 64: ascending)
+        const uint64_t lo = min(e0, e1), hi = max(e0, e1);
+        e0 = lo;
+        e1 = hi;
+      } else {
+        const uint64_t o0 = __shfl_xor_sync(0xffffffffu, e0, j), o1 = __shfl_xor_sync(0xffffffffu, e1, j);
+        const bool lower = ((uint32_t)lane & j) == 0;
+        const bool asc0 = ((uint32_t)lane & k) == 0, asc1 = ((32u + (uint32_t)lane) & k) == 0;
+        e0 = (asc0 == lower) ? min(e0, o0) : max(e0, o0);
+        e1 = (asc1 == lower) ? min(e1, o1) : max(e1, o1);
+      }
+    }
+  }
+}
+
+// load and sort a pool of m <= 64 requests into registers.  Returns 0 ok, 1 invalid level
+// (flagged), 2 fast path not applicable (some eligible q >= 2^50).
+__device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t K, const uint32_t* __restrict__ row,
+                                             const uint8_t* __restrict__ level, const uint64_t* __restrict__ dur,
+                                             uint64_t off, uint32_t m, int lane, fikit_status_t* st, RegPool& P) {
+  bool ok = true, fits = true;
+  auto one = [&](uint32_t kk, uint64_t& key, uint64_t& d, uint32_t& lv) {
+    key = ~0ull;
+    d = 0;
+    lv = 0;
+    if (kk < m) {
+      const uint32_t r = __ldg(row + off + kk);
+      const uint32_t L = __ldg(level + off + kk);
+      d = __ldg(dur + off + kk);
+      lv = L;
+      if (L < 1 || L > 9) {
+        flag_record(st, off + kk);
+        ok = false;
+      }
+      const bool el = r < K && __ldg(tab.sums + (size_t)r * 4) > 0;  // R16: no SK profile -> never a fill
+      if (el) {
+        const uint64_t q = __ldg(tab.mean + (size_t)r * 2);  // SK of the request's ID
+        if (q > kQ50) fits = false;
+        key = ((uint64_t)(L & 0xF) << 60) | ((kQ50 - (q & kQ50)) << 10) | kk;
+      }
+    }
+  };
+  uint64_t e0, e1;
+  one((uint32_t)lane, e0, P.dur0, P.lvl0);
+  one(32u + (uint32_t)lane, e1, P.dur1, P.lvl1);
+  if (!__all_sync(0xffffffffu, ok)) return 1;
+  if (!__all_sync(0xffffffffu, fits)) return 2;
+  reg_bitonic64(e0, e1, lane);
+  P.a0 = e0 != ~0ull;
+  P.a1 = e1 != ~0ull;
+  P.q0 = key_q(e0);
+  P.q1 = key_q(e1);
+  P.k0 = (uint32_t)(e0 & 1023u);
+  P.k1 = (uint32_t)(e1 & 1023u);
+  P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
+  return 0;
+}
+
+// shared-memory pool (any m <= kPoolMax): the sorted fast path or the full argmin
+struct SmemPool {
+  uint64_t* q;
+  uint8_t* meta;
+  const uint64_t* dur;  // lp_dur + lp_off
+  uint32_t m, A, nch;
+  bool fast;
+  __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, A, nch, lane); }
+  __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
+    return pool_pick(fast, q, meta, m, A, nch, R, lane, qk);
+  }
+  __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const { return __ldg(dur + kk); }
+};
+
+struct HpOut {
+  uint64_t t, hp_delay, fill_work, lp_end;
+  uint32_t n_fills;
+};
+
+// The HP template with gap filling (Alg. 1 + Alg. 2 + feedback, Case B).  t = start of the next
+// HP kernel.  Without a fill, kernel i+1 starts at T_i + d_i + a'_i; only gaps whose gate can
+// open (p >= tau, p >= qmin, and with feedback a' > 0) need the serial Alg. 1 loop, so each
+// chunk of 32 HP kernels is advanced by a prefix sum and visits just its open gates.  The next
+// chunk's inputs are loaded while this one is processed.
+template <class Pool, class MinQ>
+__device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_table_t& tab, uint32_t K,
+                                           const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
+                                           const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
+                                           const fikit_fill_params_t& prm, bool sched, int32_t* fill_gap,
+                                           uint64_t* lp_start, uint64_t so, DigestBatch& dig, int lane) {
+  const uint32_t nh = c.hp_len;
+  const uint64_t scale = c.gap_scale_q16;
+  uint64_t qmin = min_q();
+  HpOut o{0, 0, 0, 0, 0};
+  uint64_t t = 0;
+  // chunk inputs: d, raw gap, row of HP kernel base + lane (next chunk prefetched)
+  auto ld = [&](uint32_t base, uint64_t& d, uint64_t& g, uint32_t& r) {
+    const uint32_t i = base + lane;
+    d = 0;
+    g = 0;
+    r = 0xFFFFFFFFu;
+    if (i < nh) {
+      d = __ldg(hp_dur + c.hp_off + i);
+      g = i + 1 < nh ? __ldg(hp_gap + c.hp_off + i) : 0;  // no gap after the last kernel
+      r = __ldg(hp_row + c.hp_off + i);
+    }
+  };
+  uint64_t dn, gn;
+  uint32_t rn;
+  ld(0, dn, gn, rn);
+  for (uint32_t base = 0; base < nh; base += 32) {
+    const uint32_t i_l = base + lane;
+    const bool valid = i_l < nh, last = i_l == nh - 1;
+    const uint64_t d_l = dn;
+    const uint64_t a_l = (gn * scale) >> 16;  // R24
+    const uint32_t r_l = rn;
+    const uint64_t p_l = (valid && r_l < K) ? ((__ldg(tab.mean + (size_t)r_l * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
+    if (base + 32 < nh) ld(base + 32, dn, gn, rn);
+    const uint64_t x_l = d_l + a_l;
+    uint64_t X = x_l;  // inclusive prefix over the chunk
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
+      if (lane >= dd) X += y;
+    }
+    const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= qmin && (!prm.feedback || a_l > 0);
+    uint32_t gmask = __ballot_sync(0xffffffffu, gate);
+    const uint64_t T0 = t;
+    uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
+    while (gmask) {
+      const int j = __ffs(gmask) - 1;
+      gmask &= gmask - 1;
+      const uint32_t i = base + j;
+      const uint64_t Xj = __shfl_sync(0xffffffffu, X, j);
+      const uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
+      const uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
+      if (p < qmin) continue;  // the pool has shrunk since the gate was computed
+      t = T0 + shift + Xj - a;  // end of HP kernel i
+      const uint64_t r = t + a;   // the HP client's next launch arrives (R20)
+      uint64_t R = p;
+      for (;;) {
+        if (prm.feedback && t >= r) break;
+        if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
+        uint64_t qk;
+        const int k = P.pick(R, lane, qk);  // Alg. 2
+        if (k < 0) break;
+        const uint64_t e = P.dur_of((uint32_t)k);
+        if (sched && lane == 0) {
+          fill_gap[so + k] = (int32_t)i;
+          lp_start[so + k] = t;
+        }
+        dig.add((uint32_t)k, (int32_t)i, t, lane);
+        R -= qk;
+        t += e;
+        if (qk == qmin) qmin = min_q();
+        o.fill_work += e;
+        o.n_fills++;
+        o.lp_end = max(o.lp_end, t);
+      }
+      if (t > r) {  // overhead 2: kernel i+1 starts at max(t, r_{i+1})
+        o.hp_delay += t - r;
+        shift += t - r;
+      }
+    }
+    t = T0 + shift + __shfl_sync(0xffffffffu, X, 31);  // next kernel's start (or the HP end)
+  }
+  o.t = t;
+  return o;
+}
+
+// tail (R22): the requests still queued run after the HP end in Q1..Q9 order, FIFO within a
+// queue; sel(k) / dur(k) / level presence come from the pool representation
+template <class Sel, class Dur>
+__device__ __forceinline__ uint64_t replay_tail(uint64_t t, uint32_t m, uint32_t levels, Sel sel_of, Dur dur_of,
+                                                bool sched, int32_t* fill_gap, uint64_t* lp_start, uint64_t so,
+                                                uint64_t& dig, uint32_t& n_tail, int lane) {
+  while (levels) {
+    const uint32_t L = __ffs(levels) - 1;
+    levels &= levels - 1;
+    for (uint32_t b = 0; b < m; b += 32) {
+      const uint32_t k = b + lane;
+      const bool sel = k < m && sel_of(k, L);
+      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      if (!bal) continue;
+      const uint64_t e = sel ? dur_of(k) : 0;
+      uint64_t x = e;  // inclusive scan
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, dd);
+        if (lane >= dd) x += y;
+      }
+      if (sel) {
+        const uint64_t start = t + x - e;
+        if (sched) {
+          fill_gap[so + k] = -1;
+          lp_start[so + k] = start;
+        }
+        dig += digest_term(k, -1, start);
+      }
+      t += __shfl_sync(0xffffffffu, x, 31);
+      n_tail += __popc(bal);
+    }
+  }
+  return t;
+}
+
+__device__ __forceinline__ void write_result(fikit_result_t* out, uint32_t s, const HpOut& o, uint64_t t_end,
+                                             uint32_t m, uint32_t n_tail, DigestBatch& db, uint64_t tail_dig,
+                                             int lane) {
+  uint64_t lp_end = o.lp_end;
+  if (n_tail) lp_end = max(lp_end, t_end);
+  db.drain(lane);
+  uint64_t dig = db.sum + tail_dig;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, off);
+  if (lane == 0) {
+    fikit_result_t r;
+    r.hp_jct = o.t;
+    r.lp_jct = m ? lp_end : 0;
+    r.hp_delay = o.hp_delay;
+    r.fill_work = o.fill_work;
+    r.digest = dig;
+    r.n_fills = o.n_fills;
+    r.n_tail = n_tail;
+    out[s] = r;
+  }
+}
+
+// Pass 1 (no shared memory, so only registers bound its occupancy): every scenario with m <= 64
+// and all q < 2^50 runs on the register pool; any other scenario is marked deferred
+// (n_tail = kDeferred) for pass 2.  Persistent grid, one warp per scenario.
+constexpr uint32_t kDeferred = 0xFFFFFFFFu;
+constexpr int kRegWarps = kRegThreads / 32;
+
+__global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps per SM
+    k_simulate_reg(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
+                   const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
+                   const uint64_t* __restrict__ lp_dur, const uint8_t* __restrict__ lp_level,
+                   const fikit_scenario_t* __restrict__ sc, uint32_t S, fikit_fill_params_t prm,
+                   fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap, uint64_t* __restrict__ lp_start,
+                   const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t K = min(*tab.n_rows, tab.capacity);
+  const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
+  for (uint32_t s = blockIdx.x * kRegWarps + w; s < S; s += gridDim.x * kRegWarps) {
+    const fikit_scenario_t c = sc[s];
+    const uint32_t m = c.lp_len;
+    RegPool P;
+    const int rc = m <= 64 ? load_reg_pool(tab, K, lp_row, lp_level, lp_dur, c.lp_off, m, lane, st, P) : 2;
+    if (rc != 0) {  // invalid level (flagged; pass 2 flags it again) or not for this pass
+      if (lane == 0) out[s].n_tail = kDeferred;
+      continue;
+    }
+    const uint64_t so = sched ? sched_off[s] : 0;
+    DigestBatch db;
+    const HpOut o = replay_hp(P, [&]() { return P.min_q(); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
+                              fill_gap, lp_start, so, db, lane);
+    uint32_t lv = 0;  // levels still queued
+    if ((P.alive >> lane) & 1ull) lv |= 1u << P.lvl0;
+    if ((P.alive >> (32 + lane)) & 1ull) lv |= 1u << P.lvl1;
+    lv = __reduce_or_sync(0xffffffffu, lv);
+    uint64_t tail_dig = 0;
+    uint32_t n_tail = 0;
+    const uint64_t t = replay_tail(
+        o.t, m, lv,
+        [&](uint32_t k, uint32_t L) { return ((P.alive >> k) & 1ull) && (k < 32 ? P.lvl0 : P.lvl1) == L; },
+        [&](uint32_t k) { return k < 32 ? P.dur0 : P.dur1; }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
+        lane);
+    write_result(out, s, o, t, m, n_tail, db, tail_dig, lane);
+  }
+}
+
+// Pass 2: the deferred scenarios, pool in shared memory (sorted fast path or full argmin).
 __global__ void __launch_bounds__(kReplayWarps * 32)
     k_simulate(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
@@ -260,128 +594,34 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
   const uint32_t K = min(*tab.n_rows, tab.capacity);
   const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
   for (uint32_t s = blockIdx.x * kReplayWarps + w; s < S; s += gridDim.x * kReplayWarps) {
-    fikit_scenario_t c = sc[s];
-    uint32_t m = c.lp_len, nh = c.hp_len;
-    uint64_t* q = s_q[w];
-    uint8_t* meta = s_meta[w];
+    if (out[s].n_tail != kDeferred) continue;  // done in pass 1
+    const fikit_scenario_t c = sc[s];
+    const uint32_t m = c.lp_len;
     __syncwarp();
     if (m > kPoolMax) {
       if (lane == 0) atomicOr(&st->flags, kStatusArg);
       continue;
     }
+    uint64_t* q = s_q[w];
+    uint8_t* meta = s_meta[w];
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
-    const uint64_t scale = c.gap_scale_q16;
-    uint32_t A = 0, nch = 0;
-    const bool fast = make_sorted_pool(q, meta, m, lane, A, nch);
-    uint64_t qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
-    uint64_t t = 0, hp_delay = 0, fill_work = 0, lp_end = 0, dig = 0;
-    uint32_t n_fills = 0;
-    // t = start of the next HP kernel.  Without a fill, kernel i+1 starts at
-    // T_i + d_i + a'_i; only gaps whose gate can open (p >= tau, p >= qmin, and
-    // with feedback a' > 0) need the serial Alg. 1 loop, so each chunk of 32 HP
-    // kernels is advanced by a prefix sum and visits just its open gates.
-    for (uint32_t base = 0; base < nh; base += 32) {
-      uint32_t i_l = base + lane;
-      uint64_t d_l = 0, a_l = 0, p_l = 0;
-      bool valid = i_l < nh, last = i_l == nh - 1;
-      if (valid) {
-        d_l = __ldg(hp_dur + c.hp_off + i_l);
-        a_l = last ? 0 : (__ldg(hp_gap + c.hp_off + i_l) * scale) >> 16;  // R24; no gap after the last
-        uint32_t r = __ldg(hp_row + c.hp_off + i_l);
-        p_l = r < K ? ((__ldg(tab.mean + (size_t)r * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
-      }
-      const uint64_t x_l = d_l + a_l;
-      uint64_t X = x_l;  // inclusive prefix over the chunk
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
-        if (lane >= dd) X += y;
-      }
-      const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= qmin && (!prm.feedback || a_l > 0);
-      uint32_t gmask = __ballot_sync(0xffffffffu, gate);
-      const uint64_t T0 = t;
-      uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
-      while (gmask) {
-        const int j = __ffs(gmask) - 1;
-        gmask &= gmask - 1;
-        const uint32_t i = base + j;
-        const uint64_t Xj = __shfl_sync(0xffffffffu, X, j);
-        const uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
-        const uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
-        t = T0 + shift + Xj - a;  // end of HP kernel i
-        const uint64_t r = t + a;   // the HP client's next launch arrives (R20)
-        uint64_t R = p;
-        for (;;) {
-          if (prm.feedback && t >= r) break;
-          if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
-          uint64_t qk;
-          const int k = pool_pick(fast, q, meta, m, A, nch, R, lane, qk);  // Alg. 2
-          if (k < 0) break;
-          const uint64_t e = __ldg(lp_dur + c.lp_off + k);
-          if (lane == 0) {
-            if (sched) {
-              fill_gap[so + k] = (int32_t)i;
-              lp_start[so + k] = t;
-            }
-            dig += digest_term((uint32_t)k, (int32_t)i, t);
-          }
-          R -= qk;
-          t += e;
-          if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
-          fill_work += e;
-          n_fills++;
-          lp_end = max(lp_end, t);
-        }
-        if (t > r) {  // overhead 2: kernel i+1 starts at max(t, r_{i+1})
-          hp_delay += t - r;
-          shift += t - r;
-        }
-      }
-      t = T0 + shift + __shfl_sync(0xffffffffu, X, 31);  // next kernel's start (or the HP end)
-    }
-    const uint64_t hp_jct = t;
-    // tail: remaining requests in Q1..Q9 order, FIFO within a queue (R22)
+    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false};
+    P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch);
+    DigestBatch db;
+    const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
+                              fill_gap, lp_start, so, db, lane);
+    uint32_t lv = 0;
+    for (uint32_t k = lane; k < m; k += 32)
+      if (meta[k] & kAlive) lv |= 1u << (meta[k] & 0xF);
+    lv = __reduce_or_sync(0xffffffffu, lv);
+    uint64_t tail_dig = 0;
     uint32_t n_tail = 0;
-    for (uint32_t L = 1; L <= 9; L++) {
-      for (uint32_t b = 0; b < m; b += 32) {
-        uint32_t k = b + lane;
-        bool sel = k < m && (meta[k] & kAlive) && (meta[k] & 0xF) == L;
-        uint32_t bal = __ballot_sync(0xffffffffu, sel);
-        if (!bal) continue;
-        uint64_t e = sel ? __ldg(lp_dur + c.lp_off + k) : 0;
-        uint64_t x = e;  // inclusive scan
-#pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-          uint64_t y = __shfl_up_sync(0xffffffffu, x, dd);
-          if (lane >= dd) x += y;
-        }
-        if (sel) {
-          uint64_t start = t + x - e;
-          if (sched) {
-            fill_gap[so + k] = -1;
-            lp_start[so + k] = start;
-          }
-          dig += digest_term(k, -1, start);
-        }
-        t += __shfl_sync(0xffffffffu, x, 31);
-        n_tail += __popc(bal);
-      }
-    }
-    if (n_tail) lp_end = max(lp_end, t);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, off);
-    if (lane == 0) {
-      fikit_result_t o;
-      o.hp_jct = hp_jct;
-      o.lp_jct = m ? lp_end : 0;
-      o.hp_delay = hp_delay;
-      o.fill_work = fill_work;
-      o.digest = dig;
-      o.n_fills = n_fills;
-      o.n_tail = n_tail;
-      out[s] = o;
-    }
+    const uint64_t t = replay_tail(
+        o.t, m, lv, [&](uint32_t k, uint32_t L) { return (meta[k] & kAlive) && (meta[k] & 0xF) == L; },
+        [&](uint32_t k) { return __ldg(lp_dur + c.lp_off + k); }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
+        lane);
+    write_result(out, s, o, t, m, n_tail, db, tail_dig, lane);
   }
 }
 

@@ -1,0 +1,134 @@
+"""A/B timing of fikit_simulate_batch across replay.cu variants in ONE process on one GPU.
+
+  python scripts/ab_replay.py build           (here, CPU: abtest_replay/<name>/libfikit.so from the working tree)
+  python scripts/ab_replay.py run [--records N] [--scenarios S]   (on the GPU)
+
+The table and resolved inputs come from the in-tree library (zipf trace + zipf replay, as in
+bench.py); every variant replays the same device inputs and its results are compared bytewise
+with the in-tree library's.
+"""
+import ctypes as C
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+AB = os.path.join(ROOT, "abtest_replay")
+CS = "paper_2311_10359_b200/csrc/"
+sys.path.insert(0, ROOT)
+
+
+def sub(txt, old, new):
+    assert old in txt, old[:80]
+    return txt.replace(old, new)
+
+
+def reg_cfg(warps, minb):
+    def f(r, h):
+        h = sub(h, "constexpr int kRegThreads = 256;", f"constexpr int kRegThreads = {warps * 32};")
+        if minb:
+            r = sub(r, "__global__ void __launch_bounds__(kRegWarps * 32)\n",
+                    f"__global__ void __launch_bounds__(kRegWarps * 32, {minb})\n")
+        return r, h
+    return f
+
+
+VARIANTS = {
+    "base": [],
+    "w8b3": [reg_cfg(8, 3)],
+    "w4b6": [reg_cfg(4, 6)],
+    "w4": [reg_cfg(4, 0)],
+}
+
+
+def build(names):
+    os.makedirs(AB, exist_ok=True)
+    for name in names:
+        d = os.path.join(AB, name)
+        src = os.path.join(d, "src")
+        os.makedirs(os.path.join(src, CS), exist_ok=True)
+        os.makedirs(os.path.join(src, "include"), exist_ok=True)
+        for f in ("measure.cu", "finalize.cu", "capi.cu"):
+            shutil.copy(os.path.join(ROOT, CS, f), os.path.join(src, CS, f))
+        shutil.copy(os.path.join(ROOT, "include/fikit.h"), os.path.join(src, "include/fikit.h"))
+        r = open(os.path.join(ROOT, CS, "replay.cu")).read()
+        h = open(os.path.join(ROOT, CS, "fikit_internal.cuh")).read()
+        for t in VARIANTS[name]:
+            r, h = t(r, h)
+        open(os.path.join(src, CS, "replay.cu"), "w").write(r)
+        open(os.path.join(src, CS, "fikit_internal.cuh"), "w").write(h)
+        objs = []
+        for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
+            o = os.path.join(d, f + ".o")
+            res = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                                  "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-c",
+                                  os.path.join(src, CS, f), "-o", o], capture_output=True, text=True)
+            if res.returncode:
+                print(name, "FAILED", res.stderr[-2000:])
+                raise SystemExit(1)
+            if f == "replay.cu":
+                lines = res.stderr.splitlines()
+                info = []
+                for k, ln in enumerate(lines):
+                    if "Compiling" in ln and "k_simulate" in ln:
+                        info += [x.strip() for x in lines[k:k + 4] if "registers" in x or "spill" in x]
+                print(name, info)
+            objs.append(o)
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                               "-o", os.path.join(d, "libfikit.so"), *objs])
+
+
+def run(records, S):
+    import torch
+
+    import fikit_synth as F
+    import paper_2311_10359_b200 as fk
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.zipf_trace(n_runs=max(1, records // 256))
+    rp = F.zipf_replay(cfg, S=S)
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=8192, replay=rp)
+    p.step()
+    torch.cuda.synchronize()
+    r = p.replay
+    ref = r["out"].clone()
+    ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for name in sorted(os.listdir(AB)):
+        path = os.path.join(AB, name, "libfikit.so")
+        if not os.path.exists(path):
+            continue
+        L = C.CDLL(path)
+        L.fikit_simulate_batch.argtypes = [C.POINTER(fk.TableC)] + [C.c_void_p] * 7 + [C.c_uint32, fk.FillParamsC] + \
+            [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
+        prm = fk.FillParamsC(r["threshold_ns"], r["feedback"], 0)
+        out = torch.zeros_like(ref)
+        call = lambda: L.fikit_simulate_batch(C.byref(p.table.c), ptr(r["hp_row"]), ptr(r["hp_dur"]),
+                                              ptr(r["hp_gap"]), ptr(r["lp_row"]), ptr(r["lp_dur"]),
+                                              ptr(r["lp_level"]), ptr(r["sc"]), r["S"], prm, ptr(out), None, None,
+                                              None, p.ws.ptr(), p.ws.nbytes, stream)
+        for _ in range(3):
+            rc = call()
+        torch.cuda.synchronize()
+        same = bool(torch.equal(out, ref))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = []
+        for _ in range(5):
+            e0.record()
+            for _ in range(10):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 10)
+        print(name, json.dumps({"ms": min(times), "rc": rc, "same_as_intree": same}), flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2:] or list(VARIANTS))
+    else:
+        rec = int(sys.argv[sys.argv.index("--records") + 1]) if "--records" in sys.argv else 4_000_000
+        S = int(sys.argv[sys.argv.index("--scenarios") + 1]) if "--scenarios" in sys.argv else 100_000
+        run(rec, S)
