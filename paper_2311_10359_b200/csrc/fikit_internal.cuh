@@ -42,9 +42,11 @@ constexpr uint32_t kCovTask = kBuckets + 1;  // samples whose row is in its task
 constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the global hot set
 constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
 constexpr uint32_t kHotHdr = kBuckets + 8;
-constexpr uint32_t kTileLaunches = 64;
+constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
 constexpr int kRegThreads = 256;  // k_simulate_reg block (8 warps, one scenario each)
-constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)  // launches per warp-tile of the measure kernel (one TMA)
+constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
+// u32 words of the 256-B status region past fikit_status_t, zeroed with it: replay work counters
+constexpr uint32_t kSchedWord1 = 32, kSchedWord2 = 33;
 struct Phase {
   // sorted-tile range [p0, p1) (one bucket's tiles), swept by g CTAs of which this is number c:
   // warp w of this CTA takes positions p0 + c * WARPS + w + j * g * WARPS

@@ -29,6 +29,8 @@ __global__ void k_reset_status(fikit_status_t* st) {
     st->n_overlap_gaps = 0;
     st->schedule = 0;
     st->n_task_buckets = 0;
+    reinterpret_cast<uint32_t*>(st)[kSchedWord1] = 0;
+    reinterpret_cast<uint32_t*>(st)[kSchedWord2] = 0;
   }
 }
 

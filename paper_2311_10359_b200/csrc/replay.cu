@@ -538,7 +538,9 @@ __device__ __forceinline__ void write_result(fikit_result_t* out, uint32_t s, co
 
 // Pass 1 (no shared memory, so only registers bound its occupancy): every scenario with m <= 64
 // and all q < 2^50 runs on the register pool; any other scenario is marked deferred
-// (n_tail = kDeferred) for pass 2.  Persistent grid, one warp per scenario.
+// (n_tail = kDeferred) for pass 2.  Persistent grid, one warp per scenario; scenarios are
+// claimed from a counter (the next claim is in flight while one runs), so uneven scenario costs
+// do not strand warps.
 constexpr uint32_t kDeferred = 0xFFFFFFFFu;
 constexpr int kRegWarps = kRegThreads / 32;
 
@@ -552,7 +554,12 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
   const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
-  for (uint32_t s = blockIdx.x * kRegWarps + w; s < S; s += gridDim.x * kRegWarps) {
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord1;
+  const uint32_t nw = gridDim.x * kRegWarps;
+  uint32_t s = blockIdx.x * kRegWarps + w;  // first scenario: static; later ones claimed
+  uint32_t nxt = 0;
+  for (; s < S; s = nw + __shfl_sync(0xffffffffu, nxt, 0)) {
+    if (lane == 0) nxt = atomicAdd(ctr, 1u);  // claim the next one now, use it after this one
     const fikit_scenario_t c = sc[s];
     const uint32_t m = c.lp_len;
     RegPool P;
@@ -593,8 +600,18 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
   const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
-  for (uint32_t s = blockIdx.x * kReplayWarps + w; s < S; s += gridDim.x * kReplayWarps) {
-    if (out[s].n_tail != kDeferred) continue;  // done in pass 1
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord2;
+  // claim 32 scenarios at a time; run the ones pass 1 deferred
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ctr, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= S) break;
+    const uint32_t sl = base + lane;
+    uint32_t todo = __ballot_sync(0xffffffffu, sl < S && out[sl].n_tail == kDeferred);
+    while (todo) {
+    const uint32_t s = base + __ffs(todo) - 1;
+    todo &= todo - 1;
     const fikit_scenario_t c = sc[s];
     const uint32_t m = c.lp_len;
     __syncwarp();
@@ -622,6 +639,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
         [&](uint32_t k) { return __ldg(lp_dur + c.lp_off + k); }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
         lane);
     write_result(out, s, o, t, m, n_tail, db, tail_dig, lane);
+    }
   }
 }
 
