@@ -175,9 +175,10 @@ __device__ __forceinline__ int bin_of(uint64_t v) {
 __device__ __forceinline__ bool record_valid(const uint32_t* w, uint32_t n_names, uint32_t n_sigs) {
   uint64_t s = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
   uint64_t e = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-  bool ok = (w[6] != 0) & ((w[7] & 0xFFFFu) != 0) & ((w[7] >> 16) != 0) & ((w[8] & 0xFFFFu) != 0) &
-            ((w[8] >> 16) != 0) & ((w[9] & 0xFFFFu) != 0) & ((w[9] >> 16) == 0) & (w[4] < n_names) &
-            (w[5] < n_sigs) & (e >= s);
+  // grid_y, grid_z, block_x, block_y >= 1: one packed 16-bit 3-way min; 1 <= block_z and flags == 0
+  // <=> 1 <= w9 <= 0xFFFF
+  const bool dims = __vminu2(__vminu2(w[7], w[8]), 0x00010001u) == 0x00010001u;
+  bool ok = (w[6] != 0) & dims & ((w[9] - 1u) < 0xFFFFu) & (w[4] < n_names) & (w[5] < n_sigs) & (e >= s);
   return ok;
 }
 

@@ -424,8 +424,8 @@ struct Smem {
   uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6 (+ 0): two 16-B loads verify
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
-  uint32_t st[kHotMax][9];        // 0-3: sum of (v & 0xFFFF), sum of (v >> 16) for duration, gap (v < 2^32)
-                                  // 4-7: min, max (u32) for duration, gap; 8: pad
+  uint32_t st[kHotMax][5];        // 0-3: sum of (v & 0xFFFF), sum of (v >> 16) for duration, gap (v < 2^32); 4: pad
+  uint4 mm[kHotMax];              // min, max (u32) of duration, then of gap (values < 2^32): one 16-B load
   uint32_t grow[kHotMax];         // slot -> global row
   uint32_t hot_n;
   unsigned long long overlap;
@@ -461,19 +461,17 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
 // fire-and-forget shared reductions; min/max are read first (a broadcast when several lanes
 // hit the same row) and reduced only when the value improves them.  Values >= 2^32 ns
 // (4.3 s, rare) go straight to the table.
-__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, const fikit_table_t& tab, uint32_t row,
-                                        int j, uint64_t v) {
+// mn, mx: the slot's current min / max for j, loaded before any of the launch's reductions
+__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const fikit_table_t& tab,
+                                        uint32_t row, int j, uint64_t v, uint32_t mn, uint32_t mx) {
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
     const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
     red_shared_add(hist_e + 4u * (b >> 1), 1u << (16 * (b & 1)));
     red_shared_add(st_e + 8u * j, v32 & 0xFFFFu);
     red_shared_add(st_e + 8u * j + 4u, v32 >> 16);
-    uint32_t mn, mx;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mn) : "r"(st_e + 16u + 8u * j));  // 9-word rows: 4-B aligned
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mx) : "r"(st_e + 20u + 8u * j));
-    if (v32 < mn) red_shared_min(st_e + 16u + 8u * j, v32);
-    if (v32 > mx) red_shared_max(st_e + 16u + 8u * j + 4u, v32);
+    if (v32 < mn) red_shared_min(mm_e + 8u * j, v32);
+    if (v32 > mx) red_shared_max(mm_e + 8u * j + 4u, v32);
   } else {  // rare: a value >= 2^32 ns
     const int b = bin_of(v) + 32 * j;
     red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
@@ -553,6 +551,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   const uint32_t sbase = smem_u32(smem_raw);
   const uint32_t s_hist = sbase + (uint32_t)offsetof(mk::Smem, hist);
   const uint32_t s_st = sbase + (uint32_t)offsetof(mk::Smem, st);
+  const uint32_t s_mm = sbase + (uint32_t)offsetof(mk::Smem, mm);
   const uint32_t s_full = sbase + (uint32_t)offsetof(mk::Smem, full);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -567,10 +566,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
     for (int i = tid; i < (int)mk::TAG_Q; i += mk::THREADS) S.tagq[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
-    for (int i = tid; i < kHotMax * 9; i += mk::THREADS) {
-      const int w = i % 9;  // min words (4, 6) start at ~0
-      (&S.st[0][0])[i] = (w == 4 || w == 6) ? 0xFFFFFFFFu : 0u;
-    }
+    for (int i = tid; i < kHotMax * 5; i += mk::THREADS) (&S.st[0][0])[i] = 0u;
+    for (int i = tid; i < kHotMax; i += mk::THREADS) S.mm[i] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);
     __syncthreads();
     const uint32_t hn = S.hot_n;
     for (uint32_t e = tid; e < hn; e += mk::THREADS) {
@@ -589,7 +586,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       const uint32_t row = S.grow[e];
 #pragma unroll
       for (int j = 0; j < 2; j++) {
-        const uint32_t mn = S.st[e][4 + 2 * j], mx = S.st[e][5 + 2 * j];
+        const uint32_t mn = j ? S.mm[e].z : S.mm[e].x, mx = j ? S.mm[e].w : S.mm[e].y;
         if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
           red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
           red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);
@@ -746,9 +743,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto update = [&](const Rec& R, int slot) {
     const uint32_t row = S.grow[slot];
     const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
-    const uint32_t st_e = s_st + (uint32_t)slot * 36u;
-    hot_add(hist_e, st_e, tab, row, 0, R.d);
-    if (R.gap) hot_add(hist_e, st_e, tab, row, 1, R.g);
+    const uint32_t st_e = s_st + (uint32_t)slot * 20u;
+    const uint32_t mm_e = s_mm + (uint32_t)slot * 16u;
+    uint4 mm;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "r"(mm_e));
+    hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, mm.x, mm.y);
+    if (R.gap) hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, mm.z, mm.w);
     if (out_row) out_row[R.gi] = row;
   };
   // compact this tile's cold launches behind the pending ones; resolve when a batch is full
