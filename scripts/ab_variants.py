@@ -144,7 +144,7 @@ def t_gionly(m, h):
 
 
 def t_noepoch(m, h):  # diagnostic only: no epoch flushes (16-bit counters may wrap)
-    return sub(m, "constexpr int EPOCH_ROUNDS = 65535 / (SPW * TILE * WARPS);", "constexpr int EPOCH_ROUNDS = 1 << 20;"), h
+    return sub(m, "constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);", "constexpr int EPOCH_ROUNDS = 1 << 20;"), h
 
 
 VARIANTS = {
