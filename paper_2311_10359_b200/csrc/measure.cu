@@ -411,8 +411,8 @@ constexpr uint32_t TAG_Q = 1024;          // tag buckets of 4 one-word tags (409
 constexpr uint32_t TAG_HB = 0xFFFFF800u;  // tag = hash bits 11..31 (bit 31 forced to 1) | (slot + 1)
 static_assert(kHotMax < 2048, "slot + 1 must fit the 11 tag bits");
 constexpr int STAGE_BYTES = (CH + 1) * 48;  // the tile + the next launch (the tile's last gap)
-// per epoch a slot sees <= EPOCH_ROUNDS * CH * WARPS launches: packed 16-bit bins and the
-// 16-bit-split sum accumulators cannot overflow before the epoch flush
+// per epoch a slot sees <= EPOCH_ROUNDS * CH * WARPS launches: packed 16-bit bins cannot
+// overflow before the epoch flush (nor the u32 carry counters of the sums)
 constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);  // a round consumes one tile per warp
 
 struct Smem {
@@ -424,7 +424,7 @@ struct Smem {
   uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6 (+ 0): two 16-B loads verify
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
-  uint32_t st[kHotMax][5];        // 0-3: sum of (v & 0xFFFF), sum of (v >> 16) for duration, gap (v < 2^32); 4: pad
+  uint32_t st[kHotMax][5];        // duration: 0 sum mod 2^32, 1 carries out of it; gap: 2, 3 (v < 2^32); 4: pad
   uint4 mm[kHotMax];              // min, max (u32) of duration, then of gap (values < 2^32): one 16-B load
   uint32_t grow[kHotMax];         // slot -> global row
   uint32_t hot_n;
@@ -461,23 +461,33 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
 // fire-and-forget shared reductions; min/max are read first (a broadcast when several lanes
 // hit the same row) and reduced only when the value improves them.  Values >= 2^32 ns
 // (4.3 s, rare) go straight to the table.
-// mn, mx: the slot's current min / max for j, loaded before any of the launch's reductions
-__device__ __forceinline__ void hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const fikit_table_t& tab,
-                                        uint32_t row, int j, uint64_t v, uint32_t mn, uint32_t mx) {
+__device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
+  return old;
+}
+
+// mn, mx: the slot's current min / max for j, loaded before any of the launch's reductions.
+// The sum of values < 2^32 is kept mod 2^32 with a carry counter: the add returns the old
+// word and a wrap (old + v < old, exact: the atomic serializes) adds one carry.  Returns the
+// old word (the caller checks the carry after its other reductions, off the critical path).
+__device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const fikit_table_t& tab,
+                                            uint32_t row, int j, uint64_t v, uint32_t mn, uint32_t mx) {
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
     const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
+    const uint32_t old = atom_shared_add(st_e + 8u * j, v32);
     red_shared_add(hist_e + 4u * (b >> 1), 1u << (16 * (b & 1)));
-    red_shared_add(st_e + 8u * j, v32 & 0xFFFFu);
-    red_shared_add(st_e + 8u * j + 4u, v32 >> 16);
     if (v32 < mn) red_shared_min(mm_e + 8u * j, v32);
     if (v32 > mx) red_shared_max(mm_e + 8u * j + 4u, v32);
+    return old;
   } else {  // rare: a value >= 2^32 ns
     const int b = bin_of(v) + 32 * j;
     red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
     red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
+    return 0u;  // (v >> 32 != 0: the low word 0 never wraps the sum)
   }
 }
 
@@ -506,7 +516,7 @@ __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& ta
     }
 #pragma unroll
     for (int j = 0; j < 2; j++) {
-      const uint64_t sum = (uint64_t)S.st[e][2 * j] + ((uint64_t)S.st[e][2 * j + 1] << 16);
+      const uint64_t sum = (uint64_t)S.st[e][2 * j] | ((uint64_t)S.st[e][2 * j + 1] << 32);
       if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
       S.st[e][2 * j] = 0;
       S.st[e][2 * j + 1] = 0;
@@ -748,9 +758,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     uint4 mm;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "r"(mm_e));
-    hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, mm.x, mm.y);
-    if (R.gap) hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, mm.z, mm.w);
+    const uint32_t od = hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, mm.x, mm.y);
+    const uint32_t og = R.gap ? hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, mm.z, mm.w) : 0u;
     if (out_row) out_row[R.gi] = row;
+    // carries of the two sums (old + v wrapped past 2^32)
+    if ((R.d >> 32) == 0 && od + (uint32_t)R.d < od) red_shared_add(st_e + 4u, 1u);
+    if (R.gap && (R.g >> 32) == 0 && og + (uint32_t)R.g < og) red_shared_add(st_e + 12u, 1u);
   };
   // compact this tile's cold launches behind the pending ones; resolve when a batch is full
   auto compact = [&](const Rec& R, bool cold) {
