@@ -421,7 +421,11 @@ struct Smem {
   // Bucket q = hash % TAG_Q holds up to 4 tags, filled in order (the filled tags are a prefix);
   // a full bucket continues in the next one.  0 = empty.
   uint4 tagq[TAG_Q];
-  uint4 tup[kHotMax][2];          // slot -> raw identity words 0..6 (+ 0): two 16-B loads verify
+  // slot -> identity in 5 words: name | sig << 16, grid_x, grid_y | grid_z << 16,
+  // block_x | block_y << 16, block_z | task << 16 (one 16-B + one 4-B load verify).  Only
+  // identities with name, sig, task < 2^16 are kept hot; the others always take the cold path.
+  uint4 tq[kHotMax];
+  uint32_t tq4[kHotMax];
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
   uint32_t st[kHotMax][5];        // duration: 0 sum mod 2^32, 1 carries out of it; gap: 2, 3 (v < 2^32); 4: pad
@@ -471,8 +475,9 @@ __device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) 
 // The sum of values < 2^32 is kept mod 2^32 with a carry counter: the add returns the old
 // word and a wrap (old + v < old, exact: the atomic serializes) adds one carry.  Returns the
 // old word (the caller checks the carry after its other reductions, off the critical path).
+template <class RowOf>  // row_of(): the slot's table row, read only on the rare >= 2^32 path
 __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const fikit_table_t& tab,
-                                            uint32_t row, int j, uint64_t v, uint32_t mn, uint32_t mx) {
+                                            RowOf row_of, int j, uint64_t v, uint32_t mn, uint32_t mx) {
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
     const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
@@ -484,6 +489,7 @@ __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint
   } else {  // rare: a value >= 2^32 ns
     const int b = bin_of(v) + 32 * j;
     red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
+    const uint32_t row = row_of();
     red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
@@ -583,9 +589,11 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     for (uint32_t e = tid; e < hn; e += mk::THREADS) {
       Tuple t = hot[e];
       S.grow[e] = t.row;
-      S.tup[e][0] = make_uint4(t.w[0], t.w[1], t.w[2], t.w[3]);
-      S.tup[e][1] = make_uint4(t.w[4], t.w[5], t.w[6], 0u);
-      mk::tag_insert(S, tuple_hash(t.w), e);
+      if (((t.w[0] | t.w[1] | t.w[6]) >> 16) == 0u) {  // compressible: may be hot
+        S.tq[e] = make_uint4(t.w[0] | (t.w[1] << 16), t.w[2], t.w[3], t.w[4]);
+        S.tq4[e] = t.w[5] | (t.w[6] << 16);
+        mk::tag_insert(S, tuple_hash(t.w), e);
+      }
     }
     __syncthreads();
   };
@@ -666,12 +674,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       // reader that misses the new tag takes the cold path, which is also correct; two CTA warps
       // admitting the same row concurrently give two slots of one row (both flushed).
       const uint32_t same = __match_any_sync(pend, row);
-      if (row < tab.capacity && (same & ((1u << lane) - 1u)) == 0 && *(volatile uint32_t*)&S.hot_n < kHotMax) {
+      if (row < tab.capacity && (same & ((1u << lane) - 1u)) == 0 && ((key[0] | key[1] | key[6]) >> 16) == 0u &&
+          *(volatile uint32_t*)&S.hot_n < kHotMax) {
         const uint32_t e = atomicAdd(&S.hot_n, 1u);
         if (e < kHotMax) {
           S.grow[e] = row;
-          S.tup[e][0] = make_uint4(key[0], key[1], key[2], key[3]);
-          S.tup[e][1] = make_uint4(key[4], key[5], key[6], 0u);
+          S.tq[e] = make_uint4(key[0] | (key[1] << 16), key[2], key[3], key[4]);
+          S.tq4[e] = key[5] | (key[6] << 16);
           __threadfence_block();
           mk::tag_insert(S, tuple_hash(key), e);
         }
@@ -682,9 +691,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // One warp-tile in registers: identity key, K, G and flags of this lane's launch.
   struct Rec {
     uint32_t key[7];
+    uint32_t ck0, ck4;  // compressed identity words 0 and 4 (valid if cmp)
     uint32_t hk, gi;
     uint64_t d, g;
-    bool valid, gap, live;
+    bool valid, gap, live, cmp;
   };
   // read this lane's launch of half h of the stage's tile and the next launch's start/run/task
   // (lane + 1 by shuffle; lane 31 from the record after the half; the halo after the last
@@ -728,14 +738,17 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     overlap_cnt += (R.valid && ov) ? 1u : 0u;
     R.key[0] = w[4]; R.key[1] = w[5]; R.key[2] = w[6]; R.key[3] = w[7]; R.key[4] = w[8];
     R.key[5] = w[9] & 0xFFFFu; R.key[6] = w[11];
+    R.ck0 = w[4] | (w[5] << 16);
+    R.ck4 = (w[9] & 0xFFFFu) | (w[11] << 16);
+    R.cmp = ((w[4] | w[5] | w[11]) >> 16) == 0u;
     R.hk = tuple_hash(R.key);
     // every loaded word is consumed here, so the shared loads have completed
     asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
   };
-  auto verify = [&](uint32_t e, const uint32_t* key) -> bool {  // branch-free: both loads in flight
-    const uint4 a = S.tup[e][0], b = S.tup[e][1];
-    return ((a.x ^ key[0]) | (a.y ^ key[1]) | (a.z ^ key[2]) | (a.w ^ key[3]) | (b.x ^ key[4]) |
-            (b.y ^ key[5]) | (b.z ^ key[6])) == 0u;
+  auto verify = [&](uint32_t e, const Rec& R) -> bool {  // branch-free: both loads in flight
+    const uint4 a = S.tq[e];
+    const uint32_t b = S.tq4[e];
+    return ((a.x ^ R.ck0) | (a.y ^ R.key[2]) | (a.z ^ R.key[3]) | (a.w ^ R.key[4]) | (b ^ R.ck4)) == 0u;
   };
   // full lookup (rare: a full home bucket without the key, or a 20-bit tag collision)
   auto probe_slow = [&](const Rec& R) -> int {
@@ -746,12 +759,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         if (v[i] == 0u) return -1;  // end of the filled prefix: absent
-        if ((v[i] ^ hb) < 0x800u && verify((v[i] & 0x7FFu) - 1, R.key)) return (int)(v[i] & 0x7FFu) - 1;
+        if ((v[i] ^ hb) < 0x800u && verify((v[i] & 0x7FFu) - 1, R)) return (int)(v[i] & 0x7FFu) - 1;
       }
     }
   };
   auto update = [&](const Rec& R, int slot) {
-    const uint32_t row = S.grow[slot];
+    const uint32_t rowv = S.grow[slot];  // (loading it here schedules better than on demand)
+    auto row = [&]() { return rowv; };
     const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
     const uint32_t st_e = s_st + (uint32_t)slot * 20u;
     const uint32_t mm_e = s_mm + (uint32_t)slot * 16u;
@@ -760,7 +774,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
                  : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "r"(mm_e));
     const uint32_t od = hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, mm.x, mm.y);
     const uint32_t og = R.gap ? hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, mm.z, mm.w) : 0u;
-    if (out_row) out_row[R.gi] = row;
+    if (out_row) out_row[R.gi] = row();
     // carries of the two sums (old + v wrapped past 2^32)
     if ((R.d >> 32) == 0 && od + (uint32_t)R.d < od) red_shared_add(st_e + 4u, 1u);
     if (R.gap && (R.g >> 32) == 0 && og + (uint32_t)R.g < og) red_shared_add(st_e + 12u, 1u);
@@ -842,13 +856,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       // home buckets of both launches together (one 16-B load each), then speculative
       // verification of the slot whose tag matches; a miss is final unless the bucket is full
       const uint4 tA = S.tagq[A.hk & (mk::TAG_Q - 1)], tB = S.tagq[B.hk & (mk::TAG_Q - 1)];
-      const uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
+      uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
+      const bool fullA = tA.w != 0u, fullB = tB.w != 0u;
       const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
-      const bool vA = verify(eA, A.key) & (cA != 0u);
-      const bool vB = verify(eB, B.key) & (cB != 0u);
+      const bool vA = verify(eA, A) & (cA != 0u);
+      const bool vB = verify(eB, B) & (cB != 0u);
       int sA = -1, sB = -1;
-      if (A.valid) sA = vA ? (int)eA : ((cA | tA.w) ? probe_slow(A) : -1);
-      if (B.valid) sB = vB ? (int)eB : ((cB | tB.w) ? probe_slow(B) : -1);
+      if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
+      if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);
       if (sA >= 0) update(A, sA);
       if (sB >= 0) update(B, sB);
       if (A.live && !A.valid) flag_record(st, A.gi);

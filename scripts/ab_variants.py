@@ -147,7 +147,42 @@ def t_noepoch(m, h):  # diagnostic only: no epoch flushes (16-bit counters may w
     return sub(m, "constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);", "constexpr int EPOCH_ROUNDS = 1 << 20;"), h
 
 
+FIRSTTAG_NEW = """      const uint32_t* tagw = reinterpret_cast<const uint32_t*>(S.tagq);
+      const uint32_t qA = A.hk & (mk::TAG_Q - 1), qB = B.hk & (mk::TAG_Q - 1);
+      const uint32_t hbA = mk::tag_bits(A.hk), hbB = mk::tag_bits(B.hk);
+      const uint32_t fA = tagw[4 * qA], fB = tagw[4 * qB];
+      uint32_t cA = (fA ^ hbA) < 0x800u ? fA & 0x7FFu : 0u, cB = (fB ^ hbB) < 0x800u ? fB & 0x7FFu : 0u;
+      bool fullA = false, fullB = false;
+      if (fA != 0u && cA == 0u) {
+        const uint4 t = S.tagq[qA];
+        cA = mk::bucket_match(t, hbA);
+        fullA = t.w != 0u;
+      }
+      if (fB != 0u && cB == 0u) {
+        const uint4 t = S.tagq[qB];
+        cB = mk::bucket_match(t, hbB);
+        fullB = t.w != 0u;
+      }
+"""
+FIRSTTAG_OLD = """      const uint4 tA = S.tagq[A.hk & (mk::TAG_Q - 1)], tB = S.tagq[B.hk & (mk::TAG_Q - 1)];
+      uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
+      const bool fullA = tA.w != 0u, fullB = tB.w != 0u;
+"""
+
+
+def t_bucket(m, h):  # whole home bucket per probe (no first-tag step)
+    return sub(m, FIRSTTAG_NEW, FIRSTTAG_OLD), h
+
+
+def t_eagerrow(m, h):
+    return sub(m, "    auto row = [&]() { return S.grow[slot]; };",
+               "    const uint32_t rowv = S.grow[slot];\n    auto row = [&]() { return rowv; };"), h
+
+
 VARIANTS = {
+    "c_bucket": [t_bucket],
+    "c_eager": [t_eagerrow],
+    "c_bucket_eager": [t_bucket, t_eagerrow],
     "w24": [t_warps(24, 640)],
     "w16": [t_warps(16, 640)],
     "x_noepoch": [t_noepoch],

@@ -89,6 +89,34 @@ def test_measure_random(fk, orc, seed, n, kw):
         assert st["schedule"] == 1 and st["n_task_buckets"] > 1, st
 
 
+@pytest.mark.parametrize("mode", ["wide_task", "wide_name", "mixed"])
+def test_measure_wide_ids(fk, orc, mode):
+    """Identities with name, sig or task ids >= 2^16 are never kept in the compressed shared
+    dictionary (they always take the cold path); parity must hold for them and for traces
+    mixing them with compressible ones, in both schedules."""
+    tr = F.random_trace(71, 60000, n_ids=700, n_tasks=6, n_names=300, run_len_max=300)
+    rec = tr.records.copy()
+    names = tr.names
+    rng = np.random.default_rng(7)
+    if mode in ("wide_task", "mixed"):
+        wide = rec["task_id"] % 2 == 1 if mode == "mixed" else np.ones(rec.shape[0], bool)
+        rec["task_id"][wide] += np.uint32(1 << 16) + np.uint32(12345)
+    if mode in ("wide_name", "mixed"):
+        # copies of every name at indices >= 2^16: the same strings, so the same kernel IDs
+        base = [names.get(j) for j in range(names.count)]
+        pad = [b"pad%d" % j for j in range((1 << 16) - len(base))]
+        names = F.StrTab.from_list(base + pad + base)
+        move = rng.random(rec.shape[0]) < (1.0 if mode == "wide_name" else 0.3)
+        rec["name_id"][move] += np.uint32(1 << 16)
+    tr2 = F.Trace(rec, names, tr.sigs)
+    ref, rst, _ = orc.measure(tr2.records, tr2.names, tr2.sigs, want_rows=True)
+    p = run_measure(fk, tr2, capacity=max(16, 2 * ref.n_rows))
+    st = p.check()
+    assert st["n_rows_needed"] == ref.n_rows
+    assert st["n_overlap_gaps"] == rst["n_overlap_gaps"]
+    assert_tables_equal(p.table.to_numpy(), ref, mode)
+
+
 def test_identify_random(fk, orc):
     import torch
 
