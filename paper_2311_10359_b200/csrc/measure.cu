@@ -407,7 +407,8 @@ static_assert(CH == (int)kTileLaunches, "the schedule's tile is the kernel's war
 constexpr int WARPS = 20;                 // warps per CTA; every warp streams and consumes its own tiles (<= 102 registers)
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
-constexpr uint32_t TAG_Q = 1024;          // tag buckets of 4 one-word tags (4096 tags, load <= 0.16)
+constexpr uint32_t TAG_W = 2;             // one-word tags per bucket (one 8-B load per probe)
+constexpr uint32_t TAG_Q = 4096 / TAG_W;  // buckets (4096 tags, load <= 0.16)
 constexpr uint32_t TAG_HB = 0xFFFFF800u;  // tag = hash bits 11..31 (bit 31 forced to 1) | (slot + 1)
 static_assert(kHotMax < 2048, "slot + 1 must fit the 11 tag bits");
 constexpr int STAGE_BYTES = (CH + 1) * 48;  // the tile + the next launch (the tile's last gap)
@@ -418,9 +419,9 @@ constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);  // a round consumes one tile
 struct Smem {
   uint4 ring[WARPS][STAGE_BYTES / 16];  // one stage per warp (refilled as soon as it is read)
   uint64_t full[WARPS];
-  // Bucket q = hash % TAG_Q holds up to 4 tags, filled in order (the filled tags are a prefix);
-  // a full bucket continues in the next one.  0 = empty.
-  uint4 tagq[TAG_Q];
+  // Bucket q = hash % TAG_Q holds up to TAG_W tags, filled in order (the filled tags are a
+  // prefix); a full bucket continues in the next one.  0 = empty.
+  alignas(16) uint32_t tagw[TAG_Q * TAG_W];
   // slot -> identity in 5 words: name | sig << 16, grid_x, grid_y | grid_z << 16,
   // block_x | block_y << 16, block_z | task << 16 (one 16-B + one 4-B load verify).  Only
   // identities with name, sig, task < 2^16 are kept hot; the others always take the cold path.
@@ -547,12 +548,18 @@ __device__ __forceinline__ uint32_t bucket_match(const uint4 t, uint32_t hb) {
 // publish slot e under hash h (its tup words are written and fenced before)
 __device__ __forceinline__ void tag_insert(Smem& S, uint32_t h, uint32_t e) {
   const uint32_t tg = tag_bits(h) | (e + 1);
-  uint32_t* w = reinterpret_cast<uint32_t*>(S.tagq);
   for (uint32_t q = h & (TAG_Q - 1);; q = (q + 1) & (TAG_Q - 1))
 #pragma unroll
-    for (int i = 0; i < 4; i++)
-      if (atomicCAS(&w[q * 4 + i], 0u, tg) == 0u) return;
+    for (uint32_t i = 0; i < TAG_W; i++)
+      if (atomicCAS(&S.tagw[q * TAG_W + i], 0u, tg) == 0u) return;
 }
+// bucket q as up to 4 tags (missing ones 0); full: its last tag is taken
+__device__ __forceinline__ uint4 ld_bucket(const Smem& S, uint32_t q) {
+  if constexpr (TAG_W == 4) return reinterpret_cast<const uint4*>(S.tagw)[q];
+  const uint2 t = reinterpret_cast<const uint2*>(S.tagw)[q];
+  return make_uint4(t.x, t.y, 0u, 0u);
+}
+__device__ __forceinline__ bool bucket_full(const uint4 t) { return (TAG_W == 4 ? t.w : t.y) != 0u; }
 }  // namespace mk
 
 __global__ void __launch_bounds__(mk::THREADS, 1)
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto load_hot_set = [&](uint32_t bkt) {
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
     if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
-    for (int i = tid; i < (int)mk::TAG_Q; i += mk::THREADS) S.tagq[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < (int)(mk::TAG_Q * mk::TAG_W); i += mk::THREADS) S.tagw[i] = 0u;
     for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
     for (int i = tid; i < kHotMax * 5; i += mk::THREADS) (&S.st[0][0])[i] = 0u;
     for (int i = tid; i < kHotMax; i += mk::THREADS) S.mm[i] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);
@@ -706,9 +713,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     R.live = (uint32_t)lane < cnt;
     uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
     if (R.live) {
-      r0 = rp[0];
-      r1 = rp[1];
-      r2 = rp[2];
+      // one 16-B shared load per quarter record (the compiler splits rp[0] into two 8-B loads,
+      // which cost as many wavefronts each at this 48-B stride)
+      const uint32_t a = smem_u32(rp);
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w) : "r"(a));
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(r1.x), "=r"(r1.y), "=r"(r1.z), "=r"(r1.w) : "r"(a + 16u));
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(r2.x), "=r"(r2.y), "=r"(r2.z), "=r"(r2.w) : "r"(a + 32u));
     }
     uint64_t nstart = __shfl_down_sync(0xffffffffu, (uint64_t)r0.x | ((uint64_t)r0.y << 32), 1);
     uint32_t nrun = __shfl_down_sync(0xffffffffu, r2.z, 1);
@@ -754,10 +766,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto probe_slow = [&](const Rec& R) -> int {
     const uint32_t hb = mk::tag_bits(R.hk);
     for (uint32_t q = R.hk & (mk::TAG_Q - 1);; q = (q + 1) & (mk::TAG_Q - 1)) {
-      const uint4 t = S.tagq[q];
+      const uint4 t = mk::ld_bucket(S, q);
       const uint32_t v[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
+      for (int i = 0; i < (int)mk::TAG_W; i++) {
         if (v[i] == 0u) return -1;  // end of the filled prefix: absent
         if ((v[i] ^ hb) < 0x800u && verify((v[i] & 0x7FFu) - 1, R)) return (int)(v[i] & 0x7FFu) - 1;
       }
@@ -855,9 +867,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       }
       // home buckets of both launches together (one 16-B load each), then speculative
       // verification of the slot whose tag matches; a miss is final unless the bucket is full
-      const uint4 tA = S.tagq[A.hk & (mk::TAG_Q - 1)], tB = S.tagq[B.hk & (mk::TAG_Q - 1)];
+      const uint4 tA = mk::ld_bucket(S, A.hk & (mk::TAG_Q - 1)), tB = mk::ld_bucket(S, B.hk & (mk::TAG_Q - 1));
       uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
-      const bool fullA = tA.w != 0u, fullB = tB.w != 0u;
+      const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
       const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
       const bool vA = verify(eA, A) & (cA != 0u);
       const bool vB = verify(eB, B) & (cB != 0u);
