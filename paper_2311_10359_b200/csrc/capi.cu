@@ -10,7 +10,7 @@
 namespace fikit {
 // kernels (measure.cu, finalize.cu, replay.cu)
 __global__ void k_reset_status(fikit_status_t*);
-__global__ void k_strtab_hash(fikit_strtab_t, uint64_t*, int, fikit_status_t*);
+__global__ void k_strtab_hash(fikit_strtab_t, uint64_t*, fikit_strtab_t, uint64_t*, fikit_status_t*);
 __global__ void k_identify(const uint4*, uint64_t, const uint64_t*, const uint64_t*, uint32_t, uint32_t, uint64_t*,
                            fikit_status_t*);
 __global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint32_t,
@@ -135,12 +135,9 @@ inline bool table_ok(const fikit_table_t* t) {
 }
 
 int hash_strtabs(const Ws& w, const fikit_strtab_t& names, const fikit_strtab_t& sigs, cudaStream_t s) {
-  if (names.count) {
-    k_strtab_hash<<<(names.count + 127) / 128, 128, 0, s>>>(names, w.name_hash(), 1, w.st());
-    if (int r = launched()) return r;
-  }
-  if (sigs.count) {
-    k_strtab_hash<<<(sigs.count + 127) / 128, 128, 0, s>>>(sigs, w.sig_hash(), 0, w.st());
+  const uint32_t mx = names.count > sigs.count ? names.count : sigs.count;
+  if (mx) {  // one warp per string, names (y = 0) and signatures (y = 1) in one launch
+    k_strtab_hash<<<dim3((mx + 3) / 4, 2), 128, 0, s>>>(names, w.name_hash(), sigs, w.sig_hash(), w.st());
     if (int r = launched()) return r;
   }
   return FIKIT_OK;
@@ -290,12 +287,13 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   uint32_t* rank = reinterpret_cast<uint32_t*>(w.fin() + 336ull * cap);
   uint32_t* kptr = w.misc() + kMiscNRec;
   unsigned g = (cap + 255) / 256;
-  k_fin_prep<<<g, 256, 0, s>>>(w.st(), t, fin, kptr);
+  const unsigned gw = (cap + 7) / 8;  // 8 rows (warps) per 256-thread block
+  k_fin_prep<<<gw, 256, 0, s>>>(w.st(), t, fin, kptr);
   if (int r = launched()) return r;
   cudaMemsetAsync(rank, 0, 4ull * cap, s);
-  k_fin_rank<<<dim3(g, (cap + 2047) / 2048), 256, 0, s>>>(t, kptr, rank);
+  k_fin_rank<<<dim3(g, (cap + 255) / 256), 256, 0, s>>>(t, kptr, rank);
   if (int r = launched()) return r;
-  k_fin_scatter<<<g, 256, 0, s>>>(t, fin, rank, kptr);
+  k_fin_scatter<<<gw, 256, 0, s>>>(t, fin, rank, kptr);
   if (int r = launched()) return r;
   if (out_row && n) {
     k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, kptr);

@@ -27,41 +27,43 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
 
 // rows -> scratch; counts = histogram totals (SK/SG denominators)
 __global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* fin, uint32_t* n_out) {
-  uint32_t K = (uint32_t)umin64(st->n_rows_needed, tab.capacity);
-  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) *n_out = K;
+  // one warp per row: the 64 histogram words of a row are read coalesced
+  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, tab.capacity);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r == 0 && lane == 0) *n_out = K;
   if (r >= K) return;
-  FinRow f;
-  f.kid = tab.kernel_id[r];
-  f.task = tab.task_id[r];
-  f.pad = 0;
-  uint64_t dc = 0, gc = 0;
-  for (int b = 0; b < 32; b++) {
-    f.hist[b] = tab.hist[(size_t)r * 64 + b];
-    f.hist[32 + b] = tab.hist[(size_t)r * 64 + 32 + b];
-    dc += f.hist[b];
-    gc += f.hist[32 + b];
+  FinRow& f = fin[r];
+  const uint32_t h0 = tab.hist[(size_t)r * 64 + lane], h1 = tab.hist[(size_t)r * 64 + 32 + lane];
+  f.hist[lane] = h0;
+  f.hist[32 + lane] = h1;
+  // row counts < 2^32 (a call measures < 2^32 launches)
+  const uint32_t dc = __reduce_add_sync(0xffffffffu, h0), gc = __reduce_add_sync(0xffffffffu, h1);
+  if (lane < 4) f.ext[lane] = tab.ext[(size_t)r * 4 + lane];
+  if (lane == 0) {
+    f.kid = tab.kernel_id[r];
+    f.task = tab.task_id[r];
+    f.pad = 0;
+    f.sums[0] = dc;
+    f.sums[1] = tab.sums[(size_t)r * 4 + 1];
+    f.sums[2] = gc;
+    f.sums[3] = tab.sums[(size_t)r * 4 + 3];
   }
-  f.sums[0] = dc;
-  f.sums[1] = tab.sums[(size_t)r * 4 + 1];
-  f.sums[2] = gc;
-  f.sums[3] = tab.sums[(size_t)r * 4 + 3];
-  for (int j = 0; j < 4; j++) f.ext[j] = tab.ext[(size_t)r * 4 + j];
-  fin[r] = f;
 }
 
 // rank of every key among the K distinct keys = its canonical row (R11).
-// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a chunk of 2048 keys staged in
-// shared memory; partial counts are added into rank[] (zeroed by the caller).
+// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a chunk of 256 keys staged in shared
+// memory; partial counts are added into rank[] (zeroed by the caller).
 __global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const uint32_t* n_ptr,
                                                   uint32_t* __restrict__ rank) {
-  __shared__ unsigned long long sk[2048];
-  __shared__ uint32_t st[2048];
+  constexpr uint32_t CHUNK = 256;
+  __shared__ unsigned long long sk[CHUNK];
+  __shared__ uint32_t st[CHUNK];
   uint32_t K = *n_ptr;
   uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t base = blockIdx.y * 2048;
+  uint32_t base = blockIdx.y * CHUNK;
   if (blockIdx.x * blockDim.x >= K || base >= K) return;
-  uint32_t m = min(2048u, K - base);
+  uint32_t m = min(CHUNK, K - base);
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
     sk[i] = tab.kernel_id[base + i];
     st[i] = tab.task_id[base + i];
@@ -78,19 +80,26 @@ __global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const
 
 __global__ void k_fin_scatter(fikit_table_t tab, const FinRow* __restrict__ fin, const uint32_t* __restrict__ rank,
                               const uint32_t* n_ptr) {
-  uint32_t K = *n_ptr;
-  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) *tab.n_rows = K;
+  // one warp per row (coalesced 64-word histogram rows)
+  const uint32_t K = *n_ptr;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r == 0 && lane == 0) *tab.n_rows = K;
   if (r >= K) return;
   const FinRow& f = fin[r];
-  uint32_t d = rank[r];
-  tab.kernel_id[d] = f.kid;
-  tab.task_id[d] = f.task;
-  for (int j = 0; j < 4; j++) tab.sums[(size_t)d * 4 + j] = f.sums[j];
-  for (int j = 0; j < 4; j++) tab.ext[(size_t)d * 4 + j] = f.ext[j];
-  for (int b = 0; b < 64; b++) tab.hist[(size_t)d * 64 + b] = f.hist[b];
-  tab.mean[(size_t)d * 2 + 0] = mean_half_up(f.sums[1], f.sums[0]);  // SK_j
-  tab.mean[(size_t)d * 2 + 1] = mean_half_up(f.sums[3], f.sums[2]);  // SG_j
+  const uint32_t d = rank[r];
+  tab.hist[(size_t)d * 64 + lane] = f.hist[lane];
+  tab.hist[(size_t)d * 64 + 32 + lane] = f.hist[32 + lane];
+  if (lane < 4) {
+    tab.sums[(size_t)d * 4 + lane] = f.sums[lane];
+    tab.ext[(size_t)d * 4 + lane] = f.ext[lane];
+  }
+  if (lane == 0) {
+    tab.kernel_id[d] = f.kid;
+    tab.task_id[d] = f.task;
+    tab.mean[(size_t)d * 2 + 0] = mean_half_up(f.sums[1], f.sums[0]);  // SK_j
+    tab.mean[(size_t)d * 2 + 1] = mean_half_up(f.sums[3], f.sums[2]);  // SG_j
+  }
 }
 
 __global__ void k_remap_rows(uint32_t* rows, uint64_t n, const uint32_t* __restrict__ rank, const uint32_t* n_ptr) {

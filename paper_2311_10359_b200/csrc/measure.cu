@@ -34,35 +34,49 @@ __global__ void k_reset_status(fikit_status_t* st) {
   }
 }
 
-__global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t t, uint64_t* __restrict__ out, int is_name,
+// One warp per string (blockIdx.y: 0 names, 1 signatures): the lanes stage the string's
+// aligned 16-B blocks in shared memory with coalesced loads, then lane 0 runs FNV-1a over the
+// bytes (serial by definition) from shared memory.
+__global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint64_t* __restrict__ name_out,
+                                                     fikit_strtab_t sigs, uint64_t* __restrict__ sig_out,
                                                      fikit_status_t* st) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr uint32_t CH = 64;  // 16-B blocks staged per pass (1 KB per warp)
+  __shared__ uint4 buf[4][CH];
+  const bool is_name = blockIdx.y == 0;
+  const fikit_strtab_t t = is_name ? names : sigs;
+  uint64_t* out = is_name ? name_out : sig_out;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t j = blockIdx.x * 4 + w;
   if (j >= t.count) return;
-  uint32_t a = t.offsets[j], b = t.offsets[j + 1];
+  const uint32_t a = t.offsets[j], b = t.offsets[j + 1];
   if (b < a) {
-    atomicOr(&st->flags, kStatusArg);
-    out[j] = 0;
+    if (lane == 0) {
+      atomicOr(&st->flags, kStatusArg);
+      out[j] = 0;
+    }
     return;
   }
-  if (is_name && a == b) atomicOr(&st->flags, kStatusName);
+  if (is_name && a == b && lane == 0) atomicOr(&st->flags, kStatusName);
   uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a 64 (R2), bytes in order
-  // aligned 16-byte loads (independent, issued ahead), bytes consumed from registers
   const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(t.bytes) & ~uintptr_t(15));
   const uint32_t skew = (uint32_t)(reinterpret_cast<uintptr_t>(t.bytes) & 15);
   const uint32_t lo = a + skew, hi = b + skew;  // byte range relative to base
-  for (uint32_t c = lo >> 4; c < (hi + 15) >> 4; c++) {
-    const uint4 v = __ldg(base + c);
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 16; q++) {
-      const uint32_t pos = c * 16 + q;
-      if (pos >= lo && pos < hi) {
-        h ^= (uint64_t)((wv[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+  const uint32_t c_end = (hi + 15) >> 4;
+  const unsigned char* sb = reinterpret_cast<const unsigned char*>(buf[w]);
+  for (uint32_t c0 = lo >> 4; c0 < c_end; c0 += CH) {
+    const uint32_t nch = min(CH, c_end - c0);
+    for (uint32_t i = lane; i < nch; i += 32) buf[w][i] = __ldg(base + c0 + i);
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t p1 = min(hi, (c0 + nch) * 16);
+      for (uint32_t pos = max(lo, c0 * 16); pos < p1; pos++) {
+        h ^= (uint64_t)sb[pos - c0 * 16];
         h *= 0x100000001b3ULL;
       }
     }
+    __syncwarp();
   }
-  out[j] = h;
+  if (lane == 0) out[j] = h;
 }
 
 // warp-cooperative coalesced load of up to 32 records (1536 B) into a per-warp
@@ -117,6 +131,15 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
                          const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash,
                          uint32_t n_names, uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st,
                          fikit_table_t tab, Tuple* row_tuple, uint32_t* samp_cnt) {
+  // per-block counts (a skewed sample hits a few rows thousands of times: one L2 atomic per
+  // distinct row per block instead of one per sample)
+  constexpr uint32_t HS = 1024;
+  __shared__ uint32_t hrow[HS], hcnt[HS];
+  for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x) {
+    hrow[i] = 0xFFFFFFFFu;
+    hcnt[i] = 0;
+  }
+  __syncthreads();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_samples;
        j += (uint64_t)gridDim.x * blockDim.x) {
     // jittered stride: a fixed stride aliases with periodic traces (a 300-kernel template
@@ -131,8 +154,24 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
     uint32_t tw[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
     uint32_t row =
         index_find_or_insert(idx, slots, kid, w[11], tw, st, tab.kernel_id, tab.task_id, row_tuple, tab.capacity);
-    if (row < tab.capacity) atomicAdd(samp_cnt + row, 1u);
+    if (row < tab.capacity) {
+      uint32_t p = (row * 0x9E3779B1u) >> 22;  // 10 bits
+      for (uint32_t probe = 0;; probe++, p = (p + 1) & (HS - 1)) {
+        if (probe == HS) {  // table full (> HS distinct rows in this block): count directly
+          atomicAdd(samp_cnt + row, 1u);
+          break;
+        }
+        const uint32_t old = atomicCAS(&hrow[p], 0xFFFFFFFFu, row);
+        if (old == 0xFFFFFFFFu || old == row) {
+          atomicAdd(&hcnt[p], 1u);
+          break;
+        }
+      }
+    }
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x)
+    if (hcnt[i]) atomicAdd(samp_cnt + hrow[i], hcnt[i]);
 }
 
 // ---- hot sets: per task bucket, the most-sampled rows (one CTA per bucket; CTA kBuckets:
