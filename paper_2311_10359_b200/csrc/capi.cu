@@ -28,7 +28,8 @@ size_t measure_smem_bytes();
 int measure_threads();
 struct FinRow;
 __global__ void k_fin_prep(const fikit_status_t*, fikit_table_t, FinRow*, uint32_t*);
-__global__ void k_fin_rank(const fikit_table_t, const uint32_t*, uint32_t*);
+__global__ void k_fin_chunksort(const fikit_table_t, const uint32_t*, uint64_t*, uint32_t*);
+__global__ void k_fin_rank(const fikit_table_t, const uint32_t*, const uint64_t*, const uint32_t*, uint32_t*);
 __global__ void k_fin_scatter(fikit_table_t, const FinRow*, const uint32_t*, const uint32_t*);
 __global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
 __global__ void k_means(fikit_table_t);
@@ -285,13 +286,17 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   const uint32_t cap = t.capacity;
   FinRow* fin = reinterpret_cast<FinRow*>(w.fin());
   uint32_t* rank = reinterpret_cast<uint32_t*>(w.fin() + 336ull * cap);
+  uint64_t* skid = reinterpret_cast<uint64_t*>(w.fin() + ((340ull * cap + 7) & ~7ull));
+  uint32_t* stask = reinterpret_cast<uint32_t*>(skid + cap);
   uint32_t* kptr = w.misc() + kMiscNRec;
   unsigned g = (cap + 255) / 256;
   const unsigned gw = (cap + 7) / 8;  // 8 rows (warps) per 256-thread block
   k_fin_prep<<<gw, 256, 0, s>>>(w.st(), t, fin, kptr);
   if (int r = launched()) return r;
+  k_fin_chunksort<<<(cap + 255) / 256, 256, 0, s>>>(t, kptr, skid, stask);
+  if (int r = launched()) return r;
   cudaMemsetAsync(rank, 0, 4ull * cap, s);
-  k_fin_rank<<<dim3(g, (cap + 255) / 256), 256, 0, s>>>(t, kptr, rank);
+  k_fin_rank<<<dim3(g, (cap + 2047) / 2048), 256, 0, s>>>(t, kptr, skid, stask, rank);
   if (int r = launched()) return r;
   k_fin_scatter<<<gw, 256, 0, s>>>(t, fin, rank, kptr);
   if (int r = launched()) return r;

@@ -84,8 +84,8 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o = align256(o + 4ull * cap);
   L.hot = o;  // header[kHotHdr] (u32), then hot[kBuckets + 1][kHotMax] (Tuple)
   o = align256(o + 4ull * kHotHdr + sizeof(Tuple) * (size_t)kHotMax * (kBuckets + 1));
-  L.fin = o;
-  o = align256(o + 340ull * cap + 1024);
+  L.fin = o;  // FinRow[cap] (336 B), rank[cap], sorted chunk keys: kid[cap] (8-aligned), task[cap]
+  o = align256(o + 352ull * cap + 1024);
   // tiles: bcount[kBuckets], bcursor[kBuckets], nphase[kMaxCTAs], plan[kMaxCTAs][kMaxPhases],
   //        blkoff[kSortBlocks][kBuckets], tile_bucket[ntiles] (u8), order[ntiles] (u32)
   L.ntiles = (n_records + kTileLaunches - 1) / kTileLaunches;

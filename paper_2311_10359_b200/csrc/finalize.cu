@@ -51,30 +51,80 @@ __global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* 
   }
 }
 
-// rank of every key among the K distinct keys = its canonical row (R11).
-// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a chunk of 256 keys staged in shared
-// memory; partial counts are added into rank[] (zeroed by the caller).
+// rank of every key among the K distinct keys = its canonical row (R11): every 256-key chunk
+// of the table is sorted once (k_fin_chunksort, shared-memory bitonic sort), then a row's rank
+// is the sum over chunks of the number of keys below it (a binary search per chunk).
+constexpr uint32_t kRankChunk = 256;
+
+__global__ void __launch_bounds__(kRankChunk) k_fin_chunksort(const fikit_table_t tab, const uint32_t* n_ptr,
+                                                              uint64_t* __restrict__ skid,
+                                                              uint32_t* __restrict__ stask) {
+  __shared__ uint64_t sk[kRankChunk];
+  __shared__ uint32_t stk[kRankChunk];
+  const uint32_t K = *n_ptr, base = blockIdx.x * kRankChunk, i = threadIdx.x;
+  if (base >= K) return;
+  const bool in = base + i < K;
+  sk[i] = in ? tab.kernel_id[base + i] : ~0ull;  // padding sorts last
+  stk[i] = in ? tab.task_id[base + i] : 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t k = 2; k <= kRankChunk; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t l = i ^ j;
+      if (l > i) {
+        const bool asc = (i & k) == 0;
+        const bool gt = key_less(stk[l], sk[l], stk[i], sk[i]);  // key(i) > key(l)
+        if (gt == asc) {
+          const uint64_t tk = sk[i];
+          sk[i] = sk[l];
+          sk[l] = tk;
+          const uint32_t tt = stk[i];
+          stk[i] = stk[l];
+          stk[l] = tt;
+        }
+      }
+      __syncthreads();
+    }
+  if (in) {
+    skid[base + i] = sk[i];
+    stask[base + i] = stk[i];
+  }
+}
+
+// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a group of kRankGroup sorted chunks staged in
+// shared memory; each row adds the number of keys below it in those chunks (binary searches in
+// shared memory) to rank[] (zeroed by the caller).
+constexpr uint32_t kRankGroup = 8;
+
 __global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const uint32_t* n_ptr,
+                                                  const uint64_t* __restrict__ skid, const uint32_t* __restrict__ stask,
                                                   uint32_t* __restrict__ rank) {
-  constexpr uint32_t CHUNK = 256;
-  __shared__ unsigned long long sk[CHUNK];
-  __shared__ uint32_t st[CHUNK];
-  uint32_t K = *n_ptr;
-  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t base = blockIdx.y * CHUNK;
+  __shared__ uint64_t sk[kRankGroup * kRankChunk];
+  __shared__ uint32_t stk[kRankGroup * kRankChunk];
+  const uint32_t K = *n_ptr;
+  const uint32_t base = blockIdx.y * kRankGroup * kRankChunk;
   if (blockIdx.x * blockDim.x >= K || base >= K) return;
-  uint32_t m = min(CHUNK, K - base);
+  const uint32_t m = min(kRankGroup * kRankChunk, K - base);
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    sk[i] = tab.kernel_id[base + i];
-    st[i] = tab.task_id[base + i];
+    sk[i] = skid[base + i];
+    stk[i] = stask[base + i];
   }
   __syncthreads();
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= K) return;
-  uint64_t mk = tab.kernel_id[r];
-  uint32_t mt = tab.task_id[r];
+  const uint64_t mk = tab.kernel_id[r];
+  const uint32_t mt = tab.task_id[r];
   uint32_t cnt = 0;
-#pragma unroll 8
-  for (uint32_t i = 0; i < m; i++) cnt += key_less(st[i], sk[i], mt, mk) ? 1u : 0u;
+  for (uint32_t c0 = 0; c0 < m; c0 += kRankChunk) {
+    uint32_t lo = c0, hi = min(c0 + kRankChunk, m);  // keys of the chunk below (mt, mk)
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (key_less(stk[mid], sk[mid], mt, mk))
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    cnt += lo - c0;
+  }
   if (cnt) atomicAdd(rank + r, cnt);
 }
 

@@ -62,12 +62,12 @@ __global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint6
   const uint32_t skew = (uint32_t)(reinterpret_cast<uintptr_t>(t.bytes) & 15);
   const uint32_t lo = a + skew, hi = b + skew;  // byte range relative to base
   const uint32_t c_end = (hi + 15) >> 4;
-  const unsigned char* sb = reinterpret_cast<const unsigned char*>(buf[w]);
   for (uint32_t c0 = lo >> 4; c0 < c_end; c0 += CH) {
     const uint32_t nch = min(CH, c_end - c0);
     for (uint32_t i = lane; i < nch; i += 32) buf[w][i] = __ldg(base + c0 + i);
     __syncwarp();
     if (lane == 0) {
+      const unsigned char* sb = reinterpret_cast<const unsigned char*>(buf[w]);
       const uint32_t p1 = min(hi, (c0 + nch) * 16);
       for (uint32_t pos = max(lo, c0 * 16); pos < p1; pos++) {
         h ^= (uint64_t)sb[pos - c0 * 16];
