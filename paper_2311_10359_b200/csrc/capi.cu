@@ -17,13 +17,13 @@ __global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint6
                          uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*, uint32_t*);
 __global__ void k_hot_select(const fikit_status_t*, const uint32_t*, const Tuple*, uint32_t, Tuple*, uint32_t*);
 __global__ void k_tile_bucket(const fikit_record_t*, uint32_t, const uint32_t*, uint8_t*, uint32_t*);
-__global__ void k_tile_plan(uint32_t*, uint32_t, uint32_t, uint32_t, const uint32_t*, uint32_t*, Phase*,
-                            fikit_status_t*);
+__global__ void k_tile_plan(uint32_t*, uint32_t, uint32_t, uint32_t, const uint32_t*, uint32_t*, uint32_t*,
+                            uint32_t*, uint32_t*, fikit_status_t*);
 __global__ void k_tile_scatter(const uint8_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
                           uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, fikit_table_t,
-                          Tuple*, const Tuple*, const uint32_t*, const uint32_t*, const Phase*, const uint32_t*,
-                          uint32_t*);
+                          Tuple*, const Tuple*, const uint32_t*, uint32_t*, const uint32_t*, uint32_t*,
+                          const uint32_t*, const uint32_t*, uint32_t*);
 size_t measure_smem_bytes();
 int measure_threads();
 struct FinRow;
@@ -99,13 +99,13 @@ struct Ws {
   uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
   uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }  // header [kHotHdr]
   Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 4ull * kHotHdr); }  // [kBuckets + 1][kHotMax]
-  uint32_t* bcount() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }
-  uint32_t* bcursor() const { return bcount() + kBuckets; }
-  uint32_t* nphase() const { return bcursor() + kBuckets; }
-  Phase* plan() const { return reinterpret_cast<Phase*>(nphase() + kMaxCTAs); }
+  uint32_t* cur() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }  // [kSchedWords]
+  uint32_t* bend() const { return cur() + kSchedWords; }                          // [kSchedWords]
+  uint32_t* act() const { return bend() + kSchedWords; }                          // [kSchedWords]
+  uint32_t* first() const { return act() + kSchedWords; }                         // [kMaxCTAs]
   uint32_t* blkoff() const {  // [kSortBlocks][kBuckets]
     return reinterpret_cast<uint32_t*>(
-        base + align256(L.tiles + 8ull * kBuckets + 4ull * kMaxCTAs + sizeof(Phase) * (size_t)kMaxCTAs * kMaxPhases));
+        base + align256(L.tiles + 12ull * kSchedWords + 4ull * kMaxCTAs));
   }
   uint8_t* tile_bucket() const {
     return reinterpret_cast<uint8_t*>(blkoff()) + align256(4ull * kSortBlocks * kBuckets);
@@ -265,14 +265,15 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   if (sb > 2u * num_sms()) sb = 2u * num_sms();
   k_tile_bucket<<<sb, 1024, 0, s>>>(recs, ntiles, w.hot_n(), w.tile_bucket(), w.blkoff());
   if (int r = launched()) return r;
-  k_tile_plan<<<1, 1024, 0, s>>>(w.blkoff(), sb, ntiles, grid, w.hot_n(), w.nphase(), w.plan(), w.st());
+  k_tile_plan<<<1, 1024, 0, s>>>(w.blkoff(), sb, ntiles, grid, w.hot_n(), w.cur(), w.bend(), w.act(), w.first(),
+                                 w.st());
   if (int r = launched()) return r;
   k_tile_scatter<<<sb, 1024, 0, s>>>(w.tile_bucket(), ntiles, w.hot_n(), w.blkoff(), w.order());
   if (int r = launched()) return r;
   k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
                                                   sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
-                                                  t, w.row_tuple(), w.hot(), w.hot_n(), w.order(), w.plan(),
-                                                  w.nphase(), out_row);
+                                                  t, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.bend(),
+                                                  w.act(), w.first(), w.order(), out_row);
   return launched();
 }
 

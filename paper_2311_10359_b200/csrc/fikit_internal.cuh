@@ -33,7 +33,6 @@ constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (
 // Task-partitioned scheduling of fikit_measure: warp-tiles (32 launches) are bucketed by a
 // hash of their first launch's task_id; every bucket has its own hot set.
 constexpr uint32_t kBuckets = 64;
-constexpr uint32_t kMaxPhases = 8;  // bucket ranges a CTA may cover
 constexpr uint32_t kMaxCTAs = 1024;
 constexpr uint32_t kSortBlocks = 160;  // blocks of the tile counting sort (each a contiguous chunk)
 constexpr uint32_t kGlobalSet = kBuckets;  // hot-set index of the global (all-task) hot set
@@ -47,11 +46,13 @@ constexpr int kRegThreads = 256;  // k_simulate_reg block (8 warps, one scenario
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
 // u32 words of the 256-B status region past fikit_status_t, zeroed with it: replay work counters
 constexpr uint32_t kSchedWord1 = 32, kSchedWord2 = 33;
-struct Phase {
-  // sorted-tile range [p0, p1) (one bucket's tiles), swept by g CTAs of which this is number c:
-  // warp w of this CTA takes positions p0 + c * WARPS + w + j * g * WARPS
-  uint32_t bucket, p0, p1, cg;  // cg = c << 16 | g
-};
+// Dynamic tile schedule (k_tile_plan -> k_measure): bucket b's tiles are the sorted positions
+// [cur[b], bend[b]); warps claim them one at a time with an atomic on cur[b].  first[c] is the
+// bucket CTA c starts on (kNoBucket: none); a CTA whose bucket runs dry moves to the bucket
+// with the most unclaimed tiles among those nobody works on or with > 128 left (act[b]: CTAs
+// working on b).  Bucket kGlobalSet (address-order mode) is [0, ntiles).
+constexpr uint32_t kNoBucket = 0xFFFFFFFFu;
+constexpr uint32_t kSchedWords = kBuckets + 8;  // cur[] and bend[] length
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -86,11 +87,11 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o = align256(o + 4ull * kHotHdr + sizeof(Tuple) * (size_t)kHotMax * (kBuckets + 1));
   L.fin = o;  // FinRow[cap] (336 B), rank[cap], sorted chunk keys: kid[cap] (8-aligned), task[cap]
   o = align256(o + 352ull * cap + 1024);
-  // tiles: bcount[kBuckets], bcursor[kBuckets], nphase[kMaxCTAs], plan[kMaxCTAs][kMaxPhases],
+  // tiles: cur[kSchedWords], bend[kSchedWords], act[kSchedWords], first[kMaxCTAs] (u32),
   //        blkoff[kSortBlocks][kBuckets], tile_bucket[ntiles] (u8), order[ntiles] (u32)
   L.ntiles = (n_records + kTileLaunches - 1) / kTileLaunches;
   L.tiles = o;
-  o = align256(o + 8ull * kBuckets + 4ull * kMaxCTAs + sizeof(Phase) * (size_t)kMaxCTAs * kMaxPhases);
+  o = align256(o + 12ull * kSchedWords + 4ull * kMaxCTAs);
   o = align256(o + 4ull * kSortBlocks * kBuckets);
   o = align256(o + L.ntiles);
   o = align256(o + 4ull * L.ntiles);

@@ -286,26 +286,29 @@ __global__ void __launch_bounds__(1024) k_tile_bucket(const fikit_record_t* __re
   for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) blkcnt[blockIdx.x * kBuckets + i] = h[i];
 }
 
-// One block of 1024 threads.  Address-order mode: CTA c sweeps all tiles with the global hot set
-// (c-th of G interleaved CTAs).  Task mode: blk[k][b] (block k's count of bucket-b tiles) becomes
-// block k's first sorted position for bucket b (column scans in shared memory), and thread 0
-// lays out each CTA's phases.  Every non-empty bucket gets g_b >= 1 CTAs in proportion to its
-// tiles (largest remainder); the g_b CTAs of a bucket sweep its sorted range together
-// (interleaved warp-tiles), so at most one moving window per bucket touches DRAM.  With more
-// non-empty buckets than CTAs, CTA c takes a group of consecutive buckets, one phase each (the
-// last phase also takes any further buckets: correct, those launches go cold).
+// One block of 1024 threads.  Address-order mode: one bucket (kGlobalSet) = all tiles in
+// address order, every CTA starts on it.  Task mode: blk[k][b] (block k's count of bucket-b
+// tiles) becomes block k's first sorted position for bucket b (column scans in shared memory),
+// the buckets' sorted ranges go to cur[] / bend[], and each CTA gets a first bucket: every
+// non-empty bucket g_b >= 1 CTAs in proportion to its tiles (smallest per-CTA load L with
+// sum_b ceil(c_b / L) <= G, leftovers to the most loaded); with more non-empty buckets than
+// CTAs, CTA c starts on the c-th.  The rest is dynamic (warps claim tiles, CTAs move on).
 __global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, uint32_t nblk, uint32_t ntiles,
                                                     uint32_t G, const uint32_t* __restrict__ hot_hdr,
-                                                    uint32_t* __restrict__ nphase, Phase* __restrict__ plan,
+                                                    uint32_t* __restrict__ cur, uint32_t* __restrict__ bend,
+                                                    uint32_t* __restrict__ act, uint32_t* __restrict__ first,
                                                     fikit_status_t* st) {
   __shared__ uint32_t m[kSortBlocks * kBuckets];
   __shared__ uint32_t bcount[kBuckets], start[kBuckets + 1], s_g[kBuckets], s_need[2];
   const uint32_t tid = threadIdx.x;
-  if (!use_task_buckets(hot_hdr)) {
-    for (uint32_t c = tid; c < G; c += blockDim.x) {
-      plan[c * kMaxPhases] = Phase{kGlobalSet, 0u, ntiles, (c << 16) | G};
-      nphase[c] = 1;
-    }
+  const bool task_mode = use_task_buckets(hot_hdr);
+  for (uint32_t b = tid; b < kSchedWords; b += blockDim.x) {
+    cur[b] = 0;
+    bend[b] = (!task_mode && b == kGlobalSet) ? ntiles : 0u;
+    act[b] = 0;
+  }
+  if (!task_mode) {
+    for (uint32_t c = tid; c < G; c += blockDim.x) first[c] = kGlobalSet;
     return;
   }
   for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) m[i] = blk[i];
@@ -346,7 +349,11 @@ __global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, 
     }
     st->schedule = 1;
     st->n_task_buckets = nb;
-    for (uint32_t c = 0; c < G; c++) nphase[c] = 0;
+    for (uint32_t b = 0; b < kBuckets; b++) {
+      cur[b] = start[b];
+      bend[b] = start[b + 1];
+    }
+    for (uint32_t c = 0; c < G; c++) first[c] = kNoBucket;
     if (nb > 0 && nb <= G) {
       // g_b CTAs for bucket b: per-CTA load c_b / g_b balanced (see below); leftovers go to the
       // buckets with the largest per-CTA load
@@ -366,27 +373,11 @@ __global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, 
       }
       uint32_t c = 0;
       for (uint32_t b = 0; b < kBuckets; b++)
-        for (uint32_t i = 0; i < s_g[b]; i++, c++) {
-          plan[c * kMaxPhases] = Phase{b, start[b], start[b + 1], (i << 16) | s_g[b]};
-          nphase[c] = 1;
-        }
-    } else if (nb > G) {  // more non-empty buckets than CTAs: consecutive buckets per CTA
-      uint32_t b = 0;
-      for (uint32_t c = 0; c < G; c++) {
-        const uint32_t want = (uint32_t)((uint64_t)(c + 1) * nb / G) - (uint32_t)((uint64_t)c * nb / G);
-        uint32_t np = 0;
-        for (uint32_t i = 0; i < want; i++) {
-          while (!bcount[b]) b++;
-          if (np < kMaxPhases) {
-            plan[c * kMaxPhases + np] = Phase{b, start[b], start[b + 1], 1u};
-            np++;
-          } else {
-            plan[c * kMaxPhases + kMaxPhases - 1].p1 = start[b + 1];  // contiguous in sorted order
-          }
-          b++;
-        }
-        nphase[c] = np;
-      }
+        for (uint32_t i = 0; i < s_g[b]; i++, c++) first[c] = b;
+    } else if (nb > G) {  // more non-empty buckets than CTAs: CTA c starts on the c-th
+      uint32_t c = 0;
+      for (uint32_t b = 0; b < kBuckets && c < G; b++)
+        if (bcount[b]) first[c++] = b;
     }
   }
   __syncthreads();
@@ -472,6 +463,7 @@ struct Smem {
   uint4 mm[kHotMax];              // min, max (u32) of duration, then of gap (values < 2^32): one 16-B load
   uint32_t grow[kHotMax];         // slot -> global row
   uint32_t hot_n;
+  uint32_t next_bucket;
   unsigned long long overlap;
 };
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA)");
@@ -606,8 +598,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
               const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
               uint32_t n_sigs, IndexEntry* idx, uint32_t slots, Tuple* tidx, uint32_t tslots, fikit_status_t* st,
               fikit_table_t tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
-              const uint32_t* __restrict__ hot_n_all, const uint32_t* __restrict__ order,
-              const Phase* __restrict__ plan, const uint32_t* __restrict__ nphase, uint32_t* __restrict__ out_row) {
+              const uint32_t* __restrict__ hot_n_all, uint32_t* cur, const uint32_t* __restrict__ bend, uint32_t* act,
+              const uint32_t* __restrict__ first, const uint32_t* __restrict__ order, uint32_t* __restrict__ out_row) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
@@ -643,9 +635,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     __syncthreads();
   };
-  // reduce the shared rows into the table (end of a phase)
-  auto flush_hot_set = [&]() {
-    flush_epoch(S, tab, tid);
+  // min / max of the shared rows into the table (end of a phase; bins and sums were flushed
+  // by the last epoch)
+  auto flush_hot_set_ext = [&]() {
     for (uint32_t e = tid, hn = min(S.hot_n, kHotMax); e < hn; e += mk::CONSUMERS) {
       const uint32_t row = S.grow[e];
 #pragma unroll
@@ -660,32 +652,37 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   };
   __syncthreads();
 
-  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  In a phase, warp w takes sorted
-  // positions ph_p0 + w + j * ph_step; its j-th tile there is the (kk0 + j)-th tile its stage
-  // holds in this launch (mbarrier parity (kk0 + j) & 1).
+  // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  A warp's tiles are claimed one
+  // at a time from its CTA's current bucket (cur[b]: next unclaimed sorted position, bend[b]:
+  // end), through a three-round pipeline so no latency is exposed: a position is claimed (L2
+  // atomic) in round r, mapped to its tile (order[], task mode) in round r + 1, and the tile's
+  // TMA is issued in round r + 2 as soon as the stage has been read.  kk counts the tiles the
+  // warp's stage has held in this launch (mbarrier parity kk & 1).
   const uint32_t n32 = (uint32_t)n;
-  uint32_t ph_p0 = 0, ph_step = mk::WARPS, kk0 = 0, my_tiles = 0;
+  uint32_t kk = 0;
   uint32_t sfirst = 0;  // (all lanes) first launch of the tile in the stage
-  // the warp's upcoming tiles: lane l holds the tile of phase position jbase + l
-  // (ordn: the window after it, loaded one window ahead so the refill never waits on L2)
-  uint32_t ord = 0, ordn = 0, jbase = 0;
   const bool by_task = use_task_buckets(hot_n_all);  // else sorted position = tile
-  auto ld_ord = [&](uint32_t j) -> uint32_t {
-    const uint32_t p = ph_p0 + warp + j * ph_step;
-    return j < my_tiles ? (by_task ? __ldg(order + p) : p) : 0u;
+  uint32_t cb = kNoBucket, cb_end = 0;                // the CTA's current bucket
+  constexpr uint32_t kNone = 0xFFFFFFFFu;
+  // Positions are claimed kClaim at a time (one L2 atomic per kClaim tiles: a single counter
+  // serves every warp in address-order mode); the next range's atomic is issued when the
+  // current range is taken, so its result is needed only kClaim tiles later.
+  constexpr uint32_t kClaim = 8;
+  uint32_t pc = kNone;   // lane 0: claimed position
+  uint32_t tn = kNone;   // lane 0: tile of the previous claim (order[] load in flight)
+  uint32_t q_pos = 0, q_end = 0, nx = kNone;  // lane 0: current range, next range's start
+  auto claim = [&]() {   // lane 0
+    pc = kNone;
+    if (q_pos >= q_end) {
+      if (nx == kNone || nx >= cb_end) return;  // drained (claims are monotone)
+      q_pos = nx;
+      q_end = min(nx + kClaim, cb_end);
+      nx = atomicAdd(cur + cb, kClaim);
+    }
+    pc = q_pos++;
   };
-  auto load_window = [&](uint32_t jb) {
-    jbase = jb;
-    ord = ld_ord(jb + lane);
-    ordn = ld_ord(jb + 32 + lane);
-  };
-  auto next_window = [&]() {
-    jbase += 32;
-    ord = ordn;
-    ordn = ld_ord(jbase + 32 + lane);
-  };
-  auto tile_first = [&](uint32_t j) -> uint32_t {  // all lanes; task mode: j in [jbase, jbase + 32)
-    return (by_task ? __shfl_sync(0xffffffffu, ord, j - jbase) : ph_p0 + warp + j * ph_step) * mk::CH;
+  auto tile_of_claim = [&]() {  // lane 0: position pc -> tile
+    tn = pc == kNone ? kNone : (by_task ? __ldg(order + pc) : pc);
   };
   // 1-D TMA of a tile (+ the next launch) into the warp's stage (lane 0)
   auto issue = [&](uint32_t first) {
@@ -867,70 +864,99 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (np >= 24) flush_cold();
   };
 
-  const uint32_t nph = nphase[blockIdx.x];
-  for (uint32_t ph = 0; ph < nph; ph++) {
-    const Phase P = plan[blockIdx.x * kMaxPhases + ph];
-    load_hot_set(P.bucket);
-    const uint32_t pc = P.cg >> 16, pg = P.cg & 0xFFFFu;
-    ph_p0 = P.p0 + pc * mk::WARPS;          // this CTA's first position; warp w adds w
-    ph_step = pg * mk::WARPS;               // positions between a warp's consecutive tiles
-    const uint32_t span = P.p1 > ph_p0 ? P.p1 - ph_p0 : 0;
-    my_tiles = span > (uint32_t)warp ? (span - warp + ph_step - 1) / ph_step : 0;
-    const uint32_t rounds = span ? (span + ph_step - 1) / ph_step : 0;  // CTA-uniform: warp 0 has the most
-    if (by_task) load_window(0);
-    {
-      const uint32_t f0 = tile_first(0);
-      sfirst = f0;
-      if (lane == 0 && my_tiles > 0) issue(f0);
+  uint32_t* s_next = &S.next_bucket;
+  cb = first[blockIdx.x];
+  while (cb != kNoBucket) {
+    if (tid == 0) atomicAdd(act + cb, 1u);
+    load_hot_set(cb);
+    cb_end = bend[cb];
+    q_pos = q_end = 0;
+    if (lane == 0) nx = atomicAdd(cur + cb, kClaim);
+    // prime the pipeline: the first tile's TMA, the second tile's order[] load, a third claim
+    bool staged = false;  // (all lanes) a tile is in flight to the stage
+    if (lane == 0) {
+      claim();
+      tile_of_claim();
+      claim();
     }
-    // Each round reads the warp's tile (both halves, A and B) into registers, refills the stage
-    // with the next tile, then processes A and B with their identity probes interleaved (two
-    // independent dependency chains per lane).
-    for (uint32_t r = 0; r < rounds; r++) {
-      Rec A, B;
-      A.live = B.live = A.valid = B.valid = false;
-      if (r < my_tiles) {
-        mbar_wait_s(s_full + 8u * warp, (kk0 + r) & 1u);
+    {
+      const uint32_t t0 = __shfl_sync(0xffffffffu, tn, 0);
+      if (t0 != kNone) {
+        staged = true;
+        sfirst = t0 * mk::CH;
+        if (lane == 0) issue(sfirst);
+      }
+      if (lane == 0) {
+        tile_of_claim();
+        claim();
+      }
+    }
+    // epochs: up to EPOCH_ROUNDS tiles per warp between CTA barriers (16-bit accumulators)
+    for (;;) {
+      for (uint32_t r = 0; r < (uint32_t)mk::EPOCH_ROUNDS && staged; r++) {
+        // Each round reads the warp's tile (both halves, A and B) into registers, refills the
+        // stage with the next tile, then processes A and B with their identity probes
+        // interleaved (two independent dependency chains per lane).
+        Rec A, B;
+        mbar_wait_s(s_full + 8u * warp, kk & 1u);
+        kk++;
         load_half(0, A);
         load_half(1, B);
+        // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        const uint32_t tnext = __shfl_sync(0xffffffffu, tn, 0);
+        staged = tnext != kNone;
+        if (staged) {
+          sfirst = tnext * mk::CH;
+          if (lane == 0) issue(sfirst);
+        }
+        if (lane == 0) {
+          tile_of_claim();
+          claim();
+        }
+        // home buckets of both launches together (one 8-B load each), then speculative
+        // verification of the slot whose tag matches; a miss is final unless the bucket is full
+        const uint4 tA = mk::ld_bucket(S, A.hk & (mk::TAG_Q - 1)), tB = mk::ld_bucket(S, B.hk & (mk::TAG_Q - 1));
+        uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
+        const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
+        const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
+        const bool vA = verify(eA, A) & (cA != 0u);
+        const bool vB = verify(eB, B) & (cB != 0u);
+        int sA = -1, sB = -1;
+        if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
+        if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);
+        if (sA >= 0) update(A, sA);
+        if (sB >= 0) update(B, sB);
+        if (A.live && !A.valid) flag_record(st, A.gi);
+        if (B.live && !B.valid) flag_record(st, B.gi);
+        compact(A, A.valid && sA < 0);
+        compact(B, B.valid && sB < 0);
       }
-      // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      const uint32_t jn = r + 1;
-      if (by_task && jn >= jbase + 32) next_window();
-      const uint32_t fn = tile_first(jn);
-      if (jn < my_tiles) {
-        sfirst = fn;
-        if (lane == 0) issue(fn);
-      }
-      // home buckets of both launches together (one 16-B load each), then speculative
-      // verification of the slot whose tag matches; a miss is final unless the bucket is full
-      const uint4 tA = mk::ld_bucket(S, A.hk & (mk::TAG_Q - 1)), tB = mk::ld_bucket(S, B.hk & (mk::TAG_Q - 1));
-      uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
-      const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
-      const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
-      const bool vA = verify(eA, A) & (cA != 0u);
-      const bool vB = verify(eB, B) & (cB != 0u);
-      int sA = -1, sB = -1;
-      if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
-      if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);
-      if (sA >= 0) update(A, sA);
-      if (sB >= 0) update(B, sB);
-      if (A.live && !A.valid) flag_record(st, A.gi);
-      if (B.live && !B.valid) flag_record(st, B.gi);
-      compact(A, A.valid && sA < 0);
-      compact(B, B.valid && sB < 0);
-      if ((r + 1) % mk::EPOCH_ROUNDS == 0 && r + 1 < rounds) {  // 16-bit accumulators: flush before overflow
-        consumer_sync();
-        flush_epoch(S, tab, tid);
-        consumer_sync();
-      }
+      const bool all_done = __syncthreads_and(!staged);
+      flush_epoch(S, tab, tid);
+      __syncthreads();
+      if (all_done) break;
     }
-    kk0 += my_tiles;
-    __syncthreads();  // every warp is done with this bucket's tiles
-    flush_hot_set();
-    __syncthreads();  // before the next phase reloads the shared rows
+    flush_hot_set_ext();
+    // next bucket: the most unclaimed tiles among buckets nobody works on (they must be taken)
+    // or with more than 128 left (worth a hot-set reload); every claim of cb is done
+    if (tid == 0) {
+      atomicSub(act + cb, 1u);
+      uint32_t best = kNoBucket, most = 0;
+      for (uint32_t b = 0; b < kSchedWords; b++) {
+        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b);
+        const uint32_t left = e > c ? e - c : 0u;
+        if (left > most && (left > 128u || *(volatile uint32_t*)(act + b) == 0u)) {
+          most = left;
+          best = b;
+        }
+      }
+      *s_next = best;
+    }
+    __syncthreads();  // (also: every warp is done with the shared rows before they are reloaded)
+    cb = *s_next;
+    __syncthreads();
   }
   if (np) flush_cold();
   // warp-aggregate the overlap count
