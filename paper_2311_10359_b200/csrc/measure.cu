@@ -298,8 +298,9 @@ __global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, 
                                                     uint32_t* __restrict__ cur, uint32_t* __restrict__ bend,
                                                     uint32_t* __restrict__ act, uint32_t* __restrict__ first,
                                                     fikit_status_t* st) {
+  constexpr uint32_t SEGS = 16;  // column scans: 16 threads per bucket, nblk / 16 blocks each
   __shared__ uint32_t m[kSortBlocks * kBuckets];
-  __shared__ uint32_t bcount[kBuckets], start[kBuckets + 1], s_g[kBuckets], s_need[2];
+  __shared__ uint32_t segsum[SEGS][kBuckets], bcount[kBuckets], start[kBuckets + 1];
   const uint32_t tid = threadIdx.x;
   const bool task_mode = use_task_buckets(hot_hdr);
   for (uint32_t b = tid; b < kSchedWords; b += blockDim.x) {
@@ -312,73 +313,75 @@ __global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, 
     return;
   }
   for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) m[i] = blk[i];
+  for (uint32_t c = tid; c < G; c += blockDim.x) first[c] = kNoBucket;
   __syncthreads();
-  if (tid < kBuckets) {
+  // column scans: thread (seg, b) sums its segment, then rewrites it as exclusive offsets
+  const uint32_t sb = tid % kBuckets, seg = tid / kBuckets;
+  const uint32_t per = (nblk + SEGS - 1) / SEGS, k0 = seg * per, k1 = min(nblk, k0 + per);
+  if (seg < SEGS) {
+    uint32_t x = 0;
+    for (uint32_t k = k0; k < k1; k++) x += m[k * kBuckets + sb];
+    segsum[seg][sb] = x;
+  }
+  __syncthreads();
+  if (seg < SEGS) {
     uint32_t run = 0;
-    for (uint32_t k = 0; k < nblk; k++) {
-      const uint32_t c = m[k * kBuckets + tid];
-      m[k * kBuckets + tid] = run;
+    for (uint32_t q = 0; q < seg; q++) run += segsum[q][sb];
+    for (uint32_t k = k0; k < k1; k++) {
+      const uint32_t c = m[k * kBuckets + sb];
+      m[k * kBuckets + sb] = run;
       run += c;
     }
-    bcount[tid] = run;
+    if (seg == SEGS - 1) bcount[sb] = run;
   }
   __syncthreads();
-  // smallest per-CTA load L with sum_b ceil(c_b / L) <= G (binary search, 64 threads; uniform loop)
-  {
-    uint32_t lo = (ntiles + G - 1) / G, hi = ntiles;  // f(hi) = #non-empty buckets <= G assumed
-    while (lo < hi) {
-      const uint32_t mid = lo + (hi - lo) / 2;
-      uint32_t need = 0;
-      if (tid < kBuckets) need = (bcount[tid] + mid - 1) / mid;
-      need = __reduce_add_sync(0xffffffffu, need);
-      if ((tid & 31) == 0 && tid < kBuckets) s_need[tid >> 5] = need;
-      __syncthreads();
-      const uint32_t tot = s_need[0] + s_need[1];
-      __syncthreads();
-      if (tot <= G) hi = mid; else lo = mid + 1;
+  if (tid < 32) {  // one warp: bucket starts, the first-bucket assignment (2 buckets per lane)
+    const uint32_t lane = tid;
+    const uint32_t c0 = bcount[2 * lane], c1 = bcount[2 * lane + 1];
+    uint32_t x = c0 + c1;  // inclusive scan of the pairs
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= (uint32_t)d) x += y;
     }
-    if (tid < kBuckets) s_g[tid] = (bcount[tid] + lo - 1) / lo;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    start[0] = 0;
-    uint32_t nb = 0;
-    for (uint32_t b = 0; b < kBuckets; b++) {
-      start[b + 1] = start[b] + bcount[b];
-      nb += bcount[b] ? 1u : 0u;
+    const uint32_t s0 = x - c0 - c1;
+    start[2 * lane] = s0;
+    start[2 * lane + 1] = s0 + c0;
+    if (lane == 31) start[kBuckets] = x;
+    cur[2 * lane] = s0;
+    bend[2 * lane] = s0 + c0;
+    cur[2 * lane + 1] = s0 + c0;
+    bend[2 * lane + 1] = x;
+    const uint32_t nb = __reduce_add_sync(0xffffffffu, (c0 ? 1u : 0u) + (c1 ? 1u : 0u));
+    if (lane == 0) {
+      st->schedule = 1;
+      st->n_task_buckets = nb;
     }
-    st->schedule = 1;
-    st->n_task_buckets = nb;
-    for (uint32_t b = 0; b < kBuckets; b++) {
-      cur[b] = start[b];
-      bend[b] = start[b + 1];
-    }
-    for (uint32_t c = 0; c < G; c++) first[c] = kNoBucket;
-    if (nb > 0 && nb <= G) {
-      // g_b CTAs for bucket b: per-CTA load c_b / g_b balanced (see below); leftovers go to the
-      // buckets with the largest per-CTA load
-      uint32_t used = 0;
-      for (uint32_t b = 0; b < kBuckets; b++) used += s_g[b];
-      while (used < G) {
-        uint32_t best = 0;
-        uint64_t bn = 0, bd = 1;  // best ratio bn / bd
-        for (uint32_t b = 0; b < kBuckets; b++)
-          if (s_g[b] && (uint64_t)bcount[b] * bd > bn * s_g[b]) {
-            bn = bcount[b];
-            bd = s_g[b];
-            best = b;
-          }
-        s_g[best]++;
-        used++;
+    // g_b = ceil(c_b / L) for the smallest L with sum_b g_b <= G (at least one CTA per bucket
+    // when nb <= G; else every CTA starts on its own bucket); unassigned CTAs start by stealing
+    uint32_t g0, g1;
+    if (nb <= G) {
+      uint32_t lo = (ntiles + G - 1) / G, hi = ntiles;  // sum at hi = nb <= G
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        const uint32_t need = __reduce_add_sync(0xffffffffu, (c0 + mid - 1) / mid + (c1 + mid - 1) / mid);
+        if (need <= G) hi = mid; else lo = mid + 1;
       }
-      uint32_t c = 0;
-      for (uint32_t b = 0; b < kBuckets; b++)
-        for (uint32_t i = 0; i < s_g[b]; i++, c++) first[c] = b;
-    } else if (nb > G) {  // more non-empty buckets than CTAs: CTA c starts on the c-th
-      uint32_t c = 0;
-      for (uint32_t b = 0; b < kBuckets && c < G; b++)
-        if (bcount[b]) first[c++] = b;
+      g0 = (c0 + lo - 1) / lo;
+      g1 = (c1 + lo - 1) / lo;
+    } else {
+      g0 = c0 ? 1u : 0u;
+      g1 = c1 ? 1u : 0u;
     }
+    uint32_t gx = g0 + g1;  // CTA ranges: exclusive scan of g
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, gx, d);
+      if (lane >= (uint32_t)d) gx += y;
+    }
+    const uint32_t cs = gx - g0 - g1;
+    for (uint32_t i = 0; i < g0 && cs + i < G; i++) first[cs + i] = 2 * lane;
+    for (uint32_t i = 0; i < g1 && cs + g0 + i < G; i++) first[cs + g0 + i] = 2 * lane + 1;
   }
   __syncthreads();
   for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) blk[i] = m[i] + start[i % kBuckets];
@@ -865,7 +868,28 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   };
 
   uint32_t* s_next = &S.next_bucket;
+  // the bucket to move to: the most unclaimed tiles among buckets nobody works on (they must
+  // be taken) or with more than 128 left (worth a hot-set reload); CTA-uniform
+  auto pick_bucket = [&]() -> uint32_t {
+    if (tid == 0) {
+      uint32_t best = kNoBucket, most = 0;
+      for (uint32_t b = 0; b < kSchedWords; b++) {
+        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b);
+        const uint32_t left = e > c ? e - c : 0u;
+        if (left > most && (left > 128u || *(volatile uint32_t*)(act + b) == 0u)) {
+          most = left;
+          best = b;
+        }
+      }
+      *s_next = best;
+    }
+    __syncthreads();
+    const uint32_t b = *s_next;
+    __syncthreads();
+    return b;
+  };
   cb = first[blockIdx.x];
+  if (cb == kNoBucket) cb = pick_bucket();
   while (cb != kNoBucket) {
     if (tid == 0) atomicAdd(act + cb, 1u);
     load_hot_set(cb);
@@ -939,24 +963,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       if (all_done) break;
     }
     flush_hot_set_ext();
-    // next bucket: the most unclaimed tiles among buckets nobody works on (they must be taken)
-    // or with more than 128 left (worth a hot-set reload); every claim of cb is done
-    if (tid == 0) {
-      atomicSub(act + cb, 1u);
-      uint32_t best = kNoBucket, most = 0;
-      for (uint32_t b = 0; b < kSchedWords; b++) {
-        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b);
-        const uint32_t left = e > c ? e - c : 0u;
-        if (left > most && (left > 128u || *(volatile uint32_t*)(act + b) == 0u)) {
-          most = left;
-          best = b;
-        }
-      }
-      *s_next = best;
-    }
-    __syncthreads();  // (also: every warp is done with the shared rows before they are reloaded)
-    cb = *s_next;
-    __syncthreads();
+    if (tid == 0) atomicSub(act + cb, 1u);  // every claim of cb is done
+    cb = pick_bucket();  // (its barriers also keep the shared rows until every warp is done)
   }
   if (np) flush_cold();
   // warp-aggregate the overlap count

@@ -179,7 +179,15 @@ def t_eagerrow(m, h):
                "    const uint32_t rowv = S.grow[slot];\n    auto row = [&]() { return rowv; };"), h
 
 
+def t_claim(k):
+    def f(m, h):
+        return sub(m, "constexpr uint32_t kClaim = 8;", f"constexpr uint32_t kClaim = {k};"), h
+    return f
+
+
 VARIANTS = {
+    "k_claim4": [t_claim(4)],
+    "k_claim16": [t_claim(16)],
     "c_bucket": [t_bucket],
     "c_eager": [t_eagerrow],
     "c_bucket_eager": [t_bucket, t_eagerrow],
