@@ -437,7 +437,7 @@ namespace mk {
 constexpr int TILE = 32;                  // launches per half-tile (one per lane)
 constexpr int CH = 2 * TILE;              // launches per warp-tile: one TMA, one wait, two per lane
 static_assert(CH == (int)kTileLaunches, "the schedule's tile is the kernel's warp-tile");
-constexpr int WARPS = 20;                 // warps per CTA; every warp streams and consumes its own tiles (<= 102 registers)
+constexpr int WARPS = 24;                 // warps per CTA; every warp streams and consumes its own tiles (<= 85 registers)
 constexpr int CONSUMERS = WARPS * 32;
 constexpr int THREADS = CONSUMERS;
 constexpr uint32_t TAG_W = 2;             // one-word tags per bucket (one 8-B load per probe)

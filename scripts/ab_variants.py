@@ -33,7 +33,7 @@ def t_idx(n, k):
 
 def t_warps(w, k):
     def f(m, h):
-        m = sub(m, "constexpr int WARPS = 20;", f"constexpr int WARPS = {w};")
+        m = sub(m, "constexpr int WARPS = 24;", f"constexpr int WARPS = {w};")
         return m, sub(h, "constexpr uint32_t kHotMax = 640;", f"constexpr uint32_t kHotMax = {k};")
     return f
 
@@ -192,6 +192,9 @@ VARIANTS = {
     "c_eager": [t_eagerrow],
     "c_bucket_eager": [t_bucket, t_eagerrow],
     "w24": [t_warps(24, 640)],
+    "w28": [t_warps(28, 600)],
+    "w32": [t_warps(32, 520)],
+    "w28b": [t_warps(28, 560)],
     "w16": [t_warps(16, 640)],
     "x_noepoch": [t_noepoch],
     "g_gionly": [t_gionly],
