@@ -78,6 +78,8 @@ def lib():
         _lib.or_fill_batch.argtypes = [p, p, p, p, p, p, p, u32, p, p, u32, u64, u32, p, p, p, p, p,
                                        C.POINTER(Status)]
         _lib.or_simulate.argtypes = [p, p, p, u32, p, p, p, u32, u32, p, p, p, u32, u64, u32, p, p, p]
+        _lib.or_predict.restype = C.c_int
+        _lib.or_predict.argtypes = [C.POINTER(_Table), u32, u32]
         _lib.or_simulate_batch.argtypes = [p, p, p, p, p, p, p, u32, p, p, p, u32, u64, u32, p, p, p, p,
                                            C.POINTER(Status)]
     return _lib
@@ -261,10 +263,28 @@ def simulate_batch(hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, scenarios, 
     return out, fg, ls, so, st.as_dict()
 
 
-def pipeline(cfg, capacity=None):
-    """measure the config's trace, resolve its replay inputs, replay them."""
+PREDICT_MEAN, PREDICT_PERCENTILE, PREDICT_EXTREMES = 0, 1, 2
+
+
+def predict(tab: Table, mode: int, pct: int = 90) -> Table:
+    """A copy of tab whose dur_mean / gap_mean columns hold the chosen predictor (or_predict:
+    0 = the paper's means, 1 = conservative histogram percentile pct, 2 = max / min)."""
+    arrs = {k: np.array(v, copy=True) for k, v in tab.__dict__.items() if k != "n_rows"}
+    t = _Table(**{k: _ptr(v) for k, v in arrs.items()}, capacity=max(1, arrs["kernel_id"].shape[0]),
+               n_rows=tab.n_rows)
+    rc = lib().or_predict(C.byref(t), mode, pct)
+    if rc != 0:
+        raise ValueError(f"or_predict: mode {mode} pct {pct} -> {rc}")
+    return Table(n_rows=tab.n_rows, **arrs)
+
+
+def pipeline(cfg, capacity=None, predictor=None):
+    """measure the config's trace, resolve its replay inputs, replay them; predictor =
+    (mode, pct) rewrites the table's predictions first (predict())."""
     tr = cfg.trace
     tab, st, _ = measure(tr.records, tr.names, tr.sigs, capacity)
+    if predictor is not None:
+        tab = predict(tab, *predictor)
     res = {"table": tab, "status": st}
     if cfg.replay is not None:
         rp = cfg.replay

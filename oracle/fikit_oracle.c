@@ -581,3 +581,53 @@ int or_simulate_batch(const uint32_t* hp_row, const uint64_t* hp_dur, const uint
   free(ls);
   return OR_OK;
 }
+
+/* ---- predictor variants ("dynamic duration and idling
+ * prediction", the "same ID, different duration" weakness).  The replay reads a
+ * row's predicted duration q (Alg.1 line 4) from dur_mean and its predicted gap p
+ * (line 3) from gap_mean; this rewrites those two columns (readings R26-R28):
+ *   mode 0 (the paper): the integer means SK, SG (R8).
+ *   mode 1 (histogram percentile, conservative): with cum(b) the count of bins
+ *     0..b and c the row's count, b_P = the smallest b with 100*cum(b) >= P*c (and
+ *     cum(b) >= 1).  Duration: the upper edge of bin b_P (2^b - 1; bin 31 is
+ *     unbounded: the row's max), capped at the row's max.  Gap: the lower edge of
+ *     bin b_(100-P) (2^(b-1); bin 0: 0), raised to the row's min.  1 <= P <= 99.
+ *   mode 2 (extremes): duration = max, gap = min.
+ * A row without samples predicts 0 in every mode. */
+static uint32_t pct_bin(const uint32_t* h, uint64_t c, uint32_t P) {
+  uint64_t cum = 0;
+  for (uint32_t b = 0; b < 32; b++) {
+    cum += h[b];
+    if (cum >= 1 && 100 * cum >= (uint64_t)P * c) return b;
+  }
+  return 31;
+}
+
+int or_predict(otable_t* tab, uint32_t mode, uint32_t pct) {
+  if (mode > 2 || (mode == 1 && (pct < 1 || pct > 99))) return OR_E_ARG;
+  for (uint32_t r = 0; r < tab->n_rows; r++) {
+    const uint64_t dc = tab->dur_cnt[r], gc = tab->gap_cnt[r];
+    uint64_t d = 0, g = 0;
+    if (mode == 0) {
+      d = mean_of(tab->dur_sum[r], dc);
+      g = mean_of(tab->gap_sum[r], gc);
+    } else if (mode == 1) {
+      if (dc) {
+        const uint32_t b = pct_bin(tab->dur_hist + (size_t)r * 32, dc, pct);
+        const uint64_t up = b == 0 ? 0 : (b < 31 ? (1ull << b) - 1 : tab->dur_max[r]);
+        d = up < tab->dur_max[r] ? up : tab->dur_max[r];
+      }
+      if (gc) {
+        const uint32_t b = pct_bin(tab->gap_hist + (size_t)r * 32, gc, 100 - pct);
+        const uint64_t lo = b == 0 ? 0 : (1ull << (b - 1));
+        g = lo > tab->gap_min[r] ? lo : tab->gap_min[r];
+      }
+    } else {
+      d = dc ? tab->dur_max[r] : 0;
+      g = gc ? tab->gap_min[r] : 0;
+    }
+    tab->dur_mean[r] = d;
+    tab->gap_mean[r] = g;
+  }
+  return OR_OK;
+}
