@@ -180,6 +180,23 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
 /* Recompute counts and means of an already canonical table (after a multi-GPU merge). */
 int fikit_table_means(const fikit_table_t* tab, void* stream);
 
+/* ---- predictor variants ("dynamic duration and idling
+ * prediction", readings R26-R28) -------------------------------------------------
+ * Rewrites the predictions a finalized table gives the replay (mean[r*2] = the
+ * predicted duration q of Alg.1 line 4, mean[r*2+1] = the predicted gap p of
+ * line 3) for every row r < n_rows, from the row's counts, histogram and extremes:
+ *   FIKIT_PREDICT_MEAN        SK, SG (what finalize / table_means write; R8)
+ *   FIKIT_PREDICT_PERCENTILE  b_P = the smallest bin with 100*cum(b) >= P*count:
+ *                             duration = min(upper edge of b_P, max), gap =
+ *                             max(lower edge of b_(100-P), min); 1 <= pct <= 99
+ *   FIKIT_PREDICT_EXTREMES    duration = max, gap = min
+ * A row without samples predicts 0.  Device arrays of `tab` are read and written
+ * in place; stream-ordered.  Errors: FIKIT_E_ARG (bad table, mode or pct). */
+#define FIKIT_PREDICT_MEAN 0u
+#define FIKIT_PREDICT_PERCENTILE 1u
+#define FIKIT_PREDICT_EXTREMES 2u
+int fikit_table_predict(const fikit_table_t* tab, uint32_t mode, uint32_t pct, void* stream);
+
 /* ---- resolve (Alg. 1 lines 3-5) ------------------------------------
  * For fresh launches (HP template runs, LP requests): out_row[i] = canonical
  * row of (task_id, KID_i) in the finalized table or FIKIT_NO_ROW;

@@ -23,7 +23,7 @@ OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME = 0, -1, -2, -3, -4, -5
 NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
-           "fikit_table_finalize", "fikit_table_means", "fikit_resolve", "fikit_lookup", "fikit_fill",
+           "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
            "fikit_simulate_batch", "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
 
@@ -76,6 +76,7 @@ def lib():
         L.fikit_measure.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, sz, p]
         L.fikit_table_finalize.argtypes = [C.POINTER(TableC), p, u64, p, sz, p]
         L.fikit_table_means.argtypes = [C.POINTER(TableC), p]
+        L.fikit_table_predict.argtypes = [C.POINTER(TableC), u32, u32, p]
         L.fikit_resolve.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, p, p, sz, p]
         L.fikit_lookup.argtypes = [C.POINTER(TableC), p, p, u64, p, p]
         L.fikit_fill.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, u32, FillParamsC, p, p, p, p, p, p, sz, p]
@@ -253,6 +254,14 @@ def table_finalize(table: Table, ws: Workspace, out_row=None, n: int = 0, stream
 
 def table_means(table: Table, stream=None):
     _chk(lib().fikit_table_means(C.byref(table.c), _stream(stream)), "table_means")
+
+
+PREDICT_MEAN, PREDICT_PERCENTILE, PREDICT_EXTREMES = 0, 1, 2
+
+
+def table_predict(table: Table, mode: int, pct: int = 90, stream=None):
+    """fikit_table_predict: the replay's predictions from the table (0 means, 1 percentile pct, 2 extremes)."""
+    _chk(lib().fikit_table_predict(C.byref(table.c), mode, pct, _stream(stream)), "table_predict")
 
 
 def resolve(recs, n: int, names: DevStrTab, sigs: DevStrTab, table: Table, out_row, out_dur, out_gap, ws: Workspace,

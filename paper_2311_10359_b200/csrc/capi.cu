@@ -33,6 +33,7 @@ __global__ void k_fin_rank(const fikit_table_t, const uint32_t*, const uint64_t*
 __global__ void k_fin_scatter(fikit_table_t, const FinRow*, const uint32_t*, const uint32_t*);
 __global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
 __global__ void k_means(fikit_table_t);
+__global__ void k_predict(fikit_table_t, uint32_t, uint32_t);
 __global__ void k_lookup(fikit_table_t, const uint64_t*, const uint32_t*, uint64_t, uint32_t*);
 __global__ void k_resolve(const uint4*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*, uint32_t,
                           uint32_t, fikit_table_t, uint32_t*, uint64_t*, uint64_t*, fikit_status_t*);
@@ -311,6 +312,14 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
 int fikit_table_means(const fikit_table_t* tab, void* stream) {
   if (!table_ok(tab)) return FIKIT_E_ARG;
   k_means<<<(tab->capacity + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*tab);
+  return launched();
+}
+
+int fikit_table_predict(const fikit_table_t* tab, uint32_t mode, uint32_t pct, void* stream) {
+  if (!table_ok(tab) || mode > FIKIT_PREDICT_EXTREMES ||
+      (mode == FIKIT_PREDICT_PERCENTILE && (pct < 1 || pct > 99)))
+    return FIKIT_E_ARG;
+  k_predict<<<(tab->capacity + 7) / 8, 256, 0, (cudaStream_t)stream>>>(*tab, mode, pct);  // a warp per row
   return launched();
 }
 

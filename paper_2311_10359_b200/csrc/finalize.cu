@@ -192,6 +192,52 @@ __device__ __forceinline__ uint32_t find_row(const uint64_t* __restrict__ kid, c
   return (lo < K && __ldg(task + lo) == t && __ldg(kid + lo) == k) ? lo : FIKIT_NO_ROW;
 }
 
+// Predictor variants (R26-R28): a warp per row; lane b holds histogram bin b, a 64-bit
+// inclusive scan gives cum(b), and b_P = the first lane with 100*cum >= P*count (a ballot).
+__global__ void k_predict(fikit_table_t tab, uint32_t mode, uint32_t pct) {
+  const uint32_t K = min(*tab.n_rows, tab.capacity);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= K) return;
+  const uint64_t dc = tab.sums[(size_t)r * 4], ds = tab.sums[(size_t)r * 4 + 1];
+  const uint64_t gc = tab.sums[(size_t)r * 4 + 2], gs = tab.sums[(size_t)r * 4 + 3];
+  const uint64_t dmax = tab.ext[(size_t)r * 4], gmin = ~tab.ext[(size_t)r * 4 + 3];
+  uint64_t d = 0, g = 0;
+  if (mode == FIKIT_PREDICT_MEAN) {
+    d = mean_half_up(ds, dc);
+    g = mean_half_up(gs, gc);
+  } else if (mode == FIKIT_PREDICT_PERCENTILE) {
+    uint64_t cd = tab.hist[(size_t)r * 64 + lane], cg = tab.hist[(size_t)r * 64 + 32 + lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t yd = __shfl_up_sync(0xffffffffu, cd, o), yg = __shfl_up_sync(0xffffffffu, cg, o);
+      if ((int)lane >= o) {
+        cd += yd;
+        cg += yg;
+      }
+    }
+    const uint32_t md = __ballot_sync(0xffffffffu, cd >= 1 && 100 * cd >= (uint64_t)pct * dc);
+    const uint32_t mg = __ballot_sync(0xffffffffu, cg >= 1 && 100 * cg >= (uint64_t)(100 - pct) * gc);
+    if (dc) {  // md != 0: at bin 31, cum = count
+      const uint32_t b = __ffs(md) - 1;
+      const uint64_t up = b == 0 ? 0 : (b < 31 ? (1ull << b) - 1 : dmax);
+      d = up < dmax ? up : dmax;
+    }
+    if (gc) {
+      const uint32_t b = __ffs(mg) - 1;
+      const uint64_t lo = b == 0 ? 0 : (1ull << (b - 1));
+      g = lo > gmin ? lo : gmin;
+    }
+  } else {
+    d = dc ? dmax : 0;
+    g = gc ? gmin : 0;
+  }
+  if (lane == 0) {
+    tab.mean[(size_t)r * 2] = d;
+    tab.mean[(size_t)r * 2 + 1] = g;
+  }
+}
+
 __global__ void k_lookup(fikit_table_t tab, const uint64_t* __restrict__ kid, const uint32_t* __restrict__ task,
                          uint64_t n, uint32_t* __restrict__ out) {
   uint32_t K = min(*tab.n_rows, tab.capacity);

@@ -9,18 +9,20 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve,
+from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve, table_predict,
                simulate_batch, strtab_to_device, table_finalize)
 
 
 class Pipeline:
     def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
                  want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None,
-                 checked: bool = False):
+                 checked: bool = False, predictor: tuple | None = None):
         """checked: verify the workspace status after every call (tests); the
-        bench leaves it off and checks once after warm-up."""
+        bench leaves it off and checks once after warm-up.  predictor: (mode, pct) for
+        fikit_table_predict before every replay (None: the finalized means, the paper's)."""
         torch = _torch()
         self.checked = checked
+        self.predictor = predictor
         self.device = device
         self.n = int(records.shape[0])
         self.capacity = int(capacity if capacity is not None else max(1, min(self.n, 1 << 16)))
@@ -82,6 +84,8 @@ class Pipeline:
         """table: the profile to replay against (default: this pipeline's; the merged one for P > 1)."""
         r = self.replay
         tab = self.table if table is None else table
+        if self.predictor is not None:
+            table_predict(tab, *self.predictor, stream=stream)
         resolve(r["hp_recs"], r["nh"], self.names, self.sigs, tab, r["hp_row"], r["hp_dur"], r["hp_gap"],
                 self.ws, stream=stream)
         self._chk("resolve(hp)", stream)

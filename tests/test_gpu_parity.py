@@ -329,3 +329,45 @@ def test_replay_huge_durations_slow_path(fk, orc):
     tr2 = F.Trace(rec, tr.names, tr.sigs)
     rp = F.random_replay(62, tr2, 200, m_max=60, n_h_max=40, levels=4)
     _replay_parity(fk, orc, F.Config("huge", tr2, rp), 256)
+
+
+@pytest.mark.parametrize("mode,pct", [(0, 50), (1, 10), (1, 50), (1, 90), (2, 50)])
+def test_table_predict_parity(fk, orc, mode, pct):
+    """fikit_table_predict (R26-R28) vs oracle.predict on measured tables: a random trace with
+    zero / huge values and overlaps, and the Zipf structure"""
+    for tr in (F.random_trace(81, 30000, n_ids=300, n_tasks=4, zero_frac=0.1, big_frac=0.05, overlap_frac=0.05),
+               F.zipf_trace(n_runs=2000).trace):
+        ref, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=8192)
+        want = orc.predict(ref, mode, pct)
+        p = run_measure(fk, tr, capacity=8192)
+        fk.table_predict(p.table, mode, pct)
+        p.check()
+        got = p.table.to_numpy()
+        n = ref.n_rows
+        assert np.array_equal(got["dur_mean"], want.dur_mean[:n]), (mode, pct)
+        assert np.array_equal(got["gap_mean"], want.gap_mean[:n]), (mode, pct)
+
+
+@pytest.mark.parametrize("predictor", [(1, 90), (2, 50)])
+def test_replay_with_predictor(fk, orc, predictor):
+    """the whole path with a predictor variant: the replay reads the rewritten predictions"""
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.bert_vgg()
+    ref = orc.pipeline(cfg, capacity=1024, predictor=predictor)
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay,
+                 want_schedule=True, checked=True, predictor=predictor)
+    p.step()
+    assert p.results().tobytes() == ref["results"].tobytes()
+    fg, ls = p.schedule()
+    assert np.array_equal(fg, ref["fill_gap"]) and np.array_equal(ls, ref["lp_start"])
+    base = orc.pipeline(cfg, capacity=1024)
+    assert ref["results"].tobytes() != base["results"].tobytes()  # the predictor changes the schedule
+
+
+def test_table_predict_bad_args(fk):
+    tr = F.random_trace(82, 500)
+    p = run_measure(fk, tr, capacity=64)
+    for mode, pct in ((3, 50), (1, 0), (1, 100)):
+        with pytest.raises(Exception):
+            fk.table_predict(p.table, mode, pct)
