@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--workload", default="zipf", choices=["zipf", "resnet", "bert_vgg", "sweep"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
+    ap.add_argument("--predictor", default=None,
+                    help="mode,pct for fikit_table_predict before each replay (SURVEY §8f row 3; default: the "
+                         "paper's means)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,7 +270,9 @@ def main():
     wl = make_workload(args, rank, world)
     t_gen = time.perf_counter() - t_gen
     stream = torch.cuda.current_stream()
-    p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"])
+    pred = tuple(int(x) for x in args.predictor.split(",")) if args.predictor else None
+    p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"],
+                 predictor=pred)
     n_local = p.n
     dense = fk.Table(wl["cap"]) if world > 1 else None
     ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None
@@ -348,7 +353,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (fikit_synth, seeded)",
-            "config": {"workload": wl["desc"], "records": N, "records_per_gpu": n_local, "scenarios": S_total,
+            "config": {"workload": wl["desc"] + (f" predictor={args.predictor}" if args.predictor else ""),
+                       "records": N, "records_per_gpu": n_local, "scenarios": S_total,
                        "table_rows": p.table.n_rows() if world == 1 else dense.n_rows(),
                        "l2": "inputs (4.8 GB trace) larger than the 126 MB L2; no flush",
                        "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},
