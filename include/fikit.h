@@ -177,6 +177,13 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
 int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* fikit_measure, instrumented: ev_start / ev_stop (cudaEvent_t, created by the caller, may
+ * be null) are recorded on `stream` just before and after the fused streaming kernel
+ * (k_measure), so a benchmark can time the dominant kernel alone inside a live step. */
+int fikit_measure_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next,
+                        fikit_strtab_t names, fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row,
+                        void* ws, size_t ws_bytes, void* stream, void* ev_start, void* ev_stop);
+
 /* Recompute counts and means of an already canonical table (after a multi-GPU merge). */
 int fikit_table_means(const fikit_table_t* tab, void* stream);
 

@@ -23,7 +23,7 @@ OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME = 0, -1, -2, -3, -4, -5
 NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
-           "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
+           "fikit_measure_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
            "fikit_simulate_batch", "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
 
@@ -74,6 +74,7 @@ def lib():
         L.fikit_table_carve.argtypes = [p, u32, C.POINTER(TableC)]
         L.fikit_identify.argtypes = [p, u64, StrTabC, StrTabC, p, p, sz, p]
         L.fikit_measure.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, sz, p]
+        L.fikit_measure_timed.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, sz, p, p, p]
         L.fikit_table_finalize.argtypes = [C.POINTER(TableC), p, u64, p, sz, p]
         L.fikit_table_means.argtypes = [C.POINTER(TableC), p]
         L.fikit_table_predict.argtypes = [C.POINTER(TableC), u32, u32, p]
@@ -242,9 +243,17 @@ def identify(recs, n: int, names: DevStrTab, sigs: DevStrTab, out_kid, ws: Works
 
 
 def measure(recs, n: int, names: DevStrTab, sigs: DevStrTab, table: Table, ws: Workspace, halo=None, out_row=None,
-            stream=None):
-    _chk(lib().fikit_measure(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),
-                             ws.ptr(), ws.nbytes, _stream(stream)), "measure")
+            stream=None, events=None):
+    """events: (start, stop) torch.cuda.Event pair recorded around the fused streaming kernel
+    (fikit_measure_timed; the events must exist, i.e. have been recorded once)."""
+    if events is None:
+        _chk(lib().fikit_measure(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),
+                                 ws.ptr(), ws.nbytes, _stream(stream)), "measure")
+    else:
+        e0, e1 = events
+        _chk(lib().fikit_measure_timed(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c),
+                                       _ptr(out_row), ws.ptr(), ws.nbytes, _stream(stream),
+                                       C.c_void_p(e0.cuda_event), C.c_void_p(e1.cuda_event)), "measure_timed")
 
 
 def table_finalize(table: Table, ws: Workspace, out_row=None, n: int = 0, stream=None):

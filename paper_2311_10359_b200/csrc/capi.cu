@@ -208,9 +208,9 @@ int fikit_identify(const fikit_record_t* recs, uint64_t n, fikit_strtab_t names,
   return launched();
 }
 
-int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
-                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes,
-                  void* stream) {
+static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                        fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws,
+                        size_t ws_bytes, void* stream, cudaEvent_t ev0, cudaEvent_t ev1) {
   cudaStream_t s = (cudaStream_t)stream;
   Ws w;
   if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs) ||
@@ -271,11 +271,27 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   if (int r = launched()) return r;
   k_tile_scatter<<<sb, 1024, 0, s>>>(w.tile_bucket(), ntiles, w.hot_n(), w.blkoff(), w.order());
   if (int r = launched()) return r;
+  if (ev0 && cudaEventRecord(ev0, s) != cudaSuccess) return FIKIT_E_CUDA;
   k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
                                                   sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
                                                   t, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.bend(),
                                                   w.act(), w.first(), w.order(), out_row);
-  return launched();
+  if (int r = launched()) return r;
+  if (ev1 && cudaEventRecord(ev1, s) != cudaSuccess) return FIKIT_E_CUDA;
+  return FIKIT_OK;
+}
+
+int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes,
+                  void* stream) {
+  return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+int fikit_measure_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                        fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws,
+                        size_t ws_bytes, void* stream, void* ev_start, void* ev_stop) {
+  return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, (cudaEvent_t)ev_start,
+                      (cudaEvent_t)ev_stop);
 }
 
 int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n, void* ws, size_t ws_bytes,
