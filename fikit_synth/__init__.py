@@ -409,6 +409,58 @@ def bert_vgg(seed: int = 3, T: int = 1000, n_hp_runs: int = 1000, pop: int = 1 <
     return Config("bert_vgg", trace, Replay(hp, lp, lvl, sc), {"seed": seed, "S": S, "m": m})
 
 
+@dataclass
+class StreamReplay:
+    """STREAM-model replay inputs: as Replay, plus per LP request its stream
+    id (a stream = a maximal run of equal consecutive ids in a scenario's window).  The think
+    time after each LP kernel is its trace gap, resolved like the HP gaps."""
+
+    replay: Replay
+    lp_stream: np.ndarray  # uint32, one per LP request
+
+
+def bert_vgg_stream(seed: int = 3, T: int = 1000, n_hp_runs: int = 1000, n_lp_runs: int = 4000, S: int = 100_000,
+                    vgg_streams: int = 4, bert_streams: int = 2) -> tuple[Config, StreamReplay]:
+    """The BERT/VGG pair of configs[2] (same models and measurement trace) as kernel streams:
+    half the scenarios run an HP BERT inference against `vgg_streams` VGG inferences (40-kernel
+    streams), half HP VGG against `bert_streams` BERT inferences (176-kernel streams).  The LP
+    inferences are fresh runs with their own gaps (think times); every stream has one level
+    U{1,2,3}; HP gaps are replayed at scales 1, 2, 4, 8 (s mod 4)."""
+    rng = np.random.default_rng(seed)
+    names = _mangled_names(rng, 48)
+    sigs = _signatures(rng, 16)
+    bert = bert_model(rng, 24, 16, 0)
+    vgg = vgg_model(rng, 24, 16, 1, name_base=24)
+    rb, t1 = bert.runs(rng, T, 0)
+    rv, _ = vgg.runs(rng, T, 0, t0=t1)
+    trace = Trace(np.concatenate([rb, rv]), StrTab.from_list(names), StrTab.from_list(sigs))
+    hb, _ = bert.runs(rng, n_hp_runs, T)
+    hv, _ = vgg.runs(rng, n_hp_runs, T)
+    hp = np.concatenate([hb, hv])
+    lv, _ = vgg.runs(rng, n_lp_runs, T + n_hp_runs)  # [0, 40 n) VGG streams
+    lb, _ = bert.runs(rng, n_lp_runs, T + n_hp_runs)  # then BERT streams
+    lp = np.concatenate([lv, lb])
+    run_lvl = rng.integers(1, 4, size=2 * n_lp_runs).astype(np.uint8)
+    lvl = np.concatenate([np.repeat(run_lvl[:n_lp_runs], 40), np.repeat(run_lvl[n_lp_runs:], 176)])
+    stream = np.concatenate([np.repeat(np.arange(n_lp_runs, dtype=np.uint32), 40),
+                             np.repeat(np.arange(n_lp_runs, 2 * n_lp_runs, dtype=np.uint32), 176)])
+    s = np.arange(S, dtype=np.int64)
+    half = S // 2
+    sc = np.zeros(S, dtype=SCEN_DTYPE)
+    hp_bert = s < half
+    run = s % n_hp_runs
+    sc["hp_off"] = np.where(hp_bert, run * 176, n_hp_runs * 176 + run * 40)
+    sc["hp_len"] = np.where(hp_bert, 176, 40)
+    w_v = (s % (n_lp_runs - vgg_streams + 1)) * 40
+    w_b = 40 * n_lp_runs + (s % (n_lp_runs - bert_streams + 1)) * 176
+    sc["lp_off"] = np.where(hp_bert, w_v, w_b)
+    sc["lp_len"] = np.where(hp_bert, 40 * vgg_streams, 176 * bert_streams)
+    sc["gap_scale_q16"] = (1 << 16) << (s % 4)  # HP gaps x1, 2, 4, 8 (R24)
+    rp = Replay(hp, lp, lvl, sc)
+    cfg = Config("bert_vgg_stream", trace, rp, {"seed": seed, "S": S})
+    return cfg, StreamReplay(rp, stream)
+
+
 ZIPF_S = 1.1
 
 

@@ -631,3 +631,159 @@ int or_predict(otable_t* tab, uint32_t mode, uint32_t pct) {
   }
   return OR_OK;
 }
+
+/* ---- STREAM-model replay (readings R29-R32) ----------------
+ * The LP requests of a scenario are kernel streams (LP tasks whose hook client
+ * blocks each launch): a stream is a maximal run of equal consecutive
+ * lp_stream values; only its first undispatched request (the head) is queued
+ * (P:297-299).  Heads arrive at time 0; request k+1 of a stream arrives
+ * lp_think[k] after request k ends (the LP trace's own gap, R5) (R29).  In gap i
+ * BestPrioFit (Alg. 2) runs over the arrived heads; when none fits, the
+ * scheduler waits for the next head arrival A -- an arrival triggers a scan
+ * -- if A - t <= R and, with feedback, A < r_{i+1}; waiting consumes
+ * predicted idle (R -= A - t) (R30).  After the HP job the remaining requests run
+ * in (level, index) order among the arrived heads, time jumping to the earliest
+ * arrival when none has arrived (R31).  HP side, gate, R and feedback as
+ * or_simulate (R13, R17-R20, R24).  Singleton streams are the POOL model. */
+int or_simulate_stream(const uint32_t* hp_row, const uint64_t* hp_dur, const uint64_t* hp_gap, uint32_t n_h,
+                       const uint32_t* lp_row, const uint64_t* lp_dur, const uint8_t* lp_level,
+                       const uint32_t* lp_stream, const uint64_t* lp_think, uint32_t m, uint32_t gap_scale_q16,
+                       const uint64_t* dur_mean, const uint64_t* dur_cnt, const uint64_t* gap_mean, uint32_t n_rows,
+                       uint64_t threshold, uint32_t feedback, oresult_t* out, int32_t* fill_gap, uint64_t* lp_start) {
+  uint32_t M = m ? m : 1;
+  uint64_t* q = (uint64_t*)malloc(M * 8);
+  uint8_t* el = (uint8_t*)malloc(M);
+  uint32_t* head = (uint32_t*)malloc(M * 4); /* per stream: next request, one past its last */
+  uint32_t* send = (uint32_t*)malloc(M * 4);
+  uint64_t* arr = (uint64_t*)malloc(M * 8);
+  uint32_t ns = 0;
+  for (uint32_t k = 0; k < m; k++) {
+    uint32_t r = lp_row[k];
+    el[k] = (r < n_rows && dur_cnt[r] > 0); /* R16 */
+    q[k] = el[k] ? dur_mean[r] : 0;
+    fill_gap[k] = -1;
+    lp_start[k] = 0;
+    if (k == 0 || lp_stream[k] != lp_stream[k - 1]) {
+      head[ns] = k;
+      arr[ns] = 0;
+      ns++;
+    }
+    send[ns - 1] = k + 1;
+  }
+  uint64_t s = gap_scale_q16;
+  uint64_t t = 0, hp_delay = 0, fill_work = 0;
+  uint32_t n_fills = 0;
+  for (uint32_t i = 0; i < n_h; i++) {
+    uint64_t end = t + hp_dur[i];
+    t = end;
+    if (i == n_h - 1) break;
+    uint64_t r = end + ((hp_gap[i] * s) >> 16); /* R20, R24 */
+    uint32_t hr = hp_row[i];
+    uint64_t p = (hr < n_rows) ? ((gap_mean[hr] * s) >> 16) : 0;
+    uint64_t R = p;
+    if (p >= threshold) { /* R13 */
+      for (;;) {
+        if (feedback && t >= r) break; /* R19 */
+        /* BestPrioFit (Alg. 2) over the arrived heads: the first level with a fit, the longest
+           q there, ties to the earliest request (R14-R16) */
+        int64_t bs = -1;
+        for (uint32_t L = 1; L <= 9 && bs < 0; L++)
+          for (uint32_t j = 0; j < ns; j++) {
+            if (head[j] >= send[j] || arr[j] > t) continue;
+            uint32_t k = head[j];
+            if (!el[k] || lp_level[k] != L || q[k] > R) continue;
+            if (bs < 0 || q[k] > q[head[bs]] || (q[k] == q[head[bs]] && k < head[bs])) bs = j;
+          }
+        if (bs >= 0) {
+          uint32_t k = head[bs];
+          fill_gap[k] = (int32_t)i;
+          lp_start[k] = t;
+          t += lp_dur[k];
+          R -= q[k];
+          fill_work += lp_dur[k];
+          n_fills++;
+          head[bs]++;
+          arr[bs] = t + lp_think[k];
+          continue;
+        }
+        /* no arrived head fits: wait for the next arrival within the predicted idle (R30) */
+        uint64_t A = UINT64_MAX;
+        for (uint32_t j = 0; j < ns; j++)
+          if (head[j] < send[j] && arr[j] > t && arr[j] < A) A = arr[j];
+        if (A == UINT64_MAX || A - t > R || (feedback && A >= r)) break;
+        R -= A - t;
+        t = A;
+      }
+    }
+    if (t > r) hp_delay += t - r;
+    t = (t > r) ? t : r;
+  }
+  uint64_t hp_jct = t; /* R23 */
+  uint32_t n_tail = 0;
+  for (;;) { /* tail (R31) */
+    int64_t bs = -1;
+    uint64_t A = UINT64_MAX;
+    for (uint32_t j = 0; j < ns; j++) {
+      if (head[j] >= send[j]) continue;
+      if (arr[j] > t) {
+        if (arr[j] < A) A = arr[j];
+        continue;
+      }
+      uint32_t k = head[j];
+      if (bs < 0 || lp_level[k] < lp_level[head[bs]] || (lp_level[k] == lp_level[head[bs]] && k < head[bs]))
+        bs = j;
+    }
+    if (bs < 0) {
+      if (A == UINT64_MAX) break;
+      t = A;
+      continue;
+    }
+    uint32_t k = head[bs];
+    lp_start[k] = t;
+    t += lp_dur[k];
+    head[bs]++;
+    arr[bs] = t + lp_think[k];
+    n_tail++;
+  }
+  uint64_t lp_jct = 0, digest = 0;
+  for (uint32_t k = 0; k < m; k++) {
+    uint64_t e = lp_start[k] + lp_dur[k];
+    if (e > lp_jct) lp_jct = e;
+    digest += digest_term(k, fill_gap[k], lp_start[k]);
+  }
+  out->hp_jct = hp_jct;
+  out->lp_jct = m ? lp_jct : 0;
+  out->hp_delay = hp_delay;
+  out->fill_work = fill_work;
+  out->digest = digest;
+  out->n_fills = n_fills;
+  out->n_tail = n_tail;
+  free(q);
+  free(el);
+  free(head);
+  free(send);
+  free(arr);
+  return OR_OK;
+}
+
+int or_simulate_stream_batch(const uint32_t* hp_row, const uint64_t* hp_dur, const uint64_t* hp_gap,
+                             const uint32_t* lp_row, const uint64_t* lp_dur, const uint8_t* lp_level,
+                             const uint32_t* lp_stream, const uint64_t* lp_think, const oscen_t* sc, uint32_t S,
+                             const uint64_t* dur_mean, const uint64_t* dur_cnt, const uint64_t* gap_mean,
+                             uint32_t n_rows, uint64_t threshold, uint32_t feedback, oresult_t* out,
+                             int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off) {
+  for (uint32_t i = 0; i < S; i++) {
+    const oscen_t* c = sc + i;
+    for (uint32_t k = 0; k < c->lp_len; k++) {
+      uint8_t L = lp_level[c->lp_off + k];
+      if (L < 1 || L > 9) return OR_E_RECORD;
+    }
+    int rc = or_simulate_stream(hp_row + c->hp_off, hp_dur + c->hp_off, hp_gap + c->hp_off, c->hp_len,
+                                lp_row + c->lp_off, lp_dur + c->lp_off, lp_level + c->lp_off, lp_stream + c->lp_off,
+                                lp_think + c->lp_off, c->lp_len, c->gap_scale_q16, dur_mean, dur_cnt, gap_mean,
+                                n_rows, threshold, feedback, out + i, fill_gap + sched_off[i],
+                                lp_start + sched_off[i]);
+    if (rc) return rc;
+  }
+  return OR_OK;
+}
