@@ -248,6 +248,27 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
                          fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* ---- STREAM-model replay (readings R29-R32) ----------------
+ * As fikit_simulate_batch, but the LP requests of a scenario are kernel streams
+ * (a hooked client has one launch in flight): a stream
+ * is a maximal run of equal consecutive lp_stream[] ids in the scenario's window
+ * (device u32 per LP request); only each stream's first undispatched request is
+ * queued.  Streams' first requests arrive at t = 0; request k+1 arrives
+ * lp_think[k] ns (device u64 per LP request, e.g. fikit_resolve's out_gap of
+ * the LP launches) after request k ends.  In a gap, BestPrioFit runs over the
+ * arrived heads; when none fits the scheduler waits for the next arrival A if
+ * A - t <= R (and, with feedback, A < r_{i+1}), consuming R by the wait.  After
+ * the HP job the rest runs in (level, index) order among arrived heads.
+ * Results, schedule and digest as fikit_simulate_batch.  Limits: m <= 1024 and
+ * <= 64 streams per scenario (else FIKIT_E_ARG in the status; singleton streams
+ * are the POOL model: use fikit_simulate_batch).  One warp per scenario. */
+int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
+                                const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
+                                const uint8_t* lp_level, const uint32_t* lp_stream, const uint64_t* lp_think,
+                                const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t params,
+                                fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
+                                const uint64_t* sched_off, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- multi-GPU merge ------------------------------------------
  * Each rank finalizes its local table, all-gathers the sorted keys
  * (P lists of n_list[r] keys, padded to stride Kmax), then:

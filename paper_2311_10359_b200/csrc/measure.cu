@@ -31,6 +31,7 @@ __global__ void k_reset_status(fikit_status_t* st) {
     st->n_task_buckets = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord1] = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord2] = 0;
+    reinterpret_cast<uint32_t*>(st)[kSchedWord3] = 0;
   }
 }
 

@@ -392,15 +392,14 @@ struct HpOut {
 // open (p >= tau, p >= qmin, and with feedback a' > 0) need the serial Alg. 1 loop, so each
 // chunk of 32 HP kernels is advanced by a prefix sum and visits just its open gates.  The next
 // chunk's inputs are loaded while this one is processed.
-template <class Pool, class MinQ>
-__device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_table_t& tab, uint32_t K,
-                                           const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
-                                           const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
-                                           const fikit_fill_params_t& prm, bool sched, int32_t* fill_gap,
-                                           uint64_t* lp_start, uint64_t so, DigestBatch& dig, int lane) {
+template <class GateMin, class Fill>
+__device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, const fikit_table_t& tab, uint32_t K,
+                                                const uint32_t* __restrict__ hp_row,
+                                                const uint64_t* __restrict__ hp_dur,
+                                                const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
+                                                const fikit_fill_params_t& prm, int lane) {
   const uint32_t nh = c.hp_len;
   const uint64_t scale = c.gap_scale_q16;
-  uint64_t qmin = min_q();
   HpOut o{0, 0, 0, 0, 0};
   uint64_t t = 0;
   // chunk inputs: d, raw gap, row of HP kernel base + lane (next chunk prefetched)
@@ -433,7 +432,7 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
       uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
       if (lane >= dd) X += y;
     }
-    const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= qmin && (!prm.feedback || a_l > 0);
+    const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= gate_min() && (!prm.feedback || a_l > 0);
     uint32_t gmask = __ballot_sync(0xffffffffu, gate);
     const uint64_t T0 = t;
     uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
@@ -444,29 +443,10 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
       const uint64_t Xj = __shfl_sync(0xffffffffu, X, j);
       const uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
       const uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
-      if (p < qmin) continue;  // the pool has shrunk since the gate was computed
+      if (p < gate_min()) continue;  // the pool has shrunk since the gate was computed
       t = T0 + shift + Xj - a;  // end of HP kernel i
       const uint64_t r = t + a;   // the HP client's next launch arrives (R20)
-      uint64_t R = p;
-      for (;;) {
-        if (prm.feedback && t >= r) break;
-        if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
-        uint64_t qk;
-        const int k = P.pick(R, lane, qk);  // Alg. 2
-        if (k < 0) break;
-        const uint64_t e = P.dur_of((uint32_t)k);
-        if (sched && lane == 0) {
-          fill_gap[so + k] = (int32_t)i;
-          lp_start[so + k] = t;
-        }
-        dig.add((uint32_t)k, (int32_t)i, t, lane);
-        R -= qk;
-        t += e;
-        if (qk == qmin) qmin = min_q();
-        o.fill_work += e;
-        o.n_fills++;
-        o.lp_end = max(o.lp_end, t);
-      }
+      t = fill(i, t, r, p, o);    // Alg. 1 over this gap (R = p)
       if (t > r) {  // overhead 2: kernel i+1 starts at max(t, r_{i+1})
         o.hp_delay += t - r;
         shift += t - r;
@@ -476,6 +456,39 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
   }
   o.t = t;
   return o;
+}
+
+// The POOL model's gap loop on a pool representation (RegPool / SmemPool)
+template <class Pool, class MinQ>
+__device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_table_t& tab, uint32_t K,
+                                           const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
+                                           const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
+                                           const fikit_fill_params_t& prm, bool sched, int32_t* fill_gap,
+                                           uint64_t* lp_start, uint64_t so, DigestBatch& dig, int lane) {
+  uint64_t qmin = min_q();
+  auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
+    for (;;) {
+      if (prm.feedback && t >= r) break;
+      if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
+      uint64_t qk;
+      const int k = P.pick(R, lane, qk);  // Alg. 2
+      if (k < 0) break;
+      const uint64_t e = P.dur_of((uint32_t)k);
+      if (sched && lane == 0) {
+        fill_gap[so + k] = (int32_t)i;
+        lp_start[so + k] = t;
+      }
+      dig.add((uint32_t)k, (int32_t)i, t, lane);
+      R -= qk;
+      t += e;
+      if (qk == qmin) qmin = min_q();
+      o.fill_work += e;
+      o.n_fills++;
+      o.lp_end = max(o.lp_end, t);
+    }
+    return t;
+  };
+  return replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane);
 }
 
 // tail (R22): the requests still queued run after the HP end in Q1..Q9 order, FIFO within a
@@ -639,6 +652,225 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
         [&](uint32_t k) { return __ldg(lp_dur + c.lp_off + k); }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
         lane);
     write_result(out, s, o, t, m, n_tail, db, tail_dig, lane);
+    }
+  }
+}
+
+// ---- fikit_simulate_stream_batch: the STREAM model (R29-R32), one warp per scenario --------
+// Up to 64 streams per scenario: lane l owns streams l (slot 0) and 32 + l (slot 1) with, for
+// each, its head request (window index), end, the head's arrival time and the head's q,
+// level, eligibility, duration and think time (loaded when it becomes the head).
+constexpr int kStreamWarps = 8;
+constexpr uint32_t kMaxStreams = 64;
+
+struct StreamHeads {
+  uint32_t hd[2], se[2], lv[2];
+  uint64_t A[2], q[2], e[2], th[2];
+  bool el[2];
+};
+
+struct StreamPick {  // the best head of a warp reduction (valid: lv != 0xFF)
+  uint32_t lv, k, sid;
+  uint64_t q;
+};
+
+// a better than b: (level asc, q desc, index asc) for fills (q_desc = true), (level, index) for the tail
+__device__ __forceinline__ bool stream_better(const StreamPick& a, const StreamPick& b, bool q_desc) {
+  if (a.lv != b.lv) return a.lv < b.lv;
+  if (q_desc && a.q != b.q) return a.q > b.q;
+  return a.k < b.k;
+}
+
+__device__ __forceinline__ StreamPick warp_best_stream(StreamPick x, bool q_desc) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    StreamPick y;
+    y.lv = __shfl_xor_sync(0xffffffffu, x.lv, off);
+    y.k = __shfl_xor_sync(0xffffffffu, x.k, off);
+    y.sid = __shfl_xor_sync(0xffffffffu, x.sid, off);
+    y.q = __shfl_xor_sync(0xffffffffu, x.q, off);
+    if (y.lv != 0xFFu && (x.lv == 0xFFu || stream_better(y, x, q_desc))) x = y;
+  }
+  return x;
+}
+
+__global__ void __launch_bounds__(kStreamWarps * 32)
+    k_simulate_stream(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
+                      const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
+                      const uint64_t* __restrict__ lp_dur, const uint8_t* __restrict__ lp_level,
+                      const uint32_t* __restrict__ lp_stream, const uint64_t* __restrict__ lp_think,
+                      const fikit_scenario_t* __restrict__ sc, uint32_t S, fikit_fill_params_t prm,
+                      fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap,
+                      uint64_t* __restrict__ lp_start, const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
+  __shared__ uint32_t s_start[kStreamWarps][kMaxStreams];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t K = min(*tab.n_rows, tab.capacity);
+  const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord3;
+  uint32_t nxt = 0;  // lane 0: the next claimed scenario (in flight while one runs)
+  if (lane == 0) nxt = atomicAdd(ctr, 1u);
+  for (uint32_t cur = __shfl_sync(0xffffffffu, nxt, 0); cur < S; cur = __shfl_sync(0xffffffffu, nxt, 0)) {
+    const fikit_scenario_t c = sc[cur];
+    if (lane == 0) nxt = atomicAdd(ctr, 1u);
+    const uint32_t m = c.lp_len;
+    const uint64_t off = c.lp_off;
+    // streams: maximal runs of equal consecutive ids (R29); levels validated on the way
+    uint32_t ns = 0;
+    bool ok = m <= kPoolMax;
+    for (uint32_t b = 0; b < m && ok; b += 32) {
+      const uint32_t k = b + lane;
+      bool f = false;
+      if (k < m) {
+        f = k == 0 || __ldg(lp_stream + off + k) != __ldg(lp_stream + off + k - 1);
+        const uint32_t L = __ldg(lp_level + off + k);
+        if (L < 1 || L > 9) {
+          flag_record(st, off + k);
+          ok = false;
+        }
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      const uint32_t mask = __ballot_sync(0xffffffffu, f);
+      const uint32_t rank = ns + __popc(mask & ((1u << lane) - 1u));
+      if (f && rank < kMaxStreams) s_start[w][rank] = k;
+      ns += __popc(mask);
+    }
+    if (!ok || ns > kMaxStreams) {
+      if (ok && lane == 0) atomicOr(&st->flags, kStatusArg);  // > 64 streams or m > 1024
+      continue;
+    }
+    __syncwarp();
+    StreamHeads H;
+    auto load_head = [&](int h) {  // the head of slot h became hd[h]
+      H.lv[h] = 0xFFu;
+      H.el[h] = false;
+      if (H.hd[h] < H.se[h]) {
+        const uint64_t g = off + H.hd[h];
+        const uint32_t row = __ldg(lp_row + g);
+        H.lv[h] = __ldg(lp_level + g);
+        H.e[h] = __ldg(lp_dur + g);
+        H.th[h] = __ldg(lp_think + g);
+        H.el[h] = row < K && __ldg(tab.sums + (size_t)row * 4) > 0;  // R16
+        H.q[h] = H.el[h] ? __ldg(tab.mean + (size_t)row * 2) : 0;
+      }
+    };
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t sid = (uint32_t)h * 32u + (uint32_t)lane;
+      H.hd[h] = sid < ns ? s_start[w][sid] : 0u;
+      H.se[h] = sid < ns ? (sid + 1 < ns ? s_start[w][sid + 1] : m) : 0u;
+      H.A[h] = 0;
+      load_head(h);
+    }
+    // gate lower bound (R32): the minimum q over every eligible request of the window
+    uint64_t qmin = ~0ull;
+    for (uint32_t k = lane; k < m; k += 32) {
+      const uint32_t row = __ldg(lp_row + off + k);
+      if (row < K && __ldg(tab.sums + (size_t)row * 4) > 0) qmin = min(qmin, __ldg(tab.mean + (size_t)row * 2));
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) qmin = min(qmin, __shfl_xor_sync(0xffffffffu, qmin, o2));
+    const uint64_t so = sched ? sched_off[cur] : 0;
+    DigestBatch db;
+    uint64_t lp_end = 0;
+    // dispatch the head of stream sid at time t (all lanes): returns its duration; the owning
+    // lane advances the stream (its next request arrives think time after this one ends)
+    auto dispatch = [&](const StreamPick& b, uint64_t t, int32_t gap_i) -> uint64_t {
+      const int src = (int)(b.sid & 31u), h = (int)(b.sid >> 5);
+      const uint64_t e = __shfl_sync(0xffffffffu, h ? H.e[1] : H.e[0], src);
+      if (sched && lane == 0) {
+        fill_gap[so + b.k] = gap_i;
+        lp_start[so + b.k] = t;
+      }
+      db.add(b.k, gap_i, t, lane);
+      if (lane == src) {
+        const uint64_t arr = t + e + (h ? H.th[1] : H.th[0]);
+        if (h) {
+          H.hd[1]++;
+          H.A[1] = arr;
+          load_head(1);
+        } else {
+          H.hd[0]++;
+          H.A[0] = arr;
+          load_head(0);
+        }
+      }
+      return e;
+    };
+    auto next_arrival = [&](uint64_t t) -> uint64_t {  // earliest head arrival after t
+      uint64_t a = ~0ull;
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if (H.hd[h] < H.se[h] && H.A[h] > t) a = min(a, H.A[h]);
+#pragma unroll
+      for (int o2 = 16; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
+      return a;
+    };
+    auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
+      for (;;) {
+        if (prm.feedback && t >= r) break;  // R19
+        StreamPick x{0xFFu, 0, 0, 0};  // BestPrioFit over the arrived heads (Alg. 2)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          if (H.hd[h] < H.se[h] && H.A[h] <= t && H.el[h] && H.q[h] <= R) {
+            const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, H.q[h]};
+            if (x.lv == 0xFFu || stream_better(y, x, true)) x = y;
+          }
+        }
+        x = warp_best_stream(x, true);
+        if (x.lv != 0xFFu) {
+          const uint64_t e = dispatch(x, t, (int32_t)i);
+          t += e;
+          R -= x.q;  // R17
+          o.fill_work += e;
+          o.n_fills++;
+          lp_end = max(lp_end, t);
+          continue;
+        }
+        const uint64_t A = next_arrival(t);  // R30: wait within the predicted idle
+        if (A == ~0ull || A - t > R || (prm.feedback && A >= r)) break;
+        R -= A - t;
+        t = A;
+      }
+      return t;
+    };
+    HpOut o = replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane);
+    // tail (R31)
+    uint64_t t = o.t;
+    uint32_t n_tail = 0;
+    for (;;) {
+      StreamPick x{0xFFu, 0, 0, 0};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        if (H.hd[h] < H.se[h] && H.A[h] <= t) {
+          const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, 0};
+          if (x.lv == 0xFFu || stream_better(y, x, false)) x = y;
+        }
+      }
+      x = warp_best_stream(x, false);
+      if (x.lv == 0xFFu) {
+        const uint64_t A = next_arrival(t);
+        if (A == ~0ull) break;
+        t = A;
+        continue;
+      }
+      t += dispatch(x, t, -1);
+      lp_end = max(lp_end, t);
+      n_tail++;
+    }
+    db.drain(lane);
+    uint64_t dig = db.sum;
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, o2);
+    if (lane == 0) {
+      fikit_result_t rr;
+      rr.hp_jct = o.t;
+      rr.lp_jct = m ? lp_end : 0;
+      rr.hp_delay = o.hp_delay;
+      rr.fill_work = o.fill_work;
+      rr.digest = dig;
+      rr.n_fills = o.n_fills;
+      rr.n_tail = n_tail;
+      out[cur] = rr;
     }
   }
 }

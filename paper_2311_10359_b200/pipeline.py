@@ -9,17 +9,19 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve, table_predict,
-               simulate_batch, strtab_to_device, table_finalize)
+from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve,
+               simulate_batch, simulate_stream_batch, strtab_to_device, table_finalize, table_predict)
 
 
 class Pipeline:
     def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
                  want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None,
-                 checked: bool = False, predictor: tuple | None = None):
+                 checked: bool = False, predictor: tuple | None = None, lp_stream: np.ndarray | None = None):
         """checked: verify the workspace status after every call (tests); the
         bench leaves it off and checks once after warm-up.  predictor: (mode, pct) for
-        fikit_table_predict before every replay (None: the finalized means, the paper's)."""
+        fikit_table_predict before every replay (None: the finalized means, the paper's).
+        lp_stream: a stream id per LP request -> the STREAM-model replay (fikit_simulate_stream_batch,
+        think times = the LP launches' resolved gaps); None -> the POOL model."""
         torch = _torch()
         self.checked = checked
         self.predictor = predictor
@@ -37,6 +39,9 @@ class Pipeline:
         self.replay = None
         if replay is not None:
             self._setup_replay(replay, want_schedule)
+            if lp_stream is not None:
+                self.replay["lp_stream"] = torch.from_numpy(np.ascontiguousarray(lp_stream, dtype=np.uint32)
+                                                            .view(np.int32)).to(device)
 
     def _setup_replay(self, rp, want_schedule):
         torch = _torch()
@@ -92,10 +97,16 @@ class Pipeline:
         resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
                 self.ws, stream=stream)
         self._chk("resolve(lp)", stream)
-        simulate_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
-                       r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],
-                       fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off"),
-                       stream=stream)
+        if "lp_stream" in r:
+            simulate_stream_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
+                                  r["lp_stream"], r["lp_gap"], r["sc"], r["S"], r["out"], self.ws,
+                                  threshold_ns=r["threshold_ns"], feedback=r["feedback"], fill_gap=r.get("fill_gap"),
+                                  lp_start=r.get("lp_start"), sched_off=r.get("sched_off"), stream=stream)
+        else:
+            simulate_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
+                           r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],
+                           fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off"),
+                           stream=stream)
         self._chk("simulate_batch", stream)
 
     def _chk(self, what, stream):

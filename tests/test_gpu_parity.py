@@ -371,3 +371,64 @@ def test_table_predict_bad_args(fk):
     for mode, pct in ((3, 50), (1, 0), (1, 100)):
         with pytest.raises(Exception):
             fk.table_predict(p.table, mode, pct)
+
+
+def _stream_ref(orc, cfg, sr, feedback):
+    tr, rp = cfg.trace, cfg.replay
+    tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=1024)
+    hr, hd, hg, _ = orc.resolve(rp.hp_records, tr.names, tr.sigs, tab)
+    lr, ld, lg, _ = orc.resolve(rp.lp_records, tr.names, tr.sigs, tab)
+    return orc.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level, sr.lp_stream, lg, rp.scenarios, tab,
+                                     rp.threshold_ns, feedback)
+
+
+@pytest.mark.parametrize("feedback", [1, 0])
+def test_stream_replay_parity(fk, orc, feedback):
+    """STREAM-model replay (R29-R32): GPU vs oracle, results and schedule, on the BERT/VGG stream
+    workload (4 VGG or 2 BERT inference streams per scenario, gap scales 1-8)"""
+    from dataclasses import replace
+
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg, sr = F.bert_vgg_stream(S=3000, n_lp_runs=600)
+    cfg = F.Config(cfg.name, cfg.trace, replace(cfg.replay, feedback=feedback))
+    out, fg, ls, _ = _stream_ref(orc, cfg, sr, feedback)
+    assert out["n_fills"].sum() > 0
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay,
+                 want_schedule=True, checked=True, lp_stream=sr.lp_stream)
+    p.step()
+    got = p.results()
+    if got.tobytes() != out.tobytes():
+        bad = np.flatnonzero(got != out)[:5]
+        raise AssertionError(f"scenarios {bad.tolist()} differ: {got[bad]} vs {out[bad]}")
+    gfg, gls = p.schedule()
+    assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
+
+
+def test_stream_singletons_equal_pool_on_gpu(fk, orc):
+    """singleton streams (ids 0..m-1) through the STREAM kernel = the POOL replay (m <= 64)"""
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.bert_vgg(S=2000)
+    ids = np.arange(cfg.replay.lp_records.shape[0], dtype=np.uint32)
+    a = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay,
+                 want_schedule=True, checked=True, lp_stream=ids)
+    b = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay,
+                 want_schedule=True, checked=True)
+    a.step()
+    b.step()
+    assert a.results().tobytes() == b.results().tobytes()
+
+
+def test_stream_limits_flag(fk, orc):
+    """more than 64 streams in a scenario is an argument error (status), not a wrong answer"""
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.bert_vgg(S=4, m=128)
+    ids = np.arange(cfg.replay.lp_records.shape[0], dtype=np.uint32)  # 128 singleton streams
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay,
+                 lp_stream=ids)
+    p.step()
+    assert p.check.__self__ is p
+    with pytest.raises(Exception):
+        p.check("stream limits")
