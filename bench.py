@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
-    ap.add_argument("--workload", default="zipf", choices=["zipf", "resnet", "bert_vgg", "sweep"])
+    ap.add_argument("--workload", default="zipf", choices=["zipf", "resnet", "bert_vgg", "sweep", "stream"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
     ap.add_argument("--predictor", default=None,
@@ -77,6 +77,16 @@ def make_workload(args, rank, world):
         replay = F.zipf_replay(cfg, S=args.scenarios)
         cap = 8192
         desc = f"zipf-{N // 1_000_000}M (configs[3]) + replay-{args.scenarios // 1000}k"
+    elif args.workload == "stream":  # BERT/VGG with LP kernel streams
+        cfg, sr = F.bert_vgg_stream(S=args.scenarios)
+        N = cfg.trace.records.shape[0]
+        lo, hi = shard_range(N, rank, world)
+        recs = cfg.trace.records[lo:hi]
+        halo = cfg.trace.records[hi] if hi < N else None
+        replay = cfg.replay
+        lp_stream = sr.lp_stream
+        cap = 4096
+        desc = f"bert_vgg_stream-{args.scenarios // 1000}k (STREAM-model replay, §8f row 1)"
     else:
         cfg = {"resnet": F.resnet_trace, "bert_vgg": F.bert_vgg, "sweep": F.sweep}[args.workload]()
         N = cfg.trace.records.shape[0]
@@ -92,7 +102,7 @@ def make_workload(args, rank, world):
         replay = F.Replay(replay.hp_records, replay.lp_records, replay.lp_level, replay.scenarios[sel],
                           replay.threshold_ns, replay.feedback)
     return dict(records=recs, halo=halo, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=replay, N=N, cap=cap,
-                desc=desc, cfg=cfg)
+                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload == "stream" else None)
 
 
 class ClockSampler:
@@ -201,11 +211,15 @@ def oracle_sample_time(wl, budget_s, seed=0):
         lp_idx = np.concatenate([np.arange(c["lp_off"], c["lp_off"] + c["lp_len"]) for c in sc]).astype(np.int64)
         t = time.perf_counter()
         hr, hd, hg, _ = oracle.resolve(rp.hp_records[hp_idx], names, sigs, tab)
-        lr, ld, _, _ = oracle.resolve(rp.lp_records[lp_idx], names, sigs, tab)
+        lr, ld, lg, _ = oracle.resolve(rp.lp_records[lp_idx], names, sigs, tab)
         off_h = np.concatenate([[0], np.cumsum(sc["hp_len"][:-1])]).astype(np.uint32)
         off_l = np.concatenate([[0], np.cumsum(sc["lp_len"][:-1])]).astype(np.uint32)
         sc["hp_off"], sc["lp_off"] = off_h, off_l
-        oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
+        if wl.get("lp_stream") is not None:  # STREAM model (think times: the resolved LP gaps)
+            oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg, sc,
+                                         tab, rp.threshold_ns, rp.feedback)
+        else:
+            oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
         t_rep = time.perf_counter() - t
         job += t_rep * (S / s_n)
         desc += f" + resolve/replay of {s_n} of {S:,} scenarios"
@@ -272,7 +286,7 @@ def main():
     stream = torch.cuda.current_stream()
     pred = tuple(int(x) for x in args.predictor.split(",")) if args.predictor else None
     p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"],
-                 predictor=pred)
+                 predictor=pred, lp_stream=wl["lp_stream"])
     n_local = p.n
     dense = fk.Table(wl["cap"]) if world > 1 else None
     ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None

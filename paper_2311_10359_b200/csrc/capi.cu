@@ -439,10 +439,10 @@ int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row
   if (S == 0) return FIKIT_OK;
   // persistent, one wave; warps claim scenarios from a counter
   static int g = 0;
-  if (!g) g = one_wave((const void*)k_simulate_stream, 256);
-  const uint64_t need = ((uint64_t)S + 7) / 8;
+  if (!g) g = one_wave((const void*)k_simulate_stream, kStreamThreads);
+  const uint64_t need = ((uint64_t)S + kStreamThreads / 32 - 1) / (kStreamThreads / 32);
   const int b = (int)(need < (uint64_t)g ? need : (uint64_t)g);
-  k_simulate_stream<<<b, 256, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think,
+  k_simulate_stream<<<b, kStreamThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think,
                                       sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
   return launched();
 }

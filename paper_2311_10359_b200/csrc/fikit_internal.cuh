@@ -44,6 +44,7 @@ constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
 constexpr int kRegThreads = 256;  // k_simulate_reg block (8 warps, one scenario each)
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
+constexpr int kStreamThreads = 128;  // k_simulate_stream block (4 warps, staged windows)
 // u32 words of the 256-B status region past fikit_status_t, zeroed with it: replay work counters
 constexpr uint32_t kSchedWord1 = 32, kSchedWord2 = 33, kSchedWord3 = 34;
 // Dynamic tile schedule (k_tile_plan -> k_measure): bucket b's tiles are the sorted positions

@@ -658,14 +658,16 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
 
 // ---- fikit_simulate_stream_batch: the STREAM model (R29-R32), one warp per scenario --------
 // Up to 64 streams per scenario: lane l owns streams l (slot 0) and 32 + l (slot 1) with, for
-// each, its head request (window index), end, the head's arrival time and the head's q,
-// level, eligibility, duration and think time (loaded when it becomes the head).
-constexpr int kStreamWarps = 8;
+// each, its head request (window index), end, the head's arrival time, q, level, eligibility,
+// duration and think time, and the next request's duration and think time (prefetched).  The
+// window's q and level | eligibility are staged in shared memory at the scenario's start, so a
+// dispatch waits on no global load.
+constexpr int kStreamWarps = kStreamThreads / 32;
 constexpr uint32_t kMaxStreams = 64;
 
 struct StreamHeads {
   uint32_t hd[2], se[2], lv[2];
-  uint64_t A[2], q[2], e[2], th[2];
+  uint64_t A[2], q[2], e[2], th[2], en[2], thn[2];
   bool el[2];
 };
 
@@ -681,9 +683,9 @@ __device__ __forceinline__ bool stream_better(const StreamPick& a, const StreamP
   return a.k < b.k;
 }
 
-__device__ __forceinline__ StreamPick warp_best_stream(StreamPick x, bool q_desc) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
+// reduction over lanes [0, 2 * half): streams live on lanes < min(ns, 32)
+__device__ __forceinline__ StreamPick warp_best_stream(StreamPick x, bool q_desc, uint32_t half) {
+  for (uint32_t off = half; off; off >>= 1) {
     StreamPick y;
     y.lv = __shfl_xor_sync(0xffffffffu, x.lv, off);
     y.k = __shfl_xor_sync(0xffffffffu, x.k, off);
@@ -691,6 +693,10 @@ __device__ __forceinline__ StreamPick warp_best_stream(StreamPick x, bool q_desc
     y.q = __shfl_xor_sync(0xffffffffu, x.q, off);
     if (y.lv != 0xFFu && (x.lv == 0xFFu || stream_better(y, x, q_desc))) x = y;
   }
+  x.lv = __shfl_sync(0xffffffffu, x.lv, 0);  // lanes >= 2 * half took no part: lane 0's result
+  x.k = __shfl_sync(0xffffffffu, x.k, 0);
+  x.sid = __shfl_sync(0xffffffffu, x.sid, 0);
+  x.q = __shfl_sync(0xffffffffu, x.q, 0);
   return x;
 }
 
@@ -703,6 +709,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
                       fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap,
                       uint64_t* __restrict__ lp_start, const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
   __shared__ uint32_t s_start[kStreamWarps][kMaxStreams];
+  __shared__ uint64_t s_q[kStreamWarps][kPoolMax];
+  __shared__ uint8_t s_lv[kStreamWarps][kPoolMax];  // level | eligible << 7
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
   const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
@@ -738,19 +746,37 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
       if (ok && lane == 0) atomicOr(&st->flags, kStatusArg);  // > 64 streams or m > 1024
       continue;
     }
+    // stage q and level | eligibility of the window (R16); gate lower bound (R32): the minimum q
+    // over every eligible request of the window
+    uint64_t qmin = ~0ull;
+    for (uint32_t k = lane; k < m; k += 32) {
+      const uint32_t row = __ldg(lp_row + off + k);
+      const bool el = row < K && __ldg(tab.sums + (size_t)row * 4) > 0;
+      const uint64_t q = el ? __ldg(tab.mean + (size_t)row * 2) : 0;
+      s_q[w][k] = q;
+      s_lv[w][k] = (uint8_t)(__ldg(lp_level + off + k) | (el ? 0x80u : 0u));
+      if (el) qmin = min(qmin, q);
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) qmin = min(qmin, __shfl_xor_sync(0xffffffffu, qmin, o2));
     __syncwarp();
-    StreamHeads H;
-    auto load_head = [&](int h) {  // the head of slot h became hd[h]
+    StreamHeads H{};
+    // reduction width: the smallest power of two >= the lanes holding streams
+    const uint32_t nl = ns < 32 ? ns : 32u;
+    const uint32_t half = nl <= 1 ? 0u : (1u << (31 - __clz(nl - 1)));
+    auto prefetch_next = [&](int h) {  // duration and think time of the request after the head
+      const uint32_t k = H.hd[h] + 1;
+      H.en[h] = k < H.se[h] ? __ldg(lp_dur + off + k) : 0;
+      H.thn[h] = k < H.se[h] ? __ldg(lp_think + off + k) : 0;
+    };
+    auto set_head = [&](int h) {  // hd[h] became the head; its e / th are in e / th
       H.lv[h] = 0xFFu;
       H.el[h] = false;
       if (H.hd[h] < H.se[h]) {
-        const uint64_t g = off + H.hd[h];
-        const uint32_t row = __ldg(lp_row + g);
-        H.lv[h] = __ldg(lp_level + g);
-        H.e[h] = __ldg(lp_dur + g);
-        H.th[h] = __ldg(lp_think + g);
-        H.el[h] = row < K && __ldg(tab.sums + (size_t)row * 4) > 0;  // R16
-        H.q[h] = H.el[h] ? __ldg(tab.mean + (size_t)row * 2) : 0;
+        const uint32_t x = s_lv[w][H.hd[h]];
+        H.lv[h] = x & 0x7Fu;
+        H.el[h] = (x & 0x80u) != 0;
+        H.q[h] = s_q[w][H.hd[h]];
       }
     };
 #pragma unroll
@@ -759,16 +785,11 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
       H.hd[h] = sid < ns ? s_start[w][sid] : 0u;
       H.se[h] = sid < ns ? (sid + 1 < ns ? s_start[w][sid + 1] : m) : 0u;
       H.A[h] = 0;
-      load_head(h);
+      H.e[h] = H.hd[h] < H.se[h] ? __ldg(lp_dur + off + H.hd[h]) : 0;
+      H.th[h] = H.hd[h] < H.se[h] ? __ldg(lp_think + off + H.hd[h]) : 0;
+      set_head(h);
+      prefetch_next(h);
     }
-    // gate lower bound (R32): the minimum q over every eligible request of the window
-    uint64_t qmin = ~0ull;
-    for (uint32_t k = lane; k < m; k += 32) {
-      const uint32_t row = __ldg(lp_row + off + k);
-      if (row < K && __ldg(tab.sums + (size_t)row * 4) > 0) qmin = min(qmin, __ldg(tab.mean + (size_t)row * 2));
-    }
-#pragma unroll
-    for (int o2 = 16; o2; o2 >>= 1) qmin = min(qmin, __shfl_xor_sync(0xffffffffu, qmin, o2));
     const uint64_t so = sched ? sched_off[cur] : 0;
     DigestBatch db;
     uint64_t lp_end = 0;
@@ -787,11 +808,17 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
         if (h) {
           H.hd[1]++;
           H.A[1] = arr;
-          load_head(1);
+          H.e[1] = H.en[1];
+          H.th[1] = H.thn[1];
+          set_head(1);
+          prefetch_next(1);
         } else {
           H.hd[0]++;
           H.A[0] = arr;
-          load_head(0);
+          H.e[0] = H.en[0];
+          H.th[0] = H.thn[0];
+          set_head(0);
+          prefetch_next(0);
         }
       }
       return e;
@@ -801,9 +828,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
 #pragma unroll
       for (int h = 0; h < 2; h++)
         if (H.hd[h] < H.se[h] && H.A[h] > t) a = min(a, H.A[h]);
-#pragma unroll
-      for (int o2 = 16; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
-      return a;
+      for (uint32_t o2 = half; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
+      return __shfl_sync(0xffffffffu, a, 0);
     };
     auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
       for (;;) {
@@ -816,7 +842,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
             if (x.lv == 0xFFu || stream_better(y, x, true)) x = y;
           }
         }
-        x = warp_best_stream(x, true);
+        x = warp_best_stream(x, true, half);
         if (x.lv != 0xFFu) {
           const uint64_t e = dispatch(x, t, (int32_t)i);
           t += e;
@@ -846,7 +872,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
           if (x.lv == 0xFFu || stream_better(y, x, false)) x = y;
         }
       }
-      x = warp_best_stream(x, false);
+      x = warp_best_stream(x, false, half);
       if (x.lv == 0xFFu) {
         const uint64_t A = next_arrival(t);
         if (A == ~0ull) break;
