@@ -78,9 +78,10 @@ def lib():
         _lib.or_fill_batch.argtypes = [p, p, p, p, p, p, p, u32, p, p, u32, u64, u32, p, p, p, p, p,
                                        C.POINTER(Status)]
         _lib.or_simulate.argtypes = [p, p, p, u32, p, p, p, u32, u32, p, p, p, u32, u64, u32, p, p, p]
-        _lib.or_simulate_stream.argtypes = [p, p, p, u32, p, p, p, p, p, u32, u32, p, p, p, u32, u64, u32, p, p, p]
+        _lib.or_simulate_stream.argtypes = [p, p, p, u32, p, p, p, p, p, u32, u32, p, p, p, u32, u64, u32, u64, p, p,
+                                            p]
         _lib.or_simulate_stream_batch.restype = C.c_int
-        _lib.or_simulate_stream_batch.argtypes = [p, p, p, p, p, p, p, p, p, u32, p, p, p, u32, u64, u32, p, p, p,
+        _lib.or_simulate_stream_batch.argtypes = [p, p, p, p, p, p, p, p, p, u32, p, p, p, u32, u64, u32, p, p, p, p,
                                                   p]
         _lib.or_predict.restype = C.c_int
         _lib.or_predict.argtypes = [C.POINTER(_Table), u32, u32]
@@ -268,9 +269,11 @@ def simulate_batch(hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, scenarios, 
 
 
 def simulate_stream_batch(hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think, scenarios,
-                          tab: Table, threshold=100_000, feedback=1):
-    """STREAM-model replay (or_simulate_stream, R29-R32); returns (results, fill_gap, lp_start, sched_off)
-    with the schedule of every scenario at sched_off (cumulative lp_len)."""
+                          tab: Table, threshold=100_000, feedback=1, hp_arrival=None):
+    """STREAM-model replay (or_simulate_stream, R29-R32; hp_arrival per scenario: Case A, R33-R34);
+    returns (results, fill_gap, lp_start, sched_off) with the schedule of every scenario at sched_off
+    (cumulative lp_len)."""
+    ha = None if hp_arrival is None else _c(hp_arrival, np.uint64)
     hr, hd, hg = _c(hp_row, np.uint32), _c(hp_dur, np.uint64), _c(hp_gap, np.uint64)
     lr, ld, ll = _c(lp_row, np.uint32), _c(lp_dur, np.uint64), _c(lp_level, np.uint8)
     ls_, lt = _c(lp_stream, np.uint32), _c(lp_think, np.uint64)
@@ -286,8 +289,8 @@ def simulate_stream_batch(hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_s
     ls = np.zeros(tot, dtype=np.uint64)
     rc = lib().or_simulate_stream_batch(_ptr(hr), _ptr(hd), _ptr(hg), _ptr(lr), _ptr(ld), _ptr(ll), _ptr(ls_),
                                         _ptr(lt), _ptr(sc), S, _ptr(tab.dur_mean), _ptr(tab.dur_cnt),
-                                        _ptr(tab.gap_mean), tab.n_rows, threshold, feedback, _ptr(out), _ptr(fg),
-                                        _ptr(ls), _ptr(so))
+                                        _ptr(tab.gap_mean), tab.n_rows, threshold, feedback, _ptr(ha), _ptr(out),
+                                        _ptr(fg), _ptr(ls), _ptr(so))
     if rc != 0:
         raise ValueError(f"or_simulate_stream_batch -> {rc}")
     return out, fg, ls, so

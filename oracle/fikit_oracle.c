@@ -645,11 +645,20 @@ int or_predict(otable_t* tab, uint32_t mode, uint32_t pct) {
  * in (level, index) order among the arrived heads, time jumping to the earliest
  * arrival when none has arrived (R31).  HP side, gate, R and feedback as
  * or_simulate (R13, R17-R20, R24).  Singleton streams are the POOL model. */
+/* Case A (§8f row 2; "the scheduler withholds the next launching kernel of A to let the
+ * later arriving high-priority B's kernel run"): with t_arrive > 0 the LP streams hold
+ * the GPU from t = 0 -- heads in (level, index) order among the arrived ones, time jumping to
+ * the next arrival -- and an LP kernel may start only before the HP job arrives at t_arrive;
+ * the one running then is not preempted, so the HP's first kernel starts at
+ * max(t_arrive, its end) (R33).  hp_jct stays absolute: the HP response time is
+ * hp_jct - t_arrive (R34).  LP kernels run before the HP job count in neither n_fills nor
+ * n_tail (fill_gap -1, R31's tail counter excludes them). */
 int or_simulate_stream(const uint32_t* hp_row, const uint64_t* hp_dur, const uint64_t* hp_gap, uint32_t n_h,
                        const uint32_t* lp_row, const uint64_t* lp_dur, const uint8_t* lp_level,
                        const uint32_t* lp_stream, const uint64_t* lp_think, uint32_t m, uint32_t gap_scale_q16,
                        const uint64_t* dur_mean, const uint64_t* dur_cnt, const uint64_t* gap_mean, uint32_t n_rows,
-                       uint64_t threshold, uint32_t feedback, oresult_t* out, int32_t* fill_gap, uint64_t* lp_start) {
+                       uint64_t threshold, uint32_t feedback, uint64_t t_arrive, oresult_t* out, int32_t* fill_gap,
+                       uint64_t* lp_start) {
   uint32_t M = m ? m : 1;
   uint64_t* q = (uint64_t*)malloc(M * 8);
   uint8_t* el = (uint8_t*)malloc(M);
@@ -673,6 +682,32 @@ int or_simulate_stream(const uint32_t* hp_row, const uint64_t* hp_dur, const uin
   uint64_t s = gap_scale_q16;
   uint64_t t = 0, hp_delay = 0, fill_work = 0;
   uint32_t n_fills = 0;
+  for (;;) { /* before the HP job arrives (R33) */
+    if (t >= t_arrive) break;
+    int64_t bs = -1;
+    uint64_t A = UINT64_MAX;
+    for (uint32_t j = 0; j < ns; j++) {
+      if (head[j] >= send[j]) continue;
+      if (arr[j] > t) {
+        if (arr[j] < A) A = arr[j];
+        continue;
+      }
+      uint32_t k = head[j];
+      if (bs < 0 || lp_level[k] < lp_level[head[bs]] || (lp_level[k] == lp_level[head[bs]] && k < head[bs]))
+        bs = j;
+    }
+    if (bs < 0) {
+      if (A >= t_arrive) break;
+      t = A;
+      continue;
+    }
+    uint32_t k = head[bs];
+    lp_start[k] = t;
+    t += lp_dur[k];
+    head[bs]++;
+    arr[bs] = t + lp_think[k];
+  }
+  if (t < t_arrive) t = t_arrive; /* HP kernel 0 starts at max(t_arrive, the running LP kernel's end) */
   for (uint32_t i = 0; i < n_h; i++) {
     uint64_t end = t + hp_dur[i];
     t = end;
@@ -770,8 +805,9 @@ int or_simulate_stream_batch(const uint32_t* hp_row, const uint64_t* hp_dur, con
                              const uint32_t* lp_row, const uint64_t* lp_dur, const uint8_t* lp_level,
                              const uint32_t* lp_stream, const uint64_t* lp_think, const oscen_t* sc, uint32_t S,
                              const uint64_t* dur_mean, const uint64_t* dur_cnt, const uint64_t* gap_mean,
-                             uint32_t n_rows, uint64_t threshold, uint32_t feedback, oresult_t* out,
-                             int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off) {
+                             uint32_t n_rows, uint64_t threshold, uint32_t feedback,
+                             const uint64_t* hp_arrival /* nullable: 0 */, oresult_t* out, int32_t* fill_gap,
+                             uint64_t* lp_start, const uint64_t* sched_off) {
   for (uint32_t i = 0; i < S; i++) {
     const oscen_t* c = sc + i;
     for (uint32_t k = 0; k < c->lp_len; k++) {
@@ -781,8 +817,8 @@ int or_simulate_stream_batch(const uint32_t* hp_row, const uint64_t* hp_dur, con
     int rc = or_simulate_stream(hp_row + c->hp_off, hp_dur + c->hp_off, hp_gap + c->hp_off, c->hp_len,
                                 lp_row + c->lp_off, lp_dur + c->lp_off, lp_level + c->lp_off, lp_stream + c->lp_off,
                                 lp_think + c->lp_off, c->lp_len, c->gap_scale_q16, dur_mean, dur_cnt, gap_mean,
-                                n_rows, threshold, feedback, out + i, fill_gap + sched_off[i],
-                                lp_start + sched_off[i]);
+                                n_rows, threshold, feedback, hp_arrival ? hp_arrival[i] : 0, out + i,
+                                fill_gap + sched_off[i], lp_start + sched_off[i]);
     if (rc) return rc;
   }
   return OR_OK;

@@ -115,3 +115,41 @@ def test_stream_workload_invariants():
                 assert starts[k + 1] >= starts[k] + e[k] + think[k]
         fills = gaps >= 0  # fills run inside the HP job
         assert np.all(starts[fills] < int(out[s]["hp_jct"]))
+
+
+# ---- Case A (§8f row 2; R33-R34): the LP streams hold the GPU until the HP job arrives ----
+def _case_a(t_arrive):
+    # LP: one stream of three 1000-ns kernels, no think time; HP: one 1000-ns kernel
+    out, fg, ls, _ = O.simulate_stream_batch(
+        hp_row=[0], hp_dur=[1000], hp_gap=[0], lp_row=[1, 1, 1], lp_dur=[1000, 1000, 1000], lp_level=[1, 1, 1],
+        lp_stream=[3, 3, 3], lp_think=[0, 0, 0], scenarios=_scen(1, 3), tab=TAB, threshold=100, feedback=1,
+        hp_arrival=[t_arrive])
+    return out[0], fg.tolist(), ls.tolist()
+
+
+def test_case_a_running_kernel_is_not_preempted():
+    # HP arrives at 2500 while k2 runs [2000, 3000): the HP kernel starts when k2 ends
+    o, fg, ls = _case_a(2500)
+    assert ls == [0, 1000, 2000] and fg == [-1, -1, -1]
+    assert (o["hp_jct"], o["lp_jct"], o["n_fills"], o["n_tail"]) == (4000, 3000, 0, 0)
+
+
+def test_case_a_next_launch_is_withheld():
+    # HP arrives at 2000, the moment k2 would launch: k2 is withheld and runs after the HP job
+    o, fg, ls = _case_a(2000)
+    assert ls == [0, 1000, 3000] and fg == [-1, -1, -1]
+    assert (o["hp_jct"], o["lp_jct"], o["n_fills"], o["n_tail"]) == (3000, 4000, 0, 1)
+
+
+def test_case_a_arrival_zero_is_the_stream_model():
+    cfg, sr = F.bert_vgg_stream(S=200, n_lp_runs=100)
+    rp = cfg.replay
+    tab, hr, hd, hg, lr, ld, lg = _resolved(cfg)
+    args = (hr, hd, hg, lr, ld, rp.lp_level, sr.lp_stream, lg, rp.scenarios, tab, rp.threshold_ns, rp.feedback)
+    a = O.simulate_stream_batch(*args)
+    b = O.simulate_stream_batch(*args, hp_arrival=np.zeros(200, np.uint64))
+    assert a[0].tobytes() == b[0].tobytes() and np.array_equal(a[2], b[2])
+    # and a late arrival: the HP response time never beats running alone, fills still exact
+    late = np.full(200, 3_000_000, np.uint64)
+    c = O.simulate_stream_batch(*args, hp_arrival=late)
+    assert np.all(c[0]["hp_jct"] >= late) and c[0]["n_fills"].sum() > 0
