@@ -259,13 +259,20 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
  * arrived heads; when none fits the scheduler waits for the next arrival A if
  * A - t <= R (and, with feedback, A < r_{i+1}), consuming R by the wait.  After
  * the HP job the rest runs in (level, index) order among arrived heads.
+ * Case A (§8f row 2; R33-R34): hp_arrival (device u64 per
+ * scenario, nullable = 0) is when the HP job arrives; before it the LP streams
+ * hold the GPU (arrived heads in (level, index) order), an LP kernel launches
+ * only before hp_arrival and the running one is not preempted: HP kernel 0
+ * starts at max(hp_arrival, its end).  hp_jct stays absolute; LP kernels run
+ * before the HP job count in neither n_fills nor n_tail.
  * Results, schedule and digest as fikit_simulate_batch.  Limits: m <= 1024 and
  * <= 64 streams per scenario (else FIKIT_E_ARG in the status; singleton streams
  * are the POOL model: use fikit_simulate_batch).  One warp per scenario. */
 int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
                                 const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
                                 const uint8_t* lp_level, const uint32_t* lp_stream, const uint64_t* lp_think,
-                                const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t params,
+                                const uint64_t* hp_arrival, const fikit_scenario_t* sc, uint32_t S,
+                                fikit_fill_params_t params,
                                 fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
                                 const uint64_t* sched_off, void* ws, size_t ws_bytes, void* stream);
 

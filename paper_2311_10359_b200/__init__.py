@@ -84,8 +84,8 @@ def lib():
         L.fikit_fill.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, u32, FillParamsC, p, p, p, p, p, p, sz, p]
         L.fikit_simulate_batch.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, u32, FillParamsC, p, p, p, p, p,
                                            sz, p]
-        L.fikit_simulate_stream_batch.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, p, p, u32, FillParamsC,
-                                                  p, p, p, p, p, sz, p]
+        L.fikit_simulate_stream_batch.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, p, p, p, u32,
+                                                  FillParamsC, p, p, p, p, p, sz, p]
         L.fikit_dict_union.argtypes = [p, p, p, u32, u32, u32, p, p, u32, p, p, p, sz, p]
         L.fikit_table_remap.argtypes = [C.POINTER(TableC), p, p, p, p, C.POINTER(TableC), p]
         L.fikit_table_bias.argtypes = [C.POINTER(TableC), p]
@@ -306,12 +306,12 @@ def simulate_batch(table: Table, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_leve
 
 def simulate_stream_batch(table: Table, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think,
                           scenarios, S: int, out, ws: Workspace, threshold_ns=100_000, feedback=1, fill_gap=None,
-                          lp_start=None, sched_off=None, stream=None):
-    """fikit_simulate_stream_batch: the STREAM model (LP kernel streams, R29-R32)."""
+                          lp_start=None, sched_off=None, stream=None, hp_arrival=None):
+    """fikit_simulate_stream_batch: the STREAM model (LP kernel streams, R29-R32; hp_arrival: Case A)."""
     prm = FillParamsC(threshold_ns, feedback, 0)
     _chk(lib().fikit_simulate_stream_batch(C.byref(table.c), _ptr(hp_row), _ptr(hp_dur), _ptr(hp_gap), _ptr(lp_row),
                                            _ptr(lp_dur), _ptr(lp_level), _ptr(lp_stream), _ptr(lp_think),
-                                           _ptr(scenarios), S, prm, _ptr(out), _ptr(fill_gap), _ptr(lp_start),
+                                           _ptr(hp_arrival), _ptr(scenarios), S, prm, _ptr(out), _ptr(fill_gap), _ptr(lp_start),
                                            _ptr(sched_off), ws.ptr(), ws.nbytes, _stream(stream)),
          "simulate_stream_batch")
 

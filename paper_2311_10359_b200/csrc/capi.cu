@@ -55,7 +55,7 @@ __global__ void k_simulate_reg(fikit_table_t, const uint32_t*, const uint64_t*, 
                            const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
                            fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
 __global__ void k_simulate_stream(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
-                                  const uint64_t*, const uint8_t*, const uint32_t*, const uint64_t*,
+                                  const uint64_t*, const uint8_t*, const uint32_t*, const uint64_t*, const uint64_t*,
                                   const fikit_scenario_t*, uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*,
                                   uint64_t*, const uint64_t*, fikit_status_t*);
 }  // namespace fikit
@@ -428,7 +428,8 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
 int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
                                 const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
                                 const uint8_t* lp_level, const uint32_t* lp_stream, const uint64_t* lp_think,
-                                const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t prm, fikit_result_t* out,
+                                const uint64_t* hp_arrival, const fikit_scenario_t* sc, uint32_t S,
+                                fikit_fill_params_t prm, fikit_result_t* out,
                                 int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off, void* ws,
                                 size_t ws_bytes, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -442,8 +443,9 @@ int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row
   if (!g) g = one_wave((const void*)k_simulate_stream, kStreamThreads);
   const uint64_t need = ((uint64_t)S + kStreamThreads / 32 - 1) / (kStreamThreads / 32);
   const int b = (int)(need < (uint64_t)g ? need : (uint64_t)g);
-  k_simulate_stream<<<b, kStreamThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think,
-                                      sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
+  k_simulate_stream<<<b, kStreamThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream,
+                                                  lp_think, hp_arrival, sc, S, prm, out, fill_gap, lp_start,
+                                                  sched_off, w.st());
   return launched();
 }
 

@@ -397,11 +397,11 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
                                                 const uint32_t* __restrict__ hp_row,
                                                 const uint64_t* __restrict__ hp_dur,
                                                 const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
-                                                const fikit_fill_params_t& prm, int lane) {
+                                                const fikit_fill_params_t& prm, int lane, uint64_t t_start = 0) {
   const uint32_t nh = c.hp_len;
   const uint64_t scale = c.gap_scale_q16;
   HpOut o{0, 0, 0, 0, 0};
-  uint64_t t = 0;
+  uint64_t t = t_start;  // HP kernel 0 starts here
   // chunk inputs: d, raw gap, row of HP kernel base + lane (next chunk prefetched)
   auto ld = [&](uint32_t base, uint64_t& d, uint64_t& g, uint32_t& r) {
     const uint32_t i = base + lane;
@@ -705,7 +705,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
                       const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
                       const uint64_t* __restrict__ lp_dur, const uint8_t* __restrict__ lp_level,
                       const uint32_t* __restrict__ lp_stream, const uint64_t* __restrict__ lp_think,
-                      const fikit_scenario_t* __restrict__ sc, uint32_t S, fikit_fill_params_t prm,
+                      const uint64_t* __restrict__ hp_arrival, const fikit_scenario_t* __restrict__ sc, uint32_t S,
+                      fikit_fill_params_t prm,
                       fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap,
                       uint64_t* __restrict__ lp_start, const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
   __shared__ uint32_t s_start[kStreamWarps][kMaxStreams];
@@ -859,9 +860,33 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
       }
       return t;
     };
-    HpOut o = replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane);
+    // Case A (R33): before the HP job arrives the LP streams hold the GPU (arrived heads in
+    // (level, index) order); a kernel launches only before Ta, the running one is not preempted
+    const uint64_t Ta = hp_arrival ? hp_arrival[cur] : 0;
+    uint64_t t = 0;
+    while (t < Ta) {
+      StreamPick x{0xFFu, 0, 0, 0};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        if (H.hd[h] < H.se[h] && H.A[h] <= t) {
+          const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, 0};
+          if (x.lv == 0xFFu || stream_better(y, x, false)) x = y;
+        }
+      }
+      x = warp_best_stream(x, false, half);
+      if (x.lv == 0xFFu) {
+        const uint64_t A = next_arrival(t);
+        if (A >= Ta) break;
+        t = A;
+        continue;
+      }
+      t += dispatch(x, t, -1);  // (R34: neither a fill nor the tail)
+      lp_end = max(lp_end, t);
+    }
+    HpOut o = replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane,
+                             t > Ta ? t : Ta);
     // tail (R31)
-    uint64_t t = o.t;
+    t = o.t;
     uint32_t n_tail = 0;
     for (;;) {
       StreamPick x{0xFFu, 0, 0, 0};

@@ -16,12 +16,14 @@ from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure
 class Pipeline:
     def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
                  want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None,
-                 checked: bool = False, predictor: tuple | None = None, lp_stream: np.ndarray | None = None):
+                 checked: bool = False, predictor: tuple | None = None, lp_stream: np.ndarray | None = None,
+                 hp_arrival: np.ndarray | None = None):
         """checked: verify the workspace status after every call (tests); the
         bench leaves it off and checks once after warm-up.  predictor: (mode, pct) for
         fikit_table_predict before every replay (None: the finalized means, the paper's).
         lp_stream: a stream id per LP request -> the STREAM-model replay (fikit_simulate_stream_batch,
-        think times = the LP launches' resolved gaps); None -> the POOL model."""
+        think times = the LP launches' resolved gaps); None -> the POOL model.  hp_arrival: with lp_stream,
+        the HP job's arrival per scenario (Case A preemption)."""
         torch = _torch()
         self.checked = checked
         self.predictor = predictor
@@ -42,6 +44,9 @@ class Pipeline:
             if lp_stream is not None:
                 self.replay["lp_stream"] = torch.from_numpy(np.ascontiguousarray(lp_stream, dtype=np.uint32)
                                                             .view(np.int32)).to(device)
+            if hp_arrival is not None:
+                self.replay["hp_arrival"] = torch.from_numpy(np.ascontiguousarray(hp_arrival, dtype=np.uint64)
+                                                             .view(np.int64)).to(device)
 
     def _setup_replay(self, rp, want_schedule):
         torch = _torch()
@@ -101,7 +106,8 @@ class Pipeline:
             simulate_stream_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
                                   r["lp_stream"], r["lp_gap"], r["sc"], r["S"], r["out"], self.ws,
                                   threshold_ns=r["threshold_ns"], feedback=r["feedback"], fill_gap=r.get("fill_gap"),
-                                  lp_start=r.get("lp_start"), sched_off=r.get("sched_off"), stream=stream)
+                                  lp_start=r.get("lp_start"), sched_off=r.get("sched_off"), stream=stream,
+                                  hp_arrival=r.get("hp_arrival"))
         else:
             simulate_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
                            r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],

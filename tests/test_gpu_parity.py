@@ -432,3 +432,31 @@ def test_stream_limits_flag(fk, orc):
     assert p.check.__self__ is p
     with pytest.raises(Exception):
         p.check("stream limits")
+
+
+@pytest.mark.parametrize("feedback", [1, 0])
+def test_case_a_parity(fk, orc, feedback):
+    """Case A preemption (R33-R34): the HP job arrives while the LP streams hold the GPU"""
+    from dataclasses import replace
+
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg, sr = F.bert_vgg_stream(S=2000, n_lp_runs=400)
+    cfg = F.Config(cfg.name, cfg.trace, replace(cfg.replay, feedback=feedback))
+    arrive = np.random.default_rng(5).integers(0, 5_000_000, size=2000).astype(np.uint64)
+    tr, rp = cfg.trace, cfg.replay
+    tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=1024)
+    hr, hd, hg, _ = orc.resolve(rp.hp_records, tr.names, tr.sigs, tab)
+    lr, ld, lg, _ = orc.resolve(rp.lp_records, tr.names, tr.sigs, tab)
+    out, fg, ls, _ = orc.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level, sr.lp_stream, lg, rp.scenarios, tab,
+                                               rp.threshold_ns, feedback, hp_arrival=arrive)
+    assert np.all(out["hp_jct"] >= arrive) and out["n_fills"].sum() > 0
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=1024, replay=rp, want_schedule=True, checked=True,
+                 lp_stream=sr.lp_stream, hp_arrival=arrive)
+    p.step()
+    got = p.results()
+    if got.tobytes() != out.tobytes():
+        bad = np.flatnonzero(got != out)[:5]
+        raise AssertionError(f"scenarios {bad.tolist()} differ: {got[bad]} vs {out[bad]}")
+    gfg, gls = p.schedule()
+    assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
