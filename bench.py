@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
-    ap.add_argument("--workload", default="zipf", choices=["zipf", "resnet", "bert_vgg", "sweep", "stream"])
+    ap.add_argument("--workload", default="zipf",
+                    choices=["zipf", "resnet", "bert_vgg", "sweep", "stream", "preempt"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
     ap.add_argument("--predictor", default=None,
@@ -77,7 +78,7 @@ def make_workload(args, rank, world):
         replay = F.zipf_replay(cfg, S=args.scenarios)
         cap = 8192
         desc = f"zipf-{N // 1_000_000}M (configs[3]) + replay-{args.scenarios // 1000}k"
-    elif args.workload == "stream":  # BERT/VGG with LP kernel streams
+    elif args.workload in ("stream", "preempt"):  # LP kernel streams (+ Case A)
         cfg, sr = F.bert_vgg_stream(S=args.scenarios)
         N = cfg.trace.records.shape[0]
         lo, hi = shard_range(N, rank, world)
@@ -85,8 +86,12 @@ def make_workload(args, rank, world):
         halo = cfg.trace.records[hi] if hi < N else None
         replay = cfg.replay
         lp_stream = sr.lp_stream
+        hp_arrival = None
         cap = 4096
         desc = f"bert_vgg_stream-{args.scenarios // 1000}k (STREAM-model replay, §8f row 1)"
+        if args.workload == "preempt":  # the HP job arrives U[0, 5 ms) into the LP streams' run
+            hp_arrival = np.random.default_rng(5).integers(0, 5_000_000, size=args.scenarios).astype(np.uint64)
+            desc = f"bert_vgg_preempt-{args.scenarios // 1000}k (Case A preemption, §8f row 2)"
     else:
         cfg = {"resnet": F.resnet_trace, "bert_vgg": F.bert_vgg, "sweep": F.sweep}[args.workload]()
         N = cfg.trace.records.shape[0]
@@ -101,8 +106,11 @@ def make_workload(args, rank, world):
         sel = scenario_shard(replay.scenarios.shape[0], rank, world)
         replay = F.Replay(replay.hp_records, replay.lp_records, replay.lp_level, replay.scenarios[sel],
                           replay.threshold_ns, replay.feedback)
+        if args.workload == "preempt":
+            hp_arrival = hp_arrival[sel]
     return dict(records=recs, halo=halo, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=replay, N=N, cap=cap,
-                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload == "stream" else None)
+                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload in ("stream", "preempt") else None,
+                hp_arrival=hp_arrival if args.workload == "preempt" else None)
 
 
 class ClockSampler:
@@ -216,8 +224,9 @@ def oracle_sample_time(wl, budget_s, seed=0):
         off_l = np.concatenate([[0], np.cumsum(sc["lp_len"][:-1])]).astype(np.uint32)
         sc["hp_off"], sc["lp_off"] = off_h, off_l
         if wl.get("lp_stream") is not None:  # STREAM model (think times: the resolved LP gaps)
+            ha = wl["hp_arrival"][:s_n] if wl.get("hp_arrival") is not None else None
             oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg, sc,
-                                         tab, rp.threshold_ns, rp.feedback)
+                                         tab, rp.threshold_ns, rp.feedback, hp_arrival=ha)
         else:
             oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
         t_rep = time.perf_counter() - t
@@ -286,7 +295,7 @@ def main():
     stream = torch.cuda.current_stream()
     pred = tuple(int(x) for x in args.predictor.split(",")) if args.predictor else None
     p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"],
-                 predictor=pred, lp_stream=wl["lp_stream"])
+                 predictor=pred, lp_stream=wl["lp_stream"], hp_arrival=wl["hp_arrival"])
     n_local = p.n
     dense = fk.Table(wl["cap"]) if world > 1 else None
     ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None
