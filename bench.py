@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
     ap.add_argument("--workload", default="zipf",
-                    choices=["zipf", "resnet", "bert_vgg", "sweep", "stream", "preempt"])
+                    choices=["zipf", "resnet", "bert_vgg", "sweep", "stream", "preempt", "ratio"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
     ap.add_argument("--predictor", default=None,
@@ -92,6 +92,18 @@ def make_workload(args, rank, world):
         if args.workload == "preempt":  # the HP job arrives U[0, 5 ms) into the LP streams' run
             hp_arrival = np.random.default_rng(5).integers(0, 5_000_000, size=args.scenarios).astype(np.uint64)
             desc = f"bert_vgg_preempt-{args.scenarios // 1000}k (Case A preemption, §8f row 2)"
+    elif args.workload == "ratio":  # the §4.3.2 A:B task-ratio sweep, FIKIT + exclusive arms
+        cfg, sr, ratio = F.ratio_sweep(n_base=max(1, args.scenarios // (2 * len(F.RATIO_SCALES_Q16) * len(F.RATIOS))))
+        N = cfg.trace.records.shape[0]
+        lo, hi = shard_range(N, rank, world)
+        recs = cfg.trace.records[lo:hi]
+        halo = cfg.trace.records[hi] if hi < N else None
+        replay = cfg.replay
+        lp_stream = sr.lp_stream
+        hp_arrival = None
+        cap = 4096
+        desc = (f"ratio_sweep-{replay.scenarios.shape[0] // 1000}k (§4.3.2 A:B = 1..50:1, BERT/VGG stream pairs, "
+                f"HP gaps x1/x4/x16; FIKIT arm + exclusive arm)")
     else:
         cfg = {"resnet": F.resnet_trace, "bert_vgg": F.bert_vgg, "sweep": F.sweep}[args.workload]()
         N = cfg.trace.records.shape[0]
@@ -102,15 +114,18 @@ def make_workload(args, rank, world):
         cap = 4096
         desc = {"resnet": "resnet-3M (configs[1])", "bert_vgg": "bert_vgg-100k (configs[2])",
                 "sweep": "sweep-1M (configs[4])"}[args.workload]
+    ratio = ratio if args.workload == "ratio" else None
     if replay is not None and world > 1:
         sel = scenario_shard(replay.scenarios.shape[0], rank, world)
+        if ratio is not None:
+            ratio = ratio[sel]
         replay = F.Replay(replay.hp_records, replay.lp_records, replay.lp_level, replay.scenarios[sel],
                           replay.threshold_ns, replay.feedback)
         if args.workload == "preempt":
             hp_arrival = hp_arrival[sel]
     return dict(records=recs, halo=halo, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=replay, N=N, cap=cap,
-                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload in ("stream", "preempt") else None,
-                hp_arrival=hp_arrival if args.workload == "preempt" else None)
+                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload in ("stream", "preempt", "ratio") else None,
+                hp_arrival=hp_arrival if args.workload == "preempt" else None, ratio=ratio)
 
 
 class ClockSampler:
@@ -227,12 +242,38 @@ def oracle_sample_time(wl, budget_s, seed=0):
             ha = wl["hp_arrival"][:s_n] if wl.get("hp_arrival") is not None else None
             oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg, sc,
                                          tab, rp.threshold_ns, rp.feedback, hp_arrival=ha)
+            if wl.get("ratio") is not None:  # the exclusive arm (no gap filled)
+                oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg,
+                                             sc, tab, (1 << 64) - 1, rp.feedback)
         else:
             oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
         t_rep = time.perf_counter() - t
         job += t_rep * (S / s_n)
         desc += f" + resolve/replay of {s_n} of {S:,} scenarios"
     return job, desc + "; whole-job time extrapolated linearly"
+
+
+def ratio_summary(fik, exc, ratio, sc):
+    """Per (pair, HP gap scale) series: the mean over scenarios of exclusive / FIKIT LP JCT and
+    the mean HP slowdown (hp_delay / solo) per A:B ratio (reporting only, host side)."""
+    import fikit_synth as F
+
+    out = {}
+    pair = np.where(sc["hp_len"] // ratio == 176, "A=BERT,B=VGG", "A=VGG,B=BERT")
+    for pr in ("A=BERT,B=VGG", "A=VGG,B=BERT"):
+        for q in F.RATIO_SCALES_Q16:
+            key = f"{pr},gaps_x{q >> 16}"
+            ser = {}
+            for r in F.RATIOS:
+                sel = (pair == pr) & (sc["gap_scale_q16"] == q) & (ratio == r)
+                if not sel.any():
+                    continue
+                solo = (fik["hp_jct"][sel] - fik["hp_delay"][sel]).astype(np.float64)
+                ser[f"{r}:1"] = {"lp_excl_over_fikit": round(float(np.mean(exc["lp_jct"][sel] / fik["lp_jct"][sel])), 3),
+                                 "hp_slowdown": round(float(np.mean(fik["hp_delay"][sel] / solo)), 4),
+                                 "lp_in_gaps": round(float(np.mean(fik["n_tail"][sel] == 0)), 3)}
+            out[key] = ser
+    return out
 
 
 def run_reference(args):
@@ -295,7 +336,8 @@ def main():
     stream = torch.cuda.current_stream()
     pred = tuple(int(x) for x in args.predictor.split(",")) if args.predictor else None
     p = Pipeline(wl["records"], wl["names"], wl["sigs"], capacity=wl["cap"], replay=wl["replay"], halo=wl["halo"],
-                 predictor=pred, lp_stream=wl["lp_stream"], hp_arrival=wl["hp_arrival"])
+                 predictor=pred, lp_stream=wl["lp_stream"], hp_arrival=wl["hp_arrival"],
+                 exclusive_arm=wl["ratio"] is not None)
     n_local = p.n
     dense = fk.Table(wl["cap"]) if world > 1 else None
     ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None
@@ -397,6 +439,9 @@ def main():
             "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
             "status": {"code": st["code"], "n_rows_needed": st["n_rows_needed"]},
             "gen_s": round(t_gen, 2)}
+
+    if wl["ratio"] is not None:  # §4.3.2 trend: mean exclusive / FIKIT LP JCT per A:B ratio and series
+        line["ratio_sweep"] = ratio_summary(p.results(), p.exclusive_results(), wl["ratio"], wl["replay"].scenarios)
 
     # ---- end to end through the C-ABI with host buffers (H2D + step + D2H inside the region) ----
     if not args.no_e2e:

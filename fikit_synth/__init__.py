@@ -461,6 +461,47 @@ def bert_vgg_stream(seed: int = 3, T: int = 1000, n_hp_runs: int = 1000, n_lp_ru
     return cfg, StreamReplay(rp, stream)
 
 
+RATIOS = (1, 10, 20, 30, 40, 50)  # A:B task ratios of §4.3.2
+RATIO_SCALES_Q16 = (1 << 16, 1 << 18, 1 << 20)  # HP gaps x1, x4, x16 (R24)
+
+
+def ratio_sweep(seed: int = 3, n_base: int = 2000, T: int = 1000, n_hp_runs: int = 1000, n_lp_runs: int = 4000,
+                ratios=RATIOS, scales=RATIO_SCALES_Q16) -> tuple[Config, StreamReplay, np.ndarray]:
+    """SURVEY §8f row 4, the synthetic §4.3.2 experiment: the HP service A issues
+    r tasks (r consecutive fresh inference runs, launched back to back) for every task of the
+    LP service B (one inference, a kernel stream with its own think times), r in `ratios`.
+    Models, measurement trace and runs are those of bert_vgg_stream (same seed): pairs
+    (A BERT, B VGG) and (A VGG, B BERT), each at the HP gap scales `scales`.
+
+    Scenario s: ratio index s % R; group g = s // R -> scale index g % n_scales, pair
+    (g // n_scales) % 2, base b = g // (2 n_scales).  The HP window starts at run
+    b mod (n_hp_runs - max r + 1) for every ratio of a group, so the windows of one group
+    share their prefix (the prefix pin of tests/test_oracle_ratio.py).  Returns (config,
+    stream replay, ratio per scenario).  S = 2 * n_scales * R * n_base."""
+    cfg, sr = bert_vgg_stream(seed=seed, T=T, n_hp_runs=n_hp_runs, n_lp_runs=n_lp_runs, S=1)
+    R, ns = len(ratios), len(scales)
+    S = 2 * ns * R * n_base
+    s = np.arange(S, dtype=np.int64)
+    r = np.asarray(ratios, dtype=np.int64)[s % R]
+    g = s // R
+    scale = np.asarray(scales, dtype=np.int64)[g % ns]
+    pair = (g // ns) % 2  # 0: A = BERT, B = VGG; 1: A = VGG, B = BERT
+    b = g // (2 * ns)
+    run = b % (n_hp_runs - max(ratios) + 1)
+    L_hp = np.where(pair == 0, 176, 40)
+    sc = np.zeros(S, dtype=SCEN_DTYPE)
+    sc["hp_off"] = np.where(pair == 0, 0, n_hp_runs * 176) + run * L_hp
+    sc["hp_len"] = r * L_hp
+    lp_run = b % n_lp_runs
+    sc["lp_off"] = np.where(pair == 0, lp_run * 40, 40 * n_lp_runs + lp_run * 176)
+    sc["lp_len"] = np.where(pair == 0, 40, 176)
+    sc["gap_scale_q16"] = scale
+    rp = cfg.replay
+    rp = Replay(rp.hp_records, rp.lp_records, rp.lp_level, sc, rp.threshold_ns, rp.feedback)
+    return (Config("ratio_sweep", cfg.trace, rp, {"seed": seed, "S": S, "ratios": list(ratios)}),
+            StreamReplay(rp, sr.lp_stream), r.astype(np.uint32))
+
+
 ZIPF_S = 1.1
 
 

@@ -12,18 +12,22 @@ import numpy as np
 from . import (RESULT_DTYPE, DevStrTab, Table, Workspace, _torch, check, measure, records_to_device, resolve,
                simulate_batch, simulate_stream_batch, strtab_to_device, table_finalize, table_predict)
 
+NO_FILL = (1 << 64) - 1  # a threshold no predicted gap reaches: the exclusive-mode arm
+
 
 class Pipeline:
     def __init__(self, records: np.ndarray, names, sigs, capacity: int | None = None, replay=None, device="cuda",
                  want_rows: bool = False, want_schedule: bool = False, halo: np.ndarray | None = None,
                  checked: bool = False, predictor: tuple | None = None, lp_stream: np.ndarray | None = None,
-                 hp_arrival: np.ndarray | None = None):
+                 hp_arrival: np.ndarray | None = None, exclusive_arm: bool = False):
         """checked: verify the workspace status after every call (tests); the
         bench leaves it off and checks once after warm-up.  predictor: (mode, pct) for
         fikit_table_predict before every replay (None: the finalized means, the paper's).
         lp_stream: a stream id per LP request -> the STREAM-model replay (fikit_simulate_stream_batch,
         think times = the LP launches' resolved gaps); None -> the POOL model.  hp_arrival: with lp_stream,
-        the HP job's arrival per scenario (Case A preemption)."""
+        the HP job's arrival per scenario (Case A preemption).  exclusive_arm: every replay is followed
+        by a second one with threshold 2^64 - 1 (no gap is filled: B runs after A, the exclusive-mode
+        analogue of P:103 / P:478) into exclusive_results()."""
         torch = _torch()
         self.checked = checked
         self.predictor = predictor
@@ -41,6 +45,8 @@ class Pipeline:
         self.replay = None
         if replay is not None:
             self._setup_replay(replay, want_schedule)
+            if exclusive_arm:
+                self.replay["out_excl"] = torch.empty_like(self.replay["out"])
             if lp_stream is not None:
                 self.replay["lp_stream"] = torch.from_numpy(np.ascontiguousarray(lp_stream, dtype=np.uint32)
                                                             .view(np.int32)).to(device)
@@ -102,17 +108,23 @@ class Pipeline:
         resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
                 self.ws, stream=stream)
         self._chk("resolve(lp)", stream)
+        self._simulate(tab, r["out"], r["threshold_ns"], True, stream)
+        if "out_excl" in r:
+            self._simulate(tab, r["out_excl"], NO_FILL, False, stream)
+
+    def _simulate(self, tab, out, threshold_ns, with_schedule, stream):
+        r = self.replay
+        sched = dict(fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off")) \
+            if with_schedule else {}
         if "lp_stream" in r:
             simulate_stream_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
-                                  r["lp_stream"], r["lp_gap"], r["sc"], r["S"], r["out"], self.ws,
-                                  threshold_ns=r["threshold_ns"], feedback=r["feedback"], fill_gap=r.get("fill_gap"),
-                                  lp_start=r.get("lp_start"), sched_off=r.get("sched_off"), stream=stream,
-                                  hp_arrival=r.get("hp_arrival"))
+                                  r["lp_stream"], r["lp_gap"], r["sc"], r["S"], out, self.ws,
+                                  threshold_ns=threshold_ns, feedback=r["feedback"], stream=stream,
+                                  hp_arrival=r.get("hp_arrival"), **sched)
         else:
             simulate_batch(tab, r["hp_row"], r["hp_dur"], r["hp_gap"], r["lp_row"], r["lp_dur"], r["lp_level"],
-                           r["sc"], r["S"], r["out"], self.ws, threshold_ns=r["threshold_ns"], feedback=r["feedback"],
-                           fill_gap=r.get("fill_gap"), lp_start=r.get("lp_start"), sched_off=r.get("sched_off"),
-                           stream=stream)
+                           r["sc"], r["S"], out, self.ws, threshold_ns=threshold_ns, feedback=r["feedback"],
+                           stream=stream, **sched)
         self._chk("simulate_batch", stream)
 
     def _chk(self, what, stream):
@@ -131,6 +143,10 @@ class Pipeline:
     def results(self) -> np.ndarray:
         r = self.replay
         return r["out"].cpu().numpy()[: r["S"] * 48].view(RESULT_DTYPE)
+
+    def exclusive_results(self) -> np.ndarray:
+        r = self.replay
+        return r["out_excl"].cpu().numpy()[: r["S"] * 48].view(RESULT_DTYPE)
 
     def schedule(self):
         r = self.replay

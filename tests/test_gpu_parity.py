@@ -460,3 +460,34 @@ def test_case_a_parity(fk, orc, feedback):
         raise AssertionError(f"scenarios {bad.tolist()} differ: {got[bad]} vs {out[bad]}")
     gfg, gls = p.schedule()
     assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
+
+
+@pytest.mark.parametrize("feedback", [1, 0])
+def test_ratio_sweep_parity(fk, orc, feedback):
+    """§4.3.2 ratio sweep: HP windows of 1..50 inferences (up to
+    8800 HP kernels per scenario) against one LP inference stream; FIKIT arm and exclusive arm
+    (threshold 2^64 - 1) both bit-exact vs the oracle"""
+    from dataclasses import replace
+
+    from paper_2311_10359_b200.pipeline import NO_FILL, Pipeline
+
+    cfg, sr, rat = F.ratio_sweep(n_base=24)
+    cfg = F.Config(cfg.name, cfg.trace, replace(cfg.replay, feedback=feedback))
+    tr, rp = cfg.trace, cfg.replay
+    tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=1024)
+    hr, hd, hg, _ = orc.resolve(rp.hp_records, tr.names, tr.sigs, tab)
+    lr, ld, lg, _ = orc.resolve(rp.lp_records, tr.names, tr.sigs, tab)
+    args = (hr, hd, hg, lr, ld, rp.lp_level, sr.lp_stream, lg, rp.scenarios, tab)
+    out, fg, ls, _ = orc.simulate_stream_batch(*args, rp.threshold_ns, feedback)
+    exc, _, _, _ = orc.simulate_stream_batch(*args, NO_FILL, feedback)
+    assert out["n_fills"].sum() > 0 and np.all(exc["n_fills"] == 0)
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=1024, replay=rp, want_schedule=True, checked=True,
+                 lp_stream=sr.lp_stream, exclusive_arm=True)
+    p.step()
+    for got, ref in ((p.results(), out), (p.exclusive_results(), exc)):
+        if got.tobytes() != ref.tobytes():
+            bad = np.flatnonzero(got != ref)[:5]
+            raise AssertionError(f"scenarios {bad.tolist()} (ratios {rat[bad].tolist()}) differ: "
+                                 f"{got[bad]} vs {ref[bad]}")
+    gfg, gls = p.schedule()
+    assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
