@@ -432,18 +432,16 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
       uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
       if (lane >= dd) X += y;
     }
-    const bool gate = valid && !last && p_l >= prm.threshold_ns && p_l >= gate_min() && (!prm.feedback || a_l > 0);
-    uint32_t gmask = __ballot_sync(0xffffffffu, gate);
+    const bool gate = valid && !last && p_l >= prm.threshold_ns && (!prm.feedback || a_l > 0);
+    uint32_t gmask = __ballot_sync(0xffffffffu, gate && p_l >= gate_min());
     const uint64_t T0 = t;
     uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
     while (gmask) {
       const int j = __ffs(gmask) - 1;
-      gmask &= gmask - 1;
       const uint32_t i = base + j;
       const uint64_t Xj = __shfl_sync(0xffffffffu, X, j);
       const uint64_t a = __shfl_sync(0xffffffffu, a_l, j);
       const uint64_t p = __shfl_sync(0xffffffffu, p_l, j);
-      if (p < gate_min()) continue;  // the pool has shrunk since the gate was computed
       t = T0 + shift + Xj - a;  // end of HP kernel i
       const uint64_t r = t + a;   // the HP client's next launch arrives (R20)
       t = fill(i, t, r, p, o);    // Alg. 1 over this gap (R = p)
@@ -451,6 +449,9 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
         o.hp_delay += t - r;
         shift += t - r;
       }
+      // the gate bound may have moved either way (a fill consumed the smallest request, or a
+      // stream's next head is smaller): re-gate the rest of the chunk
+      gmask = j == 31 ? 0u : __ballot_sync(0xffffffffu, gate && p_l >= gate_min()) & (~0u << (j + 1));
     }
     t = T0 + shift + __shfl_sync(0xffffffffu, X, 31);  // next kernel's start (or the HP end)
   }
@@ -832,6 +833,19 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
       for (uint32_t o2 = half; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
       return __shfl_sync(0xffffffffu, a, 0);
     };
+    // gate bound with feedback: the minimum q over the eligible current heads.  Heads change only
+    // by a dispatch, so in a gap with p below it no head can ever fit; the waits the gap could
+    // still make end before r_{i+1} (feedback) and leave no trace: skipping the gap is exact.
+    // (Without feedback a wait may run past r_{i+1} and delay the HP job: the window bound qmin.)
+    auto heads_min = [&]() -> uint64_t {
+      uint64_t a = ~0ull;
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if (H.hd[h] < H.se[h] && H.el[h]) a = min(a, H.q[h]);
+      for (uint32_t o2 = half; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
+      return __shfl_sync(0xffffffffu, a, 0);
+    };
+    uint64_t gmin = qmin;
     auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
       for (;;) {
         if (prm.feedback && t >= r) break;  // R19
@@ -846,6 +860,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
         x = warp_best_stream(x, true, half);
         if (x.lv != 0xFFu) {
           const uint64_t e = dispatch(x, t, (int32_t)i);
+          if (prm.feedback) gmin = heads_min();
           t += e;
           R -= x.q;  // R17
           o.fill_work += e;
@@ -883,7 +898,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
       t += dispatch(x, t, -1);  // (R34: neither a fill nor the tail)
       lp_end = max(lp_end, t);
     }
-    HpOut o = replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane,
+    if (prm.feedback) gmin = heads_min();
+    HpOut o = replay_hp_core([&]() { return gmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane,
                              t > Ta ? t : Ta);
     // tail (R31)
     t = o.t;
