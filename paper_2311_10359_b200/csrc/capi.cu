@@ -10,6 +10,7 @@
 namespace fikit {
 // kernels (measure.cu, finalize.cu, replay.cu)
 __global__ void k_reset_status(fikit_status_t*);
+__global__ void k_zero(ZeroList, fikit_status_t*);
 __global__ void k_strtab_hash(fikit_strtab_t, uint64_t*, fikit_strtab_t, uint64_t*, fikit_status_t*);
 __global__ void k_identify(const uint4*, uint64_t, const uint64_t*, const uint64_t*, uint32_t, uint32_t, uint64_t*,
                            fikit_status_t*);
@@ -223,20 +224,26 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w, n)) return r;
   const fikit_table_t t = *tab;
   const uint32_t cap = t.capacity;
-  if (int r = reset_status(w, s)) return r;
-  // zero the table (an all-zero row is the identity of every statistic) and the index
-  cudaMemsetAsync(t.kernel_id, 0, 8ull * cap, s);
-  cudaMemsetAsync(t.task_id, 0, 4ull * cap, s);
-  cudaMemsetAsync(t.sums, 0, 32ull * cap, s);
-  cudaMemsetAsync(t.hist, 0, 256ull * cap, s);
-  cudaMemsetAsync(t.ext, 0, 32ull * cap, s);
-  cudaMemsetAsync(t.mean, 0, 16ull * cap, s);
-  cudaMemsetAsync(t.n_rows, 0, 4, s);
-  cudaMemsetAsync(w.index(), 0, sizeof(IndexEntry) * (size_t)w.L.slots, s);
-  cudaMemsetAsync(w.tindex(), 0, sizeof(Tuple) * (size_t)w.L.tslots, s);
-  cudaMemsetAsync(w.samp_cnt(), 0, 4ull * cap, s);
-  cudaMemsetAsync(w.hot_n(), 0, 4ull * kHotHdr, s);
-  if (cudaGetLastError() != cudaSuccess) return FIKIT_E_CUDA;
+  // reset the status and zero the table (an all-zero row is the identity of every statistic),
+  // the indexes and the sample counts: one launch
+  ZeroList z{};
+  auto add = [&](void* p, uint64_t bytes) {
+    z.p[z.k] = p;
+    z.n[z.k++] = bytes;
+  };
+  add(t.kernel_id, 8ull * cap);
+  add(t.task_id, 4ull * cap);
+  add(t.sums, 32ull * cap);
+  add(t.hist, 256ull * cap);
+  add(t.ext, 32ull * cap);
+  add(t.mean, 16ull * cap);
+  add(t.n_rows, 4);
+  add(w.index(), sizeof(IndexEntry) * (size_t)w.L.slots);
+  add(w.tindex(), sizeof(Tuple) * (size_t)w.L.tslots);
+  add(w.samp_cnt(), 4ull * cap);
+  add(w.hot_n(), 4ull * kHotHdr);
+  k_zero<<<2 * num_sms(), 256, 0, s>>>(z, w.st());
+  if (int r = launched()) return r;
   if (int r = hash_strtabs(w, names, sigs, s)) return r;
   if (n == 0) return FIKIT_OK;
   // sample ~64k launches (all of them for small traces) to choose the hot rows

@@ -32,6 +32,13 @@ struct WsLayout {
 constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (measure kernel)
 // Task-partitioned scheduling of fikit_measure: warp-tiles (32 launches) are bucketed by a
 // hash of their first launch's task_id; every bucket has its own hot set.
+// regions zeroed by k_zero (one launch instead of a memset per region)
+constexpr int kZeroRegions = 12;
+struct ZeroList {
+  void* p[kZeroRegions];
+  uint64_t n[kZeroRegions];  // bytes, multiples of 4; p 4-B aligned
+  int k;
+};
 constexpr uint32_t kBuckets = 64;
 constexpr uint32_t kMaxCTAs = 1024;
 constexpr uint32_t kSortBlocks = 160;  // blocks of the tile counting sort (each a contiguous chunk)

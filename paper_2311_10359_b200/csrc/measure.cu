@@ -20,7 +20,7 @@
 namespace fikit {
 
 // ------------------------------------------------------------------------------------
-__global__ void k_reset_status(fikit_status_t* st) {
+__device__ __forceinline__ void k_reset_status_body(fikit_status_t* st) {
   if (threadIdx.x == 0) {
     st->code = 0;
     st->flags = 0;
@@ -32,6 +32,25 @@ __global__ void k_reset_status(fikit_status_t* st) {
     reinterpret_cast<uint32_t*>(st)[kSchedWord1] = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord2] = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord3] = 0;
+  }
+}
+__global__ void k_reset_status(fikit_status_t* st) { k_reset_status_body(st); }
+
+// Zero up to kZeroRegions device regions (4-B multiples) in one launch, and (block 0) reset
+// the status as k_reset_status does: the measure call's table / index / sample zeroing.
+__global__ void k_zero(ZeroList z, fikit_status_t* st) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) k_reset_status_body(st);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < z.k; r++) {
+    unsigned char* p = static_cast<unsigned char*>(z.p[r]);
+    const uint64_t n = z.n[r];
+    const uint64_t mis = (16u - ((uintptr_t)p & 15u)) & 15u, head = n < mis ? n : mis;  // to 16-B alignment
+    const uint64_t nv = (n - head) / 16;
+    if (tid < head / 4) reinterpret_cast<uint32_t*>(p)[tid] = 0u;
+    uint4* v = reinterpret_cast<uint4*>(p + head);
+    for (uint64_t i = tid; i < nv; i += nt) v[i] = make_uint4(0, 0, 0, 0);
+    const uint64_t done = head + 16 * nv;
+    if (tid < (n - done) / 4) reinterpret_cast<uint32_t*>(p + done)[tid] = 0u;
   }
 }
 
