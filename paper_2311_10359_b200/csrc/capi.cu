@@ -28,7 +28,7 @@ __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*
 size_t measure_smem_bytes();
 int measure_threads();
 struct FinRow;
-__global__ void k_fin_prep(const fikit_status_t*, fikit_table_t, FinRow*, uint32_t*);
+__global__ void k_fin_prep(const fikit_status_t*, fikit_table_t, FinRow*, uint32_t*, uint32_t*);
 __global__ void k_fin_chunksort(const fikit_table_t, const uint32_t*, uint64_t*, uint32_t*);
 __global__ void k_fin_rank(const fikit_table_t, const uint32_t*, const uint64_t*, const uint32_t*, uint32_t*);
 __global__ void k_fin_scatter(fikit_table_t, const FinRow*, const uint32_t*, const uint32_t*);
@@ -320,11 +320,10 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   uint32_t* kptr = w.misc() + kMiscNRec;
   unsigned g = (cap + 255) / 256;
   const unsigned gw = (cap + 7) / 8;  // 8 rows (warps) per 256-thread block
-  k_fin_prep<<<gw, 256, 0, s>>>(w.st(), t, fin, kptr);
+  k_fin_prep<<<gw, 256, 0, s>>>(w.st(), t, fin, kptr, rank);  // (also zeroes rank[0, cap))
   if (int r = launched()) return r;
   k_fin_chunksort<<<(cap + 255) / 256, 256, 0, s>>>(t, kptr, skid, stask);
   if (int r = launched()) return r;
-  cudaMemsetAsync(rank, 0, 4ull * cap, s);
   k_fin_rank<<<dim3(g, (cap + 2047) / 2048), 256, 0, s>>>(t, kptr, skid, stask, rank);
   if (int r = launched()) return r;
   k_fin_scatter<<<gw, 256, 0, s>>>(t, fin, rank, kptr);

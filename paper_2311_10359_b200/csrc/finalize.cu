@@ -26,12 +26,14 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
 }
 
 // rows -> scratch; counts = histogram totals (SK/SG denominators)
-__global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* fin, uint32_t* n_out) {
+__global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* fin, uint32_t* n_out,
+                           uint32_t* rank) {
   // one warp per row: the 64 histogram words of a row are read coalesced
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, tab.capacity);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r == 0 && lane == 0) *n_out = K;
+  if (lane == 1 && r < tab.capacity) rank[r] = 0u;  // (k_fin_rank accumulates into it)
   if (r >= K) return;
   FinRow& f = fin[r];
   const uint32_t h0 = tab.hist[(size_t)r * 64 + lane], h1 = tab.hist[(size_t)r * 64 + 32 + lane];
