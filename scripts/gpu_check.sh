@@ -29,7 +29,7 @@ if [ -n "$MULTI" ]; then
 fi
 if [ -n "$EXTRA_BENCH" ]; then
   # the other configs as bench lines (context; the driver's line is the default workload)
-  for wl in resnet bert_vgg sweep; do
+  for wl in resnet bert_vgg sweep stream preempt ratio; do
     timeout 600 python bench.py --workload $wl --steps 50 --warmup 3 --no-e2e --cpu-budget-s 10 > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err
     cat gpurun_out/bench_$wl.json | head -c 600; echo
   done
