@@ -87,11 +87,27 @@ __global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint6
     for (uint32_t i = lane; i < nch; i += 32) buf[w][i] = __ldg(base + c0 + i);
     __syncwarp();
     if (lane == 0) {
-      const unsigned char* sb = reinterpret_cast<const unsigned char*>(buf[w]);
-      const uint32_t p1 = min(hi, (c0 + nch) * 16);
-      for (uint32_t pos = max(lo, c0 * 16); pos < p1; pos++) {
-        h ^= (uint64_t)sb[pos - c0 * 16];
-        h *= 0x100000001b3ULL;
+      // one 16-B shared load per block, then its bytes in order from registers (the serial
+      // multiply chain is the only latency left)
+      for (uint32_t i = 0; i < nch; i++) {
+        const uint4 v = buf[w][i];
+        const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t b0 = (c0 + i) * 16;
+        if (b0 >= lo && b0 + 16 <= hi) {
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            h ^= (uint64_t)((q[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+            h *= 0x100000001b3ULL;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            if (b0 + k >= lo && b0 + k < hi) {
+              h ^= (uint64_t)((q[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+              h *= 0x100000001b3ULL;
+            }
+          }
+        }
       }
     }
     __syncwarp();
@@ -151,13 +167,19 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
                          const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash,
                          uint32_t n_names, uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st,
                          fikit_table_t tab, Tuple* row_tuple, uint32_t* samp_cnt) {
-  // per-block counts (a skewed sample hits a few rows thousands of times: one L2 atomic per
-  // distinct row per block instead of one per sample)
-  constexpr uint32_t HS = 1024;
-  __shared__ uint32_t hrow[HS], hcnt[HS];
+  // Per-block deduplication before the global index: the block's samples are counted per
+  // distinct identity in shared memory (keyed by a 64-bit fingerprint of (kernel ID, task)),
+  // then one representative per identity resolves its row in the global index and adds the
+  // count.  A skewed sample hits a few identities thousands of times; this keeps the global
+  // index (and its first-insert races) to one access per distinct identity per block.  The
+  // sample only chooses the hot rows, so a (astronomically rare) fingerprint collision merely
+  // credits one identity's samples to another: k_measure still resolves every launch exactly.
+  constexpr uint32_t HS = 512;
+  __shared__ unsigned long long sfp[HS], skid[HS];
+  __shared__ uint32_t scnt[HS], stw[HS][7];
   for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x) {
-    hrow[i] = 0xFFFFFFFFu;
-    hcnt[i] = 0;
+    sfp[i] = 0;
+    scnt[i] = 0;
   }
   __syncthreads();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_samples;
@@ -170,28 +192,38 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
     uint4 a = __ldg(recs + i * 3), b = __ldg(recs + i * 3 + 1), c = __ldg(recs + i * 3 + 2);
     uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
     if (!record_valid(w, n_names, n_sigs)) continue;  // reported by k_measure
-    uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
-    uint32_t tw[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
-    uint32_t row =
-        index_find_or_insert(idx, slots, kid, w[11], tw, st, tab.kernel_id, tab.task_id, row_tuple, tab.capacity);
-    if (row < tab.capacity) {
-      uint32_t p = (row * 0x9E3779B1u) >> 22;  // 10 bits
-      for (uint32_t probe = 0;; probe++, p = (p + 1) & (HS - 1)) {
-        if (probe == HS) {  // table full (> HS distinct rows in this block): count directly
-          atomicAdd(samp_cnt + row, 1u);
-          break;
-        }
-        const uint32_t old = atomicCAS(&hrow[p], 0xFFFFFFFFu, row);
-        if (old == 0xFFFFFFFFu || old == row) {
-          atomicAdd(&hcnt[p], 1u);
-          break;
-        }
+    const uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+    const uint32_t tw[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
+    const unsigned long long fp = mix64(kid ^ ((uint64_t)w[11] * 0x9E3779B97F4A7C15ULL)) | 1ull;
+    uint32_t p = (uint32_t)(fp >> 32) & (HS - 1);
+    bool counted = false;
+    for (uint32_t probe = 0; probe < HS; probe++, p = (p + 1) & (HS - 1)) {
+      const unsigned long long old = atomicCAS(&sfp[p], 0ull, fp);
+      if (old == 0ull) {  // first sample of this identity in the block: the representative
+        skid[p] = kid;
+#pragma unroll
+        for (int q = 0; q < 7; q++) stw[p][q] = tw[q];
       }
+      if (old == 0ull || old == fp) {
+        atomicAdd(&scnt[p], 1u);
+        counted = true;
+        break;
+      }
+    }
+    if (!counted) {  // the block saw > HS identities: resolve and count directly
+      const uint32_t row =
+          index_find_or_insert(idx, slots, kid, w[11], tw, st, tab.kernel_id, tab.task_id, row_tuple, tab.capacity);
+      if (row < tab.capacity) atomicAdd(samp_cnt + row, 1u);
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x)
-    if (hcnt[i]) atomicAdd(samp_cnt + hrow[i], hcnt[i]);
+  for (uint32_t q = threadIdx.x; q < HS; q += blockDim.x) {
+    const uint32_t cnt = scnt[q];
+    if (!cnt) continue;
+    const uint32_t row = index_find_or_insert(idx, slots, skid[q], stw[q][6], stw[q], st, tab.kernel_id, tab.task_id,
+                                              row_tuple, tab.capacity);
+    if (row < tab.capacity) atomicAdd(samp_cnt + row, cnt);
+  }
 }
 
 // ---- hot sets: per task bucket, the most-sampled rows (one CTA per bucket; CTA kBuckets:
