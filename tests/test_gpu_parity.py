@@ -491,3 +491,38 @@ def test_ratio_sweep_parity(fk, orc, feedback):
                                  f"{got[bad]} vs {ref[bad]}")
     gfg, gls = p.schedule()
     assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
+
+
+def test_empty_inputs(fk, orc):
+    """degenerate sizes: an empty trace (no rows, status OK), an empty replay batch, and a replay
+    against the empty profile (no predictions: every LP request runs in the tail)"""
+    from dataclasses import replace
+
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    tr = F.random_trace(3, 0)
+    ref, rst, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=16)
+    assert ref.n_rows == 0 and rst["code"] == 0
+    p = run_measure(fk, tr, capacity=16)
+    st = p.check()
+    assert st["code"] == 0 and st["n_rows_needed"] == 0 and p.table.n_rows() == 0
+    src = F.random_trace(4, 500, n_ids=12)
+    rp = F.random_replay(5, src, 40, m_max=20, n_h_max=12)
+    cfg = F.Config("empty-profile", tr, rp)
+    out = _replay_parity(fk, orc, cfg, 16)["results"]
+    assert np.all(out["n_fills"] == 0) and np.array_equal(out["n_tail"], rp.scenarios["lp_len"])
+    none = replace(rp, scenarios=rp.scenarios[:0])
+    _replay_parity(fk, orc, F.Config("no-scenarios", src, none), 64)
+
+
+@pytest.mark.parametrize("zero_frac", [0.5, 1.0])
+def test_zero_durations_and_zero_threshold(fk, orc, zero_frac):
+    """R18: q = 0 requests keep fitting (each dequeued once); tau = 0 opens every gap with p >= 0
+    (zero_frac 1.0: every profiled duration and gap is 0)"""
+    from dataclasses import replace
+
+    tr = F.random_trace(41, 6000, n_ids=30, zero_frac=zero_frac)
+    for fb in (1, 0):
+        rp = replace(F.random_replay(42, tr, 400, m_max=80, n_h_max=40, levels=9), threshold_ns=0, feedback=fb)
+        ref = _replay_parity(fk, orc, F.Config("zero", tr, rp), 128)
+        assert ref["results"]["n_fills"].sum() > 0
