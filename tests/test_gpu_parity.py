@@ -512,7 +512,7 @@ def test_empty_inputs(fk, orc):
     out = _replay_parity(fk, orc, cfg, 16)["results"]
     assert np.all(out["n_fills"] == 0) and np.array_equal(out["n_tail"], rp.scenarios["lp_len"])
     none = replace(rp, scenarios=rp.scenarios[:0])
-    _replay_parity(fk, orc, F.Config("no-scenarios", src, none), 64)
+    _replay_parity(fk, orc, F.Config("no-scenarios", src, none), 64, check_schedule=False)
 
 
 @pytest.mark.parametrize("zero_frac", [0.5, 1.0])
