@@ -677,31 +677,21 @@ struct StreamPick {  // the best head of a warp reduction (valid: lv != 0xFF)
   uint64_t q;
 };
 
-// a better than b: (level asc, q desc, index asc) for fills (q_desc = true), (level, index) for the tail
-__device__ __forceinline__ bool stream_better(const StreamPick& a, const StreamPick& b, bool q_desc) {
-  if (a.lv != b.lv) return a.lv < b.lv;
-  if (q_desc && a.q != b.q) return a.q > b.q;
-  return a.k < b.k;
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t a) {
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0u);
+  return ((uint64_t)hi << 32) | lo;
 }
 
-// reduction over lanes [0, 2 * half): streams live on lanes < min(ns, 32)
-__device__ __forceinline__ StreamPick warp_best_stream(StreamPick x, bool q_desc, uint32_t half) {
-  for (uint32_t off = half; off; off >>= 1) {
-    StreamPick y;
-    y.lv = __shfl_xor_sync(0xffffffffu, x.lv, off);
-    y.k = __shfl_xor_sync(0xffffffffu, x.k, off);
-    y.sid = __shfl_xor_sync(0xffffffffu, x.sid, off);
-    y.q = __shfl_xor_sync(0xffffffffu, x.q, off);
-    if (y.lv != 0xFFu && (x.lv == 0xFFu || stream_better(y, x, q_desc))) x = y;
-  }
-  x.lv = __shfl_sync(0xffffffffu, x.lv, 0);  // lanes >= 2 * half took no part: lane 0's result
-  x.k = __shfl_sync(0xffffffffu, x.k, 0);
-  x.sid = __shfl_sync(0xffffffffu, x.sid, 0);
-  x.q = __shfl_sync(0xffffffffu, x.q, 0);
-  return x;
+// warp minimum of a u64 (all lanes): REDUX on the high words, then on the low words of the
+// lanes holding the minimal high word
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t a) {
+  const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32));
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0xFFFFFFFFu);
+  return ((uint64_t)hi << 32) | lo;
 }
 
-__global__ void __launch_bounds__(kStreamWarps * 32)
+__global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20 warps per SM
     k_simulate_stream(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                       const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
                       const uint64_t* __restrict__ lp_dur, const uint8_t* __restrict__ lp_level,
@@ -763,9 +753,6 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
     for (int o2 = 16; o2; o2 >>= 1) qmin = min(qmin, __shfl_xor_sync(0xffffffffu, qmin, o2));
     __syncwarp();
     StreamHeads H{};
-    // reduction width: the smallest power of two >= the lanes holding streams
-    const uint32_t nl = ns < 32 ? ns : 32u;
-    const uint32_t half = nl <= 1 ? 0u : (1u << (31 - __clz(nl - 1)));
     auto prefetch_next = [&](int h) {  // duration and think time of the request after the head
       const uint32_t k = H.hd[h] + 1;
       H.en[h] = k < H.se[h] ? __ldg(lp_dur + off + k) : 0;
@@ -830,8 +817,51 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
 #pragma unroll
       for (int h = 0; h < 2; h++)
         if (H.hd[h] < H.se[h] && H.A[h] > t) a = min(a, H.A[h]);
-      for (uint32_t o2 = half; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
-      return __shfl_sync(0xffffffffu, a, 0);
+      return warp_min_u64(a);
+    };
+    // Alg. 2 over the arrived eligible heads with q <= R, preference (level asc, q desc, index
+    // asc): three warp reductions (REDUX) narrow the candidates level, then q, then index
+    auto pick_fill = [&](uint64_t t, uint64_t R, StreamPick& x) -> bool {
+      bool c0 = H.hd[0] < H.se[0] && H.A[0] <= t && H.el[0] && H.q[0] <= R;
+      bool c1 = H.hd[1] < H.se[1] && H.A[1] <= t && H.el[1] && H.q[1] <= R;
+      if (ns == 1) {  // one stream (lane 0, slot 0): its head or nothing
+        if (!(__ballot_sync(0xffffffffu, c0) & 1u)) return false;
+        x.sid = 0;
+        x.k = __shfl_sync(0xffffffffu, H.hd[0], 0);
+        x.lv = __shfl_sync(0xffffffffu, H.lv[0], 0);
+        x.q = __shfl_sync(0xffffffffu, H.q[0], 0);
+        return true;
+      }
+      const uint32_t L = __reduce_min_sync(0xffffffffu, min(c0 ? H.lv[0] : 0xFFu, c1 ? H.lv[1] : 0xFFu));
+      if (L == 0xFFu) return false;
+      c0 = c0 && H.lv[0] == L;
+      c1 = c1 && H.lv[1] == L;
+      const uint64_t qb = warp_max_u64(max(c0 ? H.q[0] : 0ull, c1 ? H.q[1] : 0ull));
+      c0 = c0 && H.q[0] == qb;
+      c1 = c1 && H.q[1] == qb;
+      const uint32_t kb = __reduce_min_sync(0xffffffffu, min(c0 ? H.hd[0] : 0xFFFFFFFFu, c1 ? H.hd[1] : 0xFFFFFFFFu));
+      const uint32_t b0 = __ballot_sync(0xffffffffu, c0 && H.hd[0] == kb);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, c1 && H.hd[1] == kb);
+      x.sid = b0 ? (uint32_t)(__ffs(b0) - 1) : 32u + (uint32_t)(__ffs(b1) - 1);
+      x.k = kb;
+      x.lv = L;
+      x.q = qb;
+      return true;
+    };
+    // the tail's / Case A's pick (R31, R33): the arrived head first in (level, index) order, as
+    // one 32-bit key per slot (level <= 9, index < 1024) and one warp min (REDUX)
+    auto pick_level_index = [&](uint64_t t, StreamPick& x) -> bool {
+      uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
+      if (H.hd[0] < H.se[0] && H.A[0] <= t) k0 = (H.lv[0] << 16) | H.hd[0];
+      if (H.hd[1] < H.se[1] && H.A[1] <= t) k1 = (H.lv[1] << 16) | H.hd[1];
+      const uint32_t best = __reduce_min_sync(0xffffffffu, min(k0, k1));
+      if (best == 0xFFFFFFFFu) return false;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, k0 == best), b1 = __ballot_sync(0xffffffffu, k1 == best);
+      x.sid = b0 ? (uint32_t)(__ffs(b0) - 1) : 32u + (uint32_t)(__ffs(b1) - 1);
+      x.k = best & 0xFFFFu;
+      x.lv = best >> 16;
+      x.q = 0;
+      return true;
     };
     // gate bound with feedback: the minimum q over the eligible current heads.  Heads change only
     // by a dispatch, so in a gap with p below it no head can ever fit; the waits the gap could
@@ -842,23 +872,14 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
 #pragma unroll
       for (int h = 0; h < 2; h++)
         if (H.hd[h] < H.se[h] && H.el[h]) a = min(a, H.q[h]);
-      for (uint32_t o2 = half; o2; o2 >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o2));
-      return __shfl_sync(0xffffffffu, a, 0);
+      return warp_min_u64(a);
     };
     uint64_t gmin = qmin;
     auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
       for (;;) {
         if (prm.feedback && t >= r) break;  // R19
         StreamPick x{0xFFu, 0, 0, 0};  // BestPrioFit over the arrived heads (Alg. 2)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          if (H.hd[h] < H.se[h] && H.A[h] <= t && H.el[h] && H.q[h] <= R) {
-            const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, H.q[h]};
-            if (x.lv == 0xFFu || stream_better(y, x, true)) x = y;
-          }
-        }
-        x = warp_best_stream(x, true, half);
-        if (x.lv != 0xFFu) {
+        if (pick_fill(t, R, x)) {
           const uint64_t e = dispatch(x, t, (int32_t)i);
           if (prm.feedback) gmin = heads_min();
           t += e;
@@ -881,15 +902,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
     uint64_t t = 0;
     while (t < Ta) {
       StreamPick x{0xFFu, 0, 0, 0};
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        if (H.hd[h] < H.se[h] && H.A[h] <= t) {
-          const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, 0};
-          if (x.lv == 0xFFu || stream_better(y, x, false)) x = y;
-        }
-      }
-      x = warp_best_stream(x, false, half);
-      if (x.lv == 0xFFu) {
+      if (!pick_level_index(t, x)) {
         const uint64_t A = next_arrival(t);
         if (A >= Ta) break;
         t = A;
@@ -905,16 +918,47 @@ __global__ void __launch_bounds__(kStreamWarps * 32)
     t = o.t;
     uint32_t n_tail = 0;
     for (;;) {
-      StreamPick x{0xFFu, 0, 0, 0};
+      // one stream left: its requests run back to back, each think time after the previous
+      // one ends (the device is otherwise idle), so their starts are a prefix sum over e + think
+      // (32 requests per step) -- exactly what the loop below would dispatch one at a time
+      const uint32_t v0 = __ballot_sync(0xffffffffu, H.hd[0] < H.se[0]);
+      const uint32_t v1 = __ballot_sync(0xffffffffu, H.hd[1] < H.se[1]);
+      if (__popc(v0) + __popc(v1) == 1) {
+        const int h = v0 ? 0 : 1, src = __ffs(v0 ? v0 : v1) - 1;
+        const uint32_t k0 = __shfl_sync(0xffffffffu, h ? H.hd[1] : H.hd[0], src);
+        const uint32_t ke = __shfl_sync(0xffffffffu, h ? H.se[1] : H.se[0], src);
+        t = max(t, __shfl_sync(0xffffffffu, h ? H.A[1] : H.A[0], src));  // the head's arrival
+        for (uint32_t c = k0; c < ke; c += 32) {
+          const uint32_t k = c + lane;
+          const bool in = k < ke;
+          const uint64_t e = in ? __ldg(lp_dur + off + k) : 0;
+          const uint64_t th = (in && k + 1 < ke) ? __ldg(lp_think + off + k) : 0;
+          uint64_t X = e + th;  // inclusive scan
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        if (H.hd[h] < H.se[h] && H.A[h] <= t) {
-          const StreamPick y{H.lv[h], H.hd[h], (uint32_t)h * 32u + (uint32_t)lane, 0};
-          if (x.lv == 0xFFu || stream_better(y, x, false)) x = y;
+          for (int dd = 1; dd < 32; dd <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
+            if (lane >= dd) X += y;
+          }
+          const uint64_t start = t + X - e - th;
+          if (in) {
+            if (sched) {
+              fill_gap[so + k] = -1;
+              lp_start[so + k] = start;
+            }
+            db.sum += digest_term(k, -1, start);
+          }
+          t += __shfl_sync(0xffffffffu, X, 31);  // (no think time after the last request)
         }
+        lp_end = max(lp_end, t);
+        n_tail += ke - k0;
+        if (lane == src) {
+          if (h) H.hd[1] = H.se[1];
+          else H.hd[0] = H.se[0];
+        }
+        break;
       }
-      x = warp_best_stream(x, false, half);
-      if (x.lv == 0xFFu) {
+      StreamPick x{0xFFu, 0, 0, 0};
+      if (!pick_level_index(t, x)) {
         const uint64_t A = next_arrival(t);
         if (A == ~0ull) break;
         t = A;
