@@ -202,6 +202,16 @@ class Table:
     def zero(self):
         self.block.zero_()
 
+    def sum_span(self):
+        """int64 view over the SUM block and the histogram block when they are adjacent
+        (fikit_table_carve: capacity a multiple of 8), else None.  Summing the u32 bins pairwise
+        as u64 words is exact while every summed bin stays < 2^32 (R37)."""
+        torch = _torch()
+        if self.c.hist != self.c.sums + 32 * self.capacity:
+            return None
+        o = self.c.sums - self.block.data_ptr()
+        return self.block[o:o + 288 * self.capacity].view(torch.int64)
+
     def n_rows(self) -> int:
         return int(self.n_rows_t.item()) & 0xFFFFFFFF
 

@@ -9,7 +9,7 @@ kernels (`LibOps`); this module only sequences them around the collectives:
     all_gather(n_rows) ; all_gather(kernel_id) ; all_gather(task_id)
     fikit_dict_union -> identical sorted union on every rank + local->union map
     fikit_table_remap (dense table, zeroed) ; fikit_table_bias
-    all_reduce SUM(sums u64) ; all_reduce SUM(hist u32) ; all_reduce MAX(ext, biased)
+    all_reduce SUM(sums u64 + hist u32 pairs as u64: one span, R37) ; all_reduce MAX(ext, biased)
     fikit_table_bias ; fikit_table_means
 
 Integer sum / min / max are associative and commutative and the halo gives
@@ -62,15 +62,14 @@ def merge_tables(local, dense, ops, group=None):
     r = dist.get_rank(group)
     dev = local.kernel_id.device
     cap = local.capacity
-    n_list = [torch.empty_like(local.n_rows_t) for _ in range(P)]
-    dist.all_gather(n_list, local.n_rows_t, group=group)
-    kid_list = [torch.empty_like(local.kernel_id) for _ in range(P)]
-    dist.all_gather(kid_list, local.kernel_id, group=group)
-    task_list = [torch.empty_like(local.task_id) for _ in range(P)]
-    dist.all_gather(task_list, local.task_id, group=group)
-    n_all = torch.cat(n_list)
-    all_kid = torch.stack(kid_list)
-    all_task = torch.stack(task_list)
+    # the gathered lists land rank after rank in one tensor each (no stacking copies)
+    n_all = torch.empty(P, dtype=local.n_rows_t.dtype, device=dev)
+    dist.all_gather_into_tensor(n_all, local.n_rows_t, group=group)
+    all_kid = torch.empty(P * cap, dtype=local.kernel_id.dtype, device=dev)
+    dist.all_gather_into_tensor(all_kid, local.kernel_id, group=group)
+    all_task = torch.empty(P * cap, dtype=local.task_id.dtype, device=dev)
+    dist.all_gather_into_tensor(all_task, local.task_id, group=group)
+    all_kid, all_task = all_kid.view(P, cap), all_task.view(P, cap)
     ukid = torch.empty(dense.capacity, dtype=torch.int64, device=dev)
     utask = torch.empty(dense.capacity, dtype=torch.int32, device=dev)
     un = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -79,8 +78,12 @@ def merge_tables(local, dense, ops, group=None):
     ops.dict_union(all_kid, all_task, n_all, P, cap, r, ukid, utask, dense.capacity, un, l2u)
     ops.table_remap(local, l2u, ukid, utask, un, dense)
     ops.table_bias(dense)
-    dist.all_reduce(dense.sums, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(dense.hist, op=dist.ReduceOp.SUM, group=group)
+    span = dense.sum_span() if hasattr(dense, "sum_span") else None
+    if span is not None:  # sums and hist adjacent: one SUM over both (R37)
+        dist.all_reduce(span, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(dense.sums, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(dense.hist, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(dense.ext, op=dist.ReduceOp.MAX, group=group)
     ops.table_bias(dense)
     ops.table_means(dense)

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2 and 3, gloo, CPU) test of the multi-GPU merge
 plumbing in paper_2311_10359_b200/dist.py: record shards with a one-record
 halo, all_gather of the row keys, dictionary union, remap, the order-biased
-MAX reduction and the SUM reductions.  The per-rank tables come from the
+MAX reduction and the SUM reductions (the sums and the u32 histograms as one
+u64 span, R37, or separately).  The per-rank tables come from the
 oracle and the merge kernels are replaced by numpy doubles (there is no GPU
 here); the merged table must equal the oracle's unsharded table bit for bit."""
 import os
@@ -21,23 +22,28 @@ BIAS = np.int64(-(2**63))
 class HostTable:
     """CPU tensors in libfikit's table layout (include/fikit.h fikit_table_t)."""
 
-    def __init__(self, cap):
+    def __init__(self, cap, span=True):
         self.capacity = cap
         self.kernel_id = torch.zeros(cap, dtype=torch.int64)
         self.task_id = torch.zeros(cap, dtype=torch.int32)
-        self.sums = torch.zeros(cap * 4, dtype=torch.int64)
-        self.hist = torch.zeros(cap * 64, dtype=torch.int32)
+        # as fikit_table_carve lays them out: the SUM block, then the histograms (span=True)
+        self._span = torch.zeros(cap * 36, dtype=torch.int64) if span else None
+        self.sums = self._span[:cap * 4] if span else torch.zeros(cap * 4, dtype=torch.int64)
+        self.hist = self._span[cap * 4:].view(torch.int32) if span else torch.zeros(cap * 64, dtype=torch.int32)
         self.ext = torch.zeros(cap * 4, dtype=torch.int64)
         self.mean = torch.zeros(cap * 2, dtype=torch.int64)
         self.n_rows_t = torch.zeros(1, dtype=torch.int32)
+
+    def sum_span(self):
+        return self._span
 
     def zero(self):
         for a in (self.kernel_id, self.task_id, self.sums, self.hist, self.ext, self.mean, self.n_rows_t):
             a.zero_()
 
     @staticmethod
-    def from_oracle(tab, cap):
-        t = HostTable(cap)
+    def from_oracle(tab, cap, span=True):
+        t = HostTable(cap, span)
         n = tab.n_rows
         s = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64))
         t.kernel_id[:n] = s(tab.kernel_id[:n])
@@ -112,8 +118,9 @@ def _worker(rank, world, port, seed, q):
         lo, hi = shard_range(N, rank, world)
         halo = tr.records[hi] if hi < N else None
         tab, st, _ = oracle.measure(tr.records[lo:hi], tr.names, tr.sigs, capacity=512, halo=halo)
-        local = HostTable.from_oracle(tab, 512)
-        dense = HostTable(512)
+        span = world != 3  # 3 ranks: separate SUM reductions of the sums and the histograms
+        local = HostTable.from_oracle(tab, 512, span)
+        dense = HostTable(512, span)
         merge_tables(local, dense, NumpyOps())
         full, _, _ = oracle.measure(tr.records, tr.names, tr.sigs, capacity=512)
         ref = HostTable.from_oracle(full, 512)
