@@ -29,7 +29,7 @@ struct WsLayout {
   uint64_t ntiles;  // warp-tiles of 32 launches the workspace can schedule
 };
 
-constexpr uint32_t kHotMax = 640;  // hot rows cached in shared memory per CTA (measure kernel)
+constexpr uint32_t kHotMax = 400;  // hot rows cached in shared memory per CTA (measure kernel; u32 bins)
 // Task-partitioned scheduling of fikit_measure: warp-tiles (32 launches) are bucketed by a
 // hash of their first launch's task_id; every bucket has its own hot set.
 // regions zeroed by k_zero (one launch instead of a memset per region)

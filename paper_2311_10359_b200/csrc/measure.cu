@@ -5,14 +5,15 @@
 //   k_sample         a strided sample of launches -> (task, KID) rows in the global
 //                    index, with sample counts (picks the rows worth caching)
 //   k_hot_select     the <= kHotMax most-sampled rows -> hot dictionary (raw tuple -> row)
-//   k_measure        persistent, one CTA per SM: a producer warp streams 256-record
-//                    tiles global->shared with 1-D TMA (cp.async.bulk) into a 6-stage
-//                    mbarrier ring; 16 consumer warps validate each launch, look its raw
-//                    identity up in the shared hot dictionary, and accumulate duration
-//                    and following-gap statistics into shared memory (packed 16-bit
-//                    histograms flushed every epoch, 32-bit split sums, 64-bit min/max);
-//                    launches of cold rows take the global path (KID hash, global index,
-//                    L2 reductions).  Shared rows are reduced into the table at the end.
+//   k_measure        persistent, one CTA per SM, 24 warps: each warp streams its own
+//                    64-launch tiles global->shared with 1-D TMA (cp.async.bulk, one
+//                    mbarrier stage per warp), validates each launch, looks its raw
+//                    identity up in the shared hot dictionary (per task-bucket hot sets,
+//                    dynamic admission) and accumulates duration and following-gap
+//                    statistics into shared memory (u32 histograms, 32-bit sums with carry
+//                    counters, 32-bit min/max), flushed into the table once per phase;
+//                    launches of cold rows take the global path (tuple index, KID index,
+//                    L2 reductions).
 #include <cuda_runtime.h>
 
 #include "fikit_internal.cuh"
@@ -497,9 +498,6 @@ constexpr uint32_t TAG_Q = 4096 / TAG_W;  // buckets (4096 tags, load <= 0.16)
 constexpr uint32_t TAG_HB = 0xFFFFF800u;  // tag = hash bits 11..31 (bit 31 forced to 1) | (slot + 1)
 static_assert(kHotMax < 2048, "slot + 1 must fit the 11 tag bits");
 constexpr int STAGE_BYTES = (CH + 1) * 48;  // the tile + the next launch (the tile's last gap)
-// per epoch a slot sees <= EPOCH_ROUNDS * CH * WARPS launches: packed 16-bit bins cannot
-// overflow before the epoch flush (nor the u32 carry counters of the sums)
-constexpr int EPOCH_ROUNDS = 65535 / (CH * WARPS);  // a round consumes one tile per warp
 
 struct Smem {
   uint4 ring[WARPS][STAGE_BYTES / 16];  // one stage per warp (refilled as soon as it is read)
@@ -513,7 +511,7 @@ struct Smem {
   uint4 tq[kHotMax];
   uint32_t tq4[kHotMax];
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
-  uint32_t hist[kHotMax][kBins + 1];  // 64 bins (32 duration, 32 gap) as packed u16 pairs (+1 pad)
+  uint32_t hist[kHotMax][2 * kBins + 1];  // 64 u32 bins (32 duration, 32 gap) (+1 pad)
   uint32_t st[kHotMax][5];        // duration: 0 sum mod 2^32, 1 carries out of it; gap: 2, 3 (v < 2^32); 4: pad
   uint4 mm[kHotMax];              // min, max (u32) of duration, then of gap (values < 2^32): one 16-B load
   uint32_t grow[kHotMax];         // slot -> global row
@@ -569,13 +567,13 @@ __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint
     const uint32_t v32 = (uint32_t)v;
     const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
     const uint32_t old = atom_shared_add(st_e + 8u * j, v32);
-    red_shared_add(hist_e + 4u * (b >> 1), 1u << (16 * (b & 1)));
+    red_shared_add(hist_e + 4u * b, 1u);
     if (v32 < mn) red_shared_min(mm_e + 8u * j, v32);
     if (v32 > mx) red_shared_max(mm_e + 8u * j + 4u, v32);
     return old;
   } else {  // rare: a value >= 2^32 ns
     const int b = bin_of(v) + 32 * j;
-    red_shared_add(hist_e + 4u * (uint32_t)(b >> 1), 1u << (16 * (b & 1)));
+    red_shared_add(hist_e + 4u * (uint32_t)b, 1u);
     const uint32_t row = row_of();
     red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
     red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
@@ -592,23 +590,24 @@ __device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row,
   red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
 }
 
-// epoch flush of my slots (consumers only): packed 16-bit bins and split sums -> table, zeroed
+// phase flush of the shared rows: u32 bins and split sums -> table, zeroed
 __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& tab, int ctid) {
+  // one warp per slot: 64 u32 bins (two per lane) and the two split sums (lanes 0, 1)
   const uint32_t hn = min(S.hot_n, kHotMax);  // admission may overshoot the counter
-  for (uint32_t e = ctid; e < hn; e += mk::CONSUMERS) {
+  const uint32_t lane = (uint32_t)ctid & 31u;
+  for (uint32_t e = (uint32_t)ctid >> 5; e < hn; e += mk::WARPS) {
     const uint32_t row = S.grow[e];
     uint32_t* gh = tab.hist + (size_t)row * 64;
-#pragma unroll 4
-    for (int w = 0; w < kBins; w++) {
+#pragma unroll
+    for (uint32_t w = lane; w < 2u * kBins; w += 32u) {
       const uint32_t x = S.hist[e][w];
       if (x) {
-        if (x & 0xFFFFu) red_add_u32(gh + 2 * w, x & 0xFFFFu);
-        if (x >> 16) red_add_u32(gh + 2 * w + 1, x >> 16);
+        red_add_u32(gh + w, x);
         S.hist[e][w] = 0;
       }
     }
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
+    if (lane < 2) {
+      const uint32_t j = lane;
       const uint64_t sum = (uint64_t)S.st[e][2 * j] | ((uint64_t)S.st[e][2 * j + 1] << 32);
       if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
       S.st[e][2 * j] = 0;
@@ -674,7 +673,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
     if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
     for (int i = tid; i < (int)(mk::TAG_Q * mk::TAG_W); i += mk::THREADS) S.tagw[i] = 0u;
-    for (int i = tid; i < kHotMax * (kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
+    for (int i = tid; i < kHotMax * (2 * kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
     for (int i = tid; i < kHotMax * 5; i += mk::THREADS) (&S.st[0][0])[i] = 0u;
     for (int i = tid; i < kHotMax; i += mk::THREADS) S.mm[i] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);
     __syncthreads();
@@ -690,8 +689,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     __syncthreads();
   };
-  // min / max of the shared rows into the table (end of a phase; bins and sums were flushed
-  // by the last epoch)
+  // min / max of the shared rows into the table (end of a phase, after flush_epoch)
   auto flush_hot_set_ext = [&]() {
     for (uint32_t e = tid, hn = min(S.hot_n, kHotMax); e < hn; e += mk::CONSUMERS) {
       const uint32_t row = S.grow[e];
@@ -869,7 +867,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto update = [&](const Rec& R, int slot) {
     const uint32_t rowv = S.grow[slot];  // (loading it here schedules better than on demand)
     auto row = [&]() { return rowv; };
-    const uint32_t hist_e = s_hist + (uint32_t)slot * ((kBins + 1) * 4);
+    const uint32_t hist_e = s_hist + (uint32_t)slot * ((2 * kBins + 1) * 4);
     const uint32_t st_e = s_st + (uint32_t)slot * 20u;
     const uint32_t mm_e = s_mm + (uint32_t)slot * 16u;
     uint4 mm;
@@ -967,9 +965,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         claim();
       }
     }
-    // epochs: up to EPOCH_ROUNDS tiles per warp between CTA barriers (16-bit accumulators)
-    for (;;) {
-      for (uint32_t r = 0; r < (uint32_t)mk::EPOCH_ROUNDS && staged; r++) {
+    // one phase: every warp consumes tiles until the bucket's claims run out, then the CTA
+    // flushes once (u32 bins and carry counters cannot overflow within a call: n < 2^32)
+    {
+      while (staged) {
         // Each round reads the warp's tile (both halves, A and B) into registers, refills the
         // stage with the next tile, then processes A and B with their identity probes
         // interleaved (two independent dependency chains per lane).
@@ -1009,10 +1008,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         compact(A, A.valid && sA < 0);
         compact(B, B.valid && sB < 0);
       }
-      const bool all_done = __syncthreads_and(!staged);
+      __syncthreads();
       flush_epoch(S, tab, tid);
       __syncthreads();
-      if (all_done) break;
     }
     flush_hot_set_ext();
     if (tid == 0) atomicSub(act + cb, 1u);  // every claim of cb is done
