@@ -921,17 +921,20 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // the bucket to move to: the most unclaimed tiles among buckets nobody works on (they must
   // be taken) or with more than 128 left (worth a hot-set reload); CTA-uniform
   auto pick_bucket = [&]() -> uint32_t {
-    if (tid == 0) {
+    if (warp == 0) {  // the lanes read the buckets' counters in parallel (one L2 round trip)
       uint32_t best = kNoBucket, most = 0;
-      for (uint32_t b = 0; b < kSchedWords; b++) {
-        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b);
+      for (uint32_t b = lane; b < kSchedWords; b += 32) {
+        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b), a = *(volatile uint32_t*)(act + b);
         const uint32_t left = e > c ? e - c : 0u;
-        if (left > most && (left > 128u || *(volatile uint32_t*)(act + b) == 0u)) {
+        if (left > most && (left > 128u || a == 0u)) {
           most = left;
           best = b;
         }
       }
-      *s_next = best;
+      // the most unclaimed tiles; ties -> the smallest bucket index
+      const uint32_t mx = __reduce_max_sync(0xffffffffu, most);
+      const uint32_t bb = __reduce_min_sync(0xffffffffu, (mx != 0u && most == mx) ? best : kNoBucket);
+      if (lane == 0) *s_next = mx ? bb : kNoBucket;
     }
     __syncthreads();
     const uint32_t b = *s_next;
