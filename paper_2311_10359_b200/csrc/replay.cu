@@ -325,12 +325,34 @@ __device__ __forceinline__ void reg_bitonic64(uint64_t& e0, uint64_t& e1, int la
   }
 }
 
+// the same network on 32-bit keys (one SHFL and one min/max instruction per element and stage)
+__device__ __forceinline__ void reg_bitonic64_u32(uint32_t& e0, uint32_t& e1, int lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        const uint32_t lo = min(e0, e1), hi = max(e0, e1);
+        e0 = lo;
+        e1 = hi;
+      } else {
+        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, j), o1 = __shfl_xor_sync(0xffffffffu, e1, j);
+        const bool lower = ((uint32_t)lane & j) == 0;
+        const bool asc0 = ((uint32_t)lane & k) == 0, asc1 = ((32u + (uint32_t)lane) & k) == 0;
+        e0 = (asc0 == lower) ? min(e0, o0) : max(e0, o0);
+        e1 = (asc1 == lower) ? min(e1, o1) : max(e1, o1);
+      }
+    }
+  }
+}
+constexpr uint32_t kQ22 = (1u << 22) - 1;  // 32-bit keys: level << 28 | (kQ22 - q) << 6 | index
+
 // load and sort a pool of m <= 64 requests into registers.  Returns 0 ok, 1 invalid level
 // (flagged), 2 fast path not applicable (some eligible q >= 2^50).
 __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t K, const uint32_t* __restrict__ row,
                                              const uint8_t* __restrict__ level, const uint64_t* __restrict__ dur,
                                              uint64_t off, uint32_t m, int lane, fikit_status_t* st, RegPool& P) {
-  bool ok = true, fits = true;
+  bool ok = true, fits = true, small = true;
   auto one = [&](uint32_t kk, uint64_t& key, uint64_t& d, uint32_t& lv) {
     key = ~0ull;
     d = 0;
@@ -348,6 +370,7 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
       if (el) {
         const uint64_t q = __ldg(tab.mean + (size_t)r * 2);  // SK of the request's ID
         if (q > kQ50) fits = false;
+        if (q > kQ22) small = false;
         key = ((uint64_t)(L & 0xF) << 60) | ((kQ50 - (q & kQ50)) << 10) | kk;
       }
     }
@@ -357,6 +380,23 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
   one(32u + (uint32_t)lane, e1, P.dur1, P.lvl1);
   if (!__all_sync(0xffffffffu, ok)) return 1;
   if (!__all_sync(0xffffffffu, fits)) return 2;
+  if (__all_sync(0xffffffffu, small)) {  // every eligible q < 2^22 ns: sort 32-bit keys
+    auto k32 = [](uint64_t key) -> uint32_t {
+      if (key == ~0ull) return 0xFFFFFFFFu;
+      const uint32_t q = (uint32_t)(kQ50 - ((key >> 10) & kQ50));
+      return ((uint32_t)(key >> 60) << 28) | ((kQ22 - q) << 6) | (uint32_t)(key & 63u);
+    };
+    uint32_t f0 = k32(e0), f1 = k32(e1);
+    reg_bitonic64_u32(f0, f1, lane);
+    P.a0 = f0 != 0xFFFFFFFFu;
+    P.a1 = f1 != 0xFFFFFFFFu;
+    P.q0 = kQ22 - ((f0 >> 6) & kQ22);
+    P.q1 = kQ22 - ((f1 >> 6) & kQ22);
+    P.k0 = f0 & 63u;
+    P.k1 = f1 & 63u;
+    P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
+    return 0;
+  }
   reg_bitonic64(e0, e1, lane);
   P.a0 = e0 != ~0ull;
   P.a1 = e1 != ~0ull;
@@ -381,6 +421,27 @@ struct SmemPool {
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const { return __ldg(dur + kk); }
 };
+
+// inclusive warp prefix sum of u64 values; 32-bit shuffles and adds when every value is
+// < 2^26 (the sum of 32 then fits 32 bits), the common case for nanosecond chunk times
+__device__ __forceinline__ uint64_t warp_inclusive_scan(uint64_t v, int lane) {
+  if (__all_sync(0xffffffffu, v < (1ull << 26))) {
+    uint32_t x = (uint32_t)v;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
+      if (lane >= dd) x += y;
+    }
+    return x;
+  }
+  uint64_t x = v;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, dd);
+    if (lane >= dd) x += y;
+  }
+  return x;
+}
 
 struct HpOut {
   uint64_t t, hp_delay, fill_work, lp_end;
@@ -426,12 +487,7 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
     const uint64_t p_l = (valid && r_l < K) ? ((__ldg(tab.mean + (size_t)r_l * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
     if (base + 32 < nh) ld(base + 32, dn, gn, rn);
     const uint64_t x_l = d_l + a_l;
-    uint64_t X = x_l;  // inclusive prefix over the chunk
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
-      if (lane >= dd) X += y;
-    }
+    const uint64_t X = warp_inclusive_scan(x_l, lane);  // prefix over the chunk
     const bool gate = valid && !last && p_l >= prm.threshold_ns && (!prm.feedback || a_l > 0);
     uint32_t gmask = __ballot_sync(0xffffffffu, gate && p_l >= gate_min());
     const uint64_t T0 = t;
@@ -507,12 +563,7 @@ __device__ __forceinline__ uint64_t replay_tail(uint64_t t, uint32_t m, uint32_t
       const uint32_t bal = __ballot_sync(0xffffffffu, sel);
       if (!bal) continue;
       const uint64_t e = sel ? dur_of(k) : 0;
-      uint64_t x = e;  // inclusive scan
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, x, dd);
-        if (lane >= dd) x += y;
-      }
+      const uint64_t x = warp_inclusive_scan(e, lane);
       if (sel) {
         const uint64_t start = t + x - e;
         if (sched) {
@@ -933,12 +984,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
           const bool in = k < ke;
           const uint64_t e = in ? __ldg(lp_dur + off + k) : 0;
           const uint64_t th = (in && k + 1 < ke) ? __ldg(lp_think + off + k) : 0;
-          uint64_t X = e + th;  // inclusive scan
-#pragma unroll
-          for (int dd = 1; dd < 32; dd <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, X, dd);
-            if (lane >= dd) X += y;
-          }
+          const uint64_t X = warp_inclusive_scan(e + th, lane);
           const uint64_t start = t + X - e - th;
           if (in) {
             if (sched) {
