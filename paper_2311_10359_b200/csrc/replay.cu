@@ -97,6 +97,21 @@ __device__ __forceinline__ uint64_t warp_min_q(const uint64_t* q, const uint8_t*
 // of sorted positions [32c, 32c + 32).
 constexpr uint64_t kQ50 = (1ull << 50) - 1;
 
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t a) {
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0u);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// warp minimum of a u64 (all lanes): REDUX on the high words, then on the low words of the
+// lanes holding the minimal high word
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t a) {
+  const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32));
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0xFFFFFFFFu);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+
 __device__ __forceinline__ uint64_t key_q(uint64_t key) { return kQ50 - ((key >> 10) & kQ50); }
 
 __device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
@@ -278,10 +293,7 @@ struct RegPool {
   uint64_t alive;     // alive requests by index (warp-uniform)
 
   __device__ __forceinline__ uint64_t min_q() const {
-    uint64_t mn = min(a0 ? q0 : ~0ull, a1 ? q1 : ~0ull);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-    return mn;
+    return warp_min_u64(min(a0 ? q0 : ~0ull, a1 ? q1 : ~0ull));
   }
   // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
@@ -727,20 +739,6 @@ struct StreamPick {  // the best head of a warp reduction (valid: lv != 0xFF)
   uint32_t lv, k, sid;
   uint64_t q;
 };
-
-__device__ __forceinline__ uint64_t warp_max_u64(uint64_t a) {
-  const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32));
-  const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0u);
-  return ((uint64_t)hi << 32) | lo;
-}
-
-// warp minimum of a u64 (all lanes): REDUX on the high words, then on the low words of the
-// lanes holding the minimal high word
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t a) {
-  const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32));
-  const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(a >> 32) == hi ? (uint32_t)a : 0xFFFFFFFFu);
-  return ((uint64_t)hi << 32) | lo;
-}
 
 __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20 warps per SM
     k_simulate_stream(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
