@@ -583,3 +583,36 @@ def test_zipf_full_size_sampled_rows(fk, orc):
             if v.shape[0]:
                 assert int(tab[name + "_min"][r]) == int(v.min()) and int(tab[name + "_max"][r]) == int(v.max())
             assert np.array_equal(tab[name + "_hist"][r], np.bincount(bins(v), minlength=32)), (r, name)
+
+
+def test_sweep_full_size_sampled(fk, orc):
+    """configs[4] at its full size (1M scenarios, m = 8..1024, gap scales 1/4..32) as bench.py
+    runs it; 1,500 sampled scenarios replayed one by one by the oracle (results and schedule)"""
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.sweep()
+    tr, rp = cfg.trace, cfg.replay
+    S = rp.scenarios.shape[0]
+    assert S == 1_000_000
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=4096, replay=rp, want_schedule=True)
+    p.step()
+    p.check("sweep full size")
+    got = p.results()
+    gfg, gls = p.schedule()
+    m = rp.scenarios["lp_len"].astype(np.int64)
+    so = np.concatenate([[0], np.cumsum(m[:-1])])
+    pick = np.sort(np.random.default_rng(9).choice(S, 1500, replace=False))
+    tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=4096)
+    sc = rp.scenarios[pick].copy()
+    hp_idx = np.concatenate([np.arange(c["hp_off"], c["hp_off"] + c["hp_len"]) for c in sc])
+    lp_idx = np.concatenate([np.arange(c["lp_off"], c["lp_off"] + c["lp_len"]) for c in sc])
+    hr, hd, hg, _ = orc.resolve(rp.hp_records[hp_idx], tr.names, tr.sigs, tab)
+    lr, ld, _, _ = orc.resolve(rp.lp_records[lp_idx], tr.names, tr.sigs, tab)
+    sc["hp_off"] = np.concatenate([[0], np.cumsum(sc["hp_len"][:-1])])
+    sc["lp_off"] = np.concatenate([[0], np.cumsum(sc["lp_len"][:-1])])
+    out, fg, ls, rso, _ = orc.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns,
+                                             rp.feedback, want_schedule=True)
+    assert got[pick].tobytes() == out.tobytes()
+    for j, s in enumerate(pick):
+        a, b, n = int(so[s]), int(rso[j]), int(m[s])
+        assert np.array_equal(gfg[a:a + n], fg[b:b + n]) and np.array_equal(gls[a:a + n], ls[b:b + n]), s
