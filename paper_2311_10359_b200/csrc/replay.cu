@@ -621,6 +621,7 @@ __device__ __forceinline__ void write_result(fikit_result_t* out, uint32_t s, co
 constexpr uint32_t kDeferred = 0xFFFFFFFFu;
 constexpr int kRegWarps = kRegThreads / 32;
 
+template <bool kSched>  // schedule outputs requested (a compile-time branch: no per-fill checks)
 __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps per SM
     k_simulate_reg(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                    const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
                    const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
-  const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
+  constexpr bool sched = kSched;
   uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord1;
   const uint32_t nw = gridDim.x * kRegWarps;
   uint32_t s = blockIdx.x * kRegWarps + w;  // first scenario: static; later ones claimed
@@ -740,6 +741,7 @@ struct StreamPick {  // the best head of a warp reduction (valid: lv != 0xFF)
   uint64_t q;
 };
 
+template <bool kSched>
 __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20 warps per SM
     k_simulate_stream(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                       const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
   __shared__ uint8_t s_lv[kStreamWarps][kPoolMax];  // level | eligible << 7
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
-  const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
+  constexpr bool sched = kSched;
   uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord3;
   uint32_t nxt = 0;  // lane 0: the next claimed scenario (in flight while one runs)
   if (lane == 0) nxt = atomicAdd(ctr, 1u);
@@ -1029,5 +1031,18 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
     }
   }
 }
+
+#define FIKIT_REG_ARGS                                                                                         \
+  fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, \
+      const fikit_scenario_t*, uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*, uint64_t*, const uint64_t*,   \
+      fikit_status_t*
+template __global__ void k_simulate_reg<false>(FIKIT_REG_ARGS);
+template __global__ void k_simulate_reg<true>(FIKIT_REG_ARGS);
+#define FIKIT_STREAM_ARGS                                                                                      \
+  fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, \
+      const uint32_t*, const uint64_t*, const uint64_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,      \
+      fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*
+template __global__ void k_simulate_stream<false>(FIKIT_STREAM_ARGS);
+template __global__ void k_simulate_stream<true>(FIKIT_STREAM_ARGS);
 
 }  // namespace fikit
