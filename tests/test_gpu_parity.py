@@ -616,3 +616,21 @@ def test_sweep_full_size_sampled(fk, orc):
     for j, s in enumerate(pick):
         a, b, n = int(so[s]), int(rso[j]), int(m[s])
         assert np.array_equal(gfg[a:a + n], fg[b:b + n]) and np.array_equal(gls[a:a + n], ls[b:b + n]), s
+
+
+def test_replay_without_schedule_outputs(fk, orc):
+    """the launch configuration bench.py times: no fill_gap / lp_start buffers (the kernels'
+    no-schedule instantiations), POOL and STREAM replays, results bit-exact vs the oracle"""
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.bert_vgg(S=20000)
+    ref = orc.pipeline(cfg, capacity=1024)
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay, checked=True)
+    p.step()
+    assert "fill_gap" not in p.replay and p.results().tobytes() == ref["results"].tobytes()
+    cfg, sr = F.bert_vgg_stream(S=3000, n_lp_runs=600)
+    out, _, _, _ = _stream_ref(orc, cfg, sr, 1)
+    p = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=1024, replay=cfg.replay, checked=True,
+                 lp_stream=sr.lp_stream)
+    p.step()
+    assert p.results().tobytes() == out.tobytes()
