@@ -317,22 +317,35 @@ __global__ void __launch_bounds__(1024) k_tile_bucket(const fikit_record_t* __re
   __syncthreads();
   const uint32_t C = (ntiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * C, t1 = min(ntiles, t0 + C);
+  // Tiles are bucketed in aligned pairs by the pair's first launch (one DRAM sector per 128
+  // launches: the kernel is bound by scattered DRAM accesses).  A pair whose second tile starts
+  // another task's run is only scheduled with the first one's hot set (its launches go cold
+  // once and are admitted): a scheduling choice, never a result.
   constexpr int U = 4;  // independent one-sector loads in flight per thread
-  for (uint32_t t = t0 + threadIdx.x; t < t1; t += U * blockDim.x) {
+  const uint32_t p0 = (t0 + 1) / 2, p1 = (t1 + 1) / 2;  // pairs whose first tile is in [t0, t1)
+  for (uint32_t q = p0 + threadIdx.x; q < p1; q += U * blockDim.x) {
     uint32_t task[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t tu = t + u * blockDim.x;
-      task[u] = tu < t1 ? __ldcs(&recs[(uint64_t)tu * kTileLaunches].task_id) : 0u;
+      const uint32_t qu = q + u * blockDim.x;
+      task[u] = qu < p1 ? __ldcs(&recs[(uint64_t)qu * 2 * kTileLaunches].task_id) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t tu = t + u * blockDim.x;
-      if (tu < t1) {
+      const uint32_t qu = q + u * blockDim.x;
+      if (qu < p1) {
         const uint32_t b = bucket_of(task[u]);
-        tile_bucket[tu] = (uint8_t)b;
-        atomicAdd(&h[b], 1u);
+        const uint32_t ta = 2 * qu, tb = min(ta + 2, min(t1, ntiles));
+        for (uint32_t tt = max(ta, t0); tt < tb; tt++) tile_bucket[tt] = (uint8_t)b;
+        atomicAdd(&h[b], tb - max(ta, t0));
       }
+    }
+  }
+  if (t0 < t1 && (t0 & 1u)) {  // a chunk starting mid-pair: its first tile follows its pair
+    if (threadIdx.x == 0) {
+      const uint32_t b = bucket_of(__ldcs(&recs[(uint64_t)(t0 - 1) * kTileLaunches].task_id));
+      tile_bucket[t0] = (uint8_t)b;
+      atomicAdd(&h[b], 1u);
     }
   }
   __syncthreads();
