@@ -52,15 +52,16 @@ __global__ void k_fill(fikit_table_t, const uint64_t*, const uint64_t*, const ui
 __global__ void k_simulate(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
                            const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
                            fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
-template <bool kSched>
-__global__ void k_simulate_reg(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
-                           const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
-                           fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
-template <bool kSched>
-__global__ void k_simulate_stream(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
-                                  const uint64_t*, const uint8_t*, const uint32_t*, const uint64_t*, const uint64_t*,
-                                  const fikit_scenario_t*, uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*,
-                                  uint64_t*, const uint64_t*, fikit_status_t*);
+const void* simulate_reg_kernel(bool sched);
+void launch_simulate_reg(int, int, cudaStream_t, const fikit_table_t&, const uint32_t*, const uint64_t*,
+                         const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, const fikit_scenario_t*,
+                         uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*, uint64_t*, const uint64_t*,
+                         fikit_status_t*);
+const void* simulate_stream_kernel(bool sched);
+void launch_simulate_stream(int, int, cudaStream_t, const fikit_table_t&, const uint32_t*, const uint64_t*,
+                            const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, const uint32_t*,
+                            const uint64_t*, const uint64_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
+                            fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
 }  // namespace fikit
 
 using namespace fikit;
@@ -418,16 +419,15 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
   // Both persistent: one wave of the kernel's occupancy.
   static int g1 = 0, g2 = 0;
   if (!g1) {
-    g1 = one_wave((const void*)k_simulate_reg<false>, kRegThreads);
+    g1 = one_wave(simulate_reg_kernel(false), kRegThreads);
     g2 = one_wave((const void*)k_simulate, kSimThreads);
   }
   const uint64_t n1 = ((uint64_t)S + kRegThreads / 32 - 1) / (kRegThreads / 32);
   const uint64_t n2 = ((uint64_t)S + kSimThreads / 32 - 1) / (kSimThreads / 32);
   const int b1 = (int)(n1 < (uint64_t)g1 ? n1 : (uint64_t)g1);
   const int b2 = (int)(n2 < (uint64_t)g2 ? n2 : (uint64_t)g2);
-  const bool sched = fill_gap && lp_start && sched_off;
-  (sched ? k_simulate_reg<true> : k_simulate_reg<false>)<<<b1, kRegThreads, 0, s>>>(
-      *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
+  launch_simulate_reg(b1, kRegThreads, s, *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
+                      fill_gap, lp_start, sched_off, w.st());
   if (int r = launched()) return r;
   k_simulate<<<b2, kSimThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out, fill_gap,
                                 lp_start, sched_off, w.st());
@@ -449,13 +449,11 @@ int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row
   if (S == 0) return FIKIT_OK;
   // persistent, one wave; warps claim scenarios from a counter
   static int g = 0;
-  if (!g) g = one_wave((const void*)k_simulate_stream<false>, kStreamThreads);
+  if (!g) g = one_wave(simulate_stream_kernel(false), kStreamThreads);
   const uint64_t need = ((uint64_t)S + kStreamThreads / 32 - 1) / (kStreamThreads / 32);
   const int b = (int)(need < (uint64_t)g ? need : (uint64_t)g);
-  const bool sched = fill_gap && lp_start && sched_off;
-  (sched ? k_simulate_stream<true> : k_simulate_stream<false>)<<<b, kStreamThreads, 0, s>>>(
-      *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream, lp_think, hp_arrival, sc, S, prm, out,
-      fill_gap, lp_start, sched_off, w.st());
+  launch_simulate_stream(b, kStreamThreads, s, *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream,
+                         lp_think, hp_arrival, sc, S, prm, out, fill_gap, lp_start, sched_off, w.st());
   return launched();
 }
 

@@ -1032,17 +1032,39 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
   }
 }
 
-#define FIKIT_REG_ARGS                                                                                         \
-  fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, \
-      const fikit_scenario_t*, uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*, uint64_t*, const uint64_t*,   \
-      fikit_status_t*
-template __global__ void k_simulate_reg<false>(FIKIT_REG_ARGS);
-template __global__ void k_simulate_reg<true>(FIKIT_REG_ARGS);
-#define FIKIT_STREAM_ARGS                                                                                      \
-  fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, \
-      const uint32_t*, const uint64_t*, const uint64_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,      \
-      fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*
-template __global__ void k_simulate_stream<false>(FIKIT_STREAM_ARGS);
-template __global__ void k_simulate_stream<true>(FIKIT_STREAM_ARGS);
+// host launchers (the kernel templates are instantiated and launched in this translation unit)
+const void* simulate_reg_kernel(bool sched) {
+  return sched ? (const void*)k_simulate_reg<true> : (const void*)k_simulate_reg<false>;
+}
+const void* simulate_stream_kernel(bool sched) {
+  return sched ? (const void*)k_simulate_stream<true> : (const void*)k_simulate_stream<false>;
+}
+void launch_simulate_reg(int blocks, int threads, cudaStream_t s, const fikit_table_t& tab, const uint32_t* hp_row,
+                         const uint64_t* hp_dur, const uint64_t* hp_gap, const uint32_t* lp_row,
+                         const uint64_t* lp_dur, const uint8_t* lp_level, const fikit_scenario_t* sc, uint32_t S,
+                         fikit_fill_params_t prm, fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
+                         const uint64_t* sched_off, fikit_status_t* st) {
+  if (fill_gap && lp_start && sched_off)
+    k_simulate_reg<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+                                                     out, fill_gap, lp_start, sched_off, st);
+  else
+    k_simulate_reg<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+                                                      out, fill_gap, lp_start, sched_off, st);
+}
+void launch_simulate_stream(int blocks, int threads, cudaStream_t s, const fikit_table_t& tab,
+                            const uint32_t* hp_row, const uint64_t* hp_dur, const uint64_t* hp_gap,
+                            const uint32_t* lp_row, const uint64_t* lp_dur, const uint8_t* lp_level,
+                            const uint32_t* lp_stream, const uint64_t* lp_think, const uint64_t* hp_arrival,
+                            const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t prm, fikit_result_t* out,
+                            int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off, fikit_status_t* st) {
+  if (fill_gap && lp_start && sched_off)
+    k_simulate_stream<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
+                                                        lp_stream, lp_think, hp_arrival, sc, S, prm, out, fill_gap,
+                                                        lp_start, sched_off, st);
+  else
+    k_simulate_stream<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
+                                                         lp_stream, lp_think, hp_arrival, sc, S, prm, out, fill_gap,
+                                                         lp_start, sched_off, st);
+}
 
 }  // namespace fikit
