@@ -115,17 +115,45 @@ def make_workload(args, rank, world):
         desc = {"resnet": "resnet-3M (configs[1])", "bert_vgg": "bert_vgg-100k (configs[2])",
                 "sweep": "sweep-1M (configs[4])"}[args.workload]
     ratio = ratio if args.workload == "ratio" else None
+    lp_stream = lp_stream if args.workload in ("stream", "preempt", "ratio") else None
     if replay is not None and world > 1:
         sel = scenario_shard(replay.scenarios.shape[0], rank, world)
         if ratio is not None:
             ratio = ratio[sel]
         replay = F.Replay(replay.hp_records, replay.lp_records, replay.lp_level, replay.scenarios[sel],
                           replay.threshold_ns, replay.feedback)
+        replay, lp_stream = compact_replay(replay, lp_stream)  # this rank's launches only
         if args.workload == "preempt":
             hp_arrival = hp_arrival[sel]
     return dict(records=recs, halo=halo, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=replay, N=N, cap=cap,
-                desc=desc, cfg=cfg, lp_stream=lp_stream if args.workload in ("stream", "preempt", "ratio") else None,
+                desc=desc, cfg=cfg, lp_stream=lp_stream,
                 hp_arrival=hp_arrival if args.workload == "preempt" else None, ratio=ratio)
+
+
+def compact_replay(rp, lp_stream=None):
+    """Keep only the HP / LP launches this rank's scenarios reference (every window whole, in
+    order) and remap the scenarios' offsets: a rank resolves and stages its share of the
+    launches, not all of them (host-side data placement, outside the timed region)."""
+    import fikit_synth as F
+
+    sc = rp.scenarios.copy()
+
+    def keep(n, off, ln):
+        mark = np.zeros(n + 1, np.int64)
+        np.add.at(mark, off, 1)
+        np.add.at(mark, off + ln, -1)
+        need = np.cumsum(mark[:n]) > 0
+        return need, np.cumsum(need) - 1
+
+    off_h, len_h = sc["hp_off"].astype(np.int64), sc["hp_len"].astype(np.int64)
+    off_l, len_l = sc["lp_off"].astype(np.int64), sc["lp_len"].astype(np.int64)
+    need_h, map_h = keep(rp.hp_records.shape[0], off_h, len_h)
+    need_l, map_l = keep(rp.lp_records.shape[0], off_l, len_l)
+    sc["hp_off"] = np.where(len_h > 0, map_h[np.minimum(off_h, max(0, need_h.shape[0] - 1))], 0)
+    sc["lp_off"] = np.where(len_l > 0, map_l[np.minimum(off_l, max(0, need_l.shape[0] - 1))], 0)
+    out = F.Replay(rp.hp_records[need_h], rp.lp_records[need_l], rp.lp_level[need_l], sc, rp.threshold_ns,
+                   rp.feedback)
+    return out, (lp_stream[need_l] if lp_stream is not None else None)
 
 
 class ClockSampler:
