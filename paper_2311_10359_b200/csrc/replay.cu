@@ -591,6 +591,49 @@ __device__ __forceinline__ uint64_t replay_tail(uint64_t t, uint32_t m, uint32_t
   return t;
 }
 
+// the same for a register pool (m <= 64): each lane keeps the tail start of its two requests and
+// the digest terms are evaluated once at the end (two SIMT passes instead of one per level)
+template <class Sel, class Dur>
+__device__ __forceinline__ uint64_t replay_tail_reg(uint64_t t, uint32_t m, uint32_t levels, Sel sel_of, Dur dur_of,
+                                                    bool sched, int32_t* fill_gap, uint64_t* lp_start, uint64_t so,
+                                                    uint64_t& dig, uint32_t& n_tail, int lane) {
+  uint64_t st0 = 0, st1 = 0;
+  bool f0 = false, f1 = false;
+  while (levels) {
+    const uint32_t L = __ffs(levels) - 1;
+    levels &= levels - 1;
+#pragma unroll
+    for (uint32_t h = 0; h < 2; h++) {
+      const uint32_t k = 32u * h + (uint32_t)lane;
+      if (32u * h >= m) break;
+      const bool sel = k < m && sel_of(k, L);
+      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      if (!bal) continue;
+      const uint64_t e = sel ? dur_of(k) : 0;
+      const uint64_t x = warp_inclusive_scan(e, lane);
+      if (sel) {
+        const uint64_t start = t + x - e;
+        if (sched) {
+          fill_gap[so + k] = -1;
+          lp_start[so + k] = start;
+        }
+        if (h) {
+          st1 = start;
+          f1 = true;
+        } else {
+          st0 = start;
+          f0 = true;
+        }
+      }
+      t += __shfl_sync(0xffffffffu, x, 31);
+      n_tail += __popc(bal);
+    }
+  }
+  if (f0) dig += digest_term((uint32_t)lane, -1, st0);
+  if (f1) dig += digest_term(32u + (uint32_t)lane, -1, st1);
+  return t;
+}
+
 __device__ __forceinline__ void write_result(fikit_result_t* out, uint32_t s, const HpOut& o, uint64_t t_end,
                                              uint32_t m, uint32_t n_tail, DigestBatch& db, uint64_t tail_dig,
                                              int lane) {
@@ -656,7 +699,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
     lv = __reduce_or_sync(0xffffffffu, lv);
     uint64_t tail_dig = 0;
     uint32_t n_tail = 0;
-    const uint64_t t = replay_tail(
+    const uint64_t t = replay_tail_reg(
         o.t, m, lv,
         [&](uint32_t k, uint32_t L) { return ((P.alive >> k) & 1ull) && (k < 32 ? P.lvl0 : P.lvl1) == L; },
         [&](uint32_t k) { return k < 32 ? P.dur0 : P.dur1; }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
