@@ -134,7 +134,7 @@ __device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
 // Build the sorted pool in place of q (q[k] by index -> K[p] by sorted position).
 // Returns false (pool left by index) if the fast path does not apply.
 __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* meta, uint32_t m, int lane,
-                                                 uint32_t& A, uint32_t& nch) {
+                                                 uint32_t& A, uint32_t& nch, uint64_t& CM) {
   bool ok = true;
   for (uint32_t k = lane; k < m; k += 32)
     if ((meta[k] & kElig) && q[k] > kQ50) ok = false;
@@ -150,49 +150,58 @@ __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* met
   warp_bitonic_sort(q, P, lane);
   nch = (m + 31) / 32;
   A = 0;
+  CM = ~0ull;
   for (uint32_t c = 0; c < nch; c++) {
     const uint32_t p = c * 32 + lane;
-    const uint32_t b = __ballot_sync(0xffffffffu, p < m && q[p] != ~0ull);
-    if (lane == (int)c) A = b;
+    const bool alive = p < m && q[p] != ~0ull;
+    const uint32_t b = __ballot_sync(0xffffffffu, alive);
+    const uint64_t mn = warp_min_u64(alive ? key_q(q[p]) : ~0ull);
+    if (lane == (int)c) {
+      A = b;
+      CM = mn;
+    }
   }
   return true;
 }
 
-// first alive sorted position with q <= R, or -1 (uniform)
-__device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint32_t nch, uint64_t R, int lane) {
-  for (uint32_t c = 0; c < nch; c++) {
-    const uint32_t word = __shfl_sync(0xffffffffu, A, c);
-    if (!word) continue;
-    const bool fit = ((word >> lane) & 1u) && key_q(K[c * 32 + lane]) <= R;
-    const uint32_t b = __ballot_sync(0xffffffffu, fit);
-    if (b) return (int)(c * 32 + __ffs(b) - 1);
-  }
-  return -1;
+// chunk c's minimum q over its alive positions, after its alive word changed (to lane c)
+__device__ __forceinline__ void chunk_min_refresh(const uint64_t* K, uint32_t A, uint32_t c, uint64_t& CM,
+                                                  int lane) {
+  const uint32_t word = __shfl_sync(0xffffffffu, A, c);
+  const uint64_t mn = warp_min_u64(((word >> lane) & 1u) ? key_q(K[c * 32 + lane]) : ~0ull);
+  if (lane == (int)c) CM = mn;
 }
 
-__device__ __forceinline__ uint64_t sorted_min_q(const uint64_t* K, uint32_t A, uint32_t nch, int lane) {
-  uint64_t mn = ~0ull;
-  for (uint32_t c = 0; c < nch; c++) {
-    const uint32_t word = __shfl_sync(0xffffffffu, A, c);
-    if ((word >> lane) & 1u) mn = min(mn, key_q(K[c * 32 + lane]));
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-  return mn;
+// first alive sorted position with q <= R, or -1 (uniform): the first chunk whose alive minimum
+// fits (one ballot over the chunk lanes), then the first fitting position inside it
+__device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint64_t CM, uint32_t nch, uint64_t R,
+                                           int lane) {
+  const uint32_t cb = __ballot_sync(0xffffffffu, (uint32_t)lane < nch && CM <= R);
+  if (!cb) return -1;
+  const uint32_t c = __ffs(cb) - 1;
+  const uint32_t word = __shfl_sync(0xffffffffu, A, c);
+  const bool fit = ((word >> lane) & 1u) && key_q(K[c * 32 + lane]) <= R;
+  const uint32_t b = __ballot_sync(0xffffffffu, fit);  // != 0: the chunk's minimum fits
+  return (int)(c * 32 + __ffs(b) - 1);
+}
+
+__device__ __forceinline__ uint64_t sorted_min_q(uint64_t CM, uint32_t nch, int lane) {
+  return warp_min_u64((uint32_t)lane < nch ? CM : ~0ull);
 }
 
 // One BestPrioFit pick (Alg. 2) on either representation: returns the request index (or -1)
 // and its q; dequeues it (alive bit cleared in both views).
 __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
-                                         uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
+                                         uint64_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
   int k;
   if (fast) {
-    const int p = sorted_best(q, A, nch, R, lane);
+    const int p = sorted_best(q, A, CM, nch, R, lane);
     if (p < 0) return -1;
     const uint64_t key = q[p];
     k = (int)(key & 1023u);
     qk = key_q(key);
     if (lane == (p >> 5)) A &= ~(1u << (p & 31));
+    chunk_min_refresh(q, A, (uint32_t)p >> 5, CM, lane);
   } else {
     k = warp_best_prio_fit(q, meta, m, R, lane);
     if (k < 0) return -1;
@@ -204,8 +213,8 @@ __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, 
 }
 
 __device__ __forceinline__ uint64_t pool_min_q(bool fast, const uint64_t* q, const uint8_t* meta, uint32_t m,
-                                               uint32_t A, uint32_t nch, int lane) {
-  return fast ? sorted_min_q(q, A, nch, lane) : warp_min_q(q, meta, m, lane);
+                                               uint64_t CM, uint32_t nch, int lane) {
+  return fast ? sorted_min_q(CM, nch, lane) : warp_min_q(q, meta, m, lane);
 }
 
 __device__ __forceinline__ uint64_t digest_term(uint32_t k, int32_t fg, uint64_t start) {
@@ -238,19 +247,20 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint32_t np = 0, po = picks_off[g];
     if (R >= prm.threshold_ns) {  // Alg. 1 lines 6-8
       uint32_t A = 0, nch = 0;
-      const bool fast = make_sorted_pool(q, meta, m, lane, A, nch);
-      uint64_t qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
+      uint64_t CM;
+      const bool fast = make_sorted_pool(q, meta, m, lane, A, nch, CM);
+      uint64_t qmin = pool_min_q(fast, q, meta, m, CM, nch, lane);
       for (;;) {                             // lines 9-16
         if (prm.feedback && t >= dl) break;  // early stop on the HP launch
         if (R < qmin) break;                 // nothing can fit
         uint64_t qk;
-        const int k = pool_pick(fast, q, meta, m, A, nch, R, lane, qk);  // Alg. 2
+        const int k = pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);  // Alg. 2
         if (k < 0) break;
         if (lane == 0) picks[po + np] = (uint32_t)k;
         np++;
         t += __ldg(pool_dur + off + k);  // launched (line 14)
         R -= qk;                           // revised by the predicted duration (line 15, R17)
-        if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, A, nch, lane);
+        if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, CM, nch, lane);
       }
     }
     if (lane == 0) {
@@ -427,9 +437,10 @@ struct SmemPool {
   const uint64_t* dur;  // lp_dur + lp_off
   uint32_t m, A, nch;
   bool fast;
-  __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, A, nch, lane); }
+  uint64_t CM;  // lane c: chunk c's alive minimum q (sorted fast path)
+  __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, CM, nch, lane); }
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    return pool_pick(fast, q, meta, m, A, nch, R, lane, qk);
+    return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const { return __ldg(dur + kk); }
 };
@@ -744,8 +755,8 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint8_t* meta = s_meta[w];
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
-    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false};
-    P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch);
+    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, ~0ull};
+    P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch, P.CM);
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
                               fill_gap, lp_start, so, db, lane);
