@@ -49,9 +49,11 @@ __global__ void k_table_bias(fikit_table_t);
 __global__ void k_fill(fikit_table_t, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
                        const uint8_t*, const uint32_t*, const uint32_t*, uint32_t, fikit_fill_params_t, uint32_t*,
                        const uint32_t*, uint32_t*, uint64_t*, uint64_t*, fikit_status_t*);
-__global__ void k_simulate(fikit_table_t, const uint32_t*, const uint64_t*, const uint64_t*, const uint32_t*,
-                           const uint64_t*, const uint8_t*, const fikit_scenario_t*, uint32_t, fikit_fill_params_t,
-                           fikit_result_t*, int32_t*, uint64_t*, const uint64_t*, fikit_status_t*);
+const void* simulate_smem_kernel(bool sched);
+void launch_simulate_smem(int, int, cudaStream_t, const fikit_table_t&, const uint32_t*, const uint64_t*,
+                          const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, const fikit_scenario_t*,
+                          uint32_t, fikit_fill_params_t, fikit_result_t*, int32_t*, uint64_t*, const uint64_t*,
+                          fikit_status_t*);
 const void* simulate_reg_kernel(bool sched);
 void launch_simulate_reg(int, int, cudaStream_t, const fikit_table_t&, const uint32_t*, const uint64_t*,
                          const uint64_t*, const uint32_t*, const uint64_t*, const uint8_t*, const fikit_scenario_t*,
@@ -420,7 +422,7 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
   static int g1 = 0, g2 = 0;
   if (!g1) {
     g1 = one_wave(simulate_reg_kernel(false), kRegThreads);
-    g2 = one_wave((const void*)k_simulate, kSimThreads);
+    g2 = one_wave(simulate_smem_kernel(false), kSimThreads);
   }
   const uint64_t n1 = ((uint64_t)S + kRegThreads / 32 - 1) / (kRegThreads / 32);
   const uint64_t n2 = ((uint64_t)S + kSimThreads / 32 - 1) / (kSimThreads / 32);
@@ -429,8 +431,8 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
   launch_simulate_reg(b1, kRegThreads, s, *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
                       fill_gap, lp_start, sched_off, w.st());
   if (int r = launched()) return r;
-  k_simulate<<<b2, kSimThreads, 0, s>>>(*tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out, fill_gap,
-                                lp_start, sched_off, w.st());
+  launch_simulate_smem(b2, kSimThreads, s, *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
+                       fill_gap, lp_start, sched_off, w.st());
   return launched();
 }
 

@@ -720,6 +720,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
 }
 
 // Pass 2: the deferred scenarios, pool in shared memory (sorted fast path or full argmin).
+template <bool kSched>
 __global__ void __launch_bounds__(kReplayWarps * 32)
     k_simulate(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
   __shared__ uint8_t s_meta[kReplayWarps][kPoolMax];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
-  const bool sched = fill_gap != nullptr && lp_start != nullptr && sched_off != nullptr;
+  constexpr bool sched = kSched;
   uint32_t* ctr = reinterpret_cast<uint32_t*>(st) + kSchedWord2;
   // claim 32 scenarios at a time; run the ones pass 1 deferred
   for (;;) {
@@ -1089,6 +1090,21 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
 // host launchers (the kernel templates are instantiated and launched in this translation unit)
 const void* simulate_reg_kernel(bool sched) {
   return sched ? (const void*)k_simulate_reg<true> : (const void*)k_simulate_reg<false>;
+}
+const void* simulate_smem_kernel(bool sched) {
+  return sched ? (const void*)k_simulate<true> : (const void*)k_simulate<false>;
+}
+void launch_simulate_smem(int blocks, int threads, cudaStream_t s, const fikit_table_t& tab, const uint32_t* hp_row,
+                          const uint64_t* hp_dur, const uint64_t* hp_gap, const uint32_t* lp_row,
+                          const uint64_t* lp_dur, const uint8_t* lp_level, const fikit_scenario_t* sc, uint32_t S,
+                          fikit_fill_params_t prm, fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
+                          const uint64_t* sched_off, fikit_status_t* st) {
+  if (fill_gap && lp_start && sched_off)
+    k_simulate<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
+                                                 fill_gap, lp_start, sched_off, st);
+  else
+    k_simulate<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+                                                  out, fill_gap, lp_start, sched_off, st);
 }
 const void* simulate_stream_kernel(bool sched) {
   return sched ? (const void*)k_simulate_stream<true> : (const void*)k_simulate_stream<false>;
