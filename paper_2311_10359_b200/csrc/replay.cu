@@ -295,21 +295,23 @@ struct DigestBatch {
 // (key order = BestPrioFit's preference order, as in make_sorted_pool), and, by request index,
 // the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^50.
 struct RegPool {
-  uint64_t q0, q1;    // predicted duration at sorted positions lane, 32 + lane
+  uint32_t q0, q1;    // predicted duration at sorted positions lane, 32 + lane (< 2^22 ns)
   uint32_t k0, k1;    // request index there
   bool a0, a1;        // alive and eligible there
-  uint64_t dur0, dur1;  // LP duration of requests lane, 32 + lane
+  uint32_t dur0, dur1;  // LP duration of requests lane, 32 + lane (< 2^32 ns)
   uint32_t lvl0, lvl1;  // level of requests lane, 32 + lane
   uint64_t alive;     // alive requests by index (warp-uniform)
 
   __device__ __forceinline__ uint64_t min_q() const {
-    return warp_min_u64(min(a0 ? q0 : ~0ull, a1 ? q1 : ~0ull));
+    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? q0 : 0xFFFFFFFFu, a1 ? q1 : 0xFFFFFFFFu));
+    return v == 0xFFFFFFFFu ? ~0ull : (uint64_t)v;
   }
   // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    uint32_t b = __ballot_sync(0xffffffffu, a0 && q0 <= R);
+    const uint32_t Rc = R > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R;  // every q < 2^22
+    uint32_t b = __ballot_sync(0xffffffffu, a0 && q0 <= Rc);
     const bool hi = b == 0;
-    if (hi) b = __ballot_sync(0xffffffffu, a1 && q1 <= R);
+    if (hi) b = __ballot_sync(0xffffffffu, a1 && q1 <= Rc);
     if (!b) return -1;
     const int src = __ffs(b) - 1;
     const int kk = (int)__shfl_sync(0xffffffffu, hi ? k1 : k0, src);
@@ -321,33 +323,13 @@ struct RegPool {
     return kk;
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const {
-    const uint64_t d0 = __shfl_sync(0xffffffffu, dur0, kk & 31u), d1 = __shfl_sync(0xffffffffu, dur1, kk & 31u);
+    const uint32_t d0 = __shfl_sync(0xffffffffu, dur0, kk & 31u), d1 = __shfl_sync(0xffffffffu, dur1, kk & 31u);
     return kk < 32 ? d0 : d1;
   }
 };
 
-// register bitonic sort of 64 keys (lane holds positions lane (e0) and 32 + lane (e1)), ascending
-__device__ __forceinline__ void reg_bitonic64(uint64_t& e0, uint64_t& e1, int lane) {
-#pragma unroll
-  for (uint32_t k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      if (j == 32) {  // partner in the same lane (k == 64: ascending)
-        const uint64_t lo = min(e0, e1), hi = max(e0, e1);
-        e0 = lo;
-        e1 = hi;
-      } else {
-        const uint64_t o0 = __shfl_xor_sync(0xffffffffu, e0, j), o1 = __shfl_xor_sync(0xffffffffu, e1, j);
-        const bool lower = ((uint32_t)lane & j) == 0;
-        const bool asc0 = ((uint32_t)lane & k) == 0, asc1 = ((32u + (uint32_t)lane) & k) == 0;
-        e0 = (asc0 == lower) ? min(e0, o0) : max(e0, o0);
-        e1 = (asc1 == lower) ? min(e1, o1) : max(e1, o1);
-      }
-    }
-  }
-}
-
-// the same network on 32-bit keys (one SHFL and one min/max instruction per element and stage)
+// register bitonic sort of 64 32-bit keys (lane holds positions lane (e0) and 32 + lane (e1)),
+// ascending: one SHFL and one min/max instruction per element and stage
 __device__ __forceinline__ void reg_bitonic64_u32(uint32_t& e0, uint32_t& e1, int lane) {
 #pragma unroll
   for (uint32_t k = 2; k <= 64; k <<= 1) {
@@ -374,15 +356,19 @@ constexpr uint32_t kQ22 = (1u << 22) - 1;  // 32-bit keys: level << 28 | (kQ22 -
 __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t K, const uint32_t* __restrict__ row,
                                              const uint8_t* __restrict__ level, const uint64_t* __restrict__ dur,
                                              uint64_t off, uint32_t m, int lane, fikit_status_t* st, RegPool& P) {
-  bool ok = true, fits = true, small = true;
-  auto one = [&](uint32_t kk, uint64_t& key, uint64_t& d, uint32_t& lv) {
-    key = ~0ull;
+  // the register pool is 32-bit: every eligible q < 2^22 ns (4.2 ms) and every e < 2^32 ns;
+  // any other scenario goes to pass 2
+  bool ok = true, small = true;
+  auto one = [&](uint32_t kk, uint32_t& key, uint32_t& d, uint32_t& lv) {
+    key = 0xFFFFFFFFu;
     d = 0;
     lv = 0;
     if (kk < m) {
       const uint32_t r = __ldg(row + off + kk);
       const uint32_t L = __ldg(level + off + kk);
-      d = __ldg(dur + off + kk);
+      const uint64_t d64 = __ldg(dur + off + kk);
+      if (d64 >> 32) small = false;
+      d = (uint32_t)d64;
       lv = L;
       if (L < 1 || L > 9) {
         flag_record(st, off + kk);
@@ -391,41 +377,24 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
       const bool el = r < K && __ldg(tab.sums + (size_t)r * 4) > 0;  // R16: no SK profile -> never a fill
       if (el) {
         const uint64_t q = __ldg(tab.mean + (size_t)r * 2);  // SK of the request's ID
-        if (q > kQ50) fits = false;
         if (q > kQ22) small = false;
-        key = ((uint64_t)(L & 0xF) << 60) | ((kQ50 - (q & kQ50)) << 10) | kk;
+        // BestPrioFit's order (level asc, q desc, index asc) as one 32-bit key
+        key = ((L & 0xFu) << 28) | ((kQ22 - (uint32_t)(q & kQ22)) << 6) | kk;
       }
     }
   };
-  uint64_t e0, e1;
-  one((uint32_t)lane, e0, P.dur0, P.lvl0);
-  one(32u + (uint32_t)lane, e1, P.dur1, P.lvl1);
+  uint32_t f0, f1;
+  one((uint32_t)lane, f0, P.dur0, P.lvl0);
+  one(32u + (uint32_t)lane, f1, P.dur1, P.lvl1);
   if (!__all_sync(0xffffffffu, ok)) return 1;
-  if (!__all_sync(0xffffffffu, fits)) return 2;
-  if (__all_sync(0xffffffffu, small)) {  // every eligible q < 2^22 ns: sort 32-bit keys
-    auto k32 = [](uint64_t key) -> uint32_t {
-      if (key == ~0ull) return 0xFFFFFFFFu;
-      const uint32_t q = (uint32_t)(kQ50 - ((key >> 10) & kQ50));
-      return ((uint32_t)(key >> 60) << 28) | ((kQ22 - q) << 6) | (uint32_t)(key & 63u);
-    };
-    uint32_t f0 = k32(e0), f1 = k32(e1);
-    reg_bitonic64_u32(f0, f1, lane);
-    P.a0 = f0 != 0xFFFFFFFFu;
-    P.a1 = f1 != 0xFFFFFFFFu;
-    P.q0 = kQ22 - ((f0 >> 6) & kQ22);
-    P.q1 = kQ22 - ((f1 >> 6) & kQ22);
-    P.k0 = f0 & 63u;
-    P.k1 = f1 & 63u;
-    P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
-    return 0;
-  }
-  reg_bitonic64(e0, e1, lane);
-  P.a0 = e0 != ~0ull;
-  P.a1 = e1 != ~0ull;
-  P.q0 = key_q(e0);
-  P.q1 = key_q(e1);
-  P.k0 = (uint32_t)(e0 & 1023u);
-  P.k1 = (uint32_t)(e1 & 1023u);
+  if (!__all_sync(0xffffffffu, small)) return 2;
+  reg_bitonic64_u32(f0, f1, lane);
+  P.a0 = f0 != 0xFFFFFFFFu;
+  P.a1 = f1 != 0xFFFFFFFFu;
+  P.q0 = kQ22 - ((f0 >> 6) & kQ22);
+  P.q1 = kQ22 - ((f1 >> 6) & kQ22);
+  P.k0 = f0 & 63u;
+  P.k1 = f1 & 63u;
   P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
   return 0;
 }
