@@ -255,7 +255,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   const uint64_t target = 65536;
   uint64_t stride = n > target ? n / target : 1;
   uint64_t ns = (n + stride - 1) / stride;
-  k_sample<<<grid_for(ns, 256, num_sms() * 4), 256, 0, s>>>(
+  k_sample<<<grid_for(ns, 512, num_sms() * 2), 512, 0, s>>>(
       reinterpret_cast<const uint4*>(recs), n, stride, ns, w.name_hash(), w.sig_hash(), names.count, sigs.count,
       w.index(), w.L.slots, w.st(), t, w.row_tuple(), w.samp_cnt());
   if (int r = launched()) return r;
