@@ -134,10 +134,10 @@ __device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
 // Build the sorted pool in place of q (q[k] by index -> K[p] by sorted position).
 // Returns false (pool left by index) if the fast path does not apply.
 __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* meta, uint32_t m, int lane,
-                                                 uint32_t& A, uint32_t& nch, uint64_t& CM) {
+                                                 uint32_t& A, uint32_t& nch, uint32_t& CM) {
   bool ok = true;
   for (uint32_t k = lane; k < m; k += 32)
-    if ((meta[k] & kElig) && q[k] > kQ50) ok = false;
+    if ((meta[k] & kElig) && q[k] > 0xFFFFFFFFull) ok = false;  // fast path: every q < 2^32
   if (!__all_sync(0xffffffffu, ok) || m > 1024u) return false;
   uint32_t P = 32;
   while (P < m) P <<= 1;
@@ -148,14 +148,22 @@ __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* met
   }
   __syncwarp();
   warp_bitonic_sort(q, P, lane);
+  // sorted: the order is the position now; each entry becomes q << 32 | index (q = the high
+  // word, one 32-bit load), dead / ineligible entries stay ~0
+  for (uint32_t p = lane; p < P; p += 32) {
+    const uint64_t key = q[p];
+    if (key != ~0ull) q[p] = (key_q(key) << 32) | (key & 1023u);
+  }
+  __syncwarp();
+  const uint32_t* qh = reinterpret_cast<const uint32_t*>(q) + 1;  // qh[2 p] = q at position p
   nch = (m + 31) / 32;
   A = 0;
-  CM = ~0ull;
+  CM = 0xFFFFFFFFu;
   for (uint32_t c = 0; c < nch; c++) {
     const uint32_t p = c * 32 + lane;
     const bool alive = p < m && q[p] != ~0ull;
     const uint32_t b = __ballot_sync(0xffffffffu, alive);
-    const uint64_t mn = warp_min_u64(alive ? key_q(q[p]) : ~0ull);
+    const uint32_t mn = __reduce_min_sync(0xffffffffu, alive ? qh[2 * p] : 0xFFFFFFFFu);
     if (lane == (int)c) {
       A = b;
       CM = mn;
@@ -165,41 +173,45 @@ __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* met
 }
 
 // chunk c's minimum q over its alive positions, after its alive word changed (to lane c)
-__device__ __forceinline__ void chunk_min_refresh(const uint64_t* K, uint32_t A, uint32_t c, uint64_t& CM,
+__device__ __forceinline__ void chunk_min_refresh(const uint64_t* K, uint32_t A, uint32_t c, uint32_t& CM,
                                                   int lane) {
   const uint32_t word = __shfl_sync(0xffffffffu, A, c);
-  const uint64_t mn = warp_min_u64(((word >> lane) & 1u) ? key_q(K[c * 32 + lane]) : ~0ull);
+  const uint32_t* qh = reinterpret_cast<const uint32_t*>(K) + 1;
+  const uint32_t mn = __reduce_min_sync(0xffffffffu, ((word >> lane) & 1u) ? qh[2 * (c * 32 + lane)] : 0xFFFFFFFFu);
   if (lane == (int)c) CM = mn;
 }
 
 // first alive sorted position with q <= R, or -1 (uniform): the first chunk whose alive minimum
 // fits (one ballot over the chunk lanes), then the first fitting position inside it
-__device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint64_t CM, uint32_t nch, uint64_t R,
+__device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint32_t CM, uint32_t nch, uint64_t R,
                                            int lane) {
-  const uint32_t cb = __ballot_sync(0xffffffffu, (uint32_t)lane < nch && CM <= R);
+  const uint32_t Rc = R > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R;  // every q < 2^32
+  const uint32_t cb = __ballot_sync(0xffffffffu, (uint32_t)lane < nch && CM <= Rc);
   if (!cb) return -1;
   const uint32_t c = __ffs(cb) - 1;
   const uint32_t word = __shfl_sync(0xffffffffu, A, c);
-  const bool fit = ((word >> lane) & 1u) && key_q(K[c * 32 + lane]) <= R;
+  const uint32_t* qh = reinterpret_cast<const uint32_t*>(K) + 1;
+  const bool fit = ((word >> lane) & 1u) && qh[2 * (c * 32 + lane)] <= Rc;
   const uint32_t b = __ballot_sync(0xffffffffu, fit);  // != 0: the chunk's minimum fits
   return (int)(c * 32 + __ffs(b) - 1);
 }
 
-__device__ __forceinline__ uint64_t sorted_min_q(uint64_t CM, uint32_t nch, int lane) {
-  return warp_min_u64((uint32_t)lane < nch ? CM : ~0ull);
+__device__ __forceinline__ uint64_t sorted_min_q(uint32_t CM, uint32_t nch, int lane) {
+  const uint32_t v = __reduce_min_sync(0xffffffffu, (uint32_t)lane < nch ? CM : 0xFFFFFFFFu);
+  return v == 0xFFFFFFFFu ? ~0ull : (uint64_t)v;
 }
 
 // One BestPrioFit pick (Alg. 2) on either representation: returns the request index (or -1)
 // and its q; dequeues it (alive bit cleared in both views).
 __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
-                                         uint64_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
+                                         uint32_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
   int k;
   if (fast) {
     const int p = sorted_best(q, A, CM, nch, R, lane);
     if (p < 0) return -1;
-    const uint64_t key = q[p];
-    k = (int)(key & 1023u);
-    qk = key_q(key);
+    const uint64_t e = q[p];  // q << 32 | index
+    k = (int)(e & 1023u);
+    qk = e >> 32;
     if (lane == (p >> 5)) A &= ~(1u << (p & 31));
     chunk_min_refresh(q, A, (uint32_t)p >> 5, CM, lane);
   } else {
@@ -213,7 +225,7 @@ __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, 
 }
 
 __device__ __forceinline__ uint64_t pool_min_q(bool fast, const uint64_t* q, const uint8_t* meta, uint32_t m,
-                                               uint64_t CM, uint32_t nch, int lane) {
+                                               uint32_t CM, uint32_t nch, int lane) {
   return fast ? sorted_min_q(CM, nch, lane) : warp_min_q(q, meta, m, lane);
 }
 
@@ -247,7 +259,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint32_t np = 0, po = picks_off[g];
     if (R >= prm.threshold_ns) {  // Alg. 1 lines 6-8
       uint32_t A = 0, nch = 0;
-      uint64_t CM;
+      uint32_t CM;
       const bool fast = make_sorted_pool(q, meta, m, lane, A, nch, CM);
       uint64_t qmin = pool_min_q(fast, q, meta, m, CM, nch, lane);
       for (;;) {                             // lines 9-16
@@ -406,7 +418,7 @@ struct SmemPool {
   const uint64_t* dur;  // lp_dur + lp_off
   uint32_t m, A, nch;
   bool fast;
-  uint64_t CM;  // lane c: chunk c's alive minimum q (sorted fast path)
+  uint32_t CM;  // lane c: chunk c's alive minimum q (sorted fast path; q < 2^32 there)
   __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, CM, nch, lane); }
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
     return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);
@@ -725,7 +737,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint8_t* meta = s_meta[w];
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
-    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, ~0ull};
+    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, 0xFFFFFFFFu};
     P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch, P.CM);
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
