@@ -320,12 +320,15 @@ def test_sharded_merge_one_gpu(fk, orc, P):
     assert_tables_equal(out.to_numpy(), ref, f"merge P={P}")
 
 
-def test_replay_huge_durations_slow_path(fk, orc):
-    """Requests with SK >= 2^50 ns leave the sorted-pool fast path: the exact argmin path must agree too."""
+@pytest.mark.parametrize("extra", [1 << 52, 1 << 33, 20_000_000])
+def test_replay_huge_durations_slow_path(fk, orc, extra):
+    """Requests with large SK leave the fast paths: SK >= 2^50 (or 2^32) ns the exact argmin path,
+    SK >= 2^22 ns (here 20 ms) the 32-bit register pool (pass 1 defers to the shared-memory pass 2);
+    the replay must agree with the oracle on each."""
     tr = F.random_trace(61, 3000, n_ids=25)
     rec = tr.records.copy()
     big = rec["name_id"] == rec["name_id"][0]
-    rec["end_ns"][big] += np.uint64(1 << 52)
+    rec["end_ns"][big] += np.uint64(extra)
     tr2 = F.Trace(rec, tr.names, tr.sigs)
     rp = F.random_replay(62, tr2, 200, m_max=60, n_h_max=40, levels=4)
     _replay_parity(fk, orc, F.Config("huge", tr2, rp), 256)
@@ -634,3 +637,16 @@ def test_replay_without_schedule_outputs(fk, orc):
                  lp_stream=sr.lp_stream)
     p.step()
     assert p.results().tobytes() == out.tobytes()
+
+
+def test_replay_huge_lp_durations(fk, orc):
+    """LP requests whose actual duration is >= 2^32 ns leave the 32-bit register pool (pass 2)"""
+    from dataclasses import replace
+
+    tr = F.random_trace(63, 3000, n_ids=25)
+    rp = F.random_replay(64, tr, 200, m_max=60, n_h_max=40, levels=4)
+    lp = rp.lp_records.copy()
+    big = np.random.default_rng(65).random(lp.shape[0]) < 0.05
+    lp["end_ns"][big] += np.uint64(1 << 33)
+    ref = _replay_parity(fk, orc, F.Config("huge-e", tr, replace(rp, lp_records=lp)), 256)
+    assert ref["results"]["n_fills"].sum() > 0
