@@ -331,12 +331,34 @@ struct RegPool {
     if (lane == src) {
       if (hi) a1 = false; else a0 = false;
     }
-    alive &= ~(1ull << kk);
     return kk;
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const {
     const uint32_t d0 = __shfl_sync(0xffffffffu, dur0, kk & 31u), d1 = __shfl_sync(0xffffffffu, dur1, kk & 31u);
     return kk < 32 ? d0 : d1;
+  }
+  // the schedule of request kk (gap, start), kept by its owning lane for the digest at the end
+  int32_t fg0, fg1;
+  uint64_t st0, st1;
+  __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch&) {
+    if (lane == (int)(kk & 31u)) {
+      if (kk < 32) {
+        fg0 = g;
+        st0 = t;
+      } else {
+        fg1 = g;
+        st1 = t;
+      }
+    }
+  }
+  // requests dequeued by fills, by index (k0 / k1 = 0xFF: an ineligible position)
+  __device__ __forceinline__ uint64_t picked_mask() const {
+    uint32_t lo = 0, hi = 0;
+    if (k0 < 64 && !a0) (k0 < 32 ? lo : hi) |= 1u << (k0 & 31u);
+    if (k1 < 64 && !a1) (k1 < 32 ? lo : hi) |= 1u << (k1 & 31u);
+    lo = __reduce_or_sync(0xffffffffu, lo);
+    hi = __reduce_or_sync(0xffffffffu, hi);
+    return ((uint64_t)hi << 32) | lo;
   }
 };
 
@@ -405,8 +427,8 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
   P.a1 = f1 != 0xFFFFFFFFu;
   P.q0 = kQ22 - ((f0 >> 6) & kQ22);
   P.q1 = kQ22 - ((f1 >> 6) & kQ22);
-  P.k0 = f0 & 63u;
-  P.k1 = f1 & 63u;
+  P.k0 = P.a0 ? (f0 & 63u) : 0xFFu;
+  P.k1 = P.a1 ? (f1 & 63u) : 0xFFu;
   P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
   return 0;
 }
@@ -424,6 +446,9 @@ struct SmemPool {
     return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const { return __ldg(dur + kk); }
+  __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch& dig) {
+    dig.add(kk, g, t, lane);
+  }
 };
 
 // inclusive warp prefix sum of u64 values; 32-bit shuffles and adds when every value is
@@ -539,7 +564,7 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
         fill_gap[so + k] = (int32_t)i;
         lp_start[so + k] = t;
       }
-      dig.add((uint32_t)k, (int32_t)i, t, lane);
+      P.record((uint32_t)k, (int32_t)i, t, lane, dig);
       R -= qk;
       t += e;
       if (qk == qmin) qmin = min_q();
@@ -583,14 +608,12 @@ __device__ __forceinline__ uint64_t replay_tail(uint64_t t, uint32_t m, uint32_t
   return t;
 }
 
-// the same for a register pool (m <= 64): each lane keeps the tail start of its two requests and
-// the digest terms are evaluated once at the end (two SIMT passes instead of one per level)
+// the same for a register pool (m <= 64): the owning lanes keep each request's tail start (the
+// digest terms of fills and tail are evaluated together at the end)
 template <class Sel, class Dur>
 __device__ __forceinline__ uint64_t replay_tail_reg(uint64_t t, uint32_t m, uint32_t levels, Sel sel_of, Dur dur_of,
                                                     bool sched, int32_t* fill_gap, uint64_t* lp_start, uint64_t so,
-                                                    uint64_t& dig, uint32_t& n_tail, int lane) {
-  uint64_t st0 = 0, st1 = 0;
-  bool f0 = false, f1 = false;
+                                                    RegPool& P, uint32_t& n_tail, int lane) {
   while (levels) {
     const uint32_t L = __ffs(levels) - 1;
     levels &= levels - 1;
@@ -610,19 +633,17 @@ __device__ __forceinline__ uint64_t replay_tail_reg(uint64_t t, uint32_t m, uint
           lp_start[so + k] = start;
         }
         if (h) {
-          st1 = start;
-          f1 = true;
+          P.fg1 = -1;
+          P.st1 = start;
         } else {
-          st0 = start;
-          f0 = true;
+          P.fg0 = -1;
+          P.st0 = start;
         }
       }
       t += __shfl_sync(0xffffffffu, x, 31);
       n_tail += __popc(bal);
     }
   }
-  if (f0) dig += digest_term((uint32_t)lane, -1, st0);
-  if (f1) dig += digest_term(32u + (uint32_t)lane, -1, st1);
   return t;
 }
 
@@ -685,18 +706,21 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
                               fill_gap, lp_start, so, db, lane);
+    P.alive &= ~P.picked_mask();
     uint32_t lv = 0;  // levels still queued
     if ((P.alive >> lane) & 1ull) lv |= 1u << P.lvl0;
     if ((P.alive >> (32 + lane)) & 1ull) lv |= 1u << P.lvl1;
     lv = __reduce_or_sync(0xffffffffu, lv);
-    uint64_t tail_dig = 0;
     uint32_t n_tail = 0;
     const uint64_t t = replay_tail_reg(
         o.t, m, lv,
         [&](uint32_t k, uint32_t L) { return ((P.alive >> k) & 1ull) && (k < 32 ? P.lvl0 : P.lvl1) == L; },
-        [&](uint32_t k) { return k < 32 ? P.dur0 : P.dur1; }, sched, fill_gap, lp_start, so, tail_dig, n_tail,
-        lane);
-    write_result(out, s, o, t, m, n_tail, db, tail_dig, lane);
+        [&](uint32_t k) { return k < 32 ? P.dur0 : P.dur1; }, sched, fill_gap, lp_start, so, P, n_tail, lane);
+    // every request ran (fill or tail): its digest term from its owning lane
+    uint64_t dig = 0;
+    if ((uint32_t)lane < m) dig += digest_term((uint32_t)lane, P.fg0, P.st0);
+    if (32u + (uint32_t)lane < m) dig += digest_term(32u + (uint32_t)lane, P.fg1, P.st1);
+    write_result(out, s, o, t, m, n_tail, db, dig, lane);
   }
 }
 
