@@ -307,6 +307,7 @@ struct DigestBatch {
 // (key order = BestPrioFit's preference order, as in make_sorted_pool), and, by request index,
 // the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^50.
 struct RegPool {
+  static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
   uint32_t q0, q1;    // predicted duration at sorted positions lane, 32 + lane (< 2^22 ns)
   uint32_t k0, k1;    // request index there
   bool a0, a1;        // alive and eligible there
@@ -435,6 +436,7 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
 
 // shared-memory pool (any m <= kPoolMax): the sorted fast path or the full argmin
 struct SmemPool {
+  static constexpr bool kOwnerStats = false;
   uint64_t* q;
   uint8_t* meta;
   const uint64_t* dur;  // lp_dur + lp_off
@@ -568,9 +570,11 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
       R -= qk;
       t += e;
       if (qk == qmin) qmin = min_q();
-      o.fill_work += e;
-      o.n_fills++;
-      o.lp_end = max(o.lp_end, t);
+      if (!Pool::kOwnerStats) {  // (the register pool sums its fills from the owning lanes)
+        o.fill_work += e;
+        o.n_fills++;
+      }
+      o.lp_end = t;  // fills run in time order: the last one ends last
     }
     return t;
   };
@@ -704,8 +708,17 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps 
     }
     const uint64_t so = sched ? sched_off[s] : 0;
     DigestBatch db;
-    const HpOut o = replay_hp(P, [&]() { return P.min_q(); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
-                              fill_gap, lp_start, so, db, lane);
+    P.fg0 = P.fg1 = -1;
+    HpOut o = replay_hp(P, [&]() { return P.min_q(); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched, fill_gap,
+                        lp_start, so, db, lane);
+    {  // fills: the requests with a gap index, summed from their owning lanes
+      const bool f0 = P.fg0 >= 0 && (uint32_t)lane < m, f1 = P.fg1 >= 0 && 32u + (uint32_t)lane < m;
+      o.n_fills = __popc(__ballot_sync(0xffffffffu, f0)) + __popc(__ballot_sync(0xffffffffu, f1));
+      uint64_t fw = (f0 ? (uint64_t)P.dur0 : 0ull) + (f1 ? (uint64_t)P.dur1 : 0ull);
+#pragma unroll
+      for (int off2 = 16; off2; off2 >>= 1) fw += __shfl_xor_sync(0xffffffffu, fw, off2);
+      o.fill_work = fw;
+    }
     P.alive &= ~P.picked_mask();
     uint32_t lv = 0;  // levels still queued
     if ((P.alive >> lane) & 1ull) lv |= 1u << P.lvl0;
