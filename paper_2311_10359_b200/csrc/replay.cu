@@ -203,20 +203,25 @@ __device__ __forceinline__ uint64_t sorted_min_q(uint32_t CM, uint32_t nch, int 
 
 // One BestPrioFit pick (Alg. 2) on either representation: returns the request index (or -1)
 // and its q; dequeues it (alive bit cleared in both views).
+// ek: the pick's actual duration, its global load issued as soon as the index is known (the
+// dequeue bookkeeping below overlaps its latency)
 __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
-                                         uint32_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk) {
+                                         uint32_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk,
+                                         const uint64_t* __restrict__ dur, uint64_t& ek) {
   int k;
   if (fast) {
     const int p = sorted_best(q, A, CM, nch, R, lane);
     if (p < 0) return -1;
-    const uint64_t e = q[p];  // q << 32 | index
-    k = (int)(e & 1023u);
-    qk = e >> 32;
+    const uint64_t x = q[p];  // q << 32 | index
+    k = (int)(x & 1023u);
+    ek = __ldg(dur + k);
+    qk = x >> 32;
     if (lane == (p >> 5)) A &= ~(1u << (p & 31));
     chunk_min_refresh(q, A, (uint32_t)p >> 5, CM, lane);
   } else {
     k = warp_best_prio_fit(q, meta, m, R, lane);
     if (k < 0) return -1;
+    ek = __ldg(dur + k);
     qk = q[k];
   }
   if (lane == 0) meta[k] &= (uint8_t)~kAlive;
@@ -265,12 +270,12 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
       for (;;) {                             // lines 9-16
         if (prm.feedback && t >= dl) break;  // early stop on the HP launch
         if (R < qmin) break;                 // nothing can fit
-        uint64_t qk;
-        const int k = pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);  // Alg. 2
+        uint64_t qk, ek;
+        const int k = pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, pool_dur + off, ek);  // Alg. 2
         if (k < 0) break;
         if (lane == 0) picks[po + np] = (uint32_t)k;
         np++;
-        t += __ldg(pool_dur + off + k);  // launched (line 14)
+        t += ek;  // launched (line 14)
         R -= qk;                           // revised by the predicted duration (line 15, R17)
         if (qk == qmin) qmin = pool_min_q(fast, q, meta, m, CM, nch, lane);
       }
@@ -444,10 +449,11 @@ struct SmemPool {
   bool fast;
   uint32_t CM;  // lane c: chunk c's alive minimum q (sorted fast path; q < 2^32 there)
   __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, CM, nch, lane); }
+  uint64_t ek;  // the last pick's duration (loaded by pool_pick)
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk);
+    return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, dur, ek);
   }
-  __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const { return __ldg(dur + kk); }
+  __device__ __forceinline__ uint64_t dur_of(uint32_t) const { return ek; }  // (of the last pick)
   __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch& dig) {
     dig.add(kk, g, t, lane);
   }
@@ -774,7 +780,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint8_t* meta = s_meta[w];
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
-    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, 0xFFFFFFFFu};
+    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, 0xFFFFFFFFu, 0};
     P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch, P.CM);
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
