@@ -223,10 +223,21 @@ __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, 
     if (k < 0) return -1;
     ek = __ldg(dur + k);
     qk = q[k];
+    if (lane == 0) meta[k] &= (uint8_t)~kAlive;  // (the fast path's dequeues: sync_meta_alive)
+    __syncwarp();
   }
-  if (lane == 0) meta[k] &= (uint8_t)~kAlive;
-  __syncwarp();
   return k;
+}
+
+// after a sorted-pool replay: clear the alive bit (by index) of every request a fill dequeued
+// (eligible positions whose bit in A is clear), once instead of one shared RMW per pick
+__device__ __forceinline__ void sync_meta_alive(const uint64_t* q, uint8_t* meta, uint32_t A, uint32_t nch, int lane) {
+  for (uint32_t c = 0; c < nch; c++) {
+    const uint32_t word = __shfl_sync(0xffffffffu, A, c);
+    const uint64_t x = q[c * 32 + lane];
+    if (x != ~0ull && !((word >> lane) & 1u)) meta[x & 1023u] &= (uint8_t)~kAlive;
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ uint64_t pool_min_q(bool fast, const uint64_t* q, const uint8_t* meta, uint32_t m,
@@ -785,6 +796,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
                               fill_gap, lp_start, so, db, lane);
+    if (P.fast) sync_meta_alive(q, meta, P.A, P.nch, lane);
     uint32_t lv = 0;
     for (uint32_t k = lane; k < m; k += 32)
       if (meta[k] & kAlive) lv |= 1u << (meta[k] & 0xF);
