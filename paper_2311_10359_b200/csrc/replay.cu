@@ -607,12 +607,16 @@ __device__ __forceinline__ uint64_t replay_tail(uint64_t t, uint32_t m, uint32_t
   while (levels) {
     const uint32_t L = __ffs(levels) - 1;
     levels &= levels - 1;
+    uint64_t e_cur = (uint32_t)lane < m ? dur_of((uint32_t)lane) : 0;  // block b's durations, one block ahead
     for (uint32_t b = 0; b < m; b += 32) {
       const uint32_t k = b + lane;
+      const uint64_t e_next = k + 32 < m ? dur_of(k + 32) : 0;
       const bool sel = k < m && sel_of(k, L);
       const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      const uint64_t e_here = e_cur;
+      e_cur = e_next;
       if (!bal) continue;
-      const uint64_t e = sel ? dur_of(k) : 0;
+      const uint64_t e = sel ? e_here : 0;
       const uint64_t x = warp_inclusive_scan(e, lane);
       if (sel) {
         const uint64_t start = t + x - e;
