@@ -114,21 +114,51 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t a) {
 
 __device__ __forceinline__ uint64_t key_q(uint64_t key) { return kQ50 - ((key >> 10) & kQ50); }
 
+// Warp bitonic sort of P (power of two, >= 32) keys in shared memory.  Consecutive stages j and
+// j/2 of one merge are fused: each thread loads a group of 4 keys {b, b+h, b+j, b+j+h} (h = j/2),
+// does both compare-exchange rounds in registers and stores them (half the shared-memory
+// round trips and warp syncs of one stage at a time).
 __device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
-  for (uint32_t k = 2; k <= P; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t t = lane; t < P / 2; t += 32) {
-        const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-        const uint32_t l = i + j;
-        const uint64_t a = K[i], b = K[l];
-        const bool asc = (i & k) == 0;
-        if ((a > b) == asc) {
-          K[i] = b;
-          K[l] = a;
+  auto cx = [](uint64_t& a, uint64_t& b, bool asc) {
+    if ((a > b) == asc) {
+      const uint64_t x = a;
+      a = b;
+      b = x;
+    }
+  };
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    uint32_t j = k >> 1;
+    while (j > 0) {
+      if (j >= 2) {
+        const uint32_t h = j >> 1;
+        for (uint32_t t = lane; t < P / 4; t += 32) {
+          const uint32_t b = ((t & ~(h - 1)) << 2) | (t & (h - 1));
+          const bool asc = (b & k) == 0;
+          uint64_t a0 = K[b], a1 = K[b + h], a2 = K[b + j], a3 = K[b + j + h];
+          cx(a0, a2, asc);
+          cx(a1, a3, asc);
+          cx(a0, a1, asc);
+          cx(a2, a3, asc);
+          K[b] = a0;
+          K[b + h] = a1;
+          K[b + j] = a2;
+          K[b + j + h] = a3;
         }
+        j >>= 2;
+      } else {
+        for (uint32_t t = lane; t < P / 2; t += 32) {
+          const uint32_t i = t << 1;
+          const bool asc = (i & k) == 0;
+          uint64_t a = K[i], b = K[i + 1];
+          cx(a, b, asc);
+          K[i] = a;
+          K[i + 1] = b;
+        }
+        j = 0;
       }
       __syncwarp();
     }
+  }
 }
 
 // Build the sorted pool in place of q (q[k] by index -> K[p] by sorted position).
