@@ -501,9 +501,9 @@ struct SmemPool {
 };
 
 // inclusive warp prefix sum of u64 values; 32-bit shuffles and adds when every value is
-// < 2^26 (the sum of 32 then fits 32 bits), the common case for nanosecond chunk times
+// < 2^27 (the sum of 32 then stays below 2^32), the common case for nanosecond chunk times
 __device__ __forceinline__ uint64_t warp_inclusive_scan(uint64_t v, int lane) {
-  if (__all_sync(0xffffffffu, v < (1ull << 26))) {
+  if (__all_sync(0xffffffffu, v < (1ull << 27))) {
     uint32_t x = (uint32_t)v;
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
