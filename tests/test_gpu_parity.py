@@ -231,7 +231,10 @@ def test_zipf_small_full(fk, orc):
     assert st["schedule"] == 1 and st["n_task_buckets"] == 32, st  # 32 tasks, one bucket each
 
 
-def test_fill_batch(fk, orc):
+@pytest.mark.parametrize("G,m_max", [(3000, 80), (400, 1025)])
+def test_fill_batch(fk, orc, G, m_max):
+    """fikit_fill over G independent gaps; pools up to 1024 requests exercise the sorted pool's
+    chunk minima (32 chunks) and the fused bitonic network"""
     import torch
 
     tr = F.random_trace(51, 3000, n_ids=30)
@@ -241,8 +244,7 @@ def test_fill_batch(fk, orc):
     p = Pipeline(tr.records, tr.names, tr.sigs, capacity=128)
     p.run_measure()
     rng = np.random.default_rng(52)
-    G = 3000
-    pool_len = rng.integers(0, 80, size=G).astype(np.uint32)
+    pool_len = rng.integers(0, m_max, size=G).astype(np.uint32)
     pool_off = np.zeros(G, np.uint32)
     pool_off[1:] = np.cumsum(pool_len[:-1])
     tot = int(pool_len.sum())
