@@ -652,3 +652,32 @@ def test_replay_huge_lp_durations(fk, orc):
     lp["end_ns"][big] += np.uint64(1 << 33)
     ref = _replay_parity(fk, orc, F.Config("huge-e", tr, replace(rp, lp_records=lp)), 256)
     assert ref["results"]["n_fills"].sum() > 0
+
+
+@pytest.mark.parametrize("feedback", [1, 0])
+def test_stream_replay_many_streams(fk, orc, feedback):
+    """33-64 streams per scenario: heads in both register slots of a lane (sid = 32 + lane), the
+    REDUX picks over both, and the lone-stream tail drain reached from many streams"""
+    from dataclasses import replace
+
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    cfg = F.bert_vgg(S=1500, m=128)
+    cfg = F.Config(cfg.name, cfg.trace, replace(cfg.replay, feedback=feedback))
+    tr, rp = cfg.trace, cfg.replay
+    ids = (np.arange(rp.lp_records.shape[0]) // 3).astype(np.uint32)  # ~43 streams of 3 per window
+    tab, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=1024)
+    hr, hd, hg, _ = orc.resolve(rp.hp_records, tr.names, tr.sigs, tab)
+    lr, ld, lg, _ = orc.resolve(rp.lp_records, tr.names, tr.sigs, tab)
+    out, fg, ls, _ = orc.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level, ids, lg, rp.scenarios, tab,
+                                               rp.threshold_ns, feedback)
+    assert out["n_fills"].sum() > 0
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=1024, replay=rp, want_schedule=True, checked=True,
+                 lp_stream=ids)
+    p.step()
+    got = p.results()
+    if got.tobytes() != out.tobytes():
+        bad = np.flatnonzero(got != out)[:5]
+        raise AssertionError(f"scenarios {bad.tolist()} differ: {got[bad]} vs {out[bad]}")
+    gfg, gls = p.schedule()
+    assert np.array_equal(gfg, fg) and np.array_equal(gls, ls)
