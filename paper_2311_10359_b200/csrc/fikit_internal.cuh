@@ -49,7 +49,7 @@ constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the gl
 constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
-constexpr int kRegThreads = 256;  // k_simulate_reg block (8 warps, one scenario each)
+constexpr int kRegThreads = 512;  // k_simulate_reg block (16 warps, one scenario each)
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
 constexpr int kStreamThreads = 128;  // k_simulate_stream block (4 warps, staged windows)
 // u32 words of the 256-B status region past fikit_status_t, zeroed with it: replay work counters

@@ -733,7 +733,7 @@ constexpr uint32_t kDeferred = 0xFFFFFFFFu;
 constexpr int kRegWarps = kRegThreads / 32;
 
 template <bool kSched>  // schedule outputs requested (a compile-time branch: no per-fill checks)
-__global__ void __launch_bounds__(kRegWarps * 32, 3)  // 80 registers: 24 warps per SM
+__global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 warps per SM
     k_simulate_reg(fikit_table_t tab, const uint32_t* __restrict__ hp_row, const uint64_t* __restrict__ hp_dur,
                    const uint64_t* __restrict__ hp_gap, const uint32_t* __restrict__ lp_row,
                    const uint64_t* __restrict__ lp_dur, const uint8_t* __restrict__ lp_level,

@@ -27,20 +27,22 @@ def sub(txt, old, new):
 
 def reg_cfg(warps, minb):
     def f(r, h):
-        h = sub(h, "constexpr int kRegThreads = 256;", f"constexpr int kRegThreads = {warps * 32};")
-        r = sub(r, "__launch_bounds__(kRegWarps * 32, 3)", f"__launch_bounds__(kRegWarps * 32, {minb})")
+        h = sub(h, "constexpr int kRegThreads = 512;", f"constexpr int kRegThreads = {warps * 32};")
+        r = sub(r, "__launch_bounds__(kRegWarps * 32, 2)", f"__launch_bounds__(kRegWarps * 32, {minb})")
         return r, h
     return f
 
 
 VARIANTS = {
-    "base": [],  # 8 warps, 3 blocks per SM (80 registers)
+    "base": [],  # 16 warps, 2 blocks per SM (64 registers)
     "w8b2": [reg_cfg(8, 2)],  # 16 warps per SM, up to 128 registers
     "w4b6": [reg_cfg(4, 6)],
     "w16b1": [reg_cfg(16, 1)],
     "w4b5": [reg_cfg(4, 5)],  # 20 warps per SM, up to 102 registers
     "w4b7": [reg_cfg(4, 7)],  # 28 warps per SM, up to 72 registers
     "w4b8": [reg_cfg(4, 8)],  # 32 warps per SM, up to 64 registers
+    "w8b4": [reg_cfg(8, 4)],
+    "w16b2": [reg_cfg(16, 2)],
 }
 
 
