@@ -379,28 +379,37 @@ def main():
         a.record(stream)
         b.record(stream)
 
-    def step(timed, kpair=None):
+    def step(timed, kpair=None, checked=False):
+        # checked (first warm-up step): the workspace status after EVERY call (each validating
+        # call resets it, so one check at the end would only see the last call)
         if timed:
             ev[0].record(stream)
         fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair)
+        st = fk.check(p.ws, "bench warm-up: measure") if checked else None
         if timed:
             ev[1].record(stream)
         fk.table_finalize(p.table, p.ws)
         tab = p.table
         if world > 1:
             merge_tables(p.table, dense, ops)
+            if checked:
+                fk.check(ops.ws, "bench warm-up: merge")
             tab = dense
         if timed:
             ev[2].record(stream)
         if p.replay:
-            p.run_replay(table=tab)
+            p.checked = checked
+            p.run_replay(table=tab)  # (checked: after each resolve and replay call)
+            p.checked = False
         if timed:
             ev[3].record(stream)
+        return st
 
-    for _ in range(args.warmup):
-        step(False)
+    st = None
+    for i in range(args.warmup):
+        s_i = step(False, checked=(i == 0))
+        st = s_i if s_i is not None else st
     torch.cuda.synchronize()
-    st = fk.check(p.ws, "bench warm-up")  # the path ran clean (status of the last call)
     # per-stage breakdown on separately timed steps (events between launches)
     n_stage = min(20, args.steps)
     for _ in range(n_stage):

@@ -19,8 +19,12 @@
  *    scratch lives in the caller's workspace `ws` of `ws_bytes` bytes
  *    (fikit_ws_bytes), which must be 256-byte aligned.
  *  - Every call is stream-ordered and asynchronous on `stream` (a
- *    cudaStream_t passed as void*).  There is no global mutable state: calls
- *    on different streams with distinct workspaces may run concurrently.
+ *    cudaStream_t passed as void*) and runs on the calling thread's current
+ *    device.  The only process-wide state is (a) per-device caches of
+ *    immutable properties (SM count, occupancy, the k_measure shared-memory
+ *    opt-in), computed idempotently and published atomically, and (b) the
+ *    launch counter (fikit_launch_count).  Calls on different streams (or
+ *    devices, or host threads) with distinct workspaces may run concurrently.
  *  - The return value is a HOST status checked before any launch:
  *    FIKIT_OK, FIKIT_E_ARG (null / misaligned pointer, n >= 2^32, workspace
  *    too small) or FIKIT_E_CUDA (launch failure).
@@ -225,7 +229,9 @@ int fikit_lookup(const fikit_table_t* tab, const uint64_t* kid, const uint32_t* 
  * t >= deadline[g]: stop;  k = BestPrioFit(R) = argmin over alive eligible
  * q <= R of (level, -q, pool index);  none: stop;  t += e_k; R -= q_k }.
  * picks[picks_off[g] ..] = pool-local indices in dispatch order; n_picks[g],
- * R_left[g], t_used[g] = t.  Errors: E_RECORD (level outside [1,9]). */
+ * R_left[g], t_used[g] = t.  Errors: E_RECORD (level outside [1,9]).
+ * Limit: pool_len[g] <= 1024 (a warp's shared-memory pool); a longer pool sets
+ * FIKIT_E_ARG in the status and gap g's outputs are left unwritten. */
 int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* deadline, const uint32_t* pool_row,
                const uint64_t* pool_dur, const uint8_t* pool_level, const uint32_t* pool_off,
                const uint32_t* pool_len, uint32_t G, fikit_fill_params_t params, uint32_t* picks,
@@ -241,7 +247,10 @@ int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* dea
  * r_{i+1}; remaining requests run after the HP job in (level, index) order.
  * Writes out[s]; if fill_gap/lp_start are non-null, scenario s's m entries go
  * to [sched_off[s], sched_off[s]+m): gap index i of the fill or -1 (tail), and
- * start time.  Errors: E_RECORD (level outside [1,9]). */
+ * start time.  Errors: E_RECORD (level outside [1,9]).
+ * Limit: lp_len <= 1024 per scenario (a warp's shared-memory pool); a longer
+ * window sets FIKIT_E_ARG in the status and that scenario's out[s] is left
+ * unwritten (the other scenarios are replayed). */
 int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
                          const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
                          const uint8_t* lp_level, const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t params,
@@ -266,8 +275,9 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
  * starts at max(hp_arrival, its end).  hp_jct stays absolute; LP kernels run
  * before the HP job count in neither n_fills nor n_tail.
  * Results, schedule and digest as fikit_simulate_batch.  Limits: m <= 1024 and
- * <= 64 streams per scenario (else FIKIT_E_ARG in the status; singleton streams
- * are the POOL model: use fikit_simulate_batch).  One warp per scenario. */
+ * <= 64 streams per scenario (else FIKIT_E_ARG in the status and that
+ * scenario's out[s] is left unwritten; singleton streams are the POOL model:
+ * use fikit_simulate_batch).  One warp per scenario. */
 int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
                                 const uint64_t* hp_gap, const uint32_t* lp_row, const uint64_t* lp_dur,
                                 const uint8_t* lp_level, const uint32_t* lp_stream, const uint64_t* lp_think,

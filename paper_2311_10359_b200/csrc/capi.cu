@@ -73,16 +73,38 @@ void fikit_note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_or
 
 namespace {
 
-int g_num_sms = 0;
+// Per-device caches of immutable device / kernel properties (SM count, occupancy, the
+// k_measure shared-memory attribute).  Every entry is computed idempotently from the current
+// device and published with a relaxed atomic store, so concurrent first calls only repeat the
+// same query and a second device gets its own entry (no per-process "first device" state).
+constexpr int kMaxDevices = 64;
+enum : int { kPropSms, kPropWaveReg, kPropWaveSmem, kPropWaveStream, kPropMeasureAttr, kNumProps };
+std::atomic<int> g_prop[kMaxDevices][kNumProps];  // 0 = not computed yet
+
+int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  return dev;
+}
+
+template <class F>
+int dev_prop(int which, F compute) {
+  const int dev = cur_device();
+  if (dev >= kMaxDevices) return compute(dev);
+  int v = g_prop[dev][which].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = compute(dev);
+    if (v > 0) g_prop[dev][which].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
+  return dev_prop(kPropSms, [](int dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    return n;
+  });
 }
 
 inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
@@ -262,13 +284,15 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   // hot set of every task bucket (blocks 0..kBuckets-1) and the global one (block kBuckets)
   k_hot_select<<<kBuckets + 1, 1024, 0, s>>>(w.st(), w.samp_cnt(), w.row_tuple(), cap, w.hot(), w.hot_n());
   if (int r = launched()) return r;
-  static bool attr_set = false;
-  size_t smem = measure_smem_bytes();
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(k_measure, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return FIKIT_E_CUDA;
-    attr_set = true;
-  }
+  const size_t smem = measure_smem_bytes();
+  // the dynamic shared-memory opt-in is a per-device function attribute
+  if (dev_prop(kPropMeasureAttr, [&](int) {
+        return cudaFuncSetAttribute(k_measure, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                       cudaSuccess
+                   ? 1
+                   : -1;
+      }) < 0)
+    return FIKIT_E_CUDA;
   // persistent: one CTA per SM, fewer if there are not enough 64-launch warp-tiles for all warps
   const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
   uint64_t ctas = (ntiles + measure_threads() / 32 - 1) / (measure_threads() / 32);
@@ -399,11 +423,13 @@ int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* dea
   return launched();
 }
 
-// persistent grid: blocks of one full wave of the kernel at its occupancy
-static int one_wave(const void* kernel, int threads) {
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) occ = 1;
-  return occ * num_sms();
+// persistent grid: blocks of one full wave of the kernel at its occupancy (per device)
+static int one_wave(int which, const void* kernel, int threads) {
+  return dev_prop(which, [&](int) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+    return occ * num_sms();
+  });
 }
 
 int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const uint64_t* hp_dur,
@@ -419,11 +445,8 @@ int fikit_simulate_batch(const fikit_table_t* tab, const uint32_t* hp_row, const
   if (S == 0) return FIKIT_OK;
   // pass 1: register-pool scenarios (m <= 64); pass 2: the ones it deferred (shared-memory pool).
   // Both persistent: one wave of the kernel's occupancy.
-  static int g1 = 0, g2 = 0;
-  if (!g1) {
-    g1 = one_wave(simulate_reg_kernel(false), kRegThreads);
-    g2 = one_wave(simulate_smem_kernel(false), kSimThreads);
-  }
+  const int g1 = one_wave(kPropWaveReg, simulate_reg_kernel(false), kRegThreads);
+  const int g2 = one_wave(kPropWaveSmem, simulate_smem_kernel(false), kSimThreads);
   const uint64_t n1 = ((uint64_t)S + kRegThreads / 32 - 1) / (kRegThreads / 32);
   const uint64_t n2 = ((uint64_t)S + kSimThreads / 32 - 1) / (kSimThreads / 32);
   const int b1 = (int)(n1 < (uint64_t)g1 ? n1 : (uint64_t)g1);
@@ -450,8 +473,7 @@ int fikit_simulate_stream_batch(const fikit_table_t* tab, const uint32_t* hp_row
   if (int r = reset_status(w, s)) return r;
   if (S == 0) return FIKIT_OK;
   // persistent, one wave; warps claim scenarios from a counter
-  static int g = 0;
-  if (!g) g = one_wave(simulate_stream_kernel(false), kStreamThreads);
+  const int g = one_wave(kPropWaveStream, simulate_stream_kernel(false), kStreamThreads);
   const uint64_t need = ((uint64_t)S + kStreamThreads / 32 - 1) / (kStreamThreads / 32);
   const int b = (int)(need < (uint64_t)g ? need : (uint64_t)g);
   launch_simulate_stream(b, kStreamThreads, s, *tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, lp_stream,

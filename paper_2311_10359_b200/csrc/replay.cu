@@ -167,7 +167,7 @@ __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* met
                                                  uint32_t& A, uint32_t& nch, uint32_t& CM) {
   bool ok = true;
   for (uint32_t k = lane; k < m; k += 32)
-    if ((meta[k] & kElig) && q[k] > 0xFFFFFFFFull) ok = false;  // fast path: every q < 2^32
+    if ((meta[k] & kElig) && q[k] >= 0xFFFFFFFFull) ok = false;  // fast path: every q < 2^32 - 1
   if (!__all_sync(0xffffffffu, ok) || m > 1024u) return false;
   uint32_t P = 32;
   while (P < m) P <<= 1;
@@ -215,7 +215,9 @@ __device__ __forceinline__ void chunk_min_refresh(const uint64_t* K, uint32_t A,
 // fits (one ballot over the chunk lanes), then the first fitting position inside it
 __device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint32_t CM, uint32_t nch, uint64_t R,
                                            int lane) {
-  const uint32_t Rc = R > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R;  // every q < 2^32
+  // every q <= 2^32 - 2, so q <= R iff q <= min(R, 2^32 - 2); an empty chunk's minimum
+  // 0xFFFFFFFF then never passes the chunk ballot
+  const uint32_t Rc = R >= 0xFFFFFFFFull ? 0xFFFFFFFEu : (uint32_t)R;
   const uint32_t cb = __ballot_sync(0xffffffffu, (uint32_t)lane < nch && CM <= Rc);
   if (!cb) return -1;
   const uint32_t c = __ffs(cb) - 1;
@@ -892,7 +894,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
     const uint64_t off = c.lp_off;
     // streams: maximal runs of equal consecutive ids (R29); levels validated on the way
     uint32_t ns = 0;
-    bool ok = m <= kPoolMax;
+    const bool too_big = m > kPoolMax;
+    bool ok = !too_big;
     for (uint32_t b = 0; b < m && ok; b += 32) {
       const uint32_t k = b + lane;
       bool f = false;
@@ -910,8 +913,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
       if (f && rank < kMaxStreams) s_start[w][rank] = k;
       ns += __popc(mask);
     }
-    if (!ok || ns > kMaxStreams) {
-      if (ok && lane == 0) atomicOr(&st->flags, kStatusArg);  // > 64 streams or m > 1024
+    if (too_big || !ok || ns > kMaxStreams) {  // (an invalid level is flagged as E_RECORD above)
+      if ((too_big || ns > kMaxStreams) && lane == 0) atomicOr(&st->flags, kStatusArg);  // m > 1024 or > 64 streams
       continue;
     }
     // stage q and level | eligibility of the window (R16); gate lower bound (R32): the minimum q

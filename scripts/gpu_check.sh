@@ -6,7 +6,7 @@ cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
 if [ -z "$NOTEST" ]; then
-  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+  timeout 1500 python -m pytest tests -m gpu -q --durations=15 2>&1 | tail -40 > gpurun_out/pytest_gpu.log
   cat gpurun_out/pytest_gpu.log
 fi
 timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err

@@ -533,63 +533,6 @@ def test_zero_durations_and_zero_threshold(fk, orc, zero_frac):
         assert ref["results"]["n_fills"].sum() > 0
 
 
-def test_zipf_full_size_sampled_rows(fk, orc):
-    """configs[3] at its full size (100M launches, 8,192 rows) in the launch configuration bench.py
-    times.  Whole-table properties that hold at any size (every launch counted once, every
-    same-run neighbour pair one gap, the u64 sums of all K and G, bins summing to counts), and
-    five rows -- the hottest, four of decreasing heat -- recomputed one by one on the host from
-    the records that carry their identity (K, G, count, sum, min, max, 32 bins each, bit for
-    bit), with their kernel IDs from the oracle's hash."""
-    import os
-
-    cfg = F.zipf_trace(threads=min(16, os.cpu_count() or 8))
-    rec = cfg.trace.records
-    N = rec.shape[0]
-    assert N == 100_000_000
-    p = run_measure(fk, cfg.trace, capacity=8192, want_rows=True)
-    st = p.check()
-    tab = p.table.to_numpy()
-    K = tab["kernel_id"].shape[0]
-    assert st["n_rows_needed"] == K <= 8192 and st["schedule"] == 1
-    start, end = rec["start_ns"], rec["end_ns"]
-    same = (rec["task_id"][1:] == rec["task_id"][:-1]) & (rec["run_id"][1:] == rec["run_id"][:-1])
-    d = end - start
-    g = np.where(start[1:] >= end[:-1], start[1:] - end[:-1], np.uint64(0))[same]
-    assert int(tab["dur_cnt"].sum()) == N and int(tab["gap_cnt"].sum()) == int(same.sum())
-    u64sum = lambda a: int(np.sum(a, dtype=np.uint64))
-    assert u64sum(tab["dur_sum"]) == u64sum(d) and u64sum(tab["gap_sum"]) == u64sum(g)
-    assert np.array_equal(tab["dur_hist"].sum(1, dtype=np.uint64), tab["dur_cnt"])
-    assert np.array_equal(tab["gap_hist"].sum(1, dtype=np.uint64), tab["gap_cnt"])
-    assert tab["dur_min"].min() == d.min() and tab["dur_max"].max() == d.max()
-    rows = p.rows()
-    assert rows.max() < K
-    gap_of = np.zeros(N, np.uint64)
-    has_gap = np.zeros(N, bool)
-    gap_of[:-1][same] = g
-    has_gap[:-1] = same
-    order = np.argsort(-tab["dur_cnt"].astype(np.int64), kind="stable")
-    ident = ["name_id", "sig_id", "grid_x", "grid_y", "grid_z", "block_x", "block_y", "block_z", "task_id"]
-    pow2 = np.uint64(1) << np.arange(31, dtype=np.uint64)  # bin(v) = min(31, bit_length(v)), R9
-    bins = lambda v: np.searchsorted(pow2, v, side="right")
-    for r in order[[0, 10, 100, 1000, K - 1]]:
-        sel = rows == r
-        one = rec[np.flatnonzero(sel)[0]]
-        same_id = np.ones(N, bool)
-        for f in ident:
-            same_id &= rec[f] == one[f]
-        assert np.array_equal(sel, same_id), f"row {r}: launches of one identity split or merged"
-        nm, sg = cfg.trace.names.get(int(one["name_id"])), cfg.trace.sigs.get(int(one["sig_id"]))
-        kid = orc.kernel_id(nm, sg, (int(one["grid_x"]), int(one["grid_y"]), int(one["grid_z"])),
-                            (int(one["block_x"]), int(one["block_y"]), int(one["block_z"])))
-        assert int(tab["kernel_id"][r]) == kid and int(tab["task_id"][r]) == int(one["task_id"])
-        for name, v in (("dur", d[sel]), ("gap", gap_of[sel & has_gap])):
-            assert int(tab[name + "_cnt"][r]) == v.shape[0], (r, name)
-            assert int(tab[name + "_sum"][r]) == u64sum(v), (r, name)
-            if v.shape[0]:
-                assert int(tab[name + "_min"][r]) == int(v.min()) and int(tab[name + "_max"][r]) == int(v.max())
-            assert np.array_equal(tab[name + "_hist"][r], np.bincount(bins(v), minlength=32)), (r, name)
-
-
 def test_sweep_full_size_sampled(fk, orc):
     """configs[4] at its full size (1M scenarios, m = 8..1024, gap scales 1/4..32) as bench.py
     runs it; 1,500 sampled scenarios replayed one by one by the oracle (results and schedule)"""
