@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
     ap.add_argument("--workload", default="zipf",
-                    choices=["zipf", "resnet", "bert_vgg", "sweep", "stream", "preempt", "ratio"])
+                    choices=["zipf", "z64k", "resnet", "bert_vgg", "sweep", "stream", "preempt", "ratio"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
     ap.add_argument("--predictor", default=None,
@@ -67,17 +67,21 @@ def make_workload(args, rank, world):
     import fikit_synth as F
     from paper_2311_10359_b200.dist import scenario_shard, shard_range
 
-    if args.workload == "zipf":
+    if args.workload in ("zipf", "z64k"):
+        # z64k: SURVEY §8d's stress variant of configs[3] (2,048-kernel vocabularies: up to 65,536 rows)
+        vocab = 2048 if args.workload == "z64k" else 256
         runs = 390_625 if args.records is None else max(1, args.records // 256)
         N = runs * 256
         lo, hi = shard_range(N, rank, world)
-        cfg = F.zipf_trace(n_runs=runs, rec_lo=lo, rec_hi=min(N, hi + 1), threads=min(16, os.cpu_count() or 8))
+        cfg = F.zipf_trace(n_runs=runs, rec_lo=lo, rec_hi=min(N, hi + 1), threads=min(16, os.cpu_count() or 8),
+                           vocab_per_task=vocab)
         recs = cfg.trace.records
         halo = recs[hi - lo] if hi < N else None
         recs = recs[: hi - lo]
         replay = F.zipf_replay(cfg, S=args.scenarios)
-        cap = 8192
-        desc = f"zipf-{N // 1_000_000}M (configs[3]) + replay-{args.scenarios // 1000}k"
+        cap = 32 * vocab
+        desc = (f"zipf-{N / 1e6:g}M (configs[3]" + (", Z64k stress: 2048-kernel vocabularies" if vocab > 256 else "")
+                + f") + replay-{args.scenarios / 1000:g}k")
     elif args.workload in ("stream", "preempt"):  # LP kernel streams (+ Case A)
         cfg, sr = F.bert_vgg_stream(S=args.scenarios)
         N = cfg.trace.records.shape[0]
