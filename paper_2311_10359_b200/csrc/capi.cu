@@ -14,24 +14,15 @@ __global__ void k_zero(ZeroList, fikit_status_t*);
 __global__ void k_strtab_hash(fikit_strtab_t, uint64_t*, fikit_strtab_t, uint64_t*, fikit_status_t*);
 __global__ void k_identify(const uint4*, uint64_t, const uint64_t*, const uint64_t*, uint32_t, uint32_t, uint64_t*,
                            fikit_status_t*);
-__global__ void k_sample(const uint4*, uint64_t, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint32_t,
-                         uint32_t, IndexEntry*, uint32_t, fikit_status_t*, fikit_table_t, Tuple*, uint32_t*);
-__global__ void k_hot_select(const fikit_status_t*, const uint32_t*, const Tuple*, uint32_t, Tuple*, uint32_t*);
-__global__ void k_tile_bucket(const fikit_record_t*, uint32_t, const uint32_t*, uint8_t*, uint32_t*);
-__global__ void k_tile_plan(uint32_t*, uint32_t, uint32_t, uint32_t, const uint32_t*, uint32_t*, uint32_t*,
-                            uint32_t*, uint32_t*, fikit_status_t*);
-__global__ void k_tile_scatter(const uint8_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*);
+__global__ void k_prep(PrepArgs);
+__global__ void k_plan(PlanArgs);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
-                          uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, fikit_table_t,
-                          Tuple*, const Tuple*, const uint32_t*, uint32_t*, const uint32_t*, uint32_t*,
-                          const uint32_t*, const uint32_t*, uint32_t*);
+                          uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, RawTab, Tuple*,
+                          const Tuple*, const uint32_t*, uint32_t*, uint32_t*, const uint32_t*, const uint32_t*,
+                          const uint32_t*, const uint32_t*, uint32_t, uint32_t*);
 size_t measure_smem_bytes();
 int measure_threads();
-struct FinRow;
-__global__ void k_fin_prep(const fikit_status_t*, fikit_table_t, FinRow*, uint32_t*, uint32_t*);
-__global__ void k_fin_chunksort(const fikit_table_t, const uint32_t*, uint64_t*, uint32_t*);
-__global__ void k_fin_rank(const fikit_table_t, const uint32_t*, const uint64_t*, const uint32_t*, uint32_t*);
-__global__ void k_fin_scatter(fikit_table_t, const FinRow*, const uint32_t*, const uint32_t*);
+__global__ void k_finalize(const fikit_status_t*, const RawRow*, uint32_t, fikit_table_t, uint32_t*, uint32_t*);
 __global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
 __global__ void k_means(fikit_table_t);
 __global__ void k_predict(fikit_table_t, uint32_t, uint32_t);
@@ -123,7 +114,6 @@ struct Ws {
   unsigned char* base;
   WsLayout L;
   fikit_status_t* st() const { return reinterpret_cast<fikit_status_t*>(base + L.status); }
-  uint32_t* misc() const { return reinterpret_cast<uint32_t*>(base + L.misc); }
   uint64_t* name_hash() const { return reinterpret_cast<uint64_t*>(base + L.name_hash); }
   uint64_t* sig_hash() const { return reinterpret_cast<uint64_t*>(base + L.sig_hash); }
   IndexEntry* index() const { return reinterpret_cast<IndexEntry*>(base + L.index); }
@@ -132,18 +122,20 @@ struct Ws {
   uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
   uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }  // header [kHotHdr]
   Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 4ull * kHotHdr); }  // [kBuckets + 1][kHotMax]
-  uint32_t* cur() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }  // [kSchedWords]
-  uint32_t* bend() const { return cur() + kSchedWords; }                          // [kSchedWords]
-  uint32_t* act() const { return bend() + kSchedWords; }                          // [kSchedWords]
-  uint32_t* first() const { return act() + kSchedWords; }                         // [kMaxCTAs]
-  uint32_t* blkoff() const {  // [kSortBlocks][kBuckets]
-    return reinterpret_cast<uint32_t*>(
-        base + align256(L.tiles + 12ull * kSchedWords + 4ull * kMaxCTAs));
+  RawRow* raw() const { return reinterpret_cast<RawRow*>(base + L.raw); }
+  uint32_t* rank() const { return reinterpret_cast<uint32_t*>(base + L.rank); }  // [cap], then fin_done[]
+  uint32_t* cur() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }   // [kSchedWords]
+  uint32_t* act() const { return cur() + kSchedWords; }                           // [kSchedWords]
+  uint32_t* bstart() const { return act() + kSchedWords; }                        // [kSchedWords]
+  uint32_t* btot() const { return bstart() + kSchedWords; }                       // [kSchedWords]
+  uint32_t* first() const { return btot() + kSchedWords; }                        // [kMaxCTAs]
+  uint32_t* blkcnt() const {  // [kSortBlocks][kBuckets]
+    return reinterpret_cast<uint32_t*>(base + L.tiles + align256(16ull * kSchedWords + 4ull * kMaxCTAs));
   }
-  uint8_t* tile_bucket() const {
-    return reinterpret_cast<uint8_t*>(blkoff()) + align256(4ull * kSortBlocks * kBuckets);
+  uint8_t* grp_bucket() const {
+    return reinterpret_cast<uint8_t*>(blkcnt()) + align256(4ull * kSortBlocks * kBuckets);
   }
-  uint32_t* order() const { return reinterpret_cast<uint32_t*>(tile_bucket() + align256(L.ntiles)); }
+  uint32_t* order() const { return reinterpret_cast<uint32_t*>(grp_bucket() + align256(L.ngroups)); }
   unsigned char* fin() const { return base + L.fin; }
 };
 
@@ -249,41 +241,81 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
       !table_ok(tab))
     return FIKIT_E_ARG;
   if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w, n)) return r;
-  const fikit_table_t t = *tab;
-  const uint32_t cap = t.capacity;
-  // reset the status and zero the table (an all-zero row is the identity of every statistic),
-  // the indexes and the sample counts: one launch
+  const uint32_t cap = tab->capacity;
+  // 1. reset the status; zero the workspace's measured rows (an all-zero row is the identity of
+  //    every statistic), the indexes, the sample counts, the hot-set header, the schedule's
+  //    counters and finalize's counters: one launch
   ZeroList z{};
   auto add = [&](void* p, uint64_t bytes) {
     z.p[z.k] = p;
     z.n[z.k++] = bytes;
   };
-  add(t.kernel_id, 8ull * cap);
-  add(t.task_id, 4ull * cap);
-  add(t.sums, 32ull * cap);
-  add(t.hist, 256ull * cap);
-  add(t.ext, 32ull * cap);
-  add(t.mean, 16ull * cap);
-  add(t.n_rows, 4);
+  add(w.raw(), sizeof(RawRow) * (size_t)cap);
   add(w.index(), sizeof(IndexEntry) * (size_t)w.L.slots);
   add(w.tindex(), sizeof(Tuple) * (size_t)w.L.tslots);
   add(w.samp_cnt(), 4ull * cap);
   add(w.hot_n(), 4ull * kHotHdr);
+  add(w.cur(), 16ull * kSchedWords);  // cur, act, bstart, btot
+  add(w.rank(), 4ull * cap + 4ull * ((cap + kFinRows - 1) / kFinRows));
   k_zero<<<2 * num_sms(), 256, 0, s>>>(z, w.st());
   if (int r = launched()) return r;
-  if (int r = hash_strtabs(w, names, sigs, s)) return r;
-  if (n == 0) return FIKIT_OK;
-  // sample ~64k launches (all of them for small traces) to choose the hot rows
+  if (n == 0) return hash_strtabs(w, names, sigs, s);
+  // persistent k_measure: one CTA per SM, fewer if there are not enough 64-launch warp-tiles
+  const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
+  const uint32_t ngroups = (ntiles + kGroupTiles - 1) / kGroupTiles;
+  uint64_t ctas = (ntiles + measure_threads() / 32 - 1) / (measure_threads() / 32);
+  unsigned grid = (unsigned)(ctas < (uint64_t)num_sms() ? ctas : (uint64_t)num_sms());
+  if (grid > kMaxCTAs) grid = kMaxCTAs;
+  // 2. k_prep: string hashes | a ~64k-launch sample -> rows + counts | tile-group buckets
+  PrepArgs pa{};
+  pa.recs = reinterpret_cast<const uint4*>(recs);
+  pa.recs_t = recs;
+  pa.n = n;
   const uint64_t target = 65536;
-  uint64_t stride = n > target ? n / target : 1;
-  uint64_t ns = (n + stride - 1) / stride;
-  k_sample<<<grid_for(ns, 512, num_sms() * 2), 512, 0, s>>>(
-      reinterpret_cast<const uint4*>(recs), n, stride, ns, w.name_hash(), w.sig_hash(), names.count, sigs.count,
-      w.index(), w.L.slots, w.st(), t, w.row_tuple(), w.samp_cnt());
+  pa.stride = n > target ? n / target : 1;
+  pa.n_samples = (n + pa.stride - 1) / pa.stride;
+  pa.names = names;
+  pa.sigs = sigs;
+  pa.name_hash = w.name_hash();
+  pa.sig_hash = w.sig_hash();
+  pa.idx = w.index();
+  pa.slots = w.L.slots;
+  pa.cap = cap;
+  pa.st = w.st();
+  pa.raw = w.raw();
+  pa.row_tuple = w.row_tuple();
+  pa.samp_cnt = w.samp_cnt();
+  pa.grp_bucket = w.grp_bucket();
+  pa.blkcnt = w.blkcnt();
+  pa.ngroups = ngroups;
+  uint32_t sb = (ngroups + 2047) / 2048;  // group blocks: ~2k groups (512k launches) each
+  sb = sb < 1 ? 1 : sb > kSortBlocks ? kSortBlocks : sb;
+  pa.sb = sb;
+  const uint64_t nstr = (uint64_t)names.count + sigs.count;
+  pa.nb_hash = (uint32_t)((nstr + kPrepThreads / 32 - 1) / (kPrepThreads / 32));
+  pa.nb_samp = grid_for(pa.n_samples, 2 * kPrepThreads, num_sms());
+  k_prep<<<pa.nb_hash + pa.nb_samp + pa.sb, kPrepThreads, 0, s>>>(pa);
   if (int r = launched()) return r;
-  // hot set of every task bucket (blocks 0..kBuckets-1) and the global one (block kBuckets)
-  k_hot_select<<<kBuckets + 1, 1024, 0, s>>>(w.st(), w.samp_cnt(), w.row_tuple(), cap, w.hot(), w.hot_n());
+  // 3. k_plan: hot sets + schedule mode | the groups' counting-sort scatter, bucket ranges, first buckets
+  PlanArgs pl{};
+  pl.st = w.st();
+  pl.samp_cnt = w.samp_cnt();
+  pl.row_tuple = w.row_tuple();
+  pl.cap = cap;
+  pl.hot_all = w.hot();
+  pl.hot_hdr = w.hot_n();
+  pl.grp_bucket = w.grp_bucket();
+  pl.blkcnt = w.blkcnt();
+  pl.ngroups = ngroups;
+  pl.sb = sb;
+  pl.grid_measure = grid;
+  pl.order = w.order();
+  pl.bstart = w.bstart();
+  pl.btot = w.btot();
+  pl.first = w.first();
+  k_plan<<<kBuckets + 1 + sb, 1024, 0, s>>>(pl);
   if (int r = launched()) return r;
+  // 4. the streaming kernel
   const size_t smem = measure_smem_bytes();
   // the dynamic shared-memory opt-in is a per-device function attribute
   if (dev_prop(kPropMeasureAttr, [&](int) {
@@ -293,29 +325,11 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
                    : -1;
       }) < 0)
     return FIKIT_E_CUDA;
-  // persistent: one CTA per SM, fewer if there are not enough 64-launch warp-tiles for all warps
-  const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
-  uint64_t ctas = (ntiles + measure_threads() / 32 - 1) / (measure_threads() / 32);
-  unsigned grid = (unsigned)(ctas < (uint64_t)num_sms() ? ctas : (uint64_t)num_sms());
-  if (grid > kMaxCTAs) grid = kMaxCTAs;
-  // task-partitioned schedule: bucket every warp-tile by its first launch's task, stably
-  // counting-sort the tiles by bucket (sb blocks, each a contiguous chunk of tiles), and plan
-  // which CTAs sweep which bucket's sorted range
-  uint32_t sb = (ntiles + 4095) / 4096;
-  sb = sb < 1 ? 1 : sb > kSortBlocks ? kSortBlocks : sb;
-  if (sb > 2u * num_sms()) sb = 2u * num_sms();
-  k_tile_bucket<<<sb, 1024, 0, s>>>(recs, ntiles, w.hot_n(), w.tile_bucket(), w.blkoff());
-  if (int r = launched()) return r;
-  k_tile_plan<<<1, 1024, 0, s>>>(w.blkoff(), sb, ntiles, grid, w.hot_n(), w.cur(), w.bend(), w.act(), w.first(),
-                                 w.st());
-  if (int r = launched()) return r;
-  k_tile_scatter<<<sb, 1024, 0, s>>>(w.tile_bucket(), ntiles, w.hot_n(), w.blkoff(), w.order());
-  if (int r = launched()) return r;
   if (ev0 && cudaEventRecord(ev0, s) != cudaSuccess) return FIKIT_E_CUDA;
-  k_measure<<<grid, measure_threads(), smem, s>>>(recs, n, halo, w.name_hash(), w.sig_hash(), names.count,
-                                                  sigs.count, w.index(), w.L.slots, w.tindex(), w.L.tslots, w.st(),
-                                                  t, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.bend(),
-                                                  w.act(), w.first(), w.order(), out_row);
+  k_measure<<<grid, measure_threads(), smem, s>>>(
+      recs, n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, w.index(), w.L.slots, w.tindex(),
+      w.L.tslots, w.st(), RawTab{w.raw(), cap}, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.act(), w.bstart(),
+      w.btot(), w.first(), w.order(), ntiles, out_row);
   if (int r = launched()) return r;
   if (ev1 && cudaEventRecord(ev1, s) != cudaSuccess) return FIKIT_E_CUDA;
   return FIKIT_OK;
@@ -339,26 +353,15 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   cudaStream_t s = (cudaStream_t)stream;
   if (!table_ok(tab) || (n && !out_row) || n >= (1ull << 32)) return FIKIT_E_ARG;
   Ws w;
-  if (int r = get_ws(ws, ws_bytes, tab->capacity, 0, 0, &w)) return r;
-  const fikit_table_t t = *tab;
-  const uint32_t cap = t.capacity;
-  FinRow* fin = reinterpret_cast<FinRow*>(w.fin());
-  uint32_t* rank = reinterpret_cast<uint32_t*>(w.fin() + 336ull * cap);
-  uint64_t* skid = reinterpret_cast<uint64_t*>(w.fin() + ((340ull * cap + 7) & ~7ull));
-  uint32_t* stask = reinterpret_cast<uint32_t*>(skid + cap);
-  uint32_t* kptr = w.misc() + kMiscNRec;
-  unsigned g = (cap + 255) / 256;
-  const unsigned gw = (cap + 7) / 8;  // 8 rows (warps) per 256-thread block
-  k_fin_prep<<<gw, 256, 0, s>>>(w.st(), t, fin, kptr, rank);  // (also zeroes rank[0, cap))
-  if (int r = launched()) return r;
-  k_fin_chunksort<<<(cap + 255) / 256, 256, 0, s>>>(t, kptr, skid, stask);
-  if (int r = launched()) return r;
-  k_fin_rank<<<dim3(g, (cap + 2047) / 2048), 256, 0, s>>>(t, kptr, skid, stask, rank);
-  if (int r = launched()) return r;
-  k_fin_scatter<<<gw, 256, 0, s>>>(t, fin, rank, kptr);
+  if (int r = get_ws(ws, ws_bytes, tab->capacity, 0, 0, &w)) return r;  // (the capacity-sized regions)
+  const uint32_t cap = tab->capacity;
+  uint32_t* rank = w.rank();
+  uint32_t* done = rank + cap;
+  k_finalize<<<dim3((cap + kFinRows - 1) / kFinRows, (cap + kFinGroup - 1) / kFinGroup), kFinRows, 0, s>>>(
+      w.st(), w.raw(), cap, *tab, rank, done);
   if (int r = launched()) return r;
   if (out_row && n) {
-    k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, kptr);
+    k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, tab->n_rows);
     if (int r = launched()) return r;
   }
   return FIKIT_OK;

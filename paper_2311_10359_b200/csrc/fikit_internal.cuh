@@ -23,10 +23,29 @@ struct alignas(16) Tuple {  // a launch identity as raw record words (the hot di
   uint32_t row;
 };
 
+// A measured row in the workspace (fikit_measure accumulates here; fikit_table_finalize writes
+// the caller's table from it in canonical order).  One contiguous 336-B row: the cold path's
+// reductions of one launch touch one row.
+struct RawRow {
+  uint64_t kid;
+  uint32_t task, pad;
+  uint64_t sums[4];  // [1] duration sum, [3] gap sum (mod 2^64); [0], [2] unused (counts = hist totals)
+  uint64_t ext[4];   // duration max, ~min, gap max, ~min (an all-zero row is the identity)
+  uint32_t hist[64];           // duration bins 0..31, gap bins 32..63
+};
+static_assert(sizeof(RawRow) == 336, "RawRow");
+
+// the workspace's measured rows as k_measure sees them
+struct RawTab {
+  RawRow* rows;
+  uint32_t capacity;
+};
+
 struct WsLayout {
-  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, fin, tiles, total;
+  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, raw, rank, fin, tiles, total;
   uint32_t slots, tslots;
-  uint64_t ntiles;  // warp-tiles of 32 launches the workspace can schedule
+  uint64_t ntiles;   // warp-tiles of 64 launches the workspace can schedule
+  uint64_t ngroups;  // tile groups (kGroupTiles tiles) of the task-partitioned schedule
 };
 
 constexpr uint32_t kHotMax = 400;  // hot rows cached in shared memory per CTA (measure kernel; u32 bins)
@@ -41,7 +60,8 @@ struct ZeroList {
 };
 constexpr uint32_t kBuckets = 64;
 constexpr uint32_t kMaxCTAs = 1024;
-constexpr uint32_t kSortBlocks = 160;  // blocks of the tile counting sort (each a contiguous chunk)
+constexpr uint32_t kSortBlocks = 160;  // blocks of the tile-group counting sort (each a contiguous chunk)
+constexpr uint32_t kGroupTiles = 4;    // warp-tiles per schedule group (256 launches: one sector read each)
 constexpr uint32_t kGlobalSet = kBuckets;  // hot-set index of the global (all-task) hot set
 // hot-set header words (u32): hot_n[kBuckets + 1], then the sample coverage counters
 constexpr uint32_t kCovTask = kBuckets + 1;  // samples whose row is in its task bucket's hot set
@@ -49,18 +69,22 @@ constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the gl
 constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
+constexpr uint32_t kFinRows = 256;      // fikit_table_finalize: rows per block (x) ...
+constexpr uint32_t kFinGroup = 1024;    // ... keys per sorted group (y)
 constexpr int kRegThreads = 512;  // k_simulate_reg block (16 warps, one scenario each)
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
 constexpr int kStreamThreads = 128;  // k_simulate_stream block (4 warps, staged windows)
 // u32 words of the 256-B status region past fikit_status_t, zeroed with it: replay work counters
 constexpr uint32_t kSchedWord1 = 32, kSchedWord2 = 33, kSchedWord3 = 34;
-// Dynamic tile schedule (k_tile_plan -> k_measure): bucket b's tiles are the sorted positions
-// [cur[b], bend[b]); warps claim them one at a time with an atomic on cur[b].  first[c] is the
-// bucket CTA c starts on (kNoBucket: none); a CTA whose bucket runs dry moves to the bucket
-// with the most unclaimed tiles among those nobody works on or with > 128 left (act[b]: CTAs
-// working on b).  Bucket kGlobalSet (address-order mode) is [0, ntiles).
+// Dynamic tile schedule (k_plan -> k_measure).  Task mode: tile groups are stably counting-sorted
+// by bucket into order[]; bucket b owns the tile positions [4 bstart[b], 4 (bstart[b] + btot[b]))
+// (position p = tile 4 order[p / 4] + p % 4; positions past the last tile are skipped).
+// Address mode: bucket kGlobalSet = tiles [0, ntiles) in order.  cur[b] counts the positions of
+// b claimed so far (zeroed by k_zero); warps claim kClaim at a time.  first[c] is the bucket CTA
+// c starts on (kNoBucket: none); a CTA whose bucket runs dry moves to the bucket with the most
+// unclaimed tiles among those nobody works on or with > 128 left (act[b]: CTAs working on b).
 constexpr uint32_t kNoBucket = 0xFFFFFFFFu;
-constexpr uint32_t kSchedWords = kBuckets + 8;  // cur[] and bend[] length
+constexpr uint32_t kSchedWords = kBuckets + 8;  // cur[], act[], bstart[], btot[] length
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -70,6 +94,10 @@ inline uint32_t index_slots(uint32_t cap) {
   return s;
 }
 
+// Regions are ordered by what sizes them, so that every call finds a region at the same offset
+// from the arguments it has: capacity-sized regions first (finalize knows only the table), then
+// the string hashes (resolve knows the table and the string tables), then the tile schedule
+// (sized by the measure call's record count), then the multi-GPU union scratch.
 inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint64_t n_records) {
   WsLayout L;
   size_t o = 0;
@@ -77,10 +105,6 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o += 256;
   L.misc = o;
   o += 256;
-  L.name_hash = o;
-  o = align256(o + 8ull * (n_names ? n_names : 1));
-  L.sig_hash = o;
-  o = align256(o + 8ull * (n_sigs ? n_sigs : 1));
   L.slots = index_slots(cap);
   L.index = o;
   o = align256(o + sizeof(IndexEntry) * (size_t)L.slots);
@@ -93,19 +117,67 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o = align256(o + 4ull * cap);
   L.hot = o;  // header[kHotHdr] (u32), then hot[kBuckets + 1][kHotMax] (Tuple)
   o = align256(o + 4ull * kHotHdr + sizeof(Tuple) * (size_t)kHotMax * (kBuckets + 1));
-  L.fin = o;  // FinRow[cap] (336 B), rank[cap], sorted chunk keys: kid[cap] (8-aligned), task[cap]
-  o = align256(o + 352ull * cap + 1024);
-  // tiles: cur[kSchedWords], bend[kSchedWords], act[kSchedWords], first[kMaxCTAs] (u32),
-  //        blkoff[kSortBlocks][kBuckets], tile_bucket[ntiles] (u8), order[ntiles] (u32)
+  L.raw = o;  // RawRow[cap]
+  o = align256(o + sizeof(RawRow) * (size_t)cap);
+  L.rank = o;  // rank[cap] (u32), then fin_done[ceil(cap / kFinRows)] (u32)
+  o = align256(o + 4ull * cap + 4ull * ((cap + kFinRows - 1) / kFinRows));
+  L.name_hash = o;
+  o = align256(o + 8ull * (n_names ? n_names : 1));
+  L.sig_hash = o;
+  o = align256(o + 8ull * (n_sigs ? n_sigs : 1));
+  // tiles: cur[kSchedWords], act[kSchedWords], bstart[kSchedWords], btot[kSchedWords],
+  //        first[kMaxCTAs] (u32), blkcnt[kSortBlocks][kBuckets] (u32), grp_bucket[ngroups] (u8),
+  //        order[ngroups] (u32)
   L.ntiles = (n_records + kTileLaunches - 1) / kTileLaunches;
+  L.ngroups = (L.ntiles + kGroupTiles - 1) / kGroupTiles;
   L.tiles = o;
-  o = align256(o + 12ull * kSchedWords + 4ull * kMaxCTAs);
+  o = align256(o + 16ull * kSchedWords + 4ull * kMaxCTAs);
   o = align256(o + 4ull * kSortBlocks * kBuckets);
-  o = align256(o + L.ntiles);
-  o = align256(o + 4ull * L.ntiles);
+  o = align256(o + L.ngroups);
+  o = align256(o + 4ull * L.ngroups);
+  L.fin = o;  // last: scratch of the multi-GPU dictionary union (which also uses the caller's `extra` bytes)
+  o = align256(o + 1024);
   L.total = o;
   return L;
 }
+
+// arguments of the measure call's preamble kernels (measure.cu)
+struct PrepArgs {
+  const uint4* recs;
+  const fikit_record_t* recs_t;
+  uint64_t n, stride, n_samples;
+  fikit_strtab_t names, sigs;
+  uint64_t* name_hash;
+  uint64_t* sig_hash;
+  IndexEntry* idx;
+  uint32_t slots, cap;
+  fikit_status_t* st;
+  RawRow* raw;
+  Tuple* row_tuple;
+  uint32_t* samp_cnt;
+  uint8_t* grp_bucket;
+  uint32_t* blkcnt;
+  uint32_t ngroups, sb;     // tile groups, group-role blocks
+  uint32_t nb_hash, nb_samp;  // block ranges: [0, nb_hash) hash, then nb_samp sample blocks, then sb group blocks
+};
+constexpr int kPrepThreads = 256;
+
+struct PlanArgs {
+  const fikit_status_t* st;
+  const uint32_t* samp_cnt;
+  const Tuple* row_tuple;
+  uint32_t cap;
+  Tuple* hot_all;
+  uint32_t* hot_hdr;
+  const uint8_t* grp_bucket;
+  const uint32_t* blkcnt;
+  uint32_t ngroups, sb;
+  uint32_t grid_measure;  // k_measure CTAs (first-bucket assignment)
+  uint32_t* order;
+  uint32_t* bstart;
+  uint32_t* btot;
+  uint32_t* first;
+};
 
 // task bucket: xor-fold of the task id's 6-bit digits -- one-to-one for ids < 64 (a node's
 // tasks are usually numbered densely), and multiples of 64 still spread
@@ -221,11 +293,11 @@ __device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
 
 // KID index: find-or-insert (task, kid); returns the row (possibly >= capacity: then
 // nothing is materialised and E_CAPACITY is flagged) or FIKIT_NO_ROW if the index is
-// full.  The inserting thread records the row's key and a representative raw tuple.
+// full.  The inserting thread records the row's key (in the workspace's raw row) and a
+// representative raw tuple.
 __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32_t slots, uint64_t kid, uint32_t task,
-                                                         const uint32_t* tuple_w, fikit_status_t* st,
-                                                         uint64_t* tab_kid, uint32_t* tab_task, Tuple* row_tuple,
-                                                         uint32_t cap) {
+                                                         const uint32_t* tuple_w, fikit_status_t* st, RawRow* raw,
+                                                         Tuple* row_tuple, uint32_t cap) {
   uint32_t h = key_hash(kid, task) & (slots - 1);
   for (uint32_t probe = 0; probe < slots; probe++) {
     IndexEntry* e = &idx[h];
@@ -237,9 +309,9 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
         e->kid = kid;
         e->task = task;
         uint32_t row = (uint32_t)atomicAdd((unsigned long long*)&st->n_rows_needed, 1ull);
-        if (row < cap) {
-          tab_kid[row] = kid;
-          tab_task[row] = task;
+        if (row < cap) {  // (its statistics were zeroed by k_zero)
+          raw[row].kid = kid;
+          raw[row].task = task;
           Tuple t;
 #pragma unroll
           for (int j = 0; j < 7; j++) t.w[j] = tuple_w[j];

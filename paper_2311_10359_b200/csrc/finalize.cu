@@ -5,15 +5,6 @@
 
 namespace fikit {
 
-struct FinRow {  // scratch copy of one measured row
-  unsigned long long kid;
-  uint32_t task, pad;
-  unsigned long long sums[4];
-  unsigned long long ext[4];
-  uint32_t hist[64];
-};
-static_assert(sizeof(FinRow) == 336, "FinRow");
-
 __device__ __forceinline__ bool key_less(uint32_t ta, uint64_t ka, uint32_t tb, uint64_t kb) {
   return ta < tb || (ta == tb && ka < kb);
 }
@@ -25,99 +16,56 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
   return q + ((2 * r >= cnt) ? 1 : 0);
 }
 
-// rows -> scratch; counts = histogram totals (SK/SG denominators)
-__global__ void k_fin_prep(const fikit_status_t* st, fikit_table_t tab, FinRow* fin, uint32_t* n_out,
-                           uint32_t* rank) {
-  // one warp per row: the 64 histogram words of a row are read coalesced
-  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, tab.capacity);
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r == 0 && lane == 0) *n_out = K;
-  if (lane == 1 && r < tab.capacity) rank[r] = 0u;  // (k_fin_rank accumulates into it)
-  if (r >= K) return;
-  FinRow& f = fin[r];
-  const uint32_t h0 = tab.hist[(size_t)r * 64 + lane], h1 = tab.hist[(size_t)r * 64 + 32 + lane];
-  f.hist[lane] = h0;
-  f.hist[32 + lane] = h1;
-  // row counts < 2^32 (a call measures < 2^32 launches)
-  const uint32_t dc = __reduce_add_sync(0xffffffffu, h0), gc = __reduce_add_sync(0xffffffffu, h1);
-  if (lane < 4) f.ext[lane] = tab.ext[(size_t)r * 4 + lane];
-  if (lane == 0) {
-    f.kid = tab.kernel_id[r];
-    f.task = tab.task_id[r];
-    f.pad = 0;
-    f.sums[0] = dc;
-    f.sums[1] = tab.sums[(size_t)r * 4 + 1];
-    f.sums[2] = gc;
-    f.sums[3] = tab.sums[(size_t)r * 4 + 3];
+// fikit_table_finalize in one launch: the canonical row of measured row r (R11) is its rank
+// among the K distinct (task, kernel ID) keys.  Block (x, y) sorts key group y (kFinGroup keys,
+// a shared-memory bitonic sort) and adds, for each of its kFinRows rows x, the number of group-y
+// keys below it (a binary search) to rank[]; the last block to finish row block x (a counter per
+// x) writes those rows into the caller's table at their ranks, with counts (histogram totals,
+// P:249) and SK_j / SG_j (R8).  Reads the workspace's measured rows, writes only the
+// caller's table: no grid-wide ordering is needed.
+__global__ void __launch_bounds__(kFinRows) k_finalize(const fikit_status_t* __restrict__ st,
+                                                       const RawRow* __restrict__ raw, uint32_t cap,
+                                                       fikit_table_t tab, uint32_t* __restrict__ rank,
+                                                       uint32_t* __restrict__ done) {
+  __shared__ uint64_t sk[kFinGroup];
+  __shared__ uint32_t stk[kFinGroup];
+  __shared__ uint32_t s_last;
+  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  const uint32_t x = blockIdx.x, y = blockIdx.y, tid = threadIdx.x;
+  if (x == 0 && y == 0 && tid == 0) *tab.n_rows = K;
+  const uint32_t r0 = x * kFinRows, g0 = y * kFinGroup;
+  if (r0 >= K || g0 >= K) return;
+  const uint32_t ny = (K + kFinGroup - 1) / kFinGroup;
+  const uint32_t m = min(kFinGroup, K - g0);
+  uint32_t P = 2;
+  while (P < m) P <<= 1;
+  for (uint32_t i = tid; i < P; i += kFinRows) {
+    const bool in = i < m;
+    sk[i] = in ? raw[g0 + i].kid : ~0ull;  // padding sorts last
+    stk[i] = in ? raw[g0 + i].task : 0xFFFFFFFFu;
   }
-}
-
-// rank of every key among the K distinct keys = its canonical row (R11): every 256-key chunk
-// of the table is sorted once (k_fin_chunksort, shared-memory bitonic sort), then a row's rank
-// is the sum over chunks of the number of keys below it (a binary search per chunk).
-constexpr uint32_t kRankChunk = 256;
-
-__global__ void __launch_bounds__(kRankChunk) k_fin_chunksort(const fikit_table_t tab, const uint32_t* n_ptr,
-                                                              uint64_t* __restrict__ skid,
-                                                              uint32_t* __restrict__ stask) {
-  __shared__ uint64_t sk[kRankChunk];
-  __shared__ uint32_t stk[kRankChunk];
-  const uint32_t K = *n_ptr, base = blockIdx.x * kRankChunk, i = threadIdx.x;
-  if (base >= K) return;
-  const bool in = base + i < K;
-  sk[i] = in ? tab.kernel_id[base + i] : ~0ull;  // padding sorts last
-  stk[i] = in ? tab.task_id[base + i] : 0xFFFFFFFFu;
   __syncthreads();
-  for (uint32_t k = 2; k <= kRankChunk; k <<= 1)
+  for (uint32_t k = 2; k <= P; k <<= 1)
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t l = i ^ j;
-      if (l > i) {
-        const bool asc = (i & k) == 0;
-        const bool gt = key_less(stk[l], sk[l], stk[i], sk[i]);  // key(i) > key(l)
-        if (gt == asc) {
-          const uint64_t tk = sk[i];
-          sk[i] = sk[l];
-          sk[l] = tk;
-          const uint32_t tt = stk[i];
-          stk[i] = stk[l];
-          stk[l] = tt;
+      for (uint32_t i = tid; i < P / 2; i += kFinRows) {
+        const uint32_t a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;
+        const bool asc = (a & k) == 0;
+        const uint64_t ka = sk[a], kb = sk[b];
+        const uint32_t ta = stk[a], tb = stk[b];
+        if (key_less(tb, kb, ta, ka) == asc) {  // out of order for this direction
+          sk[a] = kb;
+          sk[b] = ka;
+          stk[a] = tb;
+          stk[b] = ta;
         }
       }
       __syncthreads();
     }
-  if (in) {
-    skid[base + i] = sk[i];
-    stask[base + i] = stk[i];
-  }
-}
-
-// 2-D grid: blockIdx.x picks 256 rows, blockIdx.y a group of kRankGroup sorted chunks staged in
-// shared memory; each row adds the number of keys below it in those chunks (binary searches in
-// shared memory) to rank[] (zeroed by the caller).
-constexpr uint32_t kRankGroup = 8;
-
-__global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const uint32_t* n_ptr,
-                                                  const uint64_t* __restrict__ skid, const uint32_t* __restrict__ stask,
-                                                  uint32_t* __restrict__ rank) {
-  __shared__ uint64_t sk[kRankGroup * kRankChunk];
-  __shared__ uint32_t stk[kRankGroup * kRankChunk];
-  const uint32_t K = *n_ptr;
-  const uint32_t base = blockIdx.y * kRankGroup * kRankChunk;
-  if (blockIdx.x * blockDim.x >= K || base >= K) return;
-  const uint32_t m = min(kRankGroup * kRankChunk, K - base);
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    sk[i] = skid[base + i];
-    stk[i] = stask[base + i];
-  }
-  __syncthreads();
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= K) return;
-  const uint64_t mk = tab.kernel_id[r];
-  const uint32_t mt = tab.task_id[r];
-  uint32_t cnt = 0;
-  for (uint32_t c0 = 0; c0 < m; c0 += kRankChunk) {
-    uint32_t lo = c0, hi = min(c0 + kRankChunk, m);  // keys of the chunk below (mt, mk)
+  const uint32_t r = r0 + tid;
+  if (r < K) {
+    const uint64_t mk = raw[r].kid;
+    const uint32_t mt = raw[r].task;
+    uint32_t lo = 0, hi = m;  // keys of group y below (mt, mk)
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       if (key_less(stk[mid], sk[mid], mt, mk))
@@ -125,33 +73,41 @@ __global__ void __launch_bounds__(256) k_fin_rank(const fikit_table_t tab, const
       else
         hi = mid;
     }
-    cnt += lo - c0;
+    if (ny == 1)
+      rank[r] = lo;
+    else if (lo)
+      atomicAdd(rank + r, lo);
   }
-  if (cnt) atomicAdd(rank + r, cnt);
-}
-
-__global__ void k_fin_scatter(fikit_table_t tab, const FinRow* __restrict__ fin, const uint32_t* __restrict__ rank,
-                              const uint32_t* n_ptr) {
-  // one warp per row (coalesced 64-word histogram rows)
-  const uint32_t K = *n_ptr;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r == 0 && lane == 0) *tab.n_rows = K;
-  if (r >= K) return;
-  const FinRow& f = fin[r];
-  const uint32_t d = rank[r];
-  tab.hist[(size_t)d * 64 + lane] = f.hist[lane];
-  tab.hist[(size_t)d * 64 + 32 + lane] = f.hist[32 + lane];
-  if (lane < 4) {
-    tab.sums[(size_t)d * 4 + lane] = f.sums[lane];
-    tab.ext[(size_t)d * 4 + lane] = f.ext[lane];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(done + x, 1u) == ny - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // the last block of row block x: one warp per row (coalesced 64-word histogram rows)
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  for (uint32_t rr = r0 + warp; rr < min(r0 + kFinRows, K); rr += kFinRows / 32) {
+    const RawRow& f = raw[rr];
+    const uint32_t d = __ldcg(rank + rr);
+    const uint32_t h0 = f.hist[lane], h1 = f.hist[32 + lane];
+    tab.hist[(size_t)d * 64 + lane] = h0;
+    tab.hist[(size_t)d * 64 + 32 + lane] = h1;
+    // row counts < 2^32 (a call measures < 2^32 launches)
+    const uint32_t dc = __reduce_add_sync(0xffffffffu, h0), gc = __reduce_add_sync(0xffffffffu, h1);
+    if (lane < 4) tab.ext[(size_t)d * 4 + lane] = f.ext[lane];
+    if (lane == 0) {
+      const uint64_t ds = f.sums[1], gs = f.sums[3];
+      tab.kernel_id[d] = f.kid;
+      tab.task_id[d] = f.task;
+      tab.sums[(size_t)d * 4 + 0] = dc;
+      tab.sums[(size_t)d * 4 + 1] = ds;
+      tab.sums[(size_t)d * 4 + 2] = gc;
+      tab.sums[(size_t)d * 4 + 3] = gs;
+      tab.mean[(size_t)d * 2 + 0] = mean_half_up(ds, dc);  // SK_j
+      tab.mean[(size_t)d * 2 + 1] = mean_half_up(gs, gc);  // SG_j
+    }
   }
-  if (lane == 0) {
-    tab.kernel_id[d] = f.kid;
-    tab.task_id[d] = f.task;
-    tab.mean[(size_t)d * 2 + 0] = mean_half_up(f.sums[1], f.sums[0]);  // SK_j
-    tab.mean[(size_t)d * 2 + 1] = mean_half_up(f.sums[3], f.sums[2]);  // SG_j
-  }
+  if (tid == 0) done[x] = 0;  // (self-cleaning; rank[] stays for the out_row remap)
 }
 
 __global__ void k_remap_rows(uint32_t* rows, uint64_t n, const uint32_t* __restrict__ rank, const uint32_t* n_ptr) {

@@ -55,27 +55,17 @@ __global__ void k_zero(ZeroList z, fikit_status_t* st) {
   }
 }
 
-// One warp per string (blockIdx.y: 0 names, 1 signatures): the lanes stage the string's
-// aligned 16-B blocks in shared memory with coalesced loads, then lane 0 runs FNV-1a over the
-// bytes (serial by definition) from shared memory.
-__global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint64_t* __restrict__ name_out,
-                                                     fikit_strtab_t sigs, uint64_t* __restrict__ sig_out,
-                                                     fikit_status_t* st) {
+// FNV-1a 64 of one string of a table, by the whole warp: the lanes stage the string's aligned
+// 16-B blocks in shared memory (buf: 64 blocks) with coalesced loads, then lane 0 runs FNV-1a
+// over the bytes (serial by definition) from shared memory.  Returns the hash on lane 0.
+// A malformed entry (offsets decreasing) flags E_ARG; an empty name flags E_NAME.
+__device__ __forceinline__ uint64_t warp_fnv_string(const fikit_strtab_t& t, uint32_t j, bool is_name, uint4* buf,
+                                                    uint32_t lane, fikit_status_t* st) {
   constexpr uint32_t CH = 64;  // 16-B blocks staged per pass (1 KB per warp)
-  __shared__ uint4 buf[4][CH];
-  const bool is_name = blockIdx.y == 0;
-  const fikit_strtab_t t = is_name ? names : sigs;
-  uint64_t* out = is_name ? name_out : sig_out;
-  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t j = blockIdx.x * 4 + w;
-  if (j >= t.count) return;
   const uint32_t a = t.offsets[j], b = t.offsets[j + 1];
   if (b < a) {
-    if (lane == 0) {
-      atomicOr(&st->flags, kStatusArg);
-      out[j] = 0;
-    }
-    return;
+    if (lane == 0) atomicOr(&st->flags, kStatusArg);
+    return 0;
   }
   if (is_name && a == b && lane == 0) atomicOr(&st->flags, kStatusName);
   uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a 64 (R2), bytes in order
@@ -85,13 +75,13 @@ __global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint6
   const uint32_t c_end = (hi + 15) >> 4;
   for (uint32_t c0 = lo >> 4; c0 < c_end; c0 += CH) {
     const uint32_t nch = min(CH, c_end - c0);
-    for (uint32_t i = lane; i < nch; i += 32) buf[w][i] = __ldg(base + c0 + i);
+    for (uint32_t i = lane; i < nch; i += 32) buf[i] = __ldg(base + c0 + i);
     __syncwarp();
     if (lane == 0) {
       // one 16-B shared load per block, then its bytes in order from registers (the serial
       // multiply chain is the only latency left)
       for (uint32_t i = 0; i < nch; i++) {
-        const uint4 v = buf[w][i];
+        const uint4 v = buf[i];
         const uint32_t q[4] = {v.x, v.y, v.z, v.w};
         const uint32_t b0 = (c0 + i) * 16;
         if (b0 >= lo && b0 + 16 <= hi) {
@@ -113,7 +103,46 @@ __global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint6
     }
     __syncwarp();
   }
-  if (lane == 0) out[j] = h;
+  return h;
+}
+
+// FNV-1a 64 of one string by one thread (the sample's representatives: a few per block)
+__device__ __forceinline__ uint64_t thread_fnv_string(const fikit_strtab_t& t, uint32_t j) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  const uint32_t a = __ldg(t.offsets + j), b = __ldg(t.offsets + j + 1);
+  if (b <= a) return h;  // (malformed: flagged by the hash role)
+  const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(t.bytes) & ~uintptr_t(15));
+  const uint32_t skew = (uint32_t)(reinterpret_cast<uintptr_t>(t.bytes) & 15);
+  const uint32_t lo = a + skew, hi = b + skew;
+  uint4 nx = __ldg(base + (lo >> 4));
+  for (uint32_t c = lo >> 4; c < (hi + 15) >> 4; c++) {
+    const uint4 v = nx;
+    if (c + 1 < (hi + 15) >> 4) nx = __ldg(base + c + 1);  // next block in flight
+    const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const uint32_t pos = c * 16 + k;
+      if (pos >= lo && pos < hi) {
+        h ^= (uint64_t)((q[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+        h *= 0x100000001b3ULL;
+      }
+    }
+  }
+  return h;
+}
+
+// One warp per string (blockIdx.y: 0 names, 1 signatures): identify / resolve
+__global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint64_t* __restrict__ name_out,
+                                                     fikit_strtab_t sigs, uint64_t* __restrict__ sig_out,
+                                                     fikit_status_t* st) {
+  __shared__ uint4 buf[4][64];
+  const bool is_name = blockIdx.y == 0;
+  const fikit_strtab_t t = is_name ? names : sigs;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t j = blockIdx.x * 4 + w;
+  if (j >= t.count) return;
+  const uint64_t h = warp_fnv_string(t, j, is_name, buf[w], lane, st);
+  if (lane == 0) (is_name ? name_out : sig_out)[j] = h;
 }
 
 // warp-cooperative coalesced load of up to 32 records (1536 B) into a per-warp
@@ -163,47 +192,68 @@ __global__ void __launch_bounds__(256) k_identify(const uint4* __restrict__ recs
   }
 }
 
-// ---- sample: which rows are hot -------------------------------------------------------
-__global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t stride, uint64_t n_samples,
-                         const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash,
-                         uint32_t n_names, uint32_t n_sigs, IndexEntry* idx, uint32_t slots, fikit_status_t* st,
-                         fikit_table_t tab, Tuple* row_tuple, uint32_t* samp_cnt) {
+// ---- the measure call's preamble: two launches (k_prep, k_plan) ---------------------------------
+// k_prep, one launch with three independent roles by block range (256 threads each):
+//   hash    the FNV-1a hashes of every name and signature (one warp per string), used by the
+//           cold path of k_measure;
+//   sample  a jittered strided sample of ~64k launches -> (task, kernel ID) rows in the global
+//           index with sample counts (picks the rows worth caching; the representatives hash
+//           their strings themselves, so this role does not wait for the hash role);
+//   group   the task bucket of every tile group (kGroupTiles warp-tiles = 256 launches, bucketed
+//           by their first launch's task: one sector read per group) and per-block bucket counts
+//           (the counting sort of the task-partitioned schedule).
+// k_plan, one launch (1024 threads per block) with two roles:
+//   hot     per task bucket (and one global set), the <= kHotMax most-sampled rows and the
+//           sample coverage that decides the schedule mode;
+//   scatter the stable counting-sort scatter of the tile groups by bucket (each block derives its
+//           own offsets from every block's counts), and (block 0) the buckets' ranges and the
+//           first bucket of every k_measure CTA.
+
+__device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uint32_t nblk, unsigned char* sm) {
   // Per-block deduplication before the global index: the block's samples are counted per
-  // distinct identity in shared memory (keyed by a 64-bit fingerprint of (kernel ID, task)),
-  // then one representative per identity resolves its row in the global index and adds the
-  // count.  A skewed sample hits a few identities thousands of times; this keeps the global
-  // index (and its first-insert races) to one access per distinct identity per block.  The
-  // sample only chooses the hot rows, so a (astronomically rare) fingerprint collision merely
-  // credits one identity's samples to another: k_measure still resolves every launch exactly.
+  // distinct identity in shared memory (keyed by a 64-bit fingerprint of the raw identity), then
+  // one representative per identity resolves its row in the global index and adds the count.  A
+  // skewed sample hits a few identities thousands of times; this keeps the global index (and its
+  // first-insert races) to one access per distinct identity per block.  The sample only chooses
+  // the hot rows, so a (astronomically rare) fingerprint collision merely credits one identity's
+  // samples to another: k_measure still resolves every launch exactly.
   constexpr uint32_t HS = 512;
-  __shared__ unsigned long long sfp[HS], skid[HS];
-  __shared__ uint32_t scnt[HS], stw[HS][7];
+  unsigned long long* sfp = reinterpret_cast<unsigned long long*>(sm);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(sfp + HS);
+  uint32_t* stw = scnt + HS;  // [HS][7]
   for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x) {
     sfp[i] = 0;
     scnt[i] = 0;
   }
   __syncthreads();
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_samples;
-       j += (uint64_t)gridDim.x * blockDim.x) {
+  auto resolve = [&](const uint32_t* tw, uint32_t cnt) {
+    const uint64_t kid = kernel_id_from(thread_fnv_string(a.names, tw[0]), thread_fnv_string(a.sigs, tw[1]), tw[2],
+                                        tw[3], tw[4], tw[5]);
+    const uint32_t row = index_find_or_insert(a.idx, a.slots, kid, tw[6], tw, a.st, a.raw, a.row_tuple, a.cap);
+    if (row < a.cap) atomicAdd(a.samp_cnt + row, cnt);
+  };
+  const uint32_t nn = a.names.count, ns = a.sigs.count;
+  for (uint64_t j = blk * (uint64_t)blockDim.x + threadIdx.x; j < a.n_samples; j += (uint64_t)nblk * blockDim.x) {
     // jittered stride: a fixed stride aliases with periodic traces (a 300-kernel template
     // sampled every 1525 launches sees only 12 of its positions); a hashed offset inside each
     // stride window covers every position
-    uint64_t i = j * stride + (stride > 1 ? mix64(j + 0x9E3779B97F4A7C15ULL) % stride : 0);
-    if (i >= n) break;
-    uint4 a = __ldg(recs + i * 3), b = __ldg(recs + i * 3 + 1), c = __ldg(recs + i * 3 + 2);
-    uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-    if (!record_valid(w, n_names, n_sigs)) continue;  // reported by k_measure
-    const uint64_t kid = kernel_id_from(__ldg(name_hash + w[4]), __ldg(sig_hash + w[5]), w[6], w[7], w[8], w[9]);
+    const uint64_t i = j * a.stride + (a.stride > 1 ? mix64(j + 0x9E3779B97F4A7C15ULL) % a.stride : 0);
+    if (i >= a.n) break;
+    const uint4 x = __ldg(a.recs + i * 3), y = __ldg(a.recs + i * 3 + 1), z = __ldg(a.recs + i * 3 + 2);
+    const uint32_t w[12] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w, z.x, z.y, z.z, z.w};
+    if (!record_valid(w, nn, ns)) continue;  // reported by k_measure
     const uint32_t tw[7] = {w[4], w[5], w[6], w[7], w[8], w[9] & 0xFFFFu, w[11]};
-    const unsigned long long fp = mix64(kid ^ ((uint64_t)w[11] * 0x9E3779B97F4A7C15ULL)) | 1ull;
-    uint32_t p = (uint32_t)(fp >> 32) & (HS - 1);
+    const uint32_t h1 = tuple_hash(tw);
+    const unsigned long long fp = (((unsigned long long)h1 << 32) | (mix64(((uint64_t)tw[0] << 32 | tw[1]) ^
+                                   ((uint64_t)tw[2] << 32 | tw[3]) * 0x9E3779B97F4A7C15ULL ^
+                                   ((uint64_t)tw[4] << 32 | tw[5]) * 0xC2B2AE3D27D4EB4FULL ^ tw[6]) >> 32)) | 1ull;
+    uint32_t p = h1 & (HS - 1);
     bool counted = false;
     for (uint32_t probe = 0; probe < HS; probe++, p = (p + 1) & (HS - 1)) {
       const unsigned long long old = atomicCAS(&sfp[p], 0ull, fp);
       if (old == 0ull) {  // first sample of this identity in the block: the representative
-        skid[p] = kid;
 #pragma unroll
-        for (int q = 0; q < 7; q++) stw[p][q] = tw[q];
+        for (int q = 0; q < 7; q++) stw[p * 7 + q] = tw[q];
       }
       if (old == 0ull || old == fp) {
         atomicAdd(&scnt[p], 1u);
@@ -211,47 +261,84 @@ __global__ void k_sample(const uint4* __restrict__ recs, uint64_t n, uint64_t st
         break;
       }
     }
-    if (!counted) {  // the block saw > HS identities: resolve and count directly
-      const uint32_t row =
-          index_find_or_insert(idx, slots, kid, w[11], tw, st, tab.kernel_id, tab.task_id, row_tuple, tab.capacity);
-      if (row < tab.capacity) atomicAdd(samp_cnt + row, 1u);
+    if (!counted) resolve(tw, 1u);  // the block saw > HS identities: resolve and count directly
+  }
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < HS; q += blockDim.x)
+    if (scnt[q]) resolve(stw + q * 7, scnt[q]);
+}
+
+__device__ __forceinline__ void prep_groups(const PrepArgs& a, uint32_t blk, uint32_t* h) {
+  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t C = (a.ngroups + a.sb - 1) / a.sb;
+  const uint32_t g0 = blk * C, g1 = min(a.ngroups, g0 + C);
+  constexpr int U = 4;  // independent one-sector loads in flight per thread
+  for (uint32_t q = g0 + threadIdx.x; q < g1; q += U * blockDim.x) {
+    uint32_t task[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t qu = q + u * blockDim.x;
+      task[u] = qu < g1 ? __ldcs(&a.recs_t[(uint64_t)qu * kGroupTiles * kTileLaunches].task_id) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t qu = q + u * blockDim.x;
+      if (qu < g1) {
+        const uint32_t b = bucket_of(task[u]);
+        a.grp_bucket[qu] = (uint8_t)b;
+        atomicAdd(&h[b], 1u);
+      }
     }
   }
   __syncthreads();
-  for (uint32_t q = threadIdx.x; q < HS; q += blockDim.x) {
-    const uint32_t cnt = scnt[q];
-    if (!cnt) continue;
-    const uint32_t row = index_find_or_insert(idx, slots, skid[q], stw[q][6], stw[q], st, tab.kernel_id, tab.task_id,
-                                              row_tuple, tab.capacity);
-    if (row < tab.capacity) atomicAdd(samp_cnt + row, cnt);
+  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) a.blkcnt[blk * kBuckets + i] = h[i];
+}
+
+__global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
+  __shared__ __align__(16) unsigned char sm[512 * 8 + 512 * 4 + 512 * 28];  // the sample role's (largest)
+  const uint32_t b = blockIdx.x;
+  if (b < a.nb_hash) {  // names, then signatures: one warp per string
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t j = b * (kPrepThreads / 32) + w;
+    const uint32_t nn = a.names.count;
+    if (j >= nn + a.sigs.count) return;
+    const bool is_name = j < nn;
+    const uint64_t h = warp_fnv_string(is_name ? a.names : a.sigs, is_name ? j : j - nn, is_name,
+                                       reinterpret_cast<uint4*>(sm) + w * 64, lane, a.st);
+    if (lane == 0) (is_name ? a.name_hash[j] : a.sig_hash[j - nn]) = h;
+  } else if (b < a.nb_hash + a.nb_samp) {
+    prep_sample(a, b - a.nb_hash, a.nb_samp, sm);
+  } else {
+    prep_groups(a, b - a.nb_hash - a.nb_samp, reinterpret_cast<uint32_t*>(sm));
   }
 }
 
-// ---- hot sets: per task bucket, the most-sampled rows (one CTA per bucket; CTA kBuckets:
-// the global set over all tasks).  Each CTA also counts the samples its set covers. -------
-__global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, const uint32_t* __restrict__ samp_cnt,
-                                                     const Tuple* __restrict__ row_tuple, uint32_t cap,
-                                                     Tuple* hot_all, uint32_t* hot_n_all) {
+
+// hot sets: per task bucket, the most-sampled rows (block bkt; block kBuckets: the global set
+// over all tasks).  Each block also counts the samples its set covers.
+__device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsigned char* sm) {
   constexpr int NB = 4096;
-  __shared__ uint32_t h[NB];
-  __shared__ uint32_t s_T, s_n;
-  const uint32_t bkt = blockIdx.x;  // kGlobalSet: every row
-  Tuple* hot = hot_all + (size_t)bkt * kHotMax;
-  auto mine = [&](uint32_t r) { return bkt == kGlobalSet || bucket_of(row_tuple[r].w[6]) == bkt; };
-  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  uint32_t* h = reinterpret_cast<uint32_t*>(sm);
+  uint32_t* wsum = h + NB;  // [32]
+  uint32_t* s_misc = wsum + 32;  // T, n, Tmin
+  Tuple* hot = a.hot_all + (size_t)bkt * kHotMax;
+  auto mine = [&](uint32_t r) { return bkt == kGlobalSet || bucket_of(a.row_tuple[r].w[6]) == bkt; };
+  const uint32_t K = (uint32_t)umin64(*(volatile const unsigned long long*)&a.st->n_rows_needed, a.cap);
   for (int i = threadIdx.x; i < NB; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    const uint32_t c = samp_cnt[r];
+    const uint32_t c = a.samp_cnt[r];
     if (c && mine(r)) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
   }
-  if (threadIdx.x == 0) s_n = 0;
+  if (threadIdx.x == 0) {
+    s_misc[1] = 0;
+    s_misc[2] = NB;
+  }
   __syncthreads();
   // T = smallest count c >= 1 whose suffix S(c) = #rows with count >= c fits kHotMax:
   // a block-wide suffix scan of the 4096-bin count histogram (4 bins per thread)
   {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t s_Tmin;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     uint32_t loc[4], x = 0;
 #pragma unroll
@@ -265,7 +352,6 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
       if (lane + d < 32) x += y;
     }
     if (lane == 0) wsum[wid] = x;
-    if (t == 0) s_Tmin = NB;
     __syncthreads();
     uint32_t later = 0;
     for (int w2 = wid + 1; w2 < 32; w2++) later += wsum[w2];
@@ -273,23 +359,21 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       uint32_t c = 4 * t + j;
-      if (c >= 1 && S <= kHotMax) atomicMin(&s_Tmin, c);
+      if (c >= 1 && S <= kHotMax) atomicMin(&s_misc[2], c);
       S -= loc[j];
     }
     __syncthreads();
-    if (t == 0) s_T = s_Tmin;
-    __syncthreads();
   }
-  const uint32_t T = s_T;
+  const uint32_t T = s_misc[2];
   uint32_t cov = 0, tot = 0;
   for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    const uint32_t c = samp_cnt[r];
+    const uint32_t c = a.samp_cnt[r];
     if (c && mine(r)) {
       tot += c;
       if (c >= T) {
-        const uint32_t e = atomicAdd(&s_n, 1u);
+        const uint32_t e = atomicAdd(&s_misc[1], 1u);
         if (e < kHotMax) {
-          hot[e] = row_tuple[r];
+          hot[e] = a.row_tuple[r];
           cov += c;
         }
       }
@@ -298,203 +382,142 @@ __global__ void __launch_bounds__(1024) k_hot_select(const fikit_status_t* st, c
   cov = __reduce_add_sync(0xffffffffu, cov);
   tot = __reduce_add_sync(0xffffffffu, tot);
   if ((threadIdx.x & 31) == 0) {
-    if (cov) atomicAdd(&hot_n_all[bkt == kGlobalSet ? kCovGlobal : kCovTask], cov);
-    if (tot && bkt == kGlobalSet) atomicAdd(&hot_n_all[kCovTotal], tot);
+    if (cov) atomicAdd(&a.hot_hdr[bkt == kGlobalSet ? kCovGlobal : kCovTask], cov);
+    if (tot && bkt == kGlobalSet) atomicAdd(&a.hot_hdr[kCovTotal], tot);
   }
   __syncthreads();
-  if (threadIdx.x == 0) hot_n_all[bkt] = min(s_n, kHotMax);
+  if (threadIdx.x == 0) a.hot_hdr[bkt] = min(s_misc[1], kHotMax);
 }
 
-// ---- task-partitioned schedule ---------------------------------------------------------------
-// bucket of every warp-tile = bucket_of(task of its first launch).  Block k owns the contiguous
-// chunk of tiles [k*C, (k+1)*C) and writes its per-bucket counts to blkcnt[k][*].
-__global__ void __launch_bounds__(1024) k_tile_bucket(const fikit_record_t* __restrict__ recs, uint32_t ntiles,
-                                                     const uint32_t* __restrict__ hot_hdr,
-                                                     uint8_t* __restrict__ tile_bucket, uint32_t* __restrict__ blkcnt) {
-  if (!use_task_buckets(hot_hdr)) return;  // address-order sweep: nothing to sort
-  __shared__ uint32_t h[kBuckets];
-  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) h[i] = 0;
+// stable counting-sort scatter of block k's chunk of tile groups: its offsets are the buckets'
+// starts plus the counts of the chunks before it (every block reads every block's counts); the
+// chunk is walked in address order 1024 groups per step, a group's position = its bucket's
+// running cursor + same-bucket groups of lower warps in the step + same-bucket lanes below it
+// (match_any).  Groups of a bucket keep address order.  Block 0 also publishes the buckets'
+// ranges and assigns every k_measure CTA its first bucket.
+__device__ __forceinline__ void plan_scatter(const PlanArgs& a, uint32_t k, unsigned char* sm) {
+  constexpr uint32_t SEGS = 16, W = 32;
+  uint32_t* ptot = reinterpret_cast<uint32_t*>(sm);  // [SEGS][kBuckets]
+  uint32_t* ppre = ptot + SEGS * kBuckets;           // [SEGS][kBuckets]
+  uint32_t* cur = ppre + SEGS * kBuckets;            // [kBuckets]
+  uint32_t* tot = cur + kBuckets;                    // [kBuckets]
+  uint32_t* wcnt = tot + kBuckets;                   // [W][kBuckets]
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // thread (seg, b): counts of bucket b over a segment of the blocks, all of them and those before k
+    const uint32_t b = tid % kBuckets, seg = tid / kBuckets;
+    const uint32_t per = (a.sb + SEGS - 1) / SEGS, k0 = seg * per, k1 = min(a.sb, k0 + per);
+    uint32_t x = 0, y = 0;
+    for (uint32_t kk = k0; kk < k1; kk++) {
+      const uint32_t c = a.blkcnt[kk * kBuckets + b];
+      x += c;
+      y += kk < k ? c : 0u;
+    }
+    ptot[seg * kBuckets + b] = x;
+    ppre[seg * kBuckets + b] = y;
+  }
+  for (uint32_t i = tid; i < W * kBuckets; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
-  const uint32_t C = (ntiles + gridDim.x - 1) / gridDim.x;
-  const uint32_t t0 = blockIdx.x * C, t1 = min(ntiles, t0 + C);
-  // Tiles are bucketed in aligned pairs by the pair's first launch (one DRAM sector per 128
-  // launches: the kernel is bound by scattered DRAM accesses).  A pair whose second tile starts
-  // another task's run is only scheduled with the first one's hot set (its launches go cold
-  // once and are admitted): a scheduling choice, never a result.
-  constexpr int U = 4;  // independent one-sector loads in flight per thread
-  const uint32_t p0 = (t0 + 1) / 2, p1 = (t1 + 1) / 2;  // pairs whose first tile is in [t0, t1)
-  for (uint32_t q = p0 + threadIdx.x; q < p1; q += U * blockDim.x) {
-    uint32_t task[U];
+  if (tid < kBuckets) {
+    uint32_t x = 0, y = 0;
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const uint32_t qu = q + u * blockDim.x;
-      task[u] = qu < p1 ? __ldcs(&recs[(uint64_t)qu * 2 * kTileLaunches].task_id) : 0u;
+    for (uint32_t seg = 0; seg < SEGS; seg++) {
+      x += ptot[seg * kBuckets + tid];
+      y += ppre[seg * kBuckets + tid];
     }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const uint32_t qu = q + u * blockDim.x;
-      if (qu < p1) {
-        const uint32_t b = bucket_of(task[u]);
-        const uint32_t ta = 2 * qu, tb = min(ta + 2, min(t1, ntiles));
-        for (uint32_t tt = max(ta, t0); tt < tb; tt++) tile_bucket[tt] = (uint8_t)b;
-        atomicAdd(&h[b], tb - max(ta, t0));
-      }
-    }
-  }
-  if (t0 < t1 && (t0 & 1u)) {  // a chunk starting mid-pair: its first tile follows its pair
-    if (threadIdx.x == 0) {
-      const uint32_t b = bucket_of(__ldcs(&recs[(uint64_t)(t0 - 1) * kTileLaunches].task_id));
-      tile_bucket[t0] = (uint8_t)b;
-      atomicAdd(&h[b], 1u);
-    }
+    tot[tid] = x;
+    cur[tid] = y;  // (+ the bucket's start, below)
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) blkcnt[blockIdx.x * kBuckets + i] = h[i];
-}
-
-// One block of 1024 threads.  Address-order mode: one bucket (kGlobalSet) = all tiles in
-// address order, every CTA starts on it.  Task mode: blk[k][b] (block k's count of bucket-b
-// tiles) becomes block k's first sorted position for bucket b (column scans in shared memory),
-// the buckets' sorted ranges go to cur[] / bend[], and each CTA gets a first bucket: every
-// non-empty bucket g_b >= 1 CTAs in proportion to its tiles (smallest per-CTA load L with
-// sum_b ceil(c_b / L) <= G, leftovers to the most loaded); with more non-empty buckets than
-// CTAs, CTA c starts on the c-th.  The rest is dynamic (warps claim tiles, CTAs move on).
-__global__ void __launch_bounds__(1024) k_tile_plan(uint32_t* __restrict__ blk, uint32_t nblk, uint32_t ntiles,
-                                                    uint32_t G, const uint32_t* __restrict__ hot_hdr,
-                                                    uint32_t* __restrict__ cur, uint32_t* __restrict__ bend,
-                                                    uint32_t* __restrict__ act, uint32_t* __restrict__ first,
-                                                    fikit_status_t* st) {
-  constexpr uint32_t SEGS = 16;  // column scans: 16 threads per bucket, nblk / 16 blocks each
-  __shared__ uint32_t m[kSortBlocks * kBuckets];
-  __shared__ uint32_t segsum[SEGS][kBuckets], bcount[kBuckets], start[kBuckets + 1];
-  const uint32_t tid = threadIdx.x;
-  const bool task_mode = use_task_buckets(hot_hdr);
-  for (uint32_t b = tid; b < kSchedWords; b += blockDim.x) {
-    cur[b] = 0;
-    bend[b] = (!task_mode && b == kGlobalSet) ? ntiles : 0u;
-    act[b] = 0;
-  }
-  if (!task_mode) {
-    for (uint32_t c = tid; c < G; c += blockDim.x) first[c] = kGlobalSet;
-    return;
-  }
-  for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) m[i] = blk[i];
-  for (uint32_t c = tid; c < G; c += blockDim.x) first[c] = kNoBucket;
-  __syncthreads();
-  // column scans: thread (seg, b) sums its segment, then rewrites it as exclusive offsets
-  const uint32_t sb = tid % kBuckets, seg = tid / kBuckets;
-  const uint32_t per = (nblk + SEGS - 1) / SEGS, k0 = seg * per, k1 = min(nblk, k0 + per);
-  if (seg < SEGS) {
-    uint32_t x = 0;
-    for (uint32_t k = k0; k < k1; k++) x += m[k * kBuckets + sb];
-    segsum[seg][sb] = x;
-  }
-  __syncthreads();
-  if (seg < SEGS) {
-    uint32_t run = 0;
-    for (uint32_t q = 0; q < seg; q++) run += segsum[q][sb];
-    for (uint32_t k = k0; k < k1; k++) {
-      const uint32_t c = m[k * kBuckets + sb];
-      m[k * kBuckets + sb] = run;
-      run += c;
-    }
-    if (seg == SEGS - 1) bcount[sb] = run;
-  }
-  __syncthreads();
-  if (tid < 32) {  // one warp: bucket starts, the first-bucket assignment (2 buckets per lane)
-    const uint32_t lane = tid;
-    const uint32_t c0 = bcount[2 * lane], c1 = bcount[2 * lane + 1];
-    uint32_t x = c0 + c1;  // inclusive scan of the pairs
+  if (warp == 0) {  // bucket starts: exclusive scan of the totals (2 buckets per lane)
+    const uint32_t c0 = tot[2 * lane], c1 = tot[2 * lane + 1];
+    uint32_t x = c0 + c1;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
       if (lane >= (uint32_t)d) x += y;
     }
     const uint32_t s0 = x - c0 - c1;
-    start[2 * lane] = s0;
-    start[2 * lane + 1] = s0 + c0;
-    if (lane == 31) start[kBuckets] = x;
-    cur[2 * lane] = s0;
-    bend[2 * lane] = s0 + c0;
-    cur[2 * lane + 1] = s0 + c0;
-    bend[2 * lane + 1] = x;
-    const uint32_t nb = __reduce_add_sync(0xffffffffu, (c0 ? 1u : 0u) + (c1 ? 1u : 0u));
-    if (lane == 0) {
-      st->schedule = 1;
-      st->n_task_buckets = nb;
-    }
-    // g_b = ceil(c_b / L) for the smallest L with sum_b g_b <= G (at least one CTA per bucket
-    // when nb <= G; else every CTA starts on its own bucket); unassigned CTAs start by stealing
-    uint32_t g0, g1;
-    if (nb <= G) {
-      uint32_t lo = (ntiles + G - 1) / G, hi = ntiles;  // sum at hi = nb <= G
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo) / 2;
-        const uint32_t need = __reduce_add_sync(0xffffffffu, (c0 + mid - 1) / mid + (c1 + mid - 1) / mid);
-        if (need <= G) hi = mid; else lo = mid + 1;
+    cur[2 * lane] += s0;
+    cur[2 * lane + 1] += s0 + c0;
+    if (k == 0) {
+      a.bstart[2 * lane] = s0;
+      a.bstart[2 * lane + 1] = s0 + c0;
+      a.btot[2 * lane] = c0;
+      a.btot[2 * lane + 1] = c1;
+      // first bucket of every CTA: g_b = ceil(c_b / L) CTAs for the smallest per-CTA load L with
+      // sum_b g_b <= G (at least one CTA per non-empty bucket when nb <= G; else every CTA
+      // starts on its own bucket); unassigned CTAs start by stealing (kNoBucket)
+      const uint32_t G = a.grid_measure;
+      const uint32_t nb = __reduce_add_sync(0xffffffffu, (c0 ? 1u : 0u) + (c1 ? 1u : 0u));
+      const uint32_t ng = __shfl_sync(0xffffffffu, x, 31);  // all groups
+      uint32_t g0, g1;
+      if (nb <= G) {
+        uint32_t lo = (ng + G - 1) / G, hi = ng > 0 ? ng : 1;
+        if (lo < 1) lo = 1;
+        while (lo < hi) {
+          const uint32_t mid = lo + (hi - lo) / 2;
+          const uint32_t need = __reduce_add_sync(0xffffffffu, (c0 + mid - 1) / mid + (c1 + mid - 1) / mid);
+          if (need <= G) hi = mid; else lo = mid + 1;
+        }
+        g0 = (c0 + lo - 1) / lo;
+        g1 = (c1 + lo - 1) / lo;
+      } else {
+        g0 = c0 ? 1u : 0u;
+        g1 = c1 ? 1u : 0u;
       }
-      g0 = (c0 + lo - 1) / lo;
-      g1 = (c1 + lo - 1) / lo;
-    } else {
-      g0 = c0 ? 1u : 0u;
-      g1 = c1 ? 1u : 0u;
-    }
-    uint32_t gx = g0 + g1;  // CTA ranges: exclusive scan of g
+      uint32_t gx = g0 + g1;  // CTA ranges: exclusive scan of g
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, gx, d);
-      if (lane >= (uint32_t)d) gx += y;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, gx, d);
+        if (lane >= (uint32_t)d) gx += y;
+      }
+      const uint32_t cs = gx - g0 - g1;
+      for (uint32_t c = lane; c < G; c += 32) a.first[c] = kNoBucket;
+      __syncwarp();
+      for (uint32_t i = 0; i < g0 && cs + i < G; i++) a.first[cs + i] = 2 * lane;
+      for (uint32_t i = 0; i < g1 && cs + g0 + i < G; i++) a.first[cs + g0 + i] = 2 * lane + 1;
     }
-    const uint32_t cs = gx - g0 - g1;
-    for (uint32_t i = 0; i < g0 && cs + i < G; i++) first[cs + i] = 2 * lane;
-    for (uint32_t i = 0; i < g1 && cs + g0 + i < G; i++) first[cs + g0 + i] = 2 * lane + 1;
   }
   __syncthreads();
-  for (uint32_t i = tid; i < nblk * kBuckets; i += blockDim.x) blk[i] = m[i] + start[i % kBuckets];
-}
-
-// stable counting-sort scatter: block k walks its chunk in address order, 256 tiles per step;
-// a tile's sorted position = its bucket's running cursor + same-bucket tiles of lower warps in
-// the step + same-bucket lanes below it (match_any).  Tiles of a bucket keep address order.
-__global__ void __launch_bounds__(1024) k_tile_scatter(const uint8_t* __restrict__ tile_bucket, uint32_t ntiles,
-                                                       const uint32_t* __restrict__ hot_hdr,
-                                                       const uint32_t* __restrict__ blkoff,
-                                                       uint32_t* __restrict__ order) {
-  if (!use_task_buckets(hot_hdr)) return;
-  constexpr int W = 32;
-  __shared__ uint32_t cur[kBuckets], wcnt[W][kBuckets];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < (int)kBuckets; i += blockDim.x) cur[i] = blkoff[blockIdx.x * kBuckets + i];
-  for (int i = threadIdx.x; i < W * (int)kBuckets; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t C = (ntiles + gridDim.x - 1) / gridDim.x;
-  const uint32_t t0 = blockIdx.x * C, t1 = min(ntiles, t0 + C);
-  auto ldb = [&](uint32_t t) -> uint32_t { return t < t1 ? (uint32_t)tile_bucket[t] : kBuckets; };
-  uint32_t bnext = ldb(t0 + threadIdx.x);  // software-pipelined one step ahead
+  const uint32_t C = (a.ngroups + a.sb - 1) / a.sb;
+  const uint32_t t0 = k * C, t1 = min(a.ngroups, t0 + C);
+  auto ldb = [&](uint32_t t) -> uint32_t { return t < t1 ? (uint32_t)a.grp_bucket[t] : kBuckets; };
+  uint32_t bnext = ldb(t0 + tid);  // software-pipelined one step ahead
   for (uint32_t base = t0; base < t1; base += blockDim.x) {
-    const uint32_t t = base + threadIdx.x;
-    const uint32_t b = bnext;  // kBuckets: no tile (tail)
+    const uint32_t t = base + tid;
+    const uint32_t b = bnext;  // kBuckets: no group (tail)
     bnext = ldb(t + blockDim.x);
     const uint32_t peers = __match_any_sync(0xffffffffu, b);
     const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-    if (b < kBuckets && rank == 0) wcnt[warp][b] = __popc(peers);
+    if (b < kBuckets && rank == 0) wcnt[warp * kBuckets + b] = __popc(peers);
     __syncthreads();
     if (b < kBuckets) {
       uint32_t pos = cur[b] + rank;
-      for (int v = 0; v < warp; v++) pos += wcnt[v][b];
-      order[pos] = t;
+      for (uint32_t v = 0; v < warp; v++) pos += wcnt[v * kBuckets + b];
+      a.order[pos] = t;
     }
     __syncthreads();
-    if (threadIdx.x < kBuckets) {
+    if (tid < kBuckets) {
       uint32_t add = 0;
 #pragma unroll
-      for (int v = 0; v < W; v++) {
-        add += wcnt[v][threadIdx.x];
-        wcnt[v][threadIdx.x] = 0;
+      for (uint32_t v = 0; v < W; v++) {
+        add += wcnt[v * kBuckets + tid];
+        wcnt[v * kBuckets + tid] = 0;
       }
-      cur[threadIdx.x] += add;
+      cur[tid] += add;
     }
     __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_plan(PlanArgs a) {
+  __shared__ __align__(16) unsigned char sm[(4096 + 32 + 4) * 4 > (2 * 16 + 2 + 32) * kBuckets * 4
+                                                ? (4096 + 32 + 4) * 4
+                                                : (2 * 16 + 2 + 32) * kBuckets * 4];
+  if (blockIdx.x <= kBuckets) {
+    plan_hot(a, blockIdx.x, sm);
+  } else {
+    plan_scatter(a, blockIdx.x - (kBuckets + 1), sm);
   }
 }
 
@@ -574,7 +597,7 @@ __device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) 
 // word and a wrap (old + v < old, exact: the atomic serializes) adds one carry.  Returns the
 // old word (the caller checks the carry after its other reductions, off the critical path).
 template <class RowOf>  // row_of(): the slot's table row, read only on the rare >= 2^32 path
-__device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const fikit_table_t& tab,
+__device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const RawTab& tab,
                                             RowOf row_of, int j, uint64_t v, uint32_t mn, uint32_t mx) {
   if ((v >> 32) == 0) {
     const uint32_t v32 = (uint32_t)v;
@@ -588,29 +611,29 @@ __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint
     const int b = bin_of(v) + 32 * j;
     red_shared_add(hist_e + 4u * (uint32_t)b, 1u);
     const uint32_t row = row_of();
-    red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
-    red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
-    red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
+    red_add_u64(tab.rows[row].sums + 2 * j + 1, v);
+    red_max_u64(tab.rows[row].ext + 2 * j, v);
+    red_max_u64(tab.rows[row].ext + 2 * j + 1, ~v);
     return 0u;  // (v >> 32 != 0: the low word 0 never wraps the sum)
   }
 }
 
-__device__ __forceinline__ void cold_add(const fikit_table_t& tab, uint32_t row, int j, uint64_t v) {
+__device__ __forceinline__ void cold_add(const RawTab& tab, uint32_t row, int j, uint64_t v) {
   // fire-and-forget L2 reductions (no read-back, no dependent latency)
-  red_add_u32(tab.hist + (size_t)row * 64 + 32 * j + bin_of(v), 1u);
-  red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, v);
-  red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, v);
-  red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~v);
+  red_add_u32(tab.rows[row].hist + 32 * j + bin_of(v), 1u);
+  red_add_u64(tab.rows[row].sums + 2 * j + 1, v);
+  red_max_u64(tab.rows[row].ext + 2 * j, v);
+  red_max_u64(tab.rows[row].ext + 2 * j + 1, ~v);
 }
 
 // phase flush of the shared rows: u32 bins and split sums -> table, zeroed
-__device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& tab, int ctid) {
+__device__ __forceinline__ void flush_epoch(mk::Smem& S, const RawTab& tab, int ctid) {
   // one warp per slot: 64 u32 bins (two per lane) and the two split sums (lanes 0, 1)
   const uint32_t hn = min(S.hot_n, kHotMax);  // admission may overshoot the counter
   const uint32_t lane = (uint32_t)ctid & 31u;
   for (uint32_t e = (uint32_t)ctid >> 5; e < hn; e += mk::WARPS) {
     const uint32_t row = S.grow[e];
-    uint32_t* gh = tab.hist + (size_t)row * 64;
+    uint32_t* gh = tab.rows[row].hist;
 #pragma unroll
     for (uint32_t w = lane; w < 2u * kBins; w += 32u) {
       const uint32_t x = S.hist[e][w];
@@ -622,7 +645,7 @@ __device__ __forceinline__ void flush_epoch(mk::Smem& S, const fikit_table_t& ta
     if (lane < 2) {
       const uint32_t j = lane;
       const uint64_t sum = (uint64_t)S.st[e][2 * j] | ((uint64_t)S.st[e][2 * j + 1] << 32);
-      if (sum) red_add_u64(tab.sums + (size_t)row * 4 + 2 * j + 1, sum);
+      if (sum) red_add_u64(tab.rows[row].sums + 2 * j + 1, sum);
       S.st[e][2 * j] = 0;
       S.st[e][2 * j + 1] = 0;
     }
@@ -664,9 +687,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     k_measure(const fikit_record_t* __restrict__ recs, uint64_t n, const fikit_record_t* __restrict__ halo,
               const uint64_t* __restrict__ name_hash, const uint64_t* __restrict__ sig_hash, uint32_t n_names,
               uint32_t n_sigs, IndexEntry* idx, uint32_t slots, Tuple* tidx, uint32_t tslots, fikit_status_t* st,
-              fikit_table_t tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
-              const uint32_t* __restrict__ hot_n_all, uint32_t* cur, const uint32_t* __restrict__ bend, uint32_t* act,
-              const uint32_t* __restrict__ first, const uint32_t* __restrict__ order, uint32_t* __restrict__ out_row) {
+              RawTab tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
+              const uint32_t* __restrict__ hot_n_all, uint32_t* cur, uint32_t* act, const uint32_t* __restrict__ bstart,
+              const uint32_t* __restrict__ btot, const uint32_t* __restrict__ first,
+              const uint32_t* __restrict__ order, uint32_t ntiles, uint32_t* __restrict__ out_row) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
@@ -710,8 +734,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       for (int j = 0; j < 2; j++) {
         const uint32_t mn = j ? S.mm[e].z : S.mm[e].x, mx = j ? S.mm[e].w : S.mm[e].y;
         if (mn != 0xFFFFFFFFu || mx != 0u) {  // a value < 2^32 was seen
-          red_max_u64(tab.ext + (size_t)row * 4 + 2 * j, (uint64_t)mx);
-          red_max_u64(tab.ext + (size_t)row * 4 + 2 * j + 1, ~(uint64_t)mn);
+          red_max_u64(tab.rows[row].ext + 2 * j, (uint64_t)mx);
+          red_max_u64(tab.rows[row].ext + 2 * j + 1, ~(uint64_t)mn);
         }
       }
     }
@@ -719,16 +743,26 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   __syncthreads();
 
   // n < 2^32 (checked by the C-ABI): 32-bit tile bookkeeping.  A warp's tiles are claimed one
-  // at a time from its CTA's current bucket (cur[b]: next unclaimed sorted position, bend[b]:
-  // end), through a three-round pipeline so no latency is exposed: a position is claimed (L2
-  // atomic) in round r, mapped to its tile (order[], task mode) in round r + 1, and the tile's
-  // TMA is issued in round r + 2 as soon as the stage has been read.  kk counts the tiles the
-  // warp's stage has held in this launch (mbarrier parity kk & 1).
+  // at a time from its CTA's current bucket (cur[b]: positions of b claimed so far, of len_of(b)),
+  // through a three-round pipeline so no latency is exposed: a position is claimed (L2 atomic)
+  // in round r, mapped to its tile (order[], task mode) in round r + 1, and the tile's TMA is
+  // issued in round r + 2 as soon as the stage has been read.  kk counts the tiles the warp's
+  // stage has held in this launch (mbarrier parity kk & 1).
   const uint32_t n32 = (uint32_t)n;
   uint32_t kk = 0;
   uint32_t sfirst = 0;  // (all lanes) first launch of the tile in the stage
   const bool by_task = use_task_buckets(hot_n_all);  // else sorted position = tile
-  uint32_t cb = kNoBucket, cb_end = 0;                // the CTA's current bucket
+  // tile positions of bucket b: [base_of(b), base_of(b) + len_of(b))
+  auto len_of = [&](uint32_t b) -> uint32_t {
+    return by_task ? (b < kBuckets ? kGroupTiles * btot[b] : 0u) : (b == kGlobalSet ? ntiles : 0u);
+  };
+  uint32_t cb = kNoBucket, cb_end = 0, cb_base = 0;  // the CTA's current bucket, its length and base
+  if (blockIdx.x == 0 && tid == 0) {
+    uint32_t nb = 0;
+    for (uint32_t b = 0; b < kBuckets; b++) nb += btot[b] ? 1u : 0u;
+    st->schedule = by_task ? 1u : 0u;
+    st->n_task_buckets = by_task ? nb : 0u;
+  }
   constexpr uint32_t kNone = 0xFFFFFFFFu;
   // Positions are claimed kClaim at a time (one L2 atomic per kClaim tiles: a single counter
   // serves every warp in address-order mode); the next range's atomic is issued when the
@@ -748,7 +782,19 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     pc = q_pos++;
   };
   auto tile_of_claim = [&]() {  // lane 0: position pc -> tile
-    tn = pc == kNone ? kNone : (by_task ? __ldg(order + pc) : pc);
+    for (;;) {
+      if (pc == kNone || !by_task) {
+        tn = pc;
+        return;
+      }
+      const uint32_t p = cb_base + pc;
+      const uint32_t t = __ldg(order + (p / kGroupTiles)) * kGroupTiles + p % kGroupTiles;
+      if (t < ntiles) {
+        tn = t;
+        return;
+      }
+      claim();  // a missing tile of the last (partial) group: the next position
+    }
   };
   // 1-D TMA of a tile (+ the next launch) into the warp's stage (lane 0)
   auto issue = [&](uint32_t first) {
@@ -770,8 +816,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
         const uint64_t kid =
             kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
-        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.kernel_id, tab.task_id, row_tuple,
-                                    tab.capacity);
+        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.rows, row_tuple, tab.capacity);
       });
       if (row < tab.capacity) {
         cold_add(tab, row, 0, pd);
@@ -937,7 +982,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (warp == 0) {  // the lanes read the buckets' counters in parallel (one L2 round trip)
       uint32_t best = kNoBucket, most = 0;
       for (uint32_t b = lane; b < kSchedWords; b += 32) {
-        const uint32_t e = bend[b], c = *(volatile uint32_t*)(cur + b), a = *(volatile uint32_t*)(act + b);
+        const uint32_t e = len_of(b), c = *(volatile uint32_t*)(cur + b), a = *(volatile uint32_t*)(act + b);
         const uint32_t left = e > c ? e - c : 0u;
         if (left > most && (left > 128u || a == 0u)) {
           most = left;
@@ -954,12 +999,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     __syncthreads();
     return b;
   };
-  cb = first[blockIdx.x];
+  cb = by_task ? first[blockIdx.x] : kGlobalSet;
   if (cb == kNoBucket) cb = pick_bucket();
   while (cb != kNoBucket) {
     if (tid == 0) atomicAdd(act + cb, 1u);
     load_hot_set(cb);
-    cb_end = bend[cb];
+    cb_end = len_of(cb);
+    cb_base = by_task ? kGroupTiles * bstart[cb] : 0u;
     q_pos = q_end = 0;
     if (lane == 0) nx = atomicAdd(cur + cb, kClaim);
     // prime the pipeline: the first tile's TMA, the second tile's order[] load, a third claim
