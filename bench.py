@@ -34,6 +34,8 @@ sys.path.insert(0, ROOT)
 METRIC = "launch-records/s (identify+measure) and fill-scenarios/s at 1/2/4/8 B200; % HBM peak"
 UNIT = "launch-records/s"
 REC_BYTES = 48  # algorithmic bytes per launch record
+L2_BYTES = 126 << 20  # B200 L2
+L2_FLUSH_BYTES = 256 << 20
 
 
 def parse():
@@ -238,51 +240,98 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------------------------
-def oracle_sample_time(wl, budget_s, seed=0):
-    """Time the CPU oracle (as it stands, single thread) on a bounded sample of
-    the workload and extrapolate the whole job.  Returns (job_seconds, sample_desc)."""
+def cpu_info():
+    """Host CPU model and the threads this process may use (the baseline's core count)."""
+    import oracle.sharded as OS
+
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": OS.host_threads(), "cpu_count": os.cpu_count()}
+
+
+def oracle_pass(wl, frac, threads):
+    """The CPU oracle (as it stands) over a leading fraction of the workload: the first frac*N
+    records are measured, then the first frac*S scenarios are resolved (only the launches they
+    reference) and replayed against that table.  threads > 1: the all-core sharded driver
+    (oracle/sharded.py: record shards + halo merged by or_table_merge, scenario slices); 1: the
+    single-threaded oracle.  Returns (seconds, records, scenarios)."""
     import oracle
+    import oracle.sharded as OS
+    import fikit_synth as F
 
     oracle.build()
     recs, names, sigs = wl["records"], wl["names"], wl["sigs"]
-    # calibrate on a small slice, then size the measure sample to ~60 % of the budget
-    n0 = min(recs.shape[0], 100_000)
-    t = time.perf_counter()
-    oracle.measure(recs[:n0], names, sigs, capacity=65536)
-    r0 = n0 / max(1e-9, time.perf_counter() - t)
-    n1 = int(min(recs.shape[0], max(n0, r0 * budget_s * 0.6)))
-    t = time.perf_counter()
-    tab, _, _ = oracle.measure(recs[:n1], names, sigs, capacity=65536)
-    t_meas = time.perf_counter() - t
-    job = t_meas * (wl["N"] / n1)
-    desc = f"oracle measure on the first {n1:,} of {wl['N']:,} records"
+    N = recs.shape[0]
+    n1 = max(1, min(N, int(round(frac * N))))
     rp = wl["replay"]
-    if rp is not None:
+    prep = None
+    if rp is not None:  # host-side data placement (outside the timed part): the scenarios' launches only
         S = rp.scenarios.shape[0]
-        # a bounded set of scenarios, resolving only the launches they reference
-        s_n = max(1, min(S, 200, int(budget_s * 40)))  # ~2.5 ms of oracle work per scenario
-        sc = rp.scenarios[:s_n].copy()
-        hp_idx = np.concatenate([np.arange(c["hp_off"], c["hp_off"] + c["hp_len"]) for c in sc]).astype(np.int64)
-        lp_idx = np.concatenate([np.arange(c["lp_off"], c["lp_off"] + c["lp_len"]) for c in sc]).astype(np.int64)
-        t = time.perf_counter()
-        hr, hd, hg, _ = oracle.resolve(rp.hp_records[hp_idx], names, sigs, tab)
-        lr, ld, lg, _ = oracle.resolve(rp.lp_records[lp_idx], names, sigs, tab)
-        off_h = np.concatenate([[0], np.cumsum(sc["hp_len"][:-1])]).astype(np.uint32)
-        off_l = np.concatenate([[0], np.cumsum(sc["lp_len"][:-1])]).astype(np.uint32)
-        sc["hp_off"], sc["lp_off"] = off_h, off_l
-        if wl.get("lp_stream") is not None:  # STREAM model (think times: the resolved LP gaps)
+        s_n = max(1, min(S, int(round(frac * S))))
+        sel = F.Replay(rp.hp_records, rp.lp_records, rp.lp_level, rp.scenarios[:s_n].copy(), rp.threshold_ns,
+                       rp.feedback)
+        lp_stream = wl["lp_stream"]
+        sub, sub_stream = compact_replay(sel, lp_stream)
+        prep = (sub, sub_stream, s_n)
+    t = time.perf_counter()
+    tab, st = OS.measure(recs[:n1], names, sigs, capacity=max(65536, wl["cap"]), threads=threads)
+    if st["code"] != 0:
+        raise RuntimeError(f"oracle measure: {st}")
+    s_n = 0
+    if prep is not None:
+        sub, sub_stream, s_n = prep
+        hr, hd, hg = OS.resolve(sub.hp_records, names, sigs, tab, threads=threads)
+        lr, ld, lg = OS.resolve(sub.lp_records, names, sigs, tab, threads=threads)
+        if sub_stream is not None:  # STREAM model (think times: the resolved LP gaps)
             ha = wl["hp_arrival"][:s_n] if wl.get("hp_arrival") is not None else None
-            oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg, sc,
-                                         tab, rp.threshold_ns, rp.feedback, hp_arrival=ha)
+            OS.simulate_stream_batch(hr, hd, hg, lr, ld, sub.lp_level, sub_stream, lg, sub.scenarios, tab,
+                                     sub.threshold_ns, sub.feedback, hp_arrival=ha, threads=threads)
             if wl.get("ratio") is not None:  # the exclusive arm (no gap filled)
-                oracle.simulate_stream_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], wl["lp_stream"][lp_idx], lg,
-                                             sc, tab, (1 << 64) - 1, rp.feedback)
+                OS.simulate_stream_batch(hr, hd, hg, lr, ld, sub.lp_level, sub_stream, lg, sub.scenarios, tab,
+                                         (1 << 64) - 1, sub.feedback, threads=threads)
         else:
-            oracle.simulate_batch(hr, hd, hg, lr, ld, rp.lp_level[lp_idx], sc, tab, rp.threshold_ns, rp.feedback)
-        t_rep = time.perf_counter() - t
-        job += t_rep * (S / s_n)
-        desc += f" + resolve/replay of {s_n} of {S:,} scenarios"
-    return job, desc + "; whole-job time extrapolated linearly"
+            OS.simulate_batch(hr, hd, hg, lr, ld, sub.lp_level, sub.scenarios, tab, sub.threshold_ns, sub.feedback,
+                              threads=threads)
+    return time.perf_counter() - t, n1, s_n
+
+
+def calibrate_frac(wl, threads, seconds):
+    """The workload fraction the oracle finishes in about `seconds` with `threads` threads."""
+    N = wl["records"].shape[0]
+    f0 = min(1.0, max(1.0 / N, 2e5 * threads / N))
+    t0, _, _ = oracle_pass(wl, f0, threads)
+    return min(1.0, f0 * seconds / max(1e-3, t0))
+
+
+def cpu_baseline(wl, budget_s):
+    """SURVEY §8d oracle timing: (ii) all host threads (the sharded driver) -- a full,
+    non-extrapolated pass when it fits the budget, else the largest leading fraction that does;
+    (i) one thread on a bounded leading fraction, extrapolated.  The baseline value is (ii)."""
+    import oracle.sharded as OS
+
+    info = cpu_info()
+    T = OS.host_threads()
+    N = wl["N"]
+    f_all = calibrate_frac(wl, T, budget_s * 0.6)
+    t_all, n_all, s_all = oracle_pass(wl, f_all, T)
+    f_one = calibrate_frac(wl, 1, budget_s * 0.25)
+    t_one, n_one, s_one = oracle_pass(wl, f_one, 1)
+    S = wl["replay"].scenarios.shape[0] if wl["replay"] is not None else 0
+    full = n_all == wl["records"].shape[0] and s_all == S
+    desc = (f"oracle, {T} threads (oracle/sharded.py): "
+            + ("the FULL workload, not extrapolated" if full else f"the first {n_all:,} records + {s_all:,} "
+               f"scenarios (a {n_all / N:.3f} fraction)") + f" in {t_all:.2f} s")
+    return {"value": n_all / t_all, "unit": UNIT, "cores": T, "kind": "oracle", "sample": desc,
+            "full_pass": bool(full), "seconds": t_all, **info,
+            "single_core": {"value": n_one / t_one, "unit": UNIT, "cores": 1,
+                            "sample": f"the first {n_one:,} records + {s_one:,} scenarios in {t_one:.2f} s "
+                                      f"(value = records / time of that leading fraction)"}}
 
 
 def ratio_summary(fik, exc, ratio, sc):
@@ -309,25 +358,35 @@ def ratio_summary(fik, exc, ratio, sc):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (the tier's reference arm), rank 0 only."""
+    """--impl reference: the CPU oracle (this tier's reference arm) on every host thread (the
+    sharded driver), rank 0 only.  A step = one oracle pass over a leading fraction of the same
+    workload (records and scenarios in the workload's proportion), sized so the whole
+    --steps/--warmup run takes about 2.5 minutes; value = records per step / step time, the same
+    definition as the fikit arm's (records / time of a step that measures and replays)."""
+    import oracle.sharded as OS
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     wl = make_workload(args, 0, 1)
-    per_step = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
-    times = []
-    desc = ""
+    T = OS.host_threads()
+    per_step = max(0.3, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    frac = calibrate_frac(wl, T, per_step)
+    times, n1, s1 = [], 0, 0
     for i in range(args.warmup + args.steps):
-        job, desc = oracle_sample_time(wl, per_step)
+        t, n1, s1 = oracle_pass(wl, frac, T)
         if i >= args.warmup:
-            times.append(job)
-    job = float(np.median(times))
-    value = wl["N"] / job
+            times.append(t)
+    step_s = float(np.mean(times))
+    value = n1 / step_s
+    desc = (f"oracle on {T} threads (oracle/sharded.py); each step: the first {n1:,} of {wl['N']:,} records + "
+            f"{s1:,} scenarios")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": job * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": wl["desc"], "records": wl["N"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (fikit_synth, seeded)",
+            "config": {"workload": wl["desc"], "records": wl["N"], "records_per_step": n1, "scenarios_per_step": s1},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle", "sample": desc,
+                             **cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -422,7 +481,16 @@ def main():
         stage_ms += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]), 0]
     stage_ms /= n_stage
 
-    # ---- timed region: K back-to-back steps, barrier + sync on both sides ----
+    # ---- timed region: K steps, barrier + sync on both sides.  Inputs larger than 2x the L2
+    # (the Zipf trace: 4.8 GB) stream from HBM anyway: the K steps run back to back between two
+    # events.  Smaller inputs (BERT/VGG: 10 MB) would stay L2-resident, so L2 is flushed before
+    # every step (a 256 MB write, outside the step's own event pair) and the step time is the sum
+    # of the per-step event pairs. ----
+    in_bytes = p.recs.numel() + (sum(p.replay[k].numel() * p.replay[k].element_size()
+                                     for k in ("hp_recs", "lp_recs", "lp_level", "sc")) if p.replay else 0)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda") if in_bytes < 2 * L2_BYTES else None
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)] \
+        if flush is not None else None
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = fk.launch_count()
     with ClockSampler(dev_index) as clk:
@@ -431,13 +499,21 @@ def main():
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+                sev[i][0].record(stream)
             step(False, kev[i])
+            if flush is not None:
+                sev[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    ms = (sum(a.elapsed_time(b) for a, b in sev) if flush is not None else t0.elapsed_time(t1)) / args.steps
+    l2_note = (f"inputs ({in_bytes / 1e6:.0f} MB) larger than 2x the 126 MB L2: steps back to back, no flush"
+               if flush is None else f"inputs ({in_bytes / 1e6:.1f} MB) fit the L2: a {L2_FLUSH_BYTES >> 20} MB "
+               f"write flushes L2 before every step (outside the step's event pair)")
     launches = fk.launch_count() - launches0
-    ms = t0.elapsed_time(t1) / args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -472,7 +548,7 @@ def main():
             "config": {"workload": wl["desc"] + (f" predictor={args.predictor}" if args.predictor else ""),
                        "records": N, "records_per_gpu": n_local, "scenarios": S_total,
                        "table_rows": p.table.n_rows() if world == 1 else dense.n_rows(),
-                       "l2": "inputs (4.8 GB trace) larger than the 126 MB L2; no flush",
+                       "l2": l2_note,
                        "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},
             "scenarios_per_s": (S_total / (ms * 1e-3)) if S_total else None,
             "stages_ms": {"measure": stage_ms[0], "finalize+merge": stage_ms[1], "resolve+replay": stage_ms[2]},
@@ -533,9 +609,7 @@ def main():
             print("verify-merge: MISMATCH", file=sys.stderr)
     # ---- CPU baseline: the oracle on the host cores, rank 0, N=1 only ----
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        job, desc = oracle_sample_time(wl, args.cpu_budget_s)
-        line["cpu_baseline"] = {"value": N / job, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "host_cores_available": os.cpu_count()}
+        line["cpu_baseline"] = cpu_baseline(wl, args.cpu_budget_s)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

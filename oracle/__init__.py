@@ -87,6 +87,7 @@ def lib():
         _lib.or_predict.argtypes = [C.POINTER(_Table), u32, u32]
         _lib.or_simulate_batch.argtypes = [p, p, p, p, p, p, p, u32, p, p, p, u32, u64, u32, p, p, p, p,
                                            C.POINTER(Status)]
+        _lib.or_table_merge.argtypes = [C.POINTER(_Table), u32, C.POINTER(_Table), C.POINTER(Status)]
     return _lib
 
 
@@ -149,16 +150,26 @@ class Table:
         return {k: (getattr(self, k)[:n]) for k in self.__dataclass_fields__ if k != "n_rows"}
 
 
-def measure(records: np.ndarray, names, sigs, capacity: int | None = None, halo: np.ndarray | None = None,
-            want_rows: bool = False):
-    n = records.shape[0]
-    cap = max(1, capacity if capacity is not None else n)
+def _table_arrays(cap: int) -> dict:
     arrs = {k: np.zeros(cap, dtype=np.uint64) for k in ("kernel_id", "dur_cnt", "dur_sum", "dur_min", "dur_max",
                                                        "gap_cnt", "gap_sum", "gap_min", "gap_max", "dur_mean",
                                                        "gap_mean")}
     arrs["task_id"] = np.zeros(cap, dtype=np.uint32)
     arrs["dur_hist"] = np.zeros((cap, NBINS), dtype=np.uint32)
     arrs["gap_hist"] = np.zeros((cap, NBINS), dtype=np.uint32)
+    return arrs
+
+
+def _ctable(tab: "Table") -> _Table:
+    arrs = {k: getattr(tab, k) for k in tab.__dataclass_fields__ if k != "n_rows"}
+    return _Table(**{k: _ptr(v) for k, v in arrs.items()}, capacity=arrs["kernel_id"].shape[0], n_rows=tab.n_rows)
+
+
+def measure(records: np.ndarray, names, sigs, capacity: int | None = None, halo: np.ndarray | None = None,
+            want_rows: bool = False):
+    n = records.shape[0]
+    cap = max(1, capacity if capacity is not None else n)
+    arrs = _table_arrays(cap)
     t = _Table(**{k: _ptr(v) for k, v in arrs.items()}, capacity=cap, n_rows=0)
     rows = np.zeros(n, dtype=np.uint32) if want_rows else None
     st = Status()
@@ -167,6 +178,16 @@ def measure(records: np.ndarray, names, sigs, capacity: int | None = None, halo:
     lib().or_measure(_ptr(rec), n, _ptr(h), _st(names), _st(sigs), C.byref(t), _ptr(rows), C.byref(st))
     tab = Table(n_rows=t.n_rows, **arrs)
     return tab, st.as_dict(), rows
+
+
+def table_merge(parts: list, capacity: int):
+    """Union of per-shard tables (or_table_merge): returns (Table, status)."""
+    arrs = _table_arrays(max(1, capacity))
+    out = _Table(**{k: _ptr(v) for k, v in arrs.items()}, capacity=max(1, capacity), n_rows=0)
+    cparts = (_Table * max(1, len(parts)))(*[_ctable(t) for t in parts])
+    st = Status()
+    lib().or_table_merge(cparts, len(parts), C.byref(out), C.byref(st))
+    return Table(n_rows=out.n_rows, **arrs), st.as_dict()
 
 
 def resolve(records: np.ndarray, names, sigs, tab: Table, halo: np.ndarray | None = None):

@@ -17,6 +17,7 @@
  *   or_best_prio_fit   Algorithm 2                    P:332-334, R14-R16
  *   or_fikit_fill      Algorithm 1 (one gap)          P:328-330, R13, R17-R19
  *   or_simulate        replay of one HP/LP scenario   P:286-313, R20-R24
+ *   or_table_merge     union of per-shard tables      P:246-256, SURVEY §8e (all-core driver)
  *
  * Parity pins (tests/test_oracle_*.py) -- none of them re-types these
  * formulas: published FNV-1a / splitmix64 vectors, the paper's worked
@@ -821,5 +822,100 @@ int or_simulate_stream_batch(const uint32_t* hp_row, const uint64_t* hp_dur, con
                                 fill_gap + sched_off[i], lp_start + sched_off[i]);
     if (rc) return rc;
   }
+  return OR_OK;
+}
+
+/* ---- merge of per-shard tables (the all-core CPU baseline's
+ * sharded driver, oracle/sharded.py).  Each part is the or_measure table of
+ * one contiguous record shard whose last gap used the next shard's first
+ * record as its halo (R5), so every launch and every gap was counted by
+ * exactly one part.  S_UID of the whole trace is the union of the
+ * parts' rows, and the statistics of a row j are sums / minima / maxima over
+ * the parts that saw j: SK_j = (sum of K over all occurrences) / (count of all
+ * occurrences), likewise SG_j; the integer mean is R8.
+ * Plain form: collect every (task, kernel_id, part, row) key, sort it in the
+ * canonical order (R11), walk runs of equal (task, kernel_id). ------------ */
+typedef struct {
+  uint32_t task;
+  uint64_t kid;
+  uint32_t part, row;
+} opkey_t;
+
+static int cmp_pkey(const void* a, const void* b) {
+  const opkey_t* x = (const opkey_t*)a;
+  const opkey_t* y = (const opkey_t*)b;
+  if (x->task != y->task) return x->task < y->task ? -1 : 1;
+  if (x->kid != y->kid) return x->kid < y->kid ? -1 : 1;
+  if (x->part != y->part) return x->part < y->part ? -1 : 1;
+  return 0;
+}
+
+int or_table_merge(const otable_t* parts, uint32_t P, otable_t* out, ostatus_t* st) {
+  status_init(st);
+  out->n_rows = 0;
+  uint64_t total = 0;
+  for (uint32_t p = 0; p < P; p++) total += parts[p].n_rows;
+  opkey_t* keys = (opkey_t*)malloc((total ? total : 1) * sizeof(opkey_t));
+  uint64_t k = 0;
+  for (uint32_t p = 0; p < P; p++)
+    for (uint32_t r = 0; r < parts[p].n_rows; r++) {
+      keys[k].task = parts[p].task_id[r];
+      keys[k].kid = parts[p].kernel_id[r];
+      keys[k].part = p;
+      keys[k].row = r;
+      k++;
+    }
+  qsort(keys, total, sizeof(opkey_t), cmp_pkey);
+  uint64_t distinct = 0;
+  for (uint64_t i = 0; i < total; i++)
+    if (i == 0 || keys[i].task != keys[i - 1].task || keys[i].kid != keys[i - 1].kid) distinct++;
+  if (distinct > out->capacity) {
+    free(keys);
+    st->code = OR_E_CAPACITY;
+    st->n_rows_needed = distinct;
+    return OR_E_CAPACITY;
+  }
+  uint32_t row = 0;
+  for (uint64_t a = 0; a < total;) {
+    uint64_t b = a;
+    while (b < total && keys[b].task == keys[a].task && keys[b].kid == keys[a].kid) b++;
+    uint64_t dc = 0, ds = 0, dmin = UINT64_MAX, dmax = 0, gc = 0, gs = 0, gmin = UINT64_MAX, gmax = 0;
+    uint32_t* dh = out->dur_hist + (uint64_t)row * NBINS;
+    uint32_t* gh = out->gap_hist + (uint64_t)row * NBINS;
+    memset(dh, 0, NBINS * sizeof(uint32_t));
+    memset(gh, 0, NBINS * sizeof(uint32_t));
+    for (uint64_t j = a; j < b; j++) {
+      const otable_t* t = &parts[keys[j].part];
+      uint32_t r = keys[j].row;
+      dc += t->dur_cnt[r];
+      ds += t->dur_sum[r];
+      if (t->dur_min[r] < dmin) dmin = t->dur_min[r];
+      if (t->dur_max[r] > dmax) dmax = t->dur_max[r];
+      gc += t->gap_cnt[r];
+      gs += t->gap_sum[r];
+      if (t->gap_min[r] < gmin) gmin = t->gap_min[r];
+      if (t->gap_max[r] > gmax) gmax = t->gap_max[r];
+      for (int x = 0; x < NBINS; x++) {
+        dh[x] += t->dur_hist[(uint64_t)r * NBINS + x];
+        gh[x] += t->gap_hist[(uint64_t)r * NBINS + x];
+      }
+    }
+    out->kernel_id[row] = keys[a].kid;
+    out->task_id[row] = keys[a].task;
+    out->dur_cnt[row] = dc;
+    out->dur_sum[row] = ds;
+    out->dur_min[row] = dmin;
+    out->dur_max[row] = dmax;
+    out->gap_cnt[row] = gc;
+    out->gap_sum[row] = gs;
+    out->gap_min[row] = gmin;
+    out->gap_max[row] = gmax;
+    out->dur_mean[row] = mean_of(ds, dc); /* SK_j over all parts */
+    out->gap_mean[row] = mean_of(gs, gc); /* SG_j over all parts */
+    row++;
+    a = b;
+  }
+  out->n_rows = row;
+  free(keys);
   return OR_OK;
 }

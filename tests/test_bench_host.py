@@ -54,3 +54,16 @@ def test_compact_replay_stream_and_empty_windows(bench):
     sub = F.Replay(rp.hp_records, rp.lp_records, rp.lp_level, sc[sel], rp.threshold_ns, rp.feedback)
     c, ls = bench.compact_replay(sub, sr.lp_stream)
     assert run(c, ls).tobytes() == full[sel].tobytes()
+
+
+def test_cpu_baseline_leg(bench):
+    # the all-core oracle leg of the bench line (SURVEY §8d oracle timing (i) + (ii)) on a small workload
+    cfg = F.bert_vgg(S=3000)
+    wl = dict(records=cfg.trace.records, names=cfg.trace.names, sigs=cfg.trace.sigs, replay=cfg.replay,
+              N=cfg.trace.records.shape[0], cap=1024, lp_stream=None, hp_arrival=None, ratio=None)
+    cb = bench.cpu_baseline(wl, 4.0)
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert cb["single_core"]["cores"] == 1 and cb["single_core"]["value"] > 0
+    assert cb["full_pass"]  # this small workload fits the budget: no extrapolation
+    t, n1, s1 = bench.oracle_pass(wl, 0.25, 2)
+    assert n1 == round(0.25 * wl["N"]) and s1 == 750 and t > 0
