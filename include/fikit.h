@@ -31,7 +31,7 @@
  *  - Data errors are detected on the device and accumulated in the
  *    workspace status (fikit_status_t), reset by every call that validates
  *    records (identify, measure, resolve, fill, simulate) and read with
- *    fikit_get_status().  Precedence: E_ARG > E_NAME > E_RECORD > E_CAPACITY.
+ *    fikit_get_status().  Precedence: E_ARG > E_NAME > E_RECORD > E_DICT > E_CAPACITY.
  *    Outputs of a call whose status is not FIKIT_OK are unspecified.
  *  - All times are unsigned 64-bit nanoseconds; sums wrap mod 2^64 (R10).
  *  - "R<k>" = reading k of a silent/garbled passage, DESIGN.md §Readings.
@@ -52,7 +52,9 @@ enum {
   FIKIT_E_RECORD = -2,   /* invalid record / LP level; first_bad_index = smallest such index */
   FIKIT_E_CAPACITY = -3, /* more distinct (task, kernel) rows than table capacity; n_rows_needed */
   FIKIT_E_CUDA = -4,     /* kernel launch failed */
-  FIKIT_E_NAME = -5      /* empty kernel name in the names table (SPEC) */
+  FIKIT_E_NAME = -5,     /* empty kernel name in the names table (SPEC) */
+  FIKIT_E_DICT = -6      /* fikit_measure_dict: a launch identity is not in the supplied dictionary;
+                            first_missing_index = smallest such launch index */
 };
 
 #define FIKIT_NBINS 32         /* log2 histogram bins per statistic (R9) */
@@ -113,6 +115,8 @@ typedef struct {
   uint32_t schedule;        /* measure: 0 = address-order sweep with one global hot set,
                                1 = warp-tiles sorted by task bucket, per-bucket hot sets */
   uint32_t n_task_buckets;  /* measure, schedule 1: non-empty task buckets */
+  uint64_t first_missing_index; /* fikit_measure_dict: smallest launch index whose (task, kernel ID)
+                                   is not in the dictionary (E_DICT); ~0 if none */
 } fikit_status_t;
 
 /* Scenario of the batch replay: HP template kernels [hp_off, hp_off+hp_len) and
@@ -172,12 +176,34 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
                   fikit_strtab_t sigs, const fikit_table_t* tab /* host struct, device arrays */,
                   uint32_t* out_row, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- measure against a supplied dictionary (SURVEY §8e "B200-native upgrade": repeated
+ * services keep their kernel IDs from run to run) ------------------------------------
+ * As fikit_measure, but the table's rows are fixed in advance: row j is the j-th key
+ * (dict_task[j], dict_kid[j]) of the dictionary, dict_n keys (host value, 1 <= dict_n <=
+ * tab->capacity) in strictly increasing canonical order (task_id, then kernel_id; R11) --
+ * e.g. the kernel_id / task_id columns of an earlier finalized or merged table.  No row is
+ * created: a launch whose (task, KID) is absent sets FIKIT_E_DICT (first_missing_index) and is
+ * not counted.  The following fikit_table_finalize keeps the dictionary order (no sort; n_rows =
+ * dict_n, rows without launches have count 0, mean 0, min 2^64-1, max 0), so tables measured
+ * against one dictionary on several ranks merge by two all-reduces alone (fikit_table_bias,
+ * SUM over sums + hist, MAX over ext, fikit_table_bias, fikit_table_means): no key exchange, no
+ * union, no remap.  A dictionary that is not strictly increasing sets FIKIT_E_ARG. */
+int fikit_measure_dict(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next, fikit_strtab_t names,
+                       fikit_strtab_t sigs, const uint64_t* dict_kid, const uint32_t* dict_task, uint32_t dict_n,
+                       const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes, void* stream);
+/* fikit_measure_dict with fikit_measure_timed's events around the streaming kernel. */
+int fikit_measure_dict_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next,
+                             fikit_strtab_t names, fikit_strtab_t sigs, const uint64_t* dict_kid,
+                             const uint32_t* dict_task, uint32_t dict_n, const fikit_table_t* tab, uint32_t* out_row,
+                             void* ws, size_t ws_bytes, void* stream, void* ev_start, void* ev_stop);
+
 /* ---- finalize --------------------------------------------------
  * Sorts the rows of a measured table by (task_id asc, kernel_id asc) (R11),
  * sets n_rows, dur_cnt/gap_cnt (histogram totals) and SK_j / SG_j =
  * floor(sum/cnt) + [2(sum mod cnt) >= cnt] (R8; cnt = 0 -> 0).  If out_row is
  * non-null its n entries are remapped to canonical rows.  Must follow the
- * fikit_measure that filled `tab` with the same workspace. */
+ * fikit_measure (or fikit_measure_dict: dictionary order kept) that filled `tab` with the same
+ * workspace. */
 int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n, void* ws, size_t ws_bytes,
                          void* stream);
 

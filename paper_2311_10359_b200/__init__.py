@@ -19,11 +19,11 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfikit.so")
 
-OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME = 0, -1, -2, -3, -4, -5
+OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME, E_DICT = 0, -1, -2, -3, -4, -5, -6
 NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
-           "fikit_measure_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
+           "fikit_measure_timed", "fikit_measure_dict", "fikit_measure_dict_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
            "fikit_simulate_batch", "fikit_simulate_stream_batch",
            "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
@@ -47,7 +47,7 @@ class TableC(C.Structure):
 class StatusC(C.Structure):
     _fields_ = [("code", C.c_int32), ("flags", C.c_uint32), ("first_bad_index", C.c_uint64),
                 ("n_rows_needed", C.c_uint64), ("n_overlap_gaps", C.c_uint64), ("schedule", C.c_uint32),
-                ("n_task_buckets", C.c_uint32)]
+                ("n_task_buckets", C.c_uint32), ("first_missing_index", C.c_uint64)]
 
 
 class FillParamsC(C.Structure):
@@ -76,6 +76,9 @@ def lib():
         L.fikit_identify.argtypes = [p, u64, StrTabC, StrTabC, p, p, sz, p]
         L.fikit_measure.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, sz, p]
         L.fikit_measure_timed.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, sz, p, p, p]
+        L.fikit_measure_dict.argtypes = [p, u64, p, StrTabC, StrTabC, p, p, u32, C.POINTER(TableC), p, p, sz, p]
+        L.fikit_measure_dict_timed.argtypes = [p, u64, p, StrTabC, StrTabC, p, p, u32, C.POINTER(TableC), p, p, sz,
+                                               p, p, p]
         L.fikit_table_finalize.argtypes = [C.POINTER(TableC), p, u64, p, sz, p]
         L.fikit_table_means.argtypes = [C.POINTER(TableC), p]
         L.fikit_table_predict.argtypes = [C.POINTER(TableC), u32, u32, p]
@@ -239,7 +242,7 @@ def get_status(ws: Workspace, stream=None) -> dict:
     lib().fikit_get_status(ws.ptr(), C.byref(st), _stream(stream))
     return {"code": st.code, "flags": st.flags, "first_bad_index": st.first_bad_index,
             "n_rows_needed": st.n_rows_needed, "n_overlap_gaps": st.n_overlap_gaps, "schedule": st.schedule,
-            "n_task_buckets": st.n_task_buckets}
+            "n_task_buckets": st.n_task_buckets, "first_missing_index": st.first_missing_index}
 
 
 def check(ws: Workspace, what="", stream=None) -> dict:
@@ -256,9 +259,23 @@ def identify(recs, n: int, names: DevStrTab, sigs: DevStrTab, out_kid, ws: Works
 
 
 def measure(recs, n: int, names: DevStrTab, sigs: DevStrTab, table: Table, ws: Workspace, halo=None, out_row=None,
-            stream=None, events=None):
+            stream=None, events=None, dictionary=None):
     """events: (start, stop) torch.cuda.Event pair recorded around the fused streaming kernel
-    (fikit_measure_timed; the events must exist, i.e. have been recorded once)."""
+    (fikit_measure_timed; the events must exist, i.e. have been recorded once).  dictionary:
+    (kid int64 device tensor, task int32 device tensor, n) -> fikit_measure_dict(_timed)."""
+    if dictionary is not None:
+        dk, dt, dn = dictionary
+        if events is None:
+            _chk(lib().fikit_measure_dict(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), _ptr(dk), _ptr(dt), int(dn),
+                                          C.byref(table.c), _ptr(out_row), ws.ptr(), ws.nbytes, _stream(stream)),
+                 "measure_dict")
+        else:
+            e0, e1 = events
+            _chk(lib().fikit_measure_dict_timed(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), _ptr(dk), _ptr(dt),
+                                                int(dn), C.byref(table.c), _ptr(out_row), ws.ptr(), ws.nbytes,
+                                                _stream(stream), C.c_void_p(e0.cuda_event),
+                                                C.c_void_p(e1.cuda_event)), "measure_dict_timed")
+        return
     if events is None:
         _chk(lib().fikit_measure(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),
                                  ws.ptr(), ws.nbytes, _stream(stream)), "measure")

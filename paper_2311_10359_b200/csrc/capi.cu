@@ -19,10 +19,14 @@ __global__ void k_plan(PlanArgs);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
                           uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, RawTab, Tuple*,
                           const Tuple*, const uint32_t*, uint32_t*, uint32_t*, const uint32_t*, const uint32_t*,
-                          const uint32_t*, const uint32_t*, uint32_t, uint32_t*);
+                          const uint32_t*, const uint32_t*, uint32_t, uint32_t*, uint32_t);
 size_t measure_smem_bytes();
 int measure_threads();
-__global__ void k_finalize(const fikit_status_t*, const RawRow*, uint32_t, fikit_table_t, uint32_t*, uint32_t*);
+__global__ void k_fin_sort(const fikit_status_t*, const RawRow*, uint32_t, fikit_table_t, FinKey*, const uint32_t*);
+__global__ void k_fin_scatter(const fikit_status_t*, const RawRow*, uint32_t, uint32_t, const FinKey*, fikit_table_t,
+                              uint32_t*, const uint32_t*);
+__global__ void k_dict_load(const uint64_t*, const uint32_t*, uint32_t, IndexEntry*, uint32_t, RawRow*,
+                            fikit_status_t*, uint32_t*);
 __global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
 __global__ void k_means(fikit_table_t);
 __global__ void k_predict(fikit_table_t, uint32_t, uint32_t);
@@ -69,7 +73,7 @@ namespace {
 // device and published with a relaxed atomic store, so concurrent first calls only repeat the
 // same query and a second device gets its own entry (no per-process "first device" state).
 constexpr int kMaxDevices = 64;
-enum : int { kPropSms, kPropWaveReg, kPropWaveSmem, kPropWaveStream, kPropMeasureAttr, kNumProps };
+enum : int { kPropSms, kPropWaveReg, kPropWaveSmem, kPropWaveStream, kPropMeasureAttr, kPropFinAttr, kNumProps };
 std::atomic<int> g_prop[kMaxDevices][kNumProps];  // 0 = not computed yet
 
 int cur_device() {
@@ -114,16 +118,23 @@ struct Ws {
   unsigned char* base;
   WsLayout L;
   fikit_status_t* st() const { return reinterpret_cast<fikit_status_t*>(base + L.status); }
+  uint32_t* misc() const { return reinterpret_cast<uint32_t*>(base + L.misc); }
   uint64_t* name_hash() const { return reinterpret_cast<uint64_t*>(base + L.name_hash); }
   uint64_t* sig_hash() const { return reinterpret_cast<uint64_t*>(base + L.sig_hash); }
   IndexEntry* index() const { return reinterpret_cast<IndexEntry*>(base + L.index); }
   Tuple* row_tuple() const { return reinterpret_cast<Tuple*>(base + L.row_tuple); }
   Tuple* tindex() const { return reinterpret_cast<Tuple*>(base + L.tindex); }
-  uint32_t* samp_cnt() const { return reinterpret_cast<uint32_t*>(base + L.samp_cnt); }
+  SampEntry* samp() const { return reinterpret_cast<SampEntry*>(base + L.samp); }
+  uint32_t* samp_list() const {
+    return reinterpret_cast<uint32_t*>(base + L.samp + align256(sizeof(SampEntry) * (size_t)kSampSlots));
+  }
   uint32_t* hot_n() const { return reinterpret_cast<uint32_t*>(base + L.hot); }  // header [kHotHdr]
   Tuple* hot() const { return reinterpret_cast<Tuple*>(base + L.hot + 4ull * kHotHdr); }  // [kBuckets + 1][kHotMax]
   RawRow* raw() const { return reinterpret_cast<RawRow*>(base + L.raw); }
-  uint32_t* rank() const { return reinterpret_cast<uint32_t*>(base + L.rank); }  // [cap], then fin_done[]
+  uint32_t* rank() const { return reinterpret_cast<uint32_t*>(base + L.rank); }  // [cap]
+  FinKey* fin_keys(uint32_t cap) const {  // [cap], after rank[]
+    return reinterpret_cast<FinKey*>(base + L.rank + align256(4ull * cap));
+  }
   uint32_t* cur() const { return reinterpret_cast<uint32_t*>(base + L.tiles); }   // [kSchedWords]
   uint32_t* act() const { return cur() + kSchedWords; }                           // [kSchedWords]
   uint32_t* bstart() const { return act() + kSchedWords; }                        // [kSchedWords]
@@ -234,11 +245,14 @@ int fikit_identify(const fikit_record_t* recs, uint64_t n, fikit_strtab_t names,
 
 static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
                         fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws,
-                        size_t ws_bytes, void* stream, cudaEvent_t ev0, cudaEvent_t ev1) {
+                        size_t ws_bytes, void* stream, cudaEvent_t ev0, cudaEvent_t ev1,
+                        const uint64_t* dict_kid = nullptr, const uint32_t* dict_task = nullptr,
+                        uint32_t dict_n = 0) {
   cudaStream_t s = (cudaStream_t)stream;
   Ws w;
+  const bool dict = dict_kid != nullptr;
   if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs) ||
-      !table_ok(tab))
+      !table_ok(tab) || (dict && (!dict_task || dict_n == 0 || dict_n > tab->capacity)))
     return FIKIT_E_ARG;
   if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w, n)) return r;
   const uint32_t cap = tab->capacity;
@@ -253,12 +267,17 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   add(w.raw(), sizeof(RawRow) * (size_t)cap);
   add(w.index(), sizeof(IndexEntry) * (size_t)w.L.slots);
   add(w.tindex(), sizeof(Tuple) * (size_t)w.L.tslots);
-  add(w.samp_cnt(), 4ull * cap);
+  add(w.samp(), sizeof(SampEntry) * (size_t)kSampSlots);
+  add(w.misc(), 256);  // (dictionary word: none unless k_dict_load sets it)
   add(w.hot_n(), 4ull * kHotHdr);
   add(w.cur(), 16ull * kSchedWords);  // cur, act, bstart, btot
-  add(w.rank(), 4ull * cap + 4ull * ((cap + kFinRows - 1) / kFinRows));
   k_zero<<<2 * num_sms(), 256, 0, s>>>(z, w.st());
   if (int r = launched()) return r;
+  if (dict) {  // rows fixed in advance: dictionary key j -> row j
+    k_dict_load<<<(dict_n + 255) / 256, 256, 0, s>>>(dict_kid, dict_task, dict_n, w.index(), w.L.slots, w.raw(),
+                                                      w.st(), w.misc());
+    if (int r = launched()) return r;
+  }
   if (n == 0) return hash_strtabs(w, names, sigs, s);
   // persistent k_measure: one CTA per SM, fewer if there are not enough 64-launch warp-tiles
   const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
@@ -278,13 +297,10 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pa.sigs = sigs;
   pa.name_hash = w.name_hash();
   pa.sig_hash = w.sig_hash();
-  pa.idx = w.index();
-  pa.slots = w.L.slots;
-  pa.cap = cap;
   pa.st = w.st();
-  pa.raw = w.raw();
-  pa.row_tuple = w.row_tuple();
-  pa.samp_cnt = w.samp_cnt();
+  pa.samp = w.samp();
+  pa.samp_list = w.samp_list();
+  pa.samp_n = w.hot_n() + kSampN;
   pa.grp_bucket = w.grp_bucket();
   pa.blkcnt = w.blkcnt();
   pa.ngroups = ngroups;
@@ -299,9 +315,16 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   // 3. k_plan: hot sets + schedule mode | the groups' counting-sort scatter, bucket ranges, first buckets
   PlanArgs pl{};
   pl.st = w.st();
-  pl.samp_cnt = w.samp_cnt();
+  pl.samp = w.samp();
+  pl.samp_list = w.samp_list();
+  pl.name_hash = w.name_hash();
+  pl.sig_hash = w.sig_hash();
+  pl.idx = w.index();
+  pl.slots = w.L.slots;
+  pl.raw = w.raw();
   pl.row_tuple = w.row_tuple();
   pl.cap = cap;
+  pl.dict = dict ? 1u : 0u;
   pl.hot_all = w.hot();
   pl.hot_hdr = w.hot_n();
   pl.grp_bucket = w.grp_bucket();
@@ -329,7 +352,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   k_measure<<<grid, measure_threads(), smem, s>>>(
       recs, n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, w.index(), w.L.slots, w.tindex(),
       w.L.tslots, w.st(), RawTab{w.raw(), cap}, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.act(), w.bstart(),
-      w.btot(), w.first(), w.order(), ntiles, out_row);
+      w.btot(), w.first(), w.order(), ntiles, out_row, dict ? 1u : 0u);
   if (int r = launched()) return r;
   if (ev1 && cudaEventRecord(ev1, s) != cudaSuccess) return FIKIT_E_CUDA;
   return FIKIT_OK;
@@ -348,6 +371,23 @@ int fikit_measure_timed(const fikit_record_t* recs, uint64_t n, const fikit_reco
                       (cudaEvent_t)ev_stop);
 }
 
+int fikit_measure_dict(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                       fikit_strtab_t sigs, const uint64_t* dict_kid, const uint32_t* dict_task, uint32_t dict_n,
+                       const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes, void* stream) {
+  if (!dict_kid) return FIKIT_E_ARG;
+  return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, nullptr, nullptr, dict_kid,
+                      dict_task, dict_n);
+}
+
+int fikit_measure_dict_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo,
+                             fikit_strtab_t names, fikit_strtab_t sigs, const uint64_t* dict_kid,
+                             const uint32_t* dict_task, uint32_t dict_n, const fikit_table_t* tab, uint32_t* out_row,
+                             void* ws, size_t ws_bytes, void* stream, void* ev_start, void* ev_stop) {
+  if (!dict_kid) return FIKIT_E_ARG;
+  return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, (cudaEvent_t)ev_start,
+                      (cudaEvent_t)ev_stop, dict_kid, dict_task, dict_n);
+}
+
 int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n, void* ws, size_t ws_bytes,
                          void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -356,9 +396,21 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   if (int r = get_ws(ws, ws_bytes, tab->capacity, 0, 0, &w)) return r;  // (the capacity-sized regions)
   const uint32_t cap = tab->capacity;
   uint32_t* rank = w.rank();
-  uint32_t* done = rank + cap;
-  k_finalize<<<dim3((cap + kFinRows - 1) / kFinRows, (cap + kFinGroup - 1) / kFinGroup), kFinRows, 0, s>>>(
-      w.st(), w.raw(), cap, *tab, rank, done);
+  k_fin_sort<<<(cap + kFinGroup - 1) / kFinGroup, kFinGroup / 2, 0, s>>>(w.st(), w.raw(), cap, *tab, w.fin_keys(cap), w.misc());
+  if (int r = launched()) return r;
+  // rows per scatter block: one wave of <= num_sms() blocks, at least 64 rows each
+  uint32_t R = (cap + num_sms() - 1) / num_sms();
+  R = R < 64 ? 64 : R > 4096 ? 4096 : (R + 31) / 32 * 32;
+  const size_t fsm = sizeof(FinKey) * (kFinChunk + (size_t)R) + 4ull * R;  // chunk + row keys + ranks
+  if (dev_prop(kPropFinAttr, [&](int) {
+        return cudaFuncSetAttribute(k_fin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(FinKey) * (kFinChunk + 4096) + 4 * 4096)) == cudaSuccess
+                   ? 1
+                   : -1;
+      }) < 0)
+    return FIKIT_E_CUDA;
+  k_fin_scatter<<<(cap + R - 1) / R, 256, fsm, s>>>(w.st(), w.raw(), cap, R, w.fin_keys(cap), *tab, rank,
+                                                    w.misc());
   if (int r = launched()) return r;
   if (out_row && n) {
     k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, tab->n_rows);
@@ -535,6 +587,7 @@ int fikit_get_status(const void* ws, fikit_status_t* out, void* stream) {
   out->code = (f & kStatusArg)        ? FIKIT_E_ARG
               : (f & kStatusName)     ? FIKIT_E_NAME
               : (f & kStatusRecord)   ? FIKIT_E_RECORD
+              : (f & kStatusDict)     ? FIKIT_E_DICT
               : (f & kStatusCapacity) ? FIKIT_E_CAPACITY
                                       : FIKIT_OK;
   return out->code;
@@ -548,6 +601,7 @@ const char* fikit_strerror(int code) {
     case FIKIT_E_CAPACITY: return "statistic table capacity exceeded";
     case FIKIT_E_CUDA: return "CUDA launch failure";
     case FIKIT_E_NAME: return "empty kernel name";
+    case FIKIT_E_DICT: return "launch identity not in the supplied dictionary";
     default: return "unknown";
   }
 }

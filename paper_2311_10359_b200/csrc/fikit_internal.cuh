@@ -7,7 +7,7 @@
 
 namespace fikit {
 
-constexpr uint32_t kStatusArg = 1u, kStatusName = 2u, kStatusRecord = 4u, kStatusCapacity = 8u;
+constexpr uint32_t kStatusArg = 1u, kStatusName = 2u, kStatusRecord = 4u, kStatusCapacity = 8u, kStatusDict = 16u;
 constexpr int kBins = FIKIT_NBINS;
 
 // ---- workspace layout ------------------------------------------------------
@@ -35,6 +35,19 @@ struct RawRow {
 };
 static_assert(sizeof(RawRow) == 336, "RawRow");
 
+// fikit_measure's launch sample (k_prep -> k_plan): distinct raw identities with their sample
+// counts, keyed by a 64-bit fingerprint of the identity (open addressing; fp 0 = empty).  The
+// sample only chooses the hot rows: a fingerprint collision merely credits one identity's
+// samples to another, and k_measure still resolves every launch exactly.
+struct SampEntry {
+  uint32_t cnt, task;  // (one 8-B load in k_plan's scans)
+  unsigned long long fp;
+  uint32_t w[6];  // the identity's other raw words (Tuple::w[0..5]; w[6] = task)
+};
+constexpr uint32_t kSampSlots = 32768;
+// the occupied slots are also listed densely (samp_list[0 .. hot header word kSampN)), so k_plan
+// scans only the distinct sampled identities
+
 // the workspace's measured rows as k_measure sees them
 struct RawTab {
   RawRow* rows;
@@ -42,7 +55,7 @@ struct RawTab {
 };
 
 struct WsLayout {
-  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp_cnt, hot, raw, rank, fin, tiles, total;
+  size_t status, misc, name_hash, sig_hash, index, tindex, row_tuple, samp, hot, raw, rank, fin, tiles, total;
   uint32_t slots, tslots;
   uint64_t ntiles;   // warp-tiles of 64 launches the workspace can schedule
   uint64_t ngroups;  // tile groups (kGroupTiles tiles) of the task-partitioned schedule
@@ -67,10 +80,15 @@ constexpr uint32_t kGlobalSet = kBuckets;  // hot-set index of the global (all-t
 constexpr uint32_t kCovTask = kBuckets + 1;  // samples whose row is in its task bucket's hot set
 constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the global hot set
 constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
+constexpr uint32_t kSampN = kBuckets + 4;  // distinct identities in the launch sample
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
-constexpr uint32_t kFinRows = 256;      // fikit_table_finalize: rows per block (x) ...
-constexpr uint32_t kFinGroup = 1024;    // ... keys per sorted group (y)
+constexpr uint32_t kFinGroup = 256;     // fikit_table_finalize: keys per sorted group (a warp's)
+constexpr uint32_t kFinChunk = 8192;    // ... sorted keys staged in shared memory at a time (128 KB)
+struct FinKey {                          // a sorted key of finalize's groups (workspace)
+  unsigned long long kid;
+  uint32_t task, pad;
+};
 constexpr int kRegThreads = 512;  // k_simulate_reg block (16 warps, one scenario each)
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
 constexpr int kStreamThreads = 128;  // k_simulate_stream block (4 warps, staged windows)
@@ -113,14 +131,16 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o = align256(o + sizeof(Tuple) * (size_t)L.tslots);
   L.row_tuple = o;
   o = align256(o + sizeof(Tuple) * (size_t)cap);
-  L.samp_cnt = o;
-  o = align256(o + 4ull * cap);
+  L.samp = o;  // SampEntry[kSampSlots], then samp_list[kSampSlots] (u32)
+  o = align256(o + sizeof(SampEntry) * (size_t)kSampSlots);
+  o = align256(o + 4ull * kSampSlots);
   L.hot = o;  // header[kHotHdr] (u32), then hot[kBuckets + 1][kHotMax] (Tuple)
   o = align256(o + 4ull * kHotHdr + sizeof(Tuple) * (size_t)kHotMax * (kBuckets + 1));
   L.raw = o;  // RawRow[cap]
   o = align256(o + sizeof(RawRow) * (size_t)cap);
-  L.rank = o;  // rank[cap] (u32), then fin_done[ceil(cap / kFinRows)] (u32)
-  o = align256(o + 4ull * cap + 4ull * ((cap + kFinRows - 1) / kFinRows));
+  L.rank = o;  // rank[cap] (u32), then the sorted key groups FinKey[cap]
+  o = align256(o + 4ull * cap);
+  o = align256(o + sizeof(FinKey) * (size_t)cap);
   L.name_hash = o;
   o = align256(o + 8ull * (n_names ? n_names : 1));
   L.sig_hash = o;
@@ -149,12 +169,10 @@ struct PrepArgs {
   fikit_strtab_t names, sigs;
   uint64_t* name_hash;
   uint64_t* sig_hash;
-  IndexEntry* idx;
-  uint32_t slots, cap;
   fikit_status_t* st;
-  RawRow* raw;
-  Tuple* row_tuple;
-  uint32_t* samp_cnt;
+  SampEntry* samp;
+  uint32_t* samp_list;
+  uint32_t* samp_n;
   uint8_t* grp_bucket;
   uint32_t* blkcnt;
   uint32_t ngroups, sb;     // tile groups, group-role blocks
@@ -163,9 +181,16 @@ struct PrepArgs {
 constexpr int kPrepThreads = 256;
 
 struct PlanArgs {
-  const fikit_status_t* st;
-  const uint32_t* samp_cnt;
-  const Tuple* row_tuple;
+  fikit_status_t* st;
+  const SampEntry* samp;
+  const uint32_t* samp_list;
+  // resolving the chosen identities to rows (kernel ID -> KID index; k_prep hashed the strings)
+  const uint64_t* name_hash;
+  const uint64_t* sig_hash;
+  IndexEntry* idx;
+  uint32_t slots;
+  RawRow* raw;
+  Tuple* row_tuple;
   uint32_t cap;
   Tuple* hot_all;
   uint32_t* hot_hdr;
@@ -177,6 +202,7 @@ struct PlanArgs {
   uint32_t* bstart;
   uint32_t* btot;
   uint32_t* first;
+  uint32_t dict;  // dictionary mode: rows are never inserted
 };
 
 // task bucket: xor-fold of the task id's 6-bit digits -- one-to-one for ids < 64 (a node's
@@ -194,7 +220,7 @@ __host__ __device__ __forceinline__ bool use_task_buckets(const uint32_t* hdr) {
 }
 
 // misc counters (u32 words at ws + misc)
-enum MiscWord { kMiscNames = 0, kMiscSigs = 1, kMiscHotN = 2, kMiscNRec = 3 };
+enum MiscWord { kMiscDict = 0 };  // dictionary mode of the last measure call: dict_n + 1, 0 = none
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
@@ -276,6 +302,17 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// release store at gpu scope: every earlier write of the thread is visible to a reader that
+// observes this value (cheaper than __threadfence() + atomicExch)
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // coherent 16-B load at gpu scope; asm volatile so it is never merged with an
 // earlier load of the same entry (the CUDA __ldcg is non-volatile asm and can be CSE'd)
 __device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
@@ -294,15 +331,17 @@ __device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
 // KID index: find-or-insert (task, kid); returns the row (possibly >= capacity: then
 // nothing is materialised and E_CAPACITY is flagged) or FIKIT_NO_ROW if the index is
 // full.  The inserting thread records the row's key (in the workspace's raw row) and a
-// representative raw tuple.
+// representative raw tuple.  insert = false (dictionary mode: every row was placed by
+// k_dict_load): an absent key returns FIKIT_NO_ROW.
 __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32_t slots, uint64_t kid, uint32_t task,
                                                          const uint32_t* tuple_w, fikit_status_t* st, RawRow* raw,
-                                                         Tuple* row_tuple, uint32_t cap) {
+                                                         Tuple* row_tuple, uint32_t cap, bool insert = true) {
   uint32_t h = key_hash(kid, task) & (slots - 1);
   for (uint32_t probe = 0; probe < slots; probe++) {
     IndexEntry* e = &idx[h];
     uint4 v = ld_relaxed_v4(e);
     uint32_t s = v.w;
+    if (s == 0 && !insert) return FIKIT_NO_ROW;
     if (s == 0) {
       uint32_t old = atomicCAS(&e->state, 0u, kBusy);
       if (old == 0) {
@@ -320,14 +359,13 @@ __device__ __forceinline__ uint32_t index_find_or_insert(IndexEntry* idx, uint32
         } else {
           atomicOr(&st->flags, kStatusCapacity);
         }
-        __threadfence();
-        atomicExch(&e->state, row + 1);
+        st_release_u32(&e->state, row + 1);  // publishes the key words and the row's key
         return row;
       }
       s = old;
     }
     if (s == kBusy) {
-      while (s == kBusy) s = ld_relaxed_u32(&e->state);
+      while (s == kBusy) s = ld_acquire_u32(&e->state);
     }
     v = ld_relaxed_v4(e);
     if ((((uint64_t)v.y << 32) | v.x) == kid && v.z == task) return v.w - 1;

@@ -16,98 +16,147 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
   return q + ((2 * r >= cnt) ? 1 : 0);
 }
 
-// fikit_table_finalize in one launch: the canonical row of measured row r (R11) is its rank
-// among the K distinct (task, kernel ID) keys.  Block (x, y) sorts key group y (kFinGroup keys,
-// a shared-memory bitonic sort) and adds, for each of its kFinRows rows x, the number of group-y
-// keys below it (a binary search) to rank[]; the last block to finish row block x (a counter per
-// x) writes those rows into the caller's table at their ranks, with counts (histogram totals,
-// P:249) and SK_j / SG_j (R8).  Reads the workspace's measured rows, writes only the
-// caller's table: no grid-wide ordering is needed.
-__global__ void __launch_bounds__(kFinRows) k_finalize(const fikit_status_t* __restrict__ st,
-                                                       const RawRow* __restrict__ raw, uint32_t cap,
-                                                       fikit_table_t tab, uint32_t* __restrict__ rank,
-                                                       uint32_t* __restrict__ done) {
+// fikit_table_finalize in two launches.  The canonical row of measured row r (R11) is its rank
+// among the K distinct (task, kernel ID) keys.
+//   k_fin_sort     one 128-thread block per group of kFinGroup = 256 keys: a shared-memory bitonic
+//                  sort (one compare-exchange per thread and stage), the sorted group to the workspace.
+//   k_fin_scatter  block b owns rows [b R, (b + 1) R): a row's rank is the sum over the sorted
+//                  groups of the keys below it (the groups staged in shared memory 8192 keys at a
+//                  time, one 8-step binary search per row and group); then the block writes its
+//                  rows into the caller's table at their ranks, a warp per half row (32 histogram
+//                  bins: the count is their sum), with the sums, extremes and
+//                  SK_j / SG_j (R8).
+// Grids follow the capacity (the row count K is on the device); blocks past K return at once.
+__device__ __forceinline__ bool fin_less(uint32_t ta, uint64_t ka, uint32_t tb, uint64_t kb) {
+  return (ta < tb) | ((ta == tb) & (ka < kb));  // (branch-free: the sort network selects, never branches)
+}
+
+__global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t* __restrict__ st,
+                                                            const RawRow* __restrict__ raw, uint32_t cap,
+                                                            fikit_table_t tab, FinKey* __restrict__ skeys,
+                                                            const uint32_t* __restrict__ misc) {
   __shared__ uint64_t sk[kFinGroup];
   __shared__ uint32_t stk[kFinGroup];
-  __shared__ uint32_t s_last;
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
-  const uint32_t x = blockIdx.x, y = blockIdx.y, tid = threadIdx.x;
-  if (x == 0 && y == 0 && tid == 0) *tab.n_rows = K;
-  const uint32_t r0 = x * kFinRows, g0 = y * kFinGroup;
-  if (r0 >= K || g0 >= K) return;
-  const uint32_t ny = (K + kFinGroup - 1) / kFinGroup;
+  const uint32_t tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) *tab.n_rows = K;
+  if (misc[kMiscDict]) return;  // dictionary mode: the rows are already canonical
+  const uint32_t g0 = blockIdx.x * kFinGroup;
+  if (g0 >= K) return;
   const uint32_t m = min(kFinGroup, K - g0);
-  uint32_t P = 2;
-  while (P < m) P <<= 1;
-  for (uint32_t i = tid; i < P; i += kFinRows) {
+  for (uint32_t i = tid; i < kFinGroup; i += blockDim.x) {
     const bool in = i < m;
     sk[i] = in ? raw[g0 + i].kid : ~0ull;  // padding sorts last
     stk[i] = in ? raw[g0 + i].task : 0xFFFFFFFFu;
   }
   __syncthreads();
-  for (uint32_t k = 2; k <= P; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < P / 2; i += kFinRows) {
-        const uint32_t a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;
-        const bool asc = (a & k) == 0;
-        const uint64_t ka = sk[a], kb = sk[b];
-        const uint32_t ta = stk[a], tb = stk[b];
-        if (key_less(tb, kb, ta, ka) == asc) {  // out of order for this direction
-          sk[a] = kb;
-          sk[b] = ka;
-          stk[a] = tb;
-          stk[b] = ta;
-        }
-      }
+  // bitonic network: one compare-exchange per thread and stage (branch-free selects)
+#pragma unroll
+  for (uint32_t kk = 2; kk <= kFinGroup; kk <<= 1)
+#pragma unroll
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      const uint32_t a = ((tid & ~(j - 1)) << 1) | (tid & (j - 1)), b = a + j;
+      const bool asc = (a & kk) == 0;
+      const uint64_t ka = sk[a], kb = sk[b];
+      const uint32_t ta = stk[a], tb = stk[b];
+      const bool sw = asc ? fin_less(tb, kb, ta, ka) : fin_less(ta, ka, tb, kb);
+      sk[a] = sw ? kb : ka;
+      sk[b] = sw ? ka : kb;
+      stk[a] = sw ? tb : ta;
+      stk[b] = sw ? ta : tb;
       __syncthreads();
     }
-  const uint32_t r = r0 + tid;
-  if (r < K) {
-    const uint64_t mk = raw[r].kid;
-    const uint32_t mt = raw[r].task;
-    uint32_t lo = 0, hi = m;  // keys of group y below (mt, mk)
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (key_less(stk[mid], sk[mid], mt, mk))
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    if (ny == 1)
-      rank[r] = lo;
-    else if (lo)
-      atomicAdd(rank + r, lo);
+  for (uint32_t i = tid; i < m; i += blockDim.x) skeys[g0 + i] = FinKey{sk[i], stk[i], 0u};
+}
+
+__global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __restrict__ st,
+                                                     const RawRow* __restrict__ raw, uint32_t cap, uint32_t R,
+                                                     const FinKey* __restrict__ skeys, fikit_table_t tab,
+                                                     uint32_t* __restrict__ rank, const uint32_t* __restrict__ misc) {
+  extern __shared__ __align__(16) unsigned char fin_sm[];
+  FinKey* gk = reinterpret_cast<FinKey*>(fin_sm);              // [kFinChunk]
+  FinKey* rk = gk + kFinChunk;                                 // [R] this block's row keys
+  uint32_t* srank = reinterpret_cast<uint32_t*>(rk + R);       // [R]
+  const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  const uint32_t r0 = blockIdx.x * R;
+  if (r0 >= K) return;
+  const uint32_t nr = min(R, K - r0), tid = threadIdx.x;
+  for (uint32_t i = tid; i < nr; i += blockDim.x) {
+    srank[i] = 0;
+    rk[i] = FinKey{raw[r0 + i].kid, raw[r0 + i].task, 0u};
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(done + x, 1u) == ny - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // the last block of row block x: one warp per row (coalesced 64-word histogram rows)
-  const uint32_t lane = tid & 31, warp = tid >> 5;
-  for (uint32_t rr = r0 + warp; rr < min(r0 + kFinRows, K); rr += kFinRows / 32) {
-    const RawRow& f = raw[rr];
-    const uint32_t d = __ldcg(rank + rr);
-    const uint32_t h0 = f.hist[lane], h1 = f.hist[32 + lane];
-    tab.hist[(size_t)d * 64 + lane] = h0;
-    tab.hist[(size_t)d * 64 + 32 + lane] = h1;
-    // row counts < 2^32 (a call measures < 2^32 launches)
-    const uint32_t dc = __reduce_add_sync(0xffffffffu, h0), gc = __reduce_add_sync(0xffffffffu, h1);
-    if (lane < 4) tab.ext[(size_t)d * 4 + lane] = f.ext[lane];
-    if (lane == 0) {
-      const uint64_t ds = f.sums[1], gs = f.sums[3];
-      tab.kernel_id[d] = f.kid;
-      tab.task_id[d] = f.task;
-      tab.sums[(size_t)d * 4 + 0] = dc;
-      tab.sums[(size_t)d * 4 + 1] = ds;
-      tab.sums[(size_t)d * 4 + 2] = gc;
-      tab.sums[(size_t)d * 4 + 3] = gs;
-      tab.mean[(size_t)d * 2 + 0] = mean_half_up(ds, dc);  // SK_j
-      tab.mean[(size_t)d * 2 + 1] = mean_half_up(gs, gc);  // SG_j
+  const bool dict = misc[kMiscDict] != 0u;  // dictionary mode: rank = row
+  if (dict)
+    for (uint32_t i = tid; i < nr; i += blockDim.x) srank[i] = r0 + i;
+  for (uint32_t c0 = 0; c0 < (dict ? 0u : K); c0 += kFinChunk) {
+    const uint32_t mc = min(kFinChunk, K - c0);
+    __syncthreads();  // (the previous chunk's searches are done)
+    for (uint32_t i = tid; i < mc; i += blockDim.x) {
+      const uint32_t d = smem_u32(gk + i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(skeys + c0 + i) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint32_t ng = (mc + kFinGroup - 1) / kFinGroup;
+    // consecutive lanes take consecutive rows of ONE group (a lane per group would put the whole
+    // warp's probes 4 KB apart: one bank, 32-way conflicts)
+    for (uint32_t it = tid; it < nr * ng; it += blockDim.x) {
+      const uint32_t g = it / nr, i = it - g * nr;
+      const FinKey* grp = gk + g * kFinGroup;
+      const uint32_t m = min(kFinGroup, mc - g * kFinGroup);
+      const uint64_t mk = rk[i].kid;
+      const uint32_t mt = rk[i].task;
+      uint32_t lo = 0, hi = m;  // keys of group g below (mt, mk)
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (fin_less(grp[mid].task, grp[mid].kid, mt, mk))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      if (lo) atomicAdd(&srank[i], lo);
     }
   }
-  if (tid == 0) done[x] = 0;  // (self-cleaning; rank[] stays for the out_row remap)
+  __syncthreads();
+  for (uint32_t i = tid; i < nr; i += blockDim.x) rank[r0 + i] = srank[i];  // (the out_row remap)
+  // a warp per half row h = 2 i + j (j = 0 duration, 1 gap): 32 bins, count, sum, extremes, mean;
+  // U half rows in flight per warp
+  constexpr uint32_t U = 4;
+  const uint32_t lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nh = 2 * nr;
+  for (uint32_t h0 = warp * U; h0 < nh; h0 += nw * U) {
+    // every load of the U half rows first: lane l's bin, and one 8-B word per lane -- lanes 0, 1
+    // the extremes, lane 2 the sum, lane 3 the key (j = 0) -- so no load waits on a store
+    uint32_t bin[U], d[U];
+    uint64_t x[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {
+      const uint32_t h = h0 + u, j = h & 1;
+      const RawRow* f = raw + r0 + (h >> 1);
+      const bool in = h < nh;
+      bin[u] = in ? f->hist[32 * j + lane] : 0u;
+      d[u] = in ? srank[h >> 1] : 0u;
+      x[u] = !in ? 0ull : lane < 2 ? f->ext[2 * j + lane] : lane == 2 ? f->sums[2 * j + 1] : lane == 3 ? f->kid : 0ull;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {
+      const uint32_t h = h0 + u;
+      if (h >= nh) break;
+      const uint32_t j = h & 1;
+      tab.hist[(size_t)d[u] * 64 + 32 * j + lane] = bin[u];
+      // row counts < 2^32 (a call measures < 2^32 launches)
+      const uint64_t c = __reduce_add_sync(0xffffffffu, bin[u]);
+      if (lane < 2) tab.ext[(size_t)d[u] * 4 + 2 * j + lane] = x[u];
+      if (lane == 2) {
+        tab.sums[(size_t)d[u] * 4 + 2 * j] = c;
+        tab.sums[(size_t)d[u] * 4 + 2 * j + 1] = x[u];
+        tab.mean[(size_t)d[u] * 2 + j] = mean_half_up(x[u], c);  // SK_j, SG_j
+      }
+      if (lane == 3 && j == 0) {
+        tab.kernel_id[d[u]] = x[u];
+        tab.task_id[d[u]] = rk[h >> 1].task;
+      }
+    }
+  }
 }
 
 __global__ void k_remap_rows(uint32_t* rows, uint64_t n, const uint32_t* __restrict__ rank, const uint32_t* n_ptr) {

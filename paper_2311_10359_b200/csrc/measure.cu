@@ -30,6 +30,7 @@ __device__ __forceinline__ void k_reset_status_body(fikit_status_t* st) {
     st->n_overlap_gaps = 0;
     st->schedule = 0;
     st->n_task_buckets = 0;
+    st->first_missing_index = ~0ull;
     reinterpret_cast<uint32_t*>(st)[kSchedWord1] = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord2] = 0;
     reinterpret_cast<uint32_t*>(st)[kSchedWord3] = 0;
@@ -52,6 +53,39 @@ __global__ void k_zero(ZeroList z, fikit_status_t* st) {
     for (uint64_t i = tid; i < nv; i += nt) v[i] = make_uint4(0, 0, 0, 0);
     const uint64_t done = head + 16 * nv;
     if (tid < (n - done) / 4) reinterpret_cast<uint32_t*>(p + done)[tid] = 0u;
+  }
+}
+
+// Dictionary mode (fikit_measure_dict): row j of the table is dictionary key j.  Each key is
+// placed in the KID index with row j (its raw row's key set; the statistics were zeroed by
+// k_zero); a key not strictly above its predecessor flags E_ARG.  Thread 0 sets the row counter
+// to dict_n and the workspace's dictionary word (read by finalize).
+__global__ void k_dict_load(const uint64_t* __restrict__ dkid, const uint32_t* __restrict__ dtask, uint32_t K,
+                            IndexEntry* idx, uint32_t slots, RawRow* raw, fikit_status_t* st, uint32_t* misc) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0) {
+    st->n_rows_needed = K;
+    misc[kMiscDict] = K + 1;
+  }
+  if (j >= K) return;
+  const uint64_t kid = dkid[j];
+  const uint32_t task = dtask[j];
+  if (j > 0) {
+    const uint32_t pt = dtask[j - 1];
+    const uint64_t pk = dkid[j - 1];
+    if (!(pt < task || (pt == task && pk < kid))) atomicOr(&st->flags, kStatusArg);
+  }
+  raw[j].kid = kid;
+  raw[j].task = task;
+  uint32_t h = key_hash(kid, task) & (slots - 1);
+  for (uint32_t probe = 0; probe < slots; probe++, h = (h + 1) & (slots - 1)) {
+    if (atomicCAS(&idx[h].state, 0u, kBusy) == 0u) {
+      idx[h].kid = kid;
+      idx[h].task = task;
+      __threadfence();
+      atomicExch(&idx[h].state, j + 1);
+      return;
+    }
   }
 }
 
@@ -210,13 +244,13 @@ __global__ void __launch_bounds__(256) k_identify(const uint4* __restrict__ recs
 //           first bucket of every k_measure CTA.
 
 __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uint32_t nblk, unsigned char* sm) {
-  // Per-block deduplication before the global index: the block's samples are counted per
-  // distinct identity in shared memory (keyed by a 64-bit fingerprint of the raw identity), then
-  // one representative per identity resolves its row in the global index and adds the count.  A
-  // skewed sample hits a few identities thousands of times; this keeps the global index (and its
-  // first-insert races) to one access per distinct identity per block.  The sample only chooses
-  // the hot rows, so a (astronomically rare) fingerprint collision merely credits one identity's
-  // samples to another: k_measure still resolves every launch exactly.
+  // The sample counts raw launch identities (no kernel IDs, no rows: k_plan resolves only the
+  // identities it keeps).  Per-block deduplication first: the block's samples are counted per
+  // distinct identity in shared memory (keyed by a 64-bit fingerprint), then one representative
+  // per identity adds the count to the global sample table (one CAS claims a slot and publishes
+  // its fingerprint; the identity words are read only by the next kernel).  A skewed sample hits
+  // a few identities thousands of times; this keeps the global table to one access per distinct
+  // identity per block.
   constexpr uint32_t HS = 512;
   unsigned long long* sfp = reinterpret_cast<unsigned long long*>(sm);
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sfp + HS);
@@ -226,11 +260,21 @@ __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uin
     scnt[i] = 0;
   }
   __syncthreads();
-  auto resolve = [&](const uint32_t* tw, uint32_t cnt) {
-    const uint64_t kid = kernel_id_from(thread_fnv_string(a.names, tw[0]), thread_fnv_string(a.sigs, tw[1]), tw[2],
-                                        tw[3], tw[4], tw[5]);
-    const uint32_t row = index_find_or_insert(a.idx, a.slots, kid, tw[6], tw, a.st, a.raw, a.row_tuple, a.cap);
-    if (row < a.cap) atomicAdd(a.samp_cnt + row, cnt);
+  auto global_add = [&](const uint32_t* tw, unsigned long long fp, uint32_t cnt) {
+    uint32_t h = (uint32_t)(fp >> 20) & (kSampSlots - 1);
+    for (uint32_t probe = 0; probe < 64; probe++, h = (h + 1) & (kSampSlots - 1)) {
+      const unsigned long long old = atomicCAS(&a.samp[h].fp, 0ull, fp);
+      if (old == 0ull) {
+#pragma unroll
+        for (int q = 0; q < 6; q++) a.samp[h].w[q] = tw[q];
+        a.samp[h].task = tw[6];
+        a.samp_list[atomicAdd(a.samp_n, 1u)] = h;
+      }
+      if (old == 0ull || old == fp) {
+        atomicAdd(&a.samp[h].cnt, cnt);
+        return;
+      }
+    }  // (a full neighbourhood: the sample is dropped)
   };
   const uint32_t nn = a.names.count, ns = a.sigs.count;
   for (uint64_t j = blk * (uint64_t)blockDim.x + threadIdx.x; j < a.n_samples; j += (uint64_t)nblk * blockDim.x) {
@@ -261,11 +305,11 @@ __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uin
         break;
       }
     }
-    if (!counted) resolve(tw, 1u);  // the block saw > HS identities: resolve and count directly
+    if (!counted) global_add(tw, fp, 1u);  // the block saw > HS identities: count it directly
   }
   __syncthreads();
   for (uint32_t q = threadIdx.x; q < HS; q += blockDim.x)
-    if (scnt[q]) resolve(stw + q * 7, scnt[q]);
+    if (scnt[q]) global_add(stw + q * 7, sfp[q], scnt[q]);
 }
 
 __device__ __forceinline__ void prep_groups(const PrepArgs& a, uint32_t blk, uint32_t* h) {
@@ -315,28 +359,45 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
 }
 
 
-// hot sets: per task bucket, the most-sampled rows (block bkt; block kBuckets: the global set
-// over all tasks).  Each block also counts the samples its set covers.
+// hot sets: per task bucket, the most-sampled identities (block bkt; block kBuckets: the global
+// set over all tasks), each resolved to its row (kernel ID from the string hashes k_prep wrote,
+// then the KID index: find or insert).  Each block also counts the samples its set covers.
 __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsigned char* sm) {
   constexpr int NB = 4096;
   uint32_t* h = reinterpret_cast<uint32_t*>(sm);
   uint32_t* wsum = h + NB;  // [32]
   uint32_t* s_misc = wsum + 32;  // T, n, Tmin
   Tuple* hot = a.hot_all + (size_t)bkt * kHotMax;
-  auto mine = [&](uint32_t r) { return bkt == kGlobalSet || bucket_of(a.row_tuple[r].w[6]) == bkt; };
-  const uint32_t K = (uint32_t)umin64(*(volatile const unsigned long long*)&a.st->n_rows_needed, a.cap);
+  auto mine = [&](uint32_t task) { return bkt == kGlobalSet || bucket_of(task) == bkt; };
+  const uint32_t nd = min(a.hot_hdr[kSampN], kSampSlots);  // distinct sampled identities
   for (int i = threadIdx.x; i < NB; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    const uint32_t c = a.samp_cnt[r];
-    if (c && mine(r)) atomicAdd(&h[min(c, (uint32_t)NB - 1)], 1u);
+  // (count, task) of 4 listed identities per thread in flight; the loop bound is warp-uniform
+  // (the histogram update below is a full-warp match)
+  constexpr uint32_t U = 4;
+  const uint32_t lane_id = threadIdx.x & 31u;
+  for (uint32_t i0 = threadIdx.x; i0 - lane_id < nd; i0 += U * blockDim.x) {
+    uint2 ct[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {
+      const uint32_t i = i0 + u * blockDim.x;
+      ct[u] = i < nd ? *reinterpret_cast<const uint2*>(a.samp + __ldg(a.samp_list + i)) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {  // warp-aggregated: skewed samples give many equal counts
+      const bool in = ct[u].x && mine(ct[u].y);
+      const uint32_t bin = in ? min(ct[u].x, (uint32_t)NB - 1) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (in && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    }
   }
   if (threadIdx.x == 0) {
+    s_misc[0] = 0;
     s_misc[1] = 0;
     s_misc[2] = NB;
   }
   __syncthreads();
-  // T = smallest count c >= 1 whose suffix S(c) = #rows with count >= c fits kHotMax:
+  // T = smallest count c >= 1 whose suffix S(c) = #identities with count >= c fits kHotMax:
   // a block-wide suffix scan of the 4096-bin count histogram (4 bins per thread)
   {
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -365,19 +426,46 @@ __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsign
     __syncthreads();
   }
   const uint32_t T = s_misc[2];
-  uint32_t cov = 0, tot = 0;
-  for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) {
-    const uint32_t c = a.samp_cnt[r];
-    if (c && mine(r)) {
+  uint32_t* chosen = h;  // (the histogram is no longer needed) [kHotMax] sample slots
+  uint32_t tot = 0;
+  for (uint32_t i0 = threadIdx.x; i0 < nd; i0 += U * blockDim.x) {
+    uint32_t ent[U];
+    uint2 ct[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {  // U (count, task) loads in flight
+      const uint32_t i = i0 + u * blockDim.x;
+      ent[u] = i < nd ? __ldg(a.samp_list + i) : 0u;
+      ct[u] = i < nd ? *reinterpret_cast<const uint2*>(a.samp + ent[u]) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {
+      const uint32_t c = ct[u].x;
+      if (c == 0 || !mine(ct[u].y)) continue;
       tot += c;
       if (c >= T) {
-        const uint32_t e = atomicAdd(&s_misc[1], 1u);
-        if (e < kHotMax) {
-          hot[e] = a.row_tuple[r];
-          cov += c;
-        }
+        const uint32_t e = atomicAdd(&s_misc[0], 1u);
+        if (e < kHotMax) chosen[e] = ent[u];
       }
     }
+  }
+  __syncthreads();
+  // resolve the chosen identities to rows, one per thread (their latency chains overlap)
+  const uint32_t nc = min(s_misc[0], kHotMax);
+  uint32_t cov = 0;
+  for (uint32_t q = threadIdx.x; q < nc; q += blockDim.x) {
+    const SampEntry& se = a.samp[chosen[q]];
+    const uint2 ct = *reinterpret_cast<const uint2*>(&se);
+    Tuple t;
+#pragma unroll
+    for (int w = 0; w < 6; w++) t.w[w] = se.w[w];
+    t.w[6] = ct.y;
+    const uint64_t kid = kernel_id_from(__ldg(a.name_hash + t.w[0]), __ldg(a.sig_hash + t.w[1]), t.w[2], t.w[3],
+                                        t.w[4], t.w[5]);
+    t.row = index_find_or_insert(a.idx, a.slots, kid, t.w[6], t.w, a.st, a.raw, a.row_tuple, a.cap, a.dict == 0u);
+    if (t.row >= a.cap) continue;  // (E_CAPACITY is flagged; the row is not materialised)
+    const uint32_t e = atomicAdd(&s_misc[1], 1u);
+    hot[e] = t;
+    cov += ct.x;
   }
   cov = __reduce_add_sync(0xffffffffu, cov);
   tot = __reduce_add_sync(0xffffffffu, tot);
@@ -690,7 +778,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
               RawTab tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
               const uint32_t* __restrict__ hot_n_all, uint32_t* cur, uint32_t* act, const uint32_t* __restrict__ bstart,
               const uint32_t* __restrict__ btot, const uint32_t* __restrict__ first,
-              const uint32_t* __restrict__ order, uint32_t ntiles, uint32_t* __restrict__ out_row) {
+              const uint32_t* __restrict__ order, uint32_t ntiles, uint32_t* __restrict__ out_row, uint32_t dict) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
@@ -816,8 +904,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       const uint32_t row = tuple_find_or_insert(tidx, tslots, key, [&]() {
         const uint64_t kid =
             kernel_id_from(__ldg(name_hash + pk0), __ldg(sig_hash + pk1), pk2, pk3, pk4, pk5 & 0xFFFFu);
-        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.rows, row_tuple, tab.capacity);
+        return index_find_or_insert(idx, slots, kid, pk6, key, st, tab.rows, row_tuple, tab.capacity, dict == 0u);
       });
+      if (dict && row >= tab.capacity) {  // not in the dictionary (E_DICT): not counted
+        atomicOr(&st->flags, kStatusDict);
+        atomicMin((unsigned long long*)&st->first_missing_index, (unsigned long long)pgi);
+      }
       if (row < tab.capacity) {
         cold_add(tab, row, 0, pd);
         if (pk5 >> 16) cold_add(tab, row, 1, pg);

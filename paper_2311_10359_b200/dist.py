@@ -12,6 +12,9 @@ kernels (`LibOps`); this module only sequences them around the collectives:
     all_reduce SUM(sums u64 + hist u32 pairs as u64: one span, R37) ; all_reduce MAX(ext, biased)
     fikit_table_bias ; fikit_table_means
 
+With a dictionary supplied to every rank (fikit_measure_dict: the rows are pre-assigned in
+global canonical order), `merge_tables_dict` needs only the two all-reduces.
+
 Integer sum / min / max are associative and commutative and the halo gives
 every boundary gap exactly once, so the merged table equals the 1-GPU table
 bit for bit.
@@ -88,6 +91,31 @@ def merge_tables(local, dense, ops, group=None):
     ops.table_bias(dense)
     ops.table_means(dense)
     return un
+
+
+def merge_tables_dict(local, ops, group=None):
+    """In place: tables measured against ONE dictionary on every rank (fikit_measure_dict +
+    fikit_table_finalize: row j = dictionary key j everywhere, SURVEY §8e "dictionary supplied",
+    repeated services keep their IDs).  The rows already line up, so the merge is the two
+    all-reduces alone -- no key gathers, no union, no remap:
+
+        fikit_table_bias ; all_reduce SUM(sums u64 + hist u32 pairs: one span, R37) ;
+        all_reduce MAX(ext, biased) ; fikit_table_bias ; fikit_table_means
+
+    Bytes per rank: 288 per row (SUM span) + 32 per row (MAX block)."""
+    import torch.distributed as dist
+
+    ops.table_bias(local)
+    span = local.sum_span() if hasattr(local, "sum_span") else None
+    if span is not None:
+        dist.all_reduce(span, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(local.sums, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(local.hist, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(local.ext, op=dist.ReduceOp.MAX, group=group)
+    ops.table_bias(local)
+    ops.table_means(local)
+    return local
 
 
 def scenario_shard(S: int, rank: int, world: int):

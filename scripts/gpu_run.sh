@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 if [ -n "$TESTS" ]; then
   [ "$TESTS" = "all" ] && TESTS="tests"
-  timeout ${TEST_TIMEOUT:-1500} python -m pytest $TESTS -m gpu -q --durations=10 -x ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
+  timeout ${TEST_TIMEOUT:-1200} python -m pytest $TESTS -m gpu -q --durations=10 -x --timeout ${PER_TEST_TIMEOUT:-400} ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
   echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log
 fi
 IFS=';' read -ra BS <<< "$BENCH"

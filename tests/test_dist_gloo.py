@@ -133,6 +133,58 @@ def _worker(rank, world, port, seed, q):
         dist.destroy_process_group()
 
 
+def dict_table(tab, keys, cap):
+    """The host double of fikit_measure_dict + finalize: row j = dictionary key j, holding the
+    shard table's statistics for that key (an all-zero row if the shard never saw it)."""
+    t = HostTable(cap)
+    pos = {k: j for j, k in enumerate(keys)}
+    src = HostTable.from_oracle(tab, cap)
+    for r in range(tab.n_rows):
+        j = pos[(int(tab.task_id[r]), int(tab.kernel_id[r]))]
+        t.sums.view(-1, 4)[j] = src.sums.view(-1, 4)[r]
+        t.hist.view(-1, 64)[j] = src.hist.view(-1, 64)[r]
+        t.ext.view(-1, 4)[j] = src.ext.view(-1, 4)[r]
+    for j, (tk, kd) in enumerate(keys):
+        t.kernel_id[j] = int(np.uint64(kd).view(np.int64))
+        t.task_id[j] = int(np.uint32(tk).view(np.int32))
+    t.n_rows_t[0] = len(keys)
+    return t
+
+
+def _worker_dict(rank, world, port, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2311_10359_b200.dist import merge_tables_dict, shard_range
+
+        tr = F.random_trace(seed, 2500, n_tasks=3, n_ids=70, run_len_max=60, overlap_frac=0.05, big_frac=0.02)
+        N = tr.records.shape[0]
+        full, _, _ = oracle.measure(tr.records, tr.names, tr.sigs, capacity=512)
+        # the dictionary: the whole trace's keys plus keys no rank sees (rows that stay empty)
+        keys = sorted({(int(full.task_id[r]), int(full.kernel_id[r])) for r in range(full.n_rows)}
+                      | {(7, 12345), (0, 1), (2, 2**64 - 1)})
+        lo, hi = shard_range(N, rank, world)
+        halo = tr.records[hi] if hi < N else None
+        tab, st, _ = oracle.measure(tr.records[lo:hi], tr.names, tr.sigs, capacity=512, halo=halo)
+        local = dict_table(tab, keys, 512)
+        merge_tables_dict(local, NumpyOps())
+        ref = dict_table(full, keys, 512)
+        NumpyOps().table_means(ref)
+        ok = int(local.n_rows_t[0]) == len(keys)
+        for a in ("kernel_id", "task_id", "sums", "hist", "ext", "mean"):
+            ok &= bool(torch.equal(getattr(local, a), getattr(ref, a)))
+        # the rows the trace has equal the oracle's unsharded table
+        pos = [keys.index((int(full.task_id[r]), int(full.kernel_id[r]))) for r in range(full.n_rows)]
+        o = HostTable.from_oracle(full, 512)
+        ok &= bool(torch.equal(local.sums.view(-1, 4)[pos], o.sums.view(-1, 4)[:full.n_rows]))
+        ok &= bool(torch.equal(local.mean.view(-1, 2)[pos], o.mean.view(-1, 2)[:full.n_rows]))
+        ok &= bool(torch.equal(local.ext.view(-1, 4)[pos], o.ext.view(-1, 4)[:full.n_rows]))
+        q.put((rank, ok, int(local.n_rows_t[0]), len(keys)))
+    finally:
+        dist.destroy_process_group()
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -154,6 +206,22 @@ def test_merge_gloo(world, seed):
         p.join(60)
     for rank, ok, got_n, n in res:
         assert ok, f"rank {rank}: merged table differs from the unsharded oracle table ({got_n} vs {n} rows)"
+
+
+@pytest.mark.parametrize("world,seed", [(2, 3), (3, 4)])
+def test_merge_dict_gloo(world, seed):
+    # dictionary-supplied mode (fikit_measure_dict): the merge is the two all-reduces alone
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dict, args=(r, world, port, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+    for rank, ok, got_n, n in res:
+        assert ok, f"rank {rank}: dictionary-mode merge differs from the oracle ({got_n} vs {n} rows)"
 
 
 def test_shard_ranges_cover():
