@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfikit.so")
+LIB_PATH = os.environ.get("FIKIT_DIAG_LIB") or os.path.join(_HERE, "libfikit.so")  # (diagnosis builds: scripts/)
 
 OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME, E_DICT = 0, -1, -2, -3, -4, -5, -6
 NO_ROW = 0xFFFFFFFF

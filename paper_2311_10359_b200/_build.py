@@ -22,7 +22,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """out / defines: a diagnosis variant (e.g. -DFIKIT_TRACE) built elsewhere; the product
+    library is LIB."""
+    if out is not None:
+        objdir = os.path.join(HERE, "..", "build", "obj_" + os.path.basename(os.path.dirname(out)))
+        os.makedirs(objdir, exist_ok=True)
+        objs = []
+        for src in SOURCES:
+            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            subprocess.check_call([NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj])
+            objs.append(obj)
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs])
+        return out
     if not force and not _stale():
         return LIB
     objdir = os.path.join(HERE, "..", "build", "obj")

@@ -160,7 +160,7 @@ int get_ws(void* ws, size_t ws_bytes, uint32_t cap, uint32_t nn, uint32_t ns, Ws
 }
 
 inline int reset_status(const Ws& w, cudaStream_t s) {
-  k_reset_status<<<1, 32, 0, s>>>(w.st());  // a kernel, so the call stays graph-capturable
+  launch_pdl(k_reset_status, 1, 32, 0, s, w.st());  // a kernel, so the call stays graph-capturable
   return launched();
 }
 
@@ -174,7 +174,7 @@ inline bool table_ok(const fikit_table_t* t) {
 int hash_strtabs(const Ws& w, const fikit_strtab_t& names, const fikit_strtab_t& sigs, cudaStream_t s) {
   const uint32_t mx = names.count > sigs.count ? names.count : sigs.count;
   if (mx) {  // one warp per string, names (y = 0) and signatures (y = 1) in one launch
-    k_strtab_hash<<<dim3((mx + 3) / 4, 2), 128, 0, s>>>(names, w.name_hash(), sigs, w.sig_hash(), w.st());
+    launch_pdl(k_strtab_hash, dim3((mx + 3) / 4, 2), 128, 0, s, names, w.name_hash(), sigs, w.sig_hash(), w.st());
     if (int r = launched()) return r;
   }
   return FIKIT_OK;
@@ -238,7 +238,7 @@ int fikit_identify(const fikit_record_t* recs, uint64_t n, fikit_strtab_t names,
   if (int r = reset_status(w, s)) return r;
   if (int r = hash_strtabs(w, names, sigs, s)) return r;
   if (n == 0) return FIKIT_OK;
-  k_identify<<<grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s>>>(
+  launch_pdl(k_identify, grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s, 
       reinterpret_cast<const uint4*>(recs), n, w.name_hash(), w.sig_hash(), names.count, sigs.count, out, w.st());
   return launched();
 }
@@ -271,10 +271,10 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   add(w.misc(), 256);  // (dictionary word: none unless k_dict_load sets it)
   add(w.hot_n(), 4ull * kHotHdr);
   add(w.cur(), 16ull * kSchedWords);  // cur, act, bstart, btot
-  k_zero<<<2 * num_sms(), 256, 0, s>>>(z, w.st());
+  launch_pdl(k_zero, 2 * num_sms(), 256, 0, s, z, w.st());
   if (int r = launched()) return r;
   if (dict) {  // rows fixed in advance: dictionary key j -> row j
-    k_dict_load<<<(dict_n + 255) / 256, 256, 0, s>>>(dict_kid, dict_task, dict_n, w.index(), w.L.slots, w.raw(),
+    launch_pdl(k_dict_load, (dict_n + 255) / 256, 256, 0, s, dict_kid, dict_task, dict_n, w.index(), w.L.slots, w.raw(),
                                                       w.st(), w.misc());
     if (int r = launched()) return r;
   }
@@ -309,8 +309,8 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pa.sb = sb;
   const uint64_t nstr = (uint64_t)names.count + sigs.count;
   pa.nb_hash = (uint32_t)((nstr + kPrepThreads / 32 - 1) / (kPrepThreads / 32));
-  pa.nb_samp = grid_for(pa.n_samples, 2 * kPrepThreads, num_sms());
-  k_prep<<<pa.nb_hash + pa.nb_samp + pa.sb, kPrepThreads, 0, s>>>(pa);
+  pa.nb_samp = (uint32_t)((pa.n_samples + 2 * kPrepThreads - 1) / (2 * kPrepThreads));  // <= 2 samples per thread
+  launch_pdl(k_prep, pa.nb_hash + pa.nb_samp + pa.sb, kPrepThreads, 0, s, pa);
   if (int r = launched()) return r;
   // 3. k_plan: hot sets + schedule mode | the groups' counting-sort scatter, bucket ranges, first buckets
   PlanArgs pl{};
@@ -336,7 +336,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pl.bstart = w.bstart();
   pl.btot = w.btot();
   pl.first = w.first();
-  k_plan<<<kBuckets + 1 + sb, 1024, 0, s>>>(pl);
+  launch_pdl(k_plan, kBuckets + 1 + sb, 1024, 0, s, pl);
   if (int r = launched()) return r;
   // 4. the streaming kernel
   const size_t smem = measure_smem_bytes();
@@ -349,7 +349,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
       }) < 0)
     return FIKIT_E_CUDA;
   if (ev0 && cudaEventRecord(ev0, s) != cudaSuccess) return FIKIT_E_CUDA;
-  k_measure<<<grid, measure_threads(), smem, s>>>(
+  launch_pdl(k_measure, grid, measure_threads(), smem, s, 
       recs, n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, w.index(), w.L.slots, w.tindex(),
       w.L.tslots, w.st(), RawTab{w.raw(), cap}, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.act(), w.bstart(),
       w.btot(), w.first(), w.order(), ntiles, out_row, dict ? 1u : 0u);
@@ -396,7 +396,7 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   if (int r = get_ws(ws, ws_bytes, tab->capacity, 0, 0, &w)) return r;  // (the capacity-sized regions)
   const uint32_t cap = tab->capacity;
   uint32_t* rank = w.rank();
-  k_fin_sort<<<(cap + kFinGroup - 1) / kFinGroup, kFinGroup / 2, 0, s>>>(w.st(), w.raw(), cap, *tab, w.fin_keys(cap), w.misc());
+  launch_pdl(k_fin_sort, (cap + kFinGroup - 1) / kFinGroup, kFinGroup / 2, 0, s, w.st(), w.raw(), cap, *tab, w.fin_keys(cap), w.misc());
   if (int r = launched()) return r;
   // rows per scatter block: one wave of <= num_sms() blocks, at least 64 rows each
   uint32_t R = (cap + num_sms() - 1) / num_sms();
@@ -409,11 +409,11 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
                    : -1;
       }) < 0)
     return FIKIT_E_CUDA;
-  k_fin_scatter<<<(cap + R - 1) / R, 256, fsm, s>>>(w.st(), w.raw(), cap, R, w.fin_keys(cap), *tab, rank,
+  launch_pdl(k_fin_scatter, (cap + R - 1) / R, 256, fsm, s, w.st(), w.raw(), cap, R, w.fin_keys(cap), *tab, rank,
                                                     w.misc());
   if (int r = launched()) return r;
   if (out_row && n) {
-    k_remap_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(out_row, n, rank, tab->n_rows);
+    launch_pdl(k_remap_rows, grid_for(n, 256, num_sms() * 8), 256, 0, s, out_row, n, rank, tab->n_rows);
     if (int r = launched()) return r;
   }
   return FIKIT_OK;
@@ -445,7 +445,7 @@ int fikit_resolve(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
   if (int r = reset_status(w, s)) return r;
   if (int r = hash_strtabs(w, names, sigs, s)) return r;
   if (n == 0) return FIKIT_OK;
-  k_resolve<<<grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s>>>(
+  launch_pdl(k_resolve, grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s, 
       reinterpret_cast<const uint4*>(recs), n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, *tab,
       out_row, out_dur, out_gap, w.st());
   return launched();
@@ -472,7 +472,7 @@ int fikit_fill(const fikit_table_t* tab, const uint64_t* R0, const uint64_t* dea
   if (int r = get_ws(ws, ws_bytes, 1, 0, 0, &w)) return r;
   if (int r = reset_status(w, s)) return r;
   if (G == 0) return FIKIT_OK;
-  k_fill<<<grid_for(G, 4, num_sms() * 16), 128, 0, s>>>(*tab, R0, deadline, pool_row, pool_dur, pool_level, pool_off,
+  launch_pdl(k_fill, grid_for(G, 4, num_sms() * 16), 128, 0, s, *tab, R0, deadline, pool_row, pool_dur, pool_level, pool_off,
                                                          pool_len, G, prm, picks, picks_off, n_picks, R_left, t_used,
                                                          w.st());
   return launched();

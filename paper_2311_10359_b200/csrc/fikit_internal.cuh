@@ -123,7 +123,8 @@ inline WsLayout ws_layout(uint32_t cap, uint32_t n_names, uint32_t n_sigs, uint6
   o += 256;
   L.misc = o;
   o += 256;
-  L.slots = index_slots(cap);
+  L.slots = index_slots(2 * cap);  // KID index: load <= 1/4 (short linear-probe chains: k_plan's
+                                   // hot-row inserts wait on the longest one)
   L.index = o;
   o = align256(o + sizeof(IndexEntry) * (size_t)L.slots);
   L.tslots = index_slots(2 * cap);
@@ -221,6 +222,34 @@ __host__ __device__ __forceinline__ bool use_task_buckets(const uint32_t* hdr) {
 
 // misc counters (u32 words at ws + misc)
 enum MiscWord { kMiscDict = 0 };  // dictionary mode of the last measure call: dict_n + 1, 0 = none
+
+// Programmatic dependent launch (the C-ABI launches the kernels of a call with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel's CTAs may be scheduled while the
+// previous kernel of the stream finishes; griddepcontrol.wait (first statement of every such
+// kernel, before any global memory access) blocks until that grid has completed and its writes
+// are visible, so only launch latency overlaps.  launch_dependents lets the next kernel's launch
+// begin as soon as every CTA of this one has started.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+// Launch with programmatic stream serialization (the kernel's first statement is pdl_entry():
+// only the launch latency overlaps the previous kernel of the stream).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  (void)cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);  // (errors surface in launched())
+}
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 

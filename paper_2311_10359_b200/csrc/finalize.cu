@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t
                                                             const RawRow* __restrict__ raw, uint32_t cap,
                                                             fikit_table_t tab, FinKey* __restrict__ skeys,
                                                             const uint32_t* __restrict__ misc) {
+  pdl_entry();
   __shared__ uint64_t sk[kFinGroup];
   __shared__ uint32_t stk[kFinGroup];
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
                                                      const RawRow* __restrict__ raw, uint32_t cap, uint32_t R,
                                                      const FinKey* __restrict__ skeys, fikit_table_t tab,
                                                      uint32_t* __restrict__ rank, const uint32_t* __restrict__ misc) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char fin_sm[];
   FinKey* gk = reinterpret_cast<FinKey*>(fin_sm);              // [kFinChunk]
   FinKey* rk = gk + kFinChunk;                                 // [R] this block's row keys
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
 }
 
 __global__ void k_remap_rows(uint32_t* rows, uint64_t n, const uint32_t* __restrict__ rank, const uint32_t* n_ptr) {
+  pdl_entry();
   uint32_t K = *n_ptr;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t r = rows[i];
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(256) k_resolve(const uint4* __restrict__ recs,
                                                  uint32_t n_sigs, fikit_table_t tab, uint32_t* __restrict__ out_row,
                                                  uint64_t* __restrict__ out_dur, uint64_t* __restrict__ out_gap,
                                                  fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint4 sbuf[8][99];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t K = min(*tab.n_rows, tab.capacity);

@@ -20,6 +20,31 @@
 
 namespace fikit {
 
+// Per-CTA timeline of k_measure for diagnosis builds only (nvcc -DFIKIT_TRACE, scripts/trace_measure.py):
+// 16 u64 per CTA -- 0 entry, 1 streaming start, 2 exit (globaltimer ns), 3 phases, 4 tiles, 5 ns loading
+// hot sets, 6 ns from the first warp's last tile to the phase barrier, 7 ns flushing / picking the
+// next bucket, 8 cold-batch resolutions.  The product build compiles none of it.
+#ifdef FIKIT_TRACE
+__device__ unsigned long long g_trace[kMaxCTAs * 16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_trace_pre[2048 * 8];  // k_prep / k_plan blocks: role, stamps
+#define FK_TP(slot) (g_trace_pre[blockIdx.x * 8 + (slot)] = gtime())
+#define FK_TQ(slot) (g_trace_pre[(1024 + blockIdx.x) * 8 + (slot)] = gtime())
+#define FK_TR_SET(slot, v) (g_trace[blockIdx.x * 16 + (slot)] = (unsigned long long)(v))
+#define FK_TR_ADD(slot, v) atomicAdd(&g_trace[blockIdx.x * 16 + (slot)], (unsigned long long)(v))
+#define FK_TR(x) x
+#else
+#define FK_TR_SET(slot, v)
+#define FK_TR_ADD(slot, v)
+#define FK_TR(x)
+#define FK_TP(slot)
+#define FK_TQ(slot)
+#endif
+
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void k_reset_status_body(fikit_status_t* st) {
   if (threadIdx.x == 0) {
@@ -36,11 +61,15 @@ __device__ __forceinline__ void k_reset_status_body(fikit_status_t* st) {
     reinterpret_cast<uint32_t*>(st)[kSchedWord3] = 0;
   }
 }
-__global__ void k_reset_status(fikit_status_t* st) { k_reset_status_body(st); }
+__global__ void k_reset_status(fikit_status_t* st) {
+  pdl_entry();
+  k_reset_status_body(st);
+}
 
 // Zero up to kZeroRegions device regions (4-B multiples) in one launch, and (block 0) reset
 // the status as k_reset_status does: the measure call's table / index / sample zeroing.
 __global__ void k_zero(ZeroList z, fikit_status_t* st) {
+  pdl_entry();
   if (blockIdx.x == 0 && threadIdx.x < 32) k_reset_status_body(st);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   for (int r = 0; r < z.k; r++) {
@@ -62,6 +91,7 @@ __global__ void k_zero(ZeroList z, fikit_status_t* st) {
 // to dict_n and the workspace's dictionary word (read by finalize).
 __global__ void k_dict_load(const uint64_t* __restrict__ dkid, const uint32_t* __restrict__ dtask, uint32_t K,
                             IndexEntry* idx, uint32_t slots, RawRow* raw, fikit_status_t* st, uint32_t* misc) {
+  pdl_entry();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j == 0) {
     st->n_rows_needed = K;
@@ -169,6 +199,7 @@ __device__ __forceinline__ uint64_t thread_fnv_string(const fikit_strtab_t& t, u
 __global__ void __launch_bounds__(128) k_strtab_hash(fikit_strtab_t names, uint64_t* __restrict__ name_out,
                                                      fikit_strtab_t sigs, uint64_t* __restrict__ sig_out,
                                                      fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint4 buf[4][64];
   const bool is_name = blockIdx.y == 0;
   const fikit_strtab_t t = is_name ? names : sigs;
@@ -204,6 +235,7 @@ __global__ void __launch_bounds__(256) k_identify(const uint4* __restrict__ recs
                                                   const uint64_t* __restrict__ name_hash,
                                                   const uint64_t* __restrict__ sig_hash, uint32_t n_names,
                                                   uint32_t n_sigs, uint64_t* __restrict__ out, fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint4 sbuf[8][96];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t nchunks = (n + 31) / 32;
@@ -251,14 +283,17 @@ __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uin
   // its fingerprint; the identity words are read only by the next kernel).  A skewed sample hits
   // a few identities thousands of times; this keeps the global table to one access per distinct
   // identity per block.
-  constexpr uint32_t HS = 512;
+  constexpr uint32_t HS = 1024;  // (<= 512 samples per block: load <= 1/2)
   unsigned long long* sfp = reinterpret_cast<unsigned long long*>(sm);
   uint32_t* scnt = reinterpret_cast<uint32_t*>(sfp + HS);
   uint32_t* stw = scnt + HS;  // [HS][7]
+  uint32_t* snew = stw + 7 * HS;  // [2 * kPrepThreads] sample slots this block claimed, then a count
+  uint32_t* snew_n = snew + 2 * kPrepThreads;
   for (uint32_t i = threadIdx.x; i < HS; i += blockDim.x) {
     sfp[i] = 0;
     scnt[i] = 0;
   }
+  if (threadIdx.x == 0) *snew_n = 0;
   __syncthreads();
   auto global_add = [&](const uint32_t* tw, unsigned long long fp, uint32_t cnt) {
     uint32_t h = (uint32_t)(fp >> 20) & (kSampSlots - 1);
@@ -268,7 +303,7 @@ __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uin
 #pragma unroll
         for (int q = 0; q < 6; q++) a.samp[h].w[q] = tw[q];
         a.samp[h].task = tw[6];
-        a.samp_list[atomicAdd(a.samp_n, 1u)] = h;
+        snew[atomicAdd(snew_n, 1u)] = h;  // (listed once per block below: no global counter per slot)
       }
       if (old == 0ull || old == fp) {
         atomicAdd(&a.samp[h].cnt, cnt);
@@ -310,6 +345,13 @@ __device__ __forceinline__ void prep_sample(const PrepArgs& a, uint32_t blk, uin
   __syncthreads();
   for (uint32_t q = threadIdx.x; q < HS; q += blockDim.x)
     if (scnt[q]) global_add(stw + q * 7, sfp[q], scnt[q]);
+  // the block's new slots join the dense list with one global atomic
+  __syncthreads();
+  const uint32_t nnew = *snew_n;
+  __shared__ uint32_t s_base;
+  if (threadIdx.x == 0 && nnew) s_base = atomicAdd(a.samp_n, nnew);
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < nnew; q += blockDim.x) a.samp_list[s_base + q] = snew[q];
 }
 
 __device__ __forceinline__ void prep_groups(const PrepArgs& a, uint32_t blk, uint32_t* h) {
@@ -340,17 +382,21 @@ __device__ __forceinline__ void prep_groups(const PrepArgs& a, uint32_t blk, uin
 }
 
 __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
-  __shared__ __align__(16) unsigned char sm[512 * 8 + 512 * 4 + 512 * 28];  // the sample role's (largest)
+  pdl_entry();
+  __shared__ __align__(16) unsigned char sm[1024 * 8 + 1024 * 4 + 1024 * 28 + 2 * kPrepThreads * 4 + 4];  // sample role's
   const uint32_t b = blockIdx.x;
+  FK_TR(if (threadIdx.x == 0) { FK_TP(0); g_trace_pre[blockIdx.x * 8 + 7] = b < a.nb_hash ? 1 : b < a.nb_hash + a.nb_samp ? 2 : 3; })
+  FK_TR(struct TrEnd { __device__ ~TrEnd() { __syncthreads(); if (threadIdx.x == 0) FK_TP(1); } } tr_end;)
   if (b < a.nb_hash) {  // names, then signatures: one warp per string
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t j = b * (kPrepThreads / 32) + w;
     const uint32_t nn = a.names.count;
-    if (j >= nn + a.sigs.count) return;
-    const bool is_name = j < nn;
-    const uint64_t h = warp_fnv_string(is_name ? a.names : a.sigs, is_name ? j : j - nn, is_name,
-                                       reinterpret_cast<uint4*>(sm) + w * 64, lane, a.st);
-    if (lane == 0) (is_name ? a.name_hash[j] : a.sig_hash[j - nn]) = h;
+    if (j < nn + a.sigs.count) {
+      const bool is_name = j < nn;
+      const uint64_t h = warp_fnv_string(is_name ? a.names : a.sigs, is_name ? j : j - nn, is_name,
+                                         reinterpret_cast<uint4*>(sm) + w * 64, lane, a.st);
+      if (lane == 0) (is_name ? a.name_hash[j] : a.sig_hash[j - nn]) = h;
+    }
   } else if (b < a.nb_hash + a.nb_samp) {
     prep_sample(a, b - a.nb_hash, a.nb_samp, sm);
   } else {
@@ -366,29 +412,56 @@ __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsign
   constexpr int NB = 4096;
   uint32_t* h = reinterpret_cast<uint32_t*>(sm);
   uint32_t* wsum = h + NB;  // [32]
-  uint32_t* s_misc = wsum + 32;  // T, n, Tmin
+  uint32_t* s_misc = wsum + 32;  // chosen, hot n, T, claims, first claimed row
   Tuple* hot = a.hot_all + (size_t)bkt * kHotMax;
   auto mine = [&](uint32_t task) { return bkt == kGlobalSet || bucket_of(task) == bkt; };
   const uint32_t nd = min(a.hot_hdr[kSampN], kSampSlots);  // distinct sampled identities
+  FK_TR(if (threadIdx.x == 0) { FK_TQ(0); g_trace_pre[(1024 + blockIdx.x) * 8 + 7] = 10; })
   for (int i = threadIdx.x; i < NB; i += blockDim.x) h[i] = 0;
   __syncthreads();
   // (count, task) of 4 listed identities per thread in flight; the loop bound is warp-uniform
-  // (the histogram update below is a full-warp match)
+  // (the histogram update below is a full-warp match).  The first two rounds stay in registers
+  // for the selection pass (no second read of the list for nd <= 8192).
   constexpr uint32_t U = 4;
   const uint32_t lane_id = threadIdx.x & 31u;
-  for (uint32_t i0 = threadIdx.x; i0 - lane_id < nd; i0 += U * blockDim.x) {
-    uint2 ct[U];
+  uint32_t e0[U], e1[U];
+  uint2 c0[U], c1[U];
+  auto load_round = [&](uint32_t i0, uint32_t* ent, uint2* ct) {
 #pragma unroll
     for (uint32_t u = 0; u < U; u++) {
       const uint32_t i = i0 + u * blockDim.x;
-      ct[u] = i < nd ? *reinterpret_cast<const uint2*>(a.samp + __ldg(a.samp_list + i)) : make_uint2(0u, 0u);
+      ent[u] = i < nd ? __ldg(a.samp_list + i) : 0u;
     }
+#pragma unroll
+    for (uint32_t u = 0; u < U; u++) {
+      const uint32_t i = i0 + u * blockDim.x;
+      ct[u] = i < nd ? *reinterpret_cast<const uint2*>(a.samp + ent[u]) : make_uint2(0u, 0u);
+    }
+  };
+  auto count_round = [&](const uint2* ct) {
 #pragma unroll
     for (uint32_t u = 0; u < U; u++) {  // warp-aggregated: skewed samples give many equal counts
       const bool in = ct[u].x && mine(ct[u].y);
       const uint32_t bin = in ? min(ct[u].x, (uint32_t)NB - 1) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (in && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+      if (in && (peers & ((1u << lane_id) - 1u)) == 0) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    }
+  };
+  {
+    uint32_t r = 0;
+    for (uint32_t i0 = threadIdx.x; i0 - lane_id < nd; i0 += U * blockDim.x, r++) {
+      if (r == 0) {
+        load_round(i0, e0, c0);
+        count_round(c0);
+      } else if (r == 1) {
+        load_round(i0, e1, c1);
+        count_round(c1);
+      } else {
+        uint32_t ent[U];
+        uint2 ct[U];
+        load_round(i0, ent, ct);
+        count_round(ct);
+      }
     }
   }
   if (threadIdx.x == 0) {
@@ -426,17 +499,10 @@ __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsign
     __syncthreads();
   }
   const uint32_t T = s_misc[2];
+  FK_TR(if (threadIdx.x == 0) FK_TQ(2);)
   uint32_t* chosen = h;  // (the histogram is no longer needed) [kHotMax] sample slots
   uint32_t tot = 0;
-  for (uint32_t i0 = threadIdx.x; i0 < nd; i0 += U * blockDim.x) {
-    uint32_t ent[U];
-    uint2 ct[U];
-#pragma unroll
-    for (uint32_t u = 0; u < U; u++) {  // U (count, task) loads in flight
-      const uint32_t i = i0 + u * blockDim.x;
-      ent[u] = i < nd ? __ldg(a.samp_list + i) : 0u;
-      ct[u] = i < nd ? *reinterpret_cast<const uint2*>(a.samp + ent[u]) : make_uint2(0u, 0u);
-    }
+  auto choose_round = [&](const uint32_t* ent, const uint2* ct) {
 #pragma unroll
     for (uint32_t u = 0; u < U; u++) {
       const uint32_t c = ct[u].x;
@@ -447,25 +513,100 @@ __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsign
         if (e < kHotMax) chosen[e] = ent[u];
       }
     }
+  };
+  {
+    uint32_t r = 0;
+    for (uint32_t i0 = threadIdx.x; i0 - lane_id < nd; i0 += U * blockDim.x, r++) {
+      if (r == 0) {
+        choose_round(e0, c0);
+      } else if (r == 1) {
+        choose_round(e1, c1);
+      } else {
+        uint32_t ent[U];
+        uint2 ct[U];
+        load_round(i0, ent, ct);
+        choose_round(ent, ct);
+      }
+    }
   }
   __syncthreads();
-  // resolve the chosen identities to rows, one per thread (their latency chains overlap)
+  FK_TR(if (threadIdx.x == 0) FK_TQ(3);)
+  // Resolve the chosen identities to rows, one per thread (nc <= kHotMax < blockDim.x), the new
+  // rows allocated with ONE global atomic per block: (1) probe the KID index, claiming an empty
+  // slot by CAS without waiting on anyone (a slot another thread is writing: pending); (2) the
+  // block counts its claims, one thread reserves their rows; (3) the claimers publish (release
+  // store); (4) pending threads finish with the ordinary find-or-insert, whose waits can only be
+  // on other blocks' claimers, which never wait.  (One row counter hit by every new row had
+  // serialised ~8k L2 atomics.)
   const uint32_t nc = min(s_misc[0], kHotMax);
-  uint32_t cov = 0;
-  for (uint32_t q = threadIdx.x; q < nc; q += blockDim.x) {
+  uint32_t* s_claims = s_misc + 3;  // claims of this block; s_misc[4]: first reserved row
+  if (threadIdx.x == 0) *s_claims = 0;
+  __syncthreads();
+  const uint32_t q = threadIdx.x;
+  Tuple t;
+  uint64_t kid = 0;
+  uint32_t cnt = 0, slot = 0, mine_n = 0;
+  int state = -1;  // -1 none, 0 row known, 1 claimed slot, 2 pending
+  if (q < nc) {
     const SampEntry& se = a.samp[chosen[q]];
     const uint2 ct = *reinterpret_cast<const uint2*>(&se);
-    Tuple t;
 #pragma unroll
     for (int w = 0; w < 6; w++) t.w[w] = se.w[w];
     t.w[6] = ct.y;
-    const uint64_t kid = kernel_id_from(__ldg(a.name_hash + t.w[0]), __ldg(a.sig_hash + t.w[1]), t.w[2], t.w[3],
-                                        t.w[4], t.w[5]);
+    cnt = ct.x;
+    kid = kernel_id_from(__ldg(a.name_hash + t.w[0]), __ldg(a.sig_hash + t.w[1]), t.w[2], t.w[3], t.w[4], t.w[5]);
+    uint32_t h = key_hash(kid, t.w[6]) & (a.slots - 1);
+    state = 2;
+    for (uint32_t probe = 0; probe < a.slots; probe++, h = (h + 1) & (a.slots - 1)) {
+      uint4 v = ld_relaxed_v4(&a.idx[h]);
+      uint32_t st_w = v.w;
+      if (st_w == 0u) {
+        if (a.dict) {  // dictionary mode: an absent key has no row
+          t.row = FIKIT_NO_ROW;
+          state = 0;
+          break;
+        }
+        st_w = atomicCAS(&a.idx[h].state, 0u, kBusy);
+        if (st_w == 0u) {
+          a.idx[h].kid = kid;
+          a.idx[h].task = t.w[6];
+          slot = h;
+          state = 1;
+          mine_n = atomicAdd(s_claims, 1u);
+          break;
+        }
+        v = ld_relaxed_v4(&a.idx[h]);
+      }
+      if (st_w == kBusy) break;  // pending: resolved after this block's claims are published
+      if ((((uint64_t)v.y << 32) | v.x) == kid && v.z == t.w[6]) {
+        t.row = st_w - 1;
+        state = 0;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && *s_claims) s_misc[4] = (uint32_t)atomicAdd((unsigned long long*)&a.st->n_rows_needed,
+                                                                   (unsigned long long)*s_claims);
+  __syncthreads();
+  if (state == 1) {  // publish: the row's key, a representative tuple, then the slot
+    t.row = s_misc[4] + mine_n;
+    if (t.row < a.cap) {
+      a.raw[t.row].kid = kid;
+      a.raw[t.row].task = t.w[6];
+      a.row_tuple[t.row] = t;
+    } else {
+      atomicOr(&a.st->flags, kStatusCapacity);
+    }
+    st_release_u32(&a.idx[slot].state, t.row + 1);
+  } else if (state == 2) {
     t.row = index_find_or_insert(a.idx, a.slots, kid, t.w[6], t.w, a.st, a.raw, a.row_tuple, a.cap, a.dict == 0u);
-    if (t.row >= a.cap) continue;  // (E_CAPACITY is flagged; the row is not materialised)
+  }
+  uint32_t cov = 0;
+  if (state >= 0 && t.row < a.cap) {  // (E_CAPACITY is flagged; the row is not materialised)
     const uint32_t e = atomicAdd(&s_misc[1], 1u);
     hot[e] = t;
-    cov += ct.x;
+    cov = cnt;
   }
   cov = __reduce_add_sync(0xffffffffu, cov);
   tot = __reduce_add_sync(0xffffffffu, tot);
@@ -475,6 +616,7 @@ __device__ __forceinline__ void plan_hot(const PlanArgs& a, uint32_t bkt, unsign
   }
   __syncthreads();
   if (threadIdx.x == 0) a.hot_hdr[bkt] = min(s_misc[1], kHotMax);
+  FK_TR(if (threadIdx.x == 0) FK_TQ(4);)
 }
 
 // stable counting-sort scatter of block k's chunk of tile groups: its offsets are the buckets'
@@ -599,13 +741,16 @@ __device__ __forceinline__ void plan_scatter(const PlanArgs& a, uint32_t k, unsi
 }
 
 __global__ void __launch_bounds__(1024) k_plan(PlanArgs a) {
-  __shared__ __align__(16) unsigned char sm[(4096 + 32 + 4) * 4 > (2 * 16 + 2 + 32) * kBuckets * 4
-                                                ? (4096 + 32 + 4) * 4
+  pdl_entry();
+  __shared__ __align__(16) unsigned char sm[(4096 + 32 + 8) * 4 > (2 * 16 + 2 + 32) * kBuckets * 4
+                                                ? (4096 + 32 + 8) * 4
                                                 : (2 * 16 + 2 + 32) * kBuckets * 4];
   if (blockIdx.x <= kBuckets) {
     plan_hot(a, blockIdx.x, sm);
   } else {
+    FK_TR(if (threadIdx.x == 0) { FK_TQ(0); g_trace_pre[(1024 + blockIdx.x) * 8 + 7] = 11; })
     plan_scatter(a, blockIdx.x - (kBuckets + 1), sm);
+    FK_TR(if (threadIdx.x == 0) FK_TQ(4);)
   }
 }
 
@@ -779,6 +924,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
               const uint32_t* __restrict__ hot_n_all, uint32_t* cur, uint32_t* act, const uint32_t* __restrict__ bstart,
               const uint32_t* __restrict__ btot, const uint32_t* __restrict__ first,
               const uint32_t* __restrict__ order, uint32_t ntiles, uint32_t* __restrict__ out_row, uint32_t dict) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
   const uint32_t sbase = smem_u32(smem_raw);
@@ -792,7 +938,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     S.overlap = 0;
     for (int i = 0; i < mk::WARPS; i++) mbar_init(&S.full[i], 1);
     fence_mbar_init();
+    FK_TR_SET(0, gtime());
   }
+  FK_TR(__shared__ unsigned long long tr_first_done; uint32_t tr_tiles = 0; unsigned long long tr_t0 = 0;)
   // load the hot set of a task bucket into the shared dictionary, zero the statistics
   auto load_hot_set = [&](uint32_t bkt) {
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
@@ -856,16 +1004,22 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // serves every warp in address-order mode); the next range's atomic is issued when the
   // current range is taken, so its result is needed only kClaim tiles later.
   constexpr uint32_t kClaim = 8;
+  // The last kTailTiles positions of a bucket are claimed one at a time: a warp that took 8 tiles
+  // at the very end would keep its CTA's other warps waiting at the phase barrier for up to 8
+  // tile times (~18 us measured with 8-tile claims throughout).
+  constexpr uint32_t kTailTiles = 32 * mk::WARPS;
   uint32_t pc = kNone;   // lane 0: claimed position
   uint32_t tn = kNone;   // lane 0: tile of the previous claim (order[] load in flight)
   uint32_t q_pos = 0, q_end = 0, nx = kNone;  // lane 0: current range, next range's start
+  uint32_t nsz = kClaim;                       // lane 0: size of the next range
   auto claim = [&]() {   // lane 0
     pc = kNone;
     if (q_pos >= q_end) {
       if (nx == kNone || nx >= cb_end) return;  // drained (claims are monotone)
       q_pos = nx;
-      q_end = min(nx + kClaim, cb_end);
-      nx = atomicAdd(cur + cb, kClaim);
+      q_end = min(nx + nsz, cb_end);
+      nsz = cb_end - q_end > kTailTiles ? kClaim : 1u;
+      nx = atomicAdd(cur + cb, nsz);
     }
     pc = q_pos++;
   };
@@ -898,6 +1052,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   uint64_t pd = 0, pg = 0;
   uint32_t np = 0;
   auto flush_cold = [&]() {
+    FK_TR(if (lane == 0) FK_TR_ADD(8, 1);)
     const uint32_t pend = __ballot_sync(0xffffffffu, lane < (int)np);
     if (lane < (int)np) {
       const uint32_t key[7] = {pk0, pk1, pk2, pk3, pk4, pk5 & 0xFFFFu, pk6};
@@ -1069,14 +1224,15 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 
   uint32_t* s_next = &S.next_bucket;
   // the bucket to move to: the most unclaimed tiles among buckets nobody works on (they must
-  // be taken) or with more than 128 left (worth a hot-set reload); CTA-uniform
+  // be taken) or with more than two tiles left per warp of the CTAs on it and ours (worth a
+  // hot-set reload); CTA-uniform
   auto pick_bucket = [&]() -> uint32_t {
     if (warp == 0) {  // the lanes read the buckets' counters in parallel (one L2 round trip)
       uint32_t best = kNoBucket, most = 0;
       for (uint32_t b = lane; b < kSchedWords; b += 32) {
         const uint32_t e = len_of(b), c = *(volatile uint32_t*)(cur + b), a = *(volatile uint32_t*)(act + b);
         const uint32_t left = e > c ? e - c : 0u;
-        if (left > most && (left > 128u || a == 0u)) {
+        if (left > most && (left > 2u * mk::WARPS * (a + 1u) || a == 0u)) {
           most = left;
           best = b;
         }
@@ -1095,11 +1251,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   if (cb == kNoBucket) cb = pick_bucket();
   while (cb != kNoBucket) {
     if (tid == 0) atomicAdd(act + cb, 1u);
+    FK_TR(if (tid == 0) { tr_t0 = gtime(); tr_first_done = ~0ull; FK_TR_ADD(3, 1); })
     load_hot_set(cb);
+    FK_TR(if (tid == 0) { const unsigned long long t = gtime(); FK_TR_ADD(5, t - tr_t0); if (g_trace[blockIdx.x * 16 + 1] == 0) FK_TR_SET(1, t); })
     cb_end = len_of(cb);
     cb_base = by_task ? kGroupTiles * bstart[cb] : 0u;
     q_pos = q_end = 0;
-    if (lane == 0) nx = atomicAdd(cur + cb, kClaim);
+    nsz = 1u;  // (the first range: one tile, the pipeline then sizes the next from its position)
+    if (lane == 0) nx = atomicAdd(cur + cb, 1u);
     // prime the pipeline: the first tile's TMA, the second tile's order[] load, a third claim
     bool staged = false;  // (all lanes) a tile is in flight to the stage
     if (lane == 0) {
@@ -1129,6 +1288,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         Rec A, B;
         mbar_wait_s(s_full + 8u * warp, kk & 1u);
         kk++;
+        FK_TR(tr_tiles++;)
         load_half(0, A);
         load_half(1, B);
         // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
@@ -1162,23 +1322,47 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         compact(A, A.valid && sA < 0);
         compact(B, B.valid && sB < 0);
       }
+      FK_TR(if (lane == 0) atomicMin(&tr_first_done, gtime());)
       __syncthreads();
+      FK_TR(if (tid == 0) { tr_t0 = gtime(); FK_TR_ADD(6, tr_t0 - tr_first_done); })
       flush_epoch(S, tab, tid);
       __syncthreads();
     }
     flush_hot_set_ext();
     if (tid == 0) atomicSub(act + cb, 1u);  // every claim of cb is done
     cb = pick_bucket();  // (its barriers also keep the shared rows until every warp is done)
+    FK_TR(if (tid == 0) FK_TR_ADD(7, gtime() - tr_t0);)
   }
+  FK_TR(if (lane == 0) FK_TR_ADD(4, tr_tiles);)
   if (np) flush_cold();
   // warp-aggregate the overlap count
   uint32_t ov_w = __reduce_add_sync(0xffffffffu, overlap_cnt);
   if (lane == 0 && ov_w) atomicAdd(&S.overlap, (unsigned long long)ov_w);
   __syncthreads();
   if (tid == 0 && S.overlap) atomicAdd((unsigned long long*)&st->n_overlap_gaps, S.overlap);
+  FK_TR(if (tid == 0) FK_TR_SET(2, gtime());)
 }
 
 size_t measure_smem_bytes() { return sizeof(mk::Smem); }
+
+#ifdef FIKIT_TRACE
+// (diagnosis builds only; not part of the C-ABI)
+extern "C" int fikit_debug_trace(void* host, int reset) {
+  if (reset) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_trace) != cudaSuccess) return -4;
+    if (cudaMemset(p, 0, sizeof(g_trace)) != cudaSuccess) return -4;
+    if (cudaGetSymbolAddress(&p, g_trace_pre) != cudaSuccess) return -4;
+    return cudaMemset(p, 0, sizeof(g_trace_pre)) == cudaSuccess ? 0 : -4;
+  }
+  return cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : -4;
+}
+// which = 1: the k_prep / k_plan block stamps of the last call (k_plan's overwrite k_prep's blocks
+// with the same index: read after a call that launched only one of them, or compare roles)
+extern "C" int fikit_debug_trace_pre(void* host) {
+  return cudaMemcpyFromSymbol(host, g_trace_pre, sizeof(g_trace_pre)) == cudaSuccess ? 0 : -4;
+}
+#endif
 int measure_threads() { return mk::THREADS; }
 
 }  // namespace fikit

@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
            const uint32_t* __restrict__ pool_len, uint32_t G, fikit_fill_params_t prm, uint32_t* __restrict__ picks,
            const uint32_t* __restrict__ picks_off, uint32_t* __restrict__ n_picks, uint64_t* __restrict__ R_left,
            uint64_t* __restrict__ t_used, fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint64_t s_q[kReplayWarps][kPoolMax];
   __shared__ uint8_t s_meta[kReplayWarps][kPoolMax];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -742,6 +743,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 war
                    const fikit_scenario_t* __restrict__ sc, uint32_t S, fikit_fill_params_t prm,
                    fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap, uint64_t* __restrict__ lp_start,
                    const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
+  pdl_entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t K = min(*tab.n_rows, tab.capacity);
   constexpr bool sched = kSched;
@@ -799,6 +801,7 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
                const fikit_scenario_t* __restrict__ sc, uint32_t S, fikit_fill_params_t prm,
                fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap, uint64_t* __restrict__ lp_start,
                const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint64_t s_q[kReplayWarps][kPoolMax];
   __shared__ uint8_t s_meta[kReplayWarps][kPoolMax];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -878,6 +881,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
                       fikit_fill_params_t prm,
                       fikit_result_t* __restrict__ out, int32_t* __restrict__ fill_gap,
                       uint64_t* __restrict__ lp_start, const uint64_t* __restrict__ sched_off, fikit_status_t* st) {
+  pdl_entry();
   __shared__ uint32_t s_start[kStreamWarps][kMaxStreams];
   __shared__ uint64_t s_q[kStreamWarps][kPoolMax];
   __shared__ uint8_t s_lv[kStreamWarps][kPoolMax];  // level | eligible << 7
@@ -1173,10 +1177,10 @@ void launch_simulate_smem(int blocks, int threads, cudaStream_t s, const fikit_t
                           fikit_fill_params_t prm, fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
                           const uint64_t* sched_off, fikit_status_t* st) {
   if (fill_gap && lp_start && sched_off)
-    k_simulate<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
+    launch_pdl(k_simulate<true>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm, out,
                                                  fill_gap, lp_start, sched_off, st);
   else
-    k_simulate<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+    launch_pdl(k_simulate<false>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
                                                   out, fill_gap, lp_start, sched_off, st);
 }
 const void* simulate_stream_kernel(bool sched) {
@@ -1188,10 +1192,10 @@ void launch_simulate_reg(int blocks, int threads, cudaStream_t s, const fikit_ta
                          fikit_fill_params_t prm, fikit_result_t* out, int32_t* fill_gap, uint64_t* lp_start,
                          const uint64_t* sched_off, fikit_status_t* st) {
   if (fill_gap && lp_start && sched_off)
-    k_simulate_reg<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+    launch_pdl(k_simulate_reg<true>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
                                                      out, fill_gap, lp_start, sched_off, st);
   else
-    k_simulate_reg<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
+    launch_pdl(k_simulate_reg<false>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level, sc, S, prm,
                                                       out, fill_gap, lp_start, sched_off, st);
 }
 void launch_simulate_stream(int blocks, int threads, cudaStream_t s, const fikit_table_t& tab,
@@ -1201,11 +1205,11 @@ void launch_simulate_stream(int blocks, int threads, cudaStream_t s, const fikit
                             const fikit_scenario_t* sc, uint32_t S, fikit_fill_params_t prm, fikit_result_t* out,
                             int32_t* fill_gap, uint64_t* lp_start, const uint64_t* sched_off, fikit_status_t* st) {
   if (fill_gap && lp_start && sched_off)
-    k_simulate_stream<true><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
+    launch_pdl(k_simulate_stream<true>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
                                                         lp_stream, lp_think, hp_arrival, sc, S, prm, out, fill_gap,
                                                         lp_start, sched_off, st);
   else
-    k_simulate_stream<false><<<blocks, threads, 0, s>>>(tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
+    launch_pdl(k_simulate_stream<false>, blocks, threads, 0, s, tab, hp_row, hp_dur, hp_gap, lp_row, lp_dur, lp_level,
                                                          lp_stream, lp_think, hp_arrival, sc, S, prm, out, fill_gap,
                                                          lp_start, sched_off, st);
 }
