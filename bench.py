@@ -52,6 +52,8 @@ def parse():
                     help="mode,pct for fikit_table_predict before each replay (SURVEY §8f row 3; default: the "
                          "paper's means)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-configs2", action="store_true",
+                    help="skip the configs[2] (BERT/VGG 100k-scenario replay) leg of the default line")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -398,6 +400,61 @@ def run_reference(args):
     return 0
 
 
+def replay_roofline(workload, scenarios, sim_ms, sm_mhz):
+    """Issue roofline of the replay kernels: achieved warp-instructions/s (ncu's per-scenario count,
+    profiles/replay_inst.json, x the scenarios of a step / the replay call's live time) against
+    the SM issue peak (SMs x 4 schedulers x one warp-instruction per cycle at the measured clock)."""
+    import torch
+
+    rec = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "replay_inst.json")) as f:
+            rec = json.load(f).get(workload)
+    except Exception:
+        pass
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    out = {"bound": "issue", "kernel": "fikit_simulate_batch (k_simulate_reg + k_simulate)", "call_ms": sim_ms,
+           "scenarios": scenarios, "scenarios_per_s": scenarios / (sim_ms * 1e-3)}
+    if rec and sm_mhz:
+        ach = rec["warp_inst_per_scenario"] * scenarios / (sim_ms * 1e-3) / 1e9
+        peak = sms * 4 * sm_mhz * 1e6 / 1e9
+        out.update({"achieved": ach, "peak": peak, "unit": "G warp-instructions/s", "frac": ach / peak,
+                    "warp_inst_per_scenario": rec["warp_inst_per_scenario"], "inst_source": rec.get("source"),
+                    "peak_source": f"{sms} SMs x 4 issue slots x {sm_mhz:.0f} MHz (measured under load)"})
+    return out
+
+
+def configs2_leg(fk, Pipeline, stream, args, steps=20, warmup=3):
+    """BASELINE configs[2] in the default line: the BERT/VGG trace (216k launches) measured and its
+    100k scenarios (one warp each) replayed, timed per step with L2 flushed before each step."""
+    import torch
+
+    import fikit_synth as F
+
+    cfg = F.bert_vgg()
+    q = Pipeline(cfg.trace.records, cfg.trace.names, cfg.trace.sigs, capacity=4096, replay=cfg.replay)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    for _ in range(warmup):
+        q.step()
+    q.check("configs2 warm-up")
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        q.run_measure()
+        q.run_replay(sim_events=(ev[i][1], ev[i][2]))
+        ev[i][3].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([e[0].elapsed_time(e[3]) for e in ev]))
+    sim = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    S = cfg.replay.scenarios.shape[0]
+    return {"workload": "bert_vgg-100k (configs[2]): 216k-launch measurement + 100k scenarios, m = 64",
+            "scenarios_per_s": S / (ms * 1e-3), "ms_per_step": ms, "replay_call_ms": sim,
+            "replay_scenarios_per_s": S / (sim * 1e-3), "steps": steps, "warmup": warmup,
+            "l2": "inputs fit the L2: a 256 MB write flushes it before every step (outside the step's events)"}
+
+
 # ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
@@ -447,6 +504,8 @@ def main():
     for a, b in kev:  # (torch creates the CUDA events on first record)
         a.record(stream)
         b.record(stream)
+    # the replay call alone (fikit_simulate_batch: its two kernels), live in every timed step
+    rev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
     # dictionary mode (repeated services keep their kernel IDs): the first
     # warm-up step measures and merges with the general path; its (merged) table's keys become the
@@ -455,12 +514,13 @@ def main():
     use_dict = (world > 1 and args.merge == "dict") or (world == 1 and args.dict)
     dict_state = None
 
-    def step(timed, kpair=None, checked=False):
+    def step(timed, kpair=None, checked=False, spair=None):
         # checked (first warm-up step): the workspace status after EVERY call (each validating
         # call resets it, so one check at the end would only see the last call)
         if timed:
             ev[0].record(stream)
         fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair, dictionary=dict_state)
+        p.measured = True  # (the workspace holds the string hashes: resolve reuses them)
         st = fk.check(p.ws, "bench warm-up: measure") if checked else None
         if timed:
             ev[1].record(stream)
@@ -479,7 +539,7 @@ def main():
             ev[2].record(stream)
         if p.replay:
             p.checked = checked
-            p.run_replay(table=tab)  # (checked: after each resolve and replay call)
+            p.run_replay(table=tab, sim_events=spair)  # (checked: after each resolve and replay call)
             p.checked = False
         if timed:
             ev[3].record(stream)
@@ -524,7 +584,7 @@ def main():
             if flush is not None:
                 flush.zero_()
                 sev[i][0].record(stream)
-            step(False, kev[i])
+            step(False, kev[i], spair=rev[i] if p.replay else None)
             if flush is not None:
                 sev[i][1].record(stream)
         t1.record(stream)
@@ -583,6 +643,12 @@ def main():
             "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
             "status": {"code": st["code"], "n_rows_needed": st["n_rows_needed"]},
             "gen_s": round(t_gen, 2)}
+
+    if p.replay:  # the replay kernels: issue-bound, warp-instructions per scenario from ncu
+        sim_ms = float(np.mean([a.elapsed_time(b) for a, b in rev]))
+        line["replay_roofline"] = replay_roofline(args.workload, S_local, sim_ms, line["clocks"].get("sm_mhz"))
+    if rank == 0 and world == 1 and args.workload == "zipf" and not args.no_configs2:
+        line["configs2_bert_vgg"] = configs2_leg(fk, Pipeline, stream, args)
 
     if wl["ratio"] is not None:  # §4.3.2 trend: mean exclusive / FIKIT LP JCT per A:B ratio and series
         line["ratio_sweep"] = ratio_summary(p.results(), p.exclusive_results(), wl["ratio"], wl["replay"].scenarios)

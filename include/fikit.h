@@ -243,6 +243,16 @@ int fikit_resolve(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
                   fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
                   uint64_t* out_gap, void* ws, size_t ws_bytes, void* stream);
 
+/* fikit_resolve with flags.  FIKIT_RESOLVE_REUSE_HASHES: skip hashing the string tables --
+ * the workspace already holds their hashes because the previous fikit_measure /
+ * fikit_measure_dict / fikit_resolve on this workspace hashed the SAME tables (same device
+ * bytes, unchanged) with a table of tab->capacity rows; requires a workspace sized for that
+ * capacity (FIKIT_E_ARG otherwise).  One measure + two resolves of a step hash the strings once. */
+#define FIKIT_RESOLVE_REUSE_HASHES 1u
+int fikit_resolve_ex(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next, fikit_strtab_t names,
+                     fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
+                     uint64_t* out_gap, uint32_t flags, void* ws, size_t ws_bytes, void* stream);
+
 /* out_row[i] = canonical row of (task[i], kid[i]) or FIKIT_NO_ROW (binary search). */
 int fikit_lookup(const fikit_table_t* tab, const uint64_t* kid, const uint32_t* task, uint64_t n, uint32_t* out_row,
                  void* stream);

@@ -23,7 +23,7 @@ OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME, E_DICT = 0, -1, -2, -3, -4, -5,
 NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
-           "fikit_measure_timed", "fikit_measure_dict", "fikit_measure_dict_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_lookup", "fikit_fill",
+           "fikit_measure_timed", "fikit_measure_dict", "fikit_measure_dict_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_resolve_ex", "fikit_lookup", "fikit_fill",
            "fikit_simulate_batch", "fikit_simulate_stream_batch",
            "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
@@ -83,6 +83,7 @@ def lib():
         L.fikit_table_means.argtypes = [C.POINTER(TableC), p]
         L.fikit_table_predict.argtypes = [C.POINTER(TableC), u32, u32, p]
         L.fikit_resolve.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, p, p, sz, p]
+        L.fikit_resolve_ex.argtypes = [p, u64, p, StrTabC, StrTabC, C.POINTER(TableC), p, p, p, u32, p, sz, p]
         L.fikit_lookup.argtypes = [C.POINTER(TableC), p, p, u64, p, p]
         L.fikit_fill.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, u32, FillParamsC, p, p, p, p, p, p, sz, p]
         L.fikit_simulate_batch.argtypes = [C.POINTER(TableC), p, p, p, p, p, p, p, u32, FillParamsC, p, p, p, p, p,
@@ -148,8 +149,13 @@ class DevStrTab:
 
 
 def strtab_to_device(tab, device="cuda") -> DevStrTab:
+    """The bytes are zero-padded to a multiple of 16: the kernels read whole aligned 16-B blocks
+    (include/fikit.h), so the padding keeps every byte they touch initialised."""
     torch = _torch()
-    data = torch.from_numpy(np.ascontiguousarray(tab.data)).to(device)
+    raw = np.ascontiguousarray(tab.data, dtype=np.uint8)
+    pad = np.zeros(((raw.shape[0] + 16) // 16) * 16, dtype=np.uint8)
+    pad[: raw.shape[0]] = raw
+    data = torch.from_numpy(pad).to(device)
     offs = torch.from_numpy(np.ascontiguousarray(tab.offsets).view(np.int32)).to(device)
     return DevStrTab(data, offs, int(tab.count))
 
@@ -304,7 +310,14 @@ def table_predict(table: Table, mode: int, pct: int = 90, stream=None):
 
 
 def resolve(recs, n: int, names: DevStrTab, sigs: DevStrTab, table: Table, out_row, out_dur, out_gap, ws: Workspace,
-            halo=None, stream=None):
+            halo=None, stream=None, reuse_hashes: bool = False):
+    """reuse_hashes: the workspace holds these string tables' hashes from the previous measure /
+    resolve call on it (FIKIT_RESOLVE_REUSE_HASHES: no re-hashing)."""
+    if reuse_hashes:
+        _chk(lib().fikit_resolve_ex(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),
+                                    _ptr(out_dur), _ptr(out_gap), 1, ws.ptr(), ws.nbytes, _stream(stream)),
+             "resolve_ex")
+        return
     _chk(lib().fikit_resolve(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),
                              _ptr(out_dur), _ptr(out_gap), ws.ptr(), ws.nbytes, _stream(stream)), "resolve")
 

@@ -73,7 +73,7 @@ namespace {
 // device and published with a relaxed atomic store, so concurrent first calls only repeat the
 // same query and a second device gets its own entry (no per-process "first device" state).
 constexpr int kMaxDevices = 64;
-enum : int { kPropSms, kPropWaveReg, kPropWaveSmem, kPropWaveStream, kPropMeasureAttr, kPropFinAttr, kNumProps };
+enum : int { kPropSms, kPropWaveReg, kPropWaveSmem, kPropWaveStream, kPropMeasureAttr, kPropFinAttr, kPropResolveAttr, kNumProps };
 std::atomic<int> g_prop[kMaxDevices][kNumProps];  // 0 = not computed yet
 
 int cur_device() {
@@ -433,22 +433,48 @@ int fikit_table_predict(const fikit_table_t* tab, uint32_t mode, uint32_t pct, v
   return launched();
 }
 
-int fikit_resolve(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
-                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
-                  uint64_t* out_gap, void* ws, size_t ws_bytes, void* stream) {
+static int resolve_impl(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                        fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
+                        uint64_t* out_gap, void* ws, size_t ws_bytes, void* stream, uint32_t flags) {
   cudaStream_t s = (cudaStream_t)stream;
   Ws w;
   if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16) || !out_row || !out_dur || !out_gap)) ||
-      !strtab_ok(names) || !strtab_ok(sigs) || !table_ok(tab))
+      !strtab_ok(names) || !strtab_ok(sigs) || !table_ok(tab) || (flags & ~FIKIT_RESOLVE_REUSE_HASHES))
     return FIKIT_E_ARG;
-  if (int r = get_ws(ws, ws_bytes, 1, names.count, sigs.count, &w)) return r;
+  // the measure call's layout (its string hashes) when the workspace holds a table of this capacity
+  const bool measure_layout =
+      ws && ws_bytes >= ws_layout(tab->capacity, names.count, sigs.count, 0).total;
+  if ((flags & FIKIT_RESOLVE_REUSE_HASHES) && !measure_layout) return FIKIT_E_ARG;
+  if (int r = get_ws(ws, ws_bytes, measure_layout ? tab->capacity : 1, names.count, sigs.count, &w)) return r;
   if (int r = reset_status(w, s)) return r;
-  if (int r = hash_strtabs(w, names, sigs, s)) return r;
+  if (!(flags & FIKIT_RESOLVE_REUSE_HASHES))
+    if (int r = hash_strtabs(w, names, sigs, s)) return r;
   if (n == 0) return FIKIT_OK;
-  launch_pdl(k_resolve, grid_for((n + 31) / 32, 8, num_sms() * 8), 256, 0, s, 
-      reinterpret_cast<const uint4*>(recs), n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, *tab,
-      out_row, out_dur, out_gap, w.st());
+  const size_t smem = sizeof(uint4) * (kResolveThreads / 32) * 99 + 12ull * kResolveSmemKeys;
+  if (dev_prop(kPropResolveAttr, [&](int) {
+        return cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess
+                   ? 1
+                   : -1;
+      }) < 0)
+    return FIKIT_E_CUDA;
+  const uint64_t nchunks = (n + 31) / 32;
+  const uint64_t blocks = (nchunks + kResolveThreads / 32 - 1) / (kResolveThreads / 32);
+  launch_pdl(k_resolve, (unsigned)(blocks < (uint64_t)num_sms() ? blocks : (uint64_t)num_sms()), kResolveThreads,
+             smem, s, reinterpret_cast<const uint4*>(recs), n, halo, w.name_hash(), w.sig_hash(), names.count,
+             sigs.count, *tab, out_row, out_dur, out_gap, w.st());
   return launched();
+}
+
+int fikit_resolve(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                  fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
+                  uint64_t* out_gap, void* ws, size_t ws_bytes, void* stream) {
+  return resolve_impl(recs, n, halo, names, sigs, tab, out_row, out_dur, out_gap, ws, ws_bytes, stream, 0u);
+}
+
+int fikit_resolve_ex(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                     fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, uint64_t* out_dur,
+                     uint64_t* out_gap, uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+  return resolve_impl(recs, n, halo, names, sigs, tab, out_row, out_dur, out_gap, ws, ws_bytes, stream, flags);
 }
 
 int fikit_lookup(const fikit_table_t* tab, const uint64_t* kid, const uint32_t* task, uint64_t n, uint32_t* out_row,

@@ -89,6 +89,8 @@ struct FinKey {                          // a sorted key of finalize's groups (w
   unsigned long long kid;
   uint32_t task, pad;
 };
+constexpr int kResolveThreads = 1024;        // k_resolve block (one per SM)
+constexpr uint32_t kResolveSmemKeys = 8192;  // table keys staged in shared memory (96 KB) up to this K
 constexpr int kRegThreads = 512;  // k_simulate_reg block (16 warps, one scenario each)
 constexpr int kSimThreads = 128;  // k_simulate block (4 warps, shared-memory pools)
 constexpr int kStreamThreads = 128;  // k_simulate_stream block (4 warps, staged windows)

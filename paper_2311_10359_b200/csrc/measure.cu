@@ -1310,8 +1310,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
         const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
         const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
-        const bool vA = verify(eA, A) & (cA != 0u);
-        const bool vB = verify(eB, B) & (cB != 0u);
+        // (verify only a matched slot: a speculative read of slot 0 would race with its admission)
+        const bool vA = cA != 0u && verify(eA, A);
+        const bool vB = cB != 0u && verify(eB, B);
         int sA = -1, sB = -1;
         if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
         if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);

@@ -357,36 +357,39 @@ struct DigestBatch {
 // the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^50.
 struct RegPool {
   static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
-  uint32_t q0, q1;    // predicted duration at sorted positions lane, 32 + lane (< 2^22 ns)
-  uint32_t k0, k1;    // request index there
+  // at sorted positions lane, 32 + lane: q << 6 | request index (q < 2^22 ns; 0xFFFFFFFF: an
+  // ineligible position), and the request's LP duration (< 2^32 ns), so a pick is one ballot on
+  // the packed word and two independent shuffles (no duration lookup by index after it)
+  uint32_t pk0, pk1;
+  uint32_t es0, es1;
   bool a0, a1;        // alive and eligible there
   uint32_t dur0, dur1;  // LP duration of requests lane, 32 + lane (< 2^32 ns)
   uint32_t lvl0, lvl1;  // level of requests lane, 32 + lane
   uint64_t alive;     // alive requests by index (warp-uniform)
+  uint32_t ek;        // the last pick's duration
 
   __device__ __forceinline__ uint64_t min_q() const {
-    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? q0 : 0xFFFFFFFFu, a1 ? q1 : 0xFFFFFFFFu));
-    return v == 0xFFFFFFFFu ? ~0ull : (uint64_t)v;
+    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? pk0 : 0xFFFFFFFFu, a1 ? pk1 : 0xFFFFFFFFu));
+    return v == 0xFFFFFFFFu ? ~0ull : (uint64_t)(v >> 6);
   }
   // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
+  // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    const uint32_t Rc = R > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R;  // every q < 2^22
-    uint32_t b = __ballot_sync(0xffffffffu, a0 && q0 <= Rc);
+    const uint32_t Rc = R >= (1ull << 22) ? 0xFFFFFFFFu : ((uint32_t)R << 6) | 63u;
+    uint32_t b = __ballot_sync(0xffffffffu, a0 && pk0 <= Rc);
     const bool hi = b == 0;
-    if (hi) b = __ballot_sync(0xffffffffu, a1 && q1 <= Rc);
+    if (hi) b = __ballot_sync(0xffffffffu, a1 && pk1 <= Rc);
     if (!b) return -1;
     const int src = __ffs(b) - 1;
-    const int kk = (int)__shfl_sync(0xffffffffu, hi ? k1 : k0, src);
-    qk = __shfl_sync(0xffffffffu, hi ? q1 : q0, src);
+    const uint32_t w = __shfl_sync(0xffffffffu, hi ? pk1 : pk0, src);
+    ek = __shfl_sync(0xffffffffu, hi ? es1 : es0, src);
+    qk = w >> 6;
     if (lane == src) {
       if (hi) a1 = false; else a0 = false;
     }
-    return kk;
+    return (int)(w & 63u);
   }
-  __device__ __forceinline__ uint64_t dur_of(uint32_t kk) const {
-    const uint32_t d0 = __shfl_sync(0xffffffffu, dur0, kk & 31u), d1 = __shfl_sync(0xffffffffu, dur1, kk & 31u);
-    return kk < 32 ? d0 : d1;
-  }
+  __device__ __forceinline__ uint64_t dur_of(uint32_t) const { return ek; }  // (of the last pick)
   // the schedule of request kk (gap, start), kept by its owning lane for the digest at the end
   int32_t fg0, fg1;
   uint64_t st0, st1;
@@ -401,11 +404,12 @@ struct RegPool {
       }
     }
   }
-  // requests dequeued by fills, by index (k0 / k1 = 0xFF: an ineligible position)
+  // requests dequeued by fills, by index (pk = 0xFFFFFFFF: an ineligible position)
   __device__ __forceinline__ uint64_t picked_mask() const {
     uint32_t lo = 0, hi = 0;
-    if (k0 < 64 && !a0) (k0 < 32 ? lo : hi) |= 1u << (k0 & 31u);
-    if (k1 < 64 && !a1) (k1 < 32 ? lo : hi) |= 1u << (k1 & 31u);
+    const uint32_t k0 = pk0 & 63u, k1 = pk1 & 63u;
+    if (pk0 != 0xFFFFFFFFu && !a0) (k0 < 32 ? lo : hi) |= 1u << (k0 & 31u);
+    if (pk1 != 0xFFFFFFFFu && !a1) (k1 < 32 ? lo : hi) |= 1u << (k1 & 31u);
     lo = __reduce_or_sync(0xffffffffu, lo);
     hi = __reduce_or_sync(0xffffffffu, hi);
     return ((uint64_t)hi << 32) | lo;
@@ -475,10 +479,15 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
   reg_bitonic64_u32(f0, f1, lane);
   P.a0 = f0 != 0xFFFFFFFFu;
   P.a1 = f1 != 0xFFFFFFFFu;
-  P.q0 = kQ22 - ((f0 >> 6) & kQ22);
-  P.q1 = kQ22 - ((f1 >> 6) & kQ22);
-  P.k0 = P.a0 ? (f0 & 63u) : 0xFFu;
-  P.k1 = P.a1 ? (f1 & 63u) : 0xFFu;
+  P.pk0 = P.a0 ? ((kQ22 - ((f0 >> 6) & kQ22)) << 6) | (f0 & 63u) : 0xFFFFFFFFu;
+  P.pk1 = P.a1 ? ((kQ22 - ((f1 >> 6) & kQ22)) << 6) | (f1 & 63u) : 0xFFFFFFFFu;
+  {  // durations to the sorted positions (request k is held by lane k % 32)
+    const uint32_t k0 = f0 & 31u, k1 = f1 & 31u;
+    const uint32_t x0 = __shfl_sync(0xffffffffu, P.dur0, k0), y0 = __shfl_sync(0xffffffffu, P.dur1, k0);
+    const uint32_t x1 = __shfl_sync(0xffffffffu, P.dur0, k1), y1 = __shfl_sync(0xffffffffu, P.dur1, k1);
+    P.es0 = (f0 & 32u) ? y0 : x0;
+    P.es1 = (f1 & 32u) ? y1 : x1;
+  }
   P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
   return 0;
 }
@@ -892,6 +901,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
   uint32_t nxt = 0;  // lane 0: the next claimed scenario (in flight while one runs)
   if (lane == 0) nxt = atomicAdd(ctr, 1u);
   for (uint32_t cur = __shfl_sync(0xffffffffu, nxt, 0); cur < S; cur = __shfl_sync(0xffffffffu, nxt, 0)) {
+    __syncwarp();  // the previous scenario's reads of the warp's staging arrays come before these writes
     const fikit_scenario_t c = sc[cur];
     if (lane == 0) nxt = atomicAdd(ctr, 1u);
     const uint32_t m = c.lp_len;

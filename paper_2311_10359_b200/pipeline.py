@@ -29,6 +29,7 @@ class Pipeline:
         by a second one with threshold 2^64 - 1 (no gap is filled: B runs after A, the exclusive-mode
         analogue of P:103 / P:478) into exclusive_results()."""
         torch = _torch()
+        self.measured = False  # (set by run_measure: the workspace then holds the string hashes)
         self.checked = checked
         self.predictor = predictor
         self.device = device
@@ -89,6 +90,7 @@ class Pipeline:
 
     # -- a1..a6: identify + measure + finalize --------------------------------------------
     def run_measure(self, stream=None):
+        self.measured = True
         measure(self.recs, self.n, self.names, self.sigs, self.table, self.ws, halo=self.halo, out_row=self.out_row,
                 stream=stream)
         self._chk("measure", stream)
@@ -96,21 +98,27 @@ class Pipeline:
                        stream=stream)
 
     # -- a8..a10: resolve the replay's launches, then the batch replay ------------------------
-    def run_replay(self, stream=None, table: Table | None = None):
-        """table: the profile to replay against (default: this pipeline's; the merged one for P > 1)."""
+    def run_replay(self, stream=None, table: Table | None = None, sim_events=None):
+        """table: the profile to replay against (default: this pipeline's; the merged one for P > 1).
+        sim_events: (start, stop) torch.cuda.Event pair recorded around the replay call(s) alone."""
         r = self.replay
         tab = self.table if table is None else table
         if self.predictor is not None:
             table_predict(tab, *self.predictor, stream=stream)
+        # (the measure call on this workspace hashed these string tables: no re-hashing)
         resolve(r["hp_recs"], r["nh"], self.names, self.sigs, tab, r["hp_row"], r["hp_dur"], r["hp_gap"],
-                self.ws, stream=stream)
+                self.ws, stream=stream, reuse_hashes=self.measured)
         self._chk("resolve(hp)", stream)
         resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
-                self.ws, stream=stream)
+                self.ws, stream=stream, reuse_hashes=True)
         self._chk("resolve(lp)", stream)
+        if sim_events is not None:
+            sim_events[0].record(stream)
         self._simulate(tab, r["out"], r["threshold_ns"], True, stream)
         if "out_excl" in r:
             self._simulate(tab, r["out_excl"], NO_FILL, False, stream)
+        if sim_events is not None:
+            sim_events[1].record(stream)
 
     def _simulate(self, tab, out, threshold_ns, with_schedule, stream):
         r = self.replay

@@ -16,16 +16,17 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+col = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"  # or "Instructions Executed"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", kern, "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "Address" and len(r) > 3][0]
 h = rows[hi]
-si = h.index("Warp Stall Sampling (All Samples)")
+si = h.index(col)
 samples = []
 for r in rows[hi + 1:]:
     try:
-        samples.append((int(r[0], 16), int(r[si]), r[1].strip()))
+        samples.append((int(r[0], 16), int(float(r[si].replace(",", ""))), r[1].strip()))
     except (ValueError, IndexError):
         pass
 # one entry per instruction (the page can repeat rows per function instance)

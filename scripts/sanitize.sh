@@ -11,10 +11,9 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 |
 SEL='toy_end_to_end or (measure_random and not 300000 and not 70000) or identify_random or invalid_record or capacity_and_empty or test_halo or test_random_replay or fill_batch or predict_parity or empty_inputs or lookup_parity or merge_one_gpu or stream_singletons or stream_limits or over_limit or sorted_pool_beyond or zero_durations'
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
-  [ "$tool" = "racecheck" ] && extra="--racecheck-report all"
-  [ "$tool" = "initcheck" ] && extra="--track-unused-memory no"
+  [ "$tool" = "racecheck" ] && extra="--racecheck-report analysis"
   start=$(date +%s)
-  timeout ${SAN_TIMEOUT:-1500} compute-sanitizer --tool $tool $extra --target-processes all --print-limit 50 \
+  timeout ${SAN_TIMEOUT:-1500} compute-sanitizer --tool $tool $extra --target-processes all --print-limit 200 \
     --log-file gpurun_out/sanitize_$tool.log \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -m gpu -q -x -p no:cacheprovider -k "$SEL" \
     > gpurun_out/sanitize_${tool}_pytest.log 2>&1

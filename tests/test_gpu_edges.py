@@ -253,3 +253,36 @@ def test_replay_huge_gaps_many_requests(fk, orc):
         assert got.tobytes() == ref.tobytes()
         assert np.array_equal(fg.cpu().numpy(), rfg) and np.array_equal(ls.cpu().numpy().view(np.uint64), rls)
         assert int(ref["n_fills"].max()) > 64
+
+
+@pytest.mark.parametrize("n_ids,reuse", [(1000, True), (1000, False), (12000, True)])
+def test_resolve_parity_table_sizes(fk, orc, n_ids, reuse):
+    """fikit_resolve(_ex) against the oracle's or_resolve (Alg. 1 lines 3-5): tables with
+    K <= 8192 rows (keys staged in shared memory) and K > 8192 (global binary search), with the
+    string hashes reused from the measure call (FIKIT_RESOLVE_REUSE_HASHES) or recomputed."""
+    import torch
+
+    from paper_2311_10359_b200.pipeline import Pipeline
+
+    tr = F.random_trace(40 + n_ids, 60000, n_tasks=5, n_ids=n_ids, run_len_max=30, overlap_frac=0.05)
+    ref, st, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=1 << 16)
+    assert st["code"] == 0
+    p = Pipeline(tr.records, tr.names, tr.sigs, capacity=1 << 16)
+    p.run_measure()
+    rng = np.random.default_rng(n_ids)
+    recs = tr.records[np.sort(rng.choice(tr.records.shape[0], 20000, replace=False))].copy()
+    recs["grid_x"][rng.random(20000) < 0.1] += 7  # ~10 % identities without a profile
+    d = fk.records_to_device(recs)
+    n = recs.shape[0]
+    row = torch.empty(n, dtype=torch.int32, device="cuda")
+    dur = torch.empty(n, dtype=torch.int64, device="cuda")
+    gap = torch.empty(n, dtype=torch.int64, device="cuda")
+    fk.resolve(d, n, p.names, p.sigs, p.table, row, dur, gap, p.ws, reuse_hashes=reuse)
+    st = fk.check(p.ws, "resolve")
+    r_row, r_dur, r_gap, r_st = orc.resolve(recs, tr.names, tr.sigs, ref)
+    assert (ref.n_rows > 8192) == (n_ids > 8192)
+    assert np.array_equal(row.cpu().numpy().view(np.uint32), r_row)
+    assert np.array_equal(dur.cpu().numpy().view(np.uint64), r_dur)
+    assert np.array_equal(gap.cpu().numpy().view(np.uint64), r_gap)
+    assert st["n_overlap_gaps"] == r_st["n_overlap_gaps"]
+    assert 0.5 < (r_row != 0xFFFFFFFF).mean() < 0.99  # most fresh launches have a profile
