@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fikit", choices=["fikit", "reference"])
     ap.add_argument("--workload", default="zipf",
-                    choices=["zipf", "z64k", "resnet", "bert_vgg", "sweep", "stream", "preempt", "ratio"])
+                    choices=["zipf", "z64k", "resnet", "bert_vgg", "sweep", "stream", "preempt", "ratio", "identify"])
     ap.add_argument("--records", type=int, default=None, help="override the Zipf trace length (runs x 256)")
     ap.add_argument("--scenarios", type=int, default=100_000)
     ap.add_argument("--predictor", default=None,
@@ -455,11 +455,64 @@ def configs2_leg(fk, Pipeline, stream, args, steps=20, warmup=3):
             "l2": "inputs fit the L2: a 256 MB write flushes it before every step (outside the step's events)"}
 
 
+def run_identify(args):
+    """--workload identify: fikit_identify alone over the 100M-launch Zipf trace (configs[3]),
+    SURVEY §8d "identify-only: 56 B/record" (48 B read + an 8-B kernel ID written per launch).
+    1 GPU; the roofline is the whole call (string hashing + k_identify) against the copy peak."""
+    import torch
+
+    import fikit_synth as F
+    from paper_2311_10359_b200 import _build
+
+    _build.build()
+    import paper_2311_10359_b200 as fk
+
+    runs = 390_625 if args.records is None else max(1, args.records // 256)
+    cfg = F.zipf_trace(n_runs=runs, threads=min(16, os.cpu_count() or 8))
+    tr = cfg.trace
+    N = tr.records.shape[0]
+    recs = fk.records_to_device(tr.records)
+    names, sigs = fk.strtab_to_device(tr.names), fk.strtab_to_device(tr.sigs)
+    out = torch.empty(N, dtype=torch.int64, device="cuda")
+    ws = fk.Workspace(1, names.count, sigs.count)
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        fk.identify(recs, N, names, sigs, out, ws)
+        if i == 0:
+            fk.check(ws, "identify warm-up")
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = fk.launch_count()
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            fk.identify(recs, N, names, sigs, out, ws)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    peak, peak_src = peaks()
+    ach = 56 * N / (ms * 1e-3) / 1e9
+    line = {"metric": "launch-records/s (identify only)", "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (fikit_synth, seeded)",
+            "config": {"workload": f"identify over zipf-{N / 1e6:g}M (configs[3] trace)", "records": N,
+                       "l2": "inputs (4.8 GB) larger than the L2: steps back to back, no flush"},
+            "roofline": {"bound": "hbm", "kernel": "fikit_identify (k_strtab_hash + k_identify)", "achieved": ach,
+                         "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": 56, "traffic": None},
+            "gpu_launches": int(fk.launch_count() - launches0), "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "identify":
+        return run_identify(args)
     import torch
     import torch.distributed as dist
 

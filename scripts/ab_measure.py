@@ -11,7 +11,7 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-AB = os.path.join(ROOT, "abtest")
+AB = os.path.join(ROOT, "ab_out")  # (git-ignored, but shipped to the GPU box by gpurun)
 sys.path.insert(0, ROOT)
 
 
@@ -55,6 +55,7 @@ def run(records, workload="zipf"):
     recs = fk.records_to_device(tr.records)
     names, sigs = fk.strtab_to_device(tr.names), fk.strtab_to_device(tr.sigs)
     out = {}
+    variants = []
     for name in sorted(os.listdir(AB)):
         path = os.path.join(AB, name, "libfikit.so")
         if not os.path.exists(path):
@@ -65,8 +66,9 @@ def run(records, workload="zipf"):
         L.fikit_table_bytes.restype = C.c_size_t
         L.fikit_table_bytes.argtypes = [C.c_uint32]
         L.fikit_table_carve.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(fk.TableC)]
-        L.fikit_measure.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, fk.StrTabC, fk.StrTabC, C.POINTER(fk.TableC),
-                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.fikit_measure_timed.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, fk.StrTabC, fk.StrTabC,
+                                          C.POINTER(fk.TableC), C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
         L.fikit_get_status.argtypes = [C.c_void_p, C.POINTER(fk.StatusC), C.c_void_p]
         cap = 8192
         wsb = L.fikit_ws_bytes(cap, names.count, sigs.count, n)
@@ -75,28 +77,42 @@ def run(records, workload="zipf"):
         tb = torch.zeros(L.fikit_table_bytes(cap) + 256, dtype=torch.uint8, device="cuda")
         t = fk.TableC()
         L.fikit_table_carve(C.c_void_p(tb.data_ptr() + (-tb.data_ptr()) % 256), cap, C.byref(t))
-        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-        call = lambda: L.fikit_measure(C.c_void_p(recs.data_ptr()), n, None, names.c(), sigs.c(), C.byref(t), None,
-                                       C.c_void_p(wsp), wsb, stream)
+        variants.append((name, L, ws, wsp, wsb, tb, t))
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record()
+    k1.record()
+
+    def call(v, ev=(None, None)):
+        name, L, ws, wsp, wsb, tb, t = v
+        return L.fikit_measure_timed(C.c_void_p(recs.data_ptr()), n, None, names.c(), sigs.c(), C.byref(t), None,
+                                     C.c_void_p(wsp), wsb, stream, ev[0], ev[1])
+
+    for v in variants:
         for _ in range(3):
-            call()
+            call(v)
         torch.cuda.synchronize()
-        if os.environ.get("AB_ONCE"):  # for an ncu launch list: 3 calls only
-            continue
         st = fk.StatusC()
-        L.fikit_get_status(C.c_void_p(wsp), C.byref(st), stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        times = []
-        for rep in range(5):
+        v[1].fikit_get_status(C.c_void_p(v[3]), C.byref(st), stream)
+        out[v[0]] = {"ms": [], "kernel_ms": [], "status": st.code, "rows": st.n_rows_needed}
+    if os.environ.get("AB_ONCE"):  # for an ncu launch list: 3 calls each only
+        return out
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(7):  # variants interleaved: clock / thermal drift hits all alike
+        for v in variants:
             e0.record()
+            kt = 0.0
             for _ in range(10):
-                call()
+                call(v, (C.c_void_p(k0.cuda_event), C.c_void_p(k1.cuda_event)))
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / 10)
-        ms = min(times)
-        out[name] = {"ms": ms, "GBps": 48 * n / ms / 1e6, "status": st.code, "rows": st.n_rows_needed}
-        print(name, json.dumps(out[name]), flush=True)
+            out[v[0]]["ms"].append(e0.elapsed_time(e1) / 10)
+            out[v[0]]["kernel_ms"].append(k0.elapsed_time(k1))  # (the last call's k_measure)
+    for name, r in out.items():
+        r["ms"], r["kernel_ms"] = min(r["ms"]), float(np.median(r["kernel_ms"]))
+        r["GBps_call"] = 48 * n / r["ms"] / 1e6
+        r["GBps_kernel"] = 48 * n / r["kernel_ms"] / 1e6
+        print(name, json.dumps(r), flush=True)
     return out
 
 
