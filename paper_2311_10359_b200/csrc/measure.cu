@@ -777,8 +777,8 @@ struct Smem {
   // slot -> identity in 5 words: name | sig << 16, grid_x, grid_y | grid_z << 16,
   // block_x | block_y << 16, block_z | task << 16 (one 16-B + one 4-B load verify).  Only
   // identities with name, sig, task < 2^16 are kept hot; the others always take the cold path.
-  uint4 tq[kHotMax];
-  uint32_t tq4[kHotMax];
+  uint4 tq[kHotMax + 1];  // (+1: the spare slot speculative verification reads without a tag match)
+  uint32_t tq4[kHotMax + 1];
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][2 * kBins + 1];  // 64 u32 bins (32 duration, 32 gap) (+1 pad)
   uint32_t st[kHotMax][5];        // duration: 0 sum mod 2^32, 1 carries out of it; gap: 2, 3 (v < 2^32); 4: pad
@@ -1309,10 +1309,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         const uint4 tA = mk::ld_bucket(S, A.hk & (mk::TAG_Q - 1)), tB = mk::ld_bucket(S, B.hk & (mk::TAG_Q - 1));
         uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
         const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
-        const uint32_t eA = cA ? cA - 1 : 0u, eB = cB ? cB - 1 : 0u;
-        // (verify only a matched slot: a speculative read of slot 0 would race with its admission)
-        const bool vA = cA != 0u && verify(eA, A);
-        const bool vB = cB != 0u && verify(eB, B);
+        // speculative verification (both loads in flight before the tag compare resolves): without
+        // a matching tag the read goes to the spare slot kHotMax, which is never admitted (no race
+        // with an admission writing a real slot)
+        const uint32_t eA = cA ? cA - 1 : kHotMax, eB = cB ? cB - 1 : kHotMax;
+        const bool vA = verify(eA, A) & (cA != 0u);
+        const bool vB = verify(eB, B) & (cB != 0u);
         int sA = -1, sB = -1;
         if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
         if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);
