@@ -163,11 +163,19 @@ __device__ void warp_bitonic_sort(uint64_t* K, uint32_t P, int lane) {
 
 // Build the sorted pool in place of q (q[k] by index -> K[p] by sorted position).
 // Returns false (pool left by index) if the fast path does not apply.
+// epack: every eligible request's duration e < 2^22 ns, so the sorted entry carries it too
+// (q << 32 | e << 10 | index): a pick reads q, e and the index in one shared load instead of
+// waiting on a global load of e.
 __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* meta, uint32_t m, int lane,
-                                                 uint32_t& A, uint32_t& nch, uint32_t& CM) {
-  bool ok = true;
+                                                 uint32_t& A, uint32_t& nch, uint32_t& CM,
+                                                 const uint64_t* __restrict__ dur, bool& epack) {
+  bool ok = true, small = true;
   for (uint32_t k = lane; k < m; k += 32)
-    if ((meta[k] & kElig) && q[k] >= 0xFFFFFFFFull) ok = false;  // fast path: every q < 2^32 - 1
+    if (meta[k] & kElig) {
+      if (q[k] >= 0xFFFFFFFFull) ok = false;  // fast path: every q < 2^32 - 1
+      if (__ldg(dur + k) >= (1ull << 22)) small = false;
+    }
+  epack = __all_sync(0xffffffffu, small);
   if (!__all_sync(0xffffffffu, ok) || m > 1024u) return false;
   uint32_t P = 32;
   while (P < m) P <<= 1;
@@ -182,7 +190,8 @@ __device__ __forceinline__ bool make_sorted_pool(uint64_t* q, const uint8_t* met
   // word, one 32-bit load), dead / ineligible entries stay ~0
   for (uint32_t p = lane; p < P; p += 32) {
     const uint64_t key = q[p];
-    if (key != ~0ull) q[p] = (key_q(key) << 32) | (key & 1023u);
+    if (key != ~0ull)
+      q[p] = (key_q(key) << 32) | (epack ? (__ldg(dur + (key & 1023u)) << 10) : 0ull) | (key & 1023u);
   }
   __syncwarp();
   const uint32_t* qh = reinterpret_cast<const uint32_t*>(q) + 1;  // qh[2 p] = q at position p
@@ -239,17 +248,19 @@ __device__ __forceinline__ uint64_t sorted_min_q(uint32_t CM, uint32_t nch, int 
 // dequeue bookkeeping below overlaps its latency)
 __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
                                          uint32_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk,
-                                         const uint64_t* __restrict__ dur, uint64_t& ek) {
+                                         const uint64_t* __restrict__ dur, uint64_t& ek, bool epack = false) {
   int k;
   if (fast) {
     const int p = sorted_best(q, A, CM, nch, R, lane);
     if (p < 0) return -1;
-    const uint64_t x = q[p];  // q << 32 | index
+    const uint64_t x = q[p];  // q << 32 | [e << 10 |] index
     k = (int)(x & 1023u);
-    ek = __ldg(dur + k);
+    ek = epack ? ((x >> 10) & 0x3FFFFFull) : __ldg(dur + k);
     qk = x >> 32;
     if (lane == (p >> 5)) A &= ~(1u << (p & 31));
-    chunk_min_refresh(q, A, (uint32_t)p >> 5, CM, lane);
+    // the chunk's alive minimum changes only if the pick was it (a pick is the largest fitting q
+    // of its level: usually not the minimum)
+    if (__shfl_sync(0xffffffffu, CM, (uint32_t)p >> 5) == (uint32_t)qk) chunk_min_refresh(q, A, (uint32_t)p >> 5, CM, lane);
   } else {
     k = warp_best_prio_fit(q, meta, m, R, lane);
     if (k < 0) return -1;
@@ -309,13 +320,14 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     if (R >= prm.threshold_ns) {  // Alg. 1 lines 6-8
       uint32_t A = 0, nch = 0;
       uint32_t CM;
-      const bool fast = make_sorted_pool(q, meta, m, lane, A, nch, CM);
+      bool epack = false;
+      const bool fast = make_sorted_pool(q, meta, m, lane, A, nch, CM, pool_dur + off, epack);
       uint64_t qmin = pool_min_q(fast, q, meta, m, CM, nch, lane);
       for (;;) {                             // lines 9-16
         if (prm.feedback && t >= dl) break;  // early stop on the HP launch
         if (R < qmin) break;                 // nothing can fit
         uint64_t qk, ek;
-        const int k = pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, pool_dur + off, ek);  // Alg. 2
+        const int k = pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, pool_dur + off, ek, epack);  // Alg. 2
         if (k < 0) break;
         if (lane == 0) picks[po + np] = (uint32_t)k;
         np++;
@@ -503,8 +515,9 @@ struct SmemPool {
   uint32_t CM;  // lane c: chunk c's alive minimum q (sorted fast path; q < 2^32 there)
   __device__ __forceinline__ uint64_t min_q(int lane) const { return pool_min_q(fast, q, meta, m, CM, nch, lane); }
   uint64_t ek;  // the last pick's duration (loaded by pool_pick)
+  bool epack;   // durations packed into the sorted entries (make_sorted_pool)
   __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, dur, ek);
+    return pool_pick(fast, q, meta, m, A, CM, nch, R, lane, qk, dur, ek, epack);
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t) const { return ek; }  // (of the last pick)
   __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch& dig) {
@@ -839,8 +852,8 @@ __global__ void __launch_bounds__(kReplayWarps * 32)
     uint8_t* meta = s_meta[w];
     if (!load_pool(tab, K, lp_row, lp_level, c.lp_off, m, q, meta, lane, st)) continue;
     const uint64_t so = sched ? sched_off[s] : 0;
-    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, 0xFFFFFFFFu, 0};
-    P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch, P.CM);
+    SmemPool P{q, meta, lp_dur + c.lp_off, m, 0, 0, false, 0xFFFFFFFFu, 0, false};
+    P.fast = make_sorted_pool(q, meta, m, lane, P.A, P.nch, P.CM, lp_dur + c.lp_off, P.epack);
     DigestBatch db;
     const HpOut o = replay_hp(P, [&]() { return P.min_q(lane); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched,
                               fill_gap, lp_start, so, db, lane);
