@@ -66,6 +66,8 @@ def parse():
                          "key all-gathers + union + remap + all-reduces every step")
     ap.add_argument("--dict", action="store_true",
                     help="N=1: measure against the dictionary of the first warm-up step (fikit_measure_dict)")
+    ap.add_argument("--no-plan-reuse", action="store_true",
+                    help="dictionary mode: rebuild the hot sets every step (no FIKIT_MEASURE_REUSE_PLAN)")
     ap.add_argument("--verify-merge", action="store_true",
                     help="N>1: rank 0 re-measures the whole trace on one GPU and checks the merged table bit-exactly")
     return ap.parse_args()
@@ -566,13 +568,17 @@ def main():
     # two all-reduces alone
     use_dict = (world > 1 and args.merge == "dict") or (world == 1 and args.dict)
     dict_state = None
+    plan_ready = [False]  # the workspace holds a dictionary call's plan (FIKIT_MEASURE_REUSE_PLAN)
 
     def step(timed, kpair=None, checked=False, spair=None):
         # checked (first warm-up step): the workspace status after EVERY call (each validating
         # call resets it, so one check at the end would only see the last call)
         if timed:
             ev[0].record(stream)
-        fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair, dictionary=dict_state)
+        fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair, dictionary=dict_state,
+                   reuse_plan=dict_state is not None and plan_ready[0])
+        if dict_state is not None:
+            plan_ready[0] = not args.no_plan_reuse  # (the next dictionary step reuses this one's plan)
         p.measured = True  # (the workspace holds the string hashes: resolve reuses them)
         st = fk.check(p.ws, "bench warm-up: measure") if checked else None
         if timed:
@@ -684,9 +690,11 @@ def main():
                        "records": N, "records_per_gpu": n_local, "scenarios": S_total,
                        "table_rows": (dense if dense is not None else p.table).n_rows(),
                        "merge": ("dictionary (fikit_measure_dict against the first warm-up step's merged keys; "
-                                 "merge = 2 all-reduces)" if dict_state is not None else
+                                 "merge = 2 all-reduces" + ("; plan reused" if plan_ready[0] else "") + ")"
+                                 if dict_state is not None else
                                  "union (key all-gathers + union + remap + 2 all-reduces)") if world > 1 else
-                                ("dictionary (fikit_measure_dict against the first warm-up step's keys)"
+                                ("dictionary (fikit_measure_dict against the first warm-up step's keys"
+                                 + ("; plan reused" if plan_ready[0] else "") + ")"
                                  if dict_state is not None else "none (1 GPU)"),
                        "l2": l2_note,
                        "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},

@@ -191,6 +191,20 @@ int fikit_measure(const fikit_record_t* recs, uint64_t n, const fikit_record_t* 
 int fikit_measure_dict(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next, fikit_strtab_t names,
                        fikit_strtab_t sigs, const uint64_t* dict_kid, const uint32_t* dict_task, uint32_t dict_n,
                        const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes, void* stream);
+/* fikit_measure_dict with flags and (nullable) fikit_measure_timed events.
+ * FIKIT_MEASURE_REUSE_PLAN: keep the string hashes and the hot sets (the most-sampled launch
+ * identities per task bucket, with their dictionary rows) of the previous fikit_measure_dict
+ * call on this workspace -- repeated services keep their kernels, so a step skips the
+ * launch sample, the hot-set choice and the string hashing; only the tile schedule is rebuilt
+ * from the new records.  Requires: that previous call used the same dictionary (checked: a
+ * different dictionary sets FIKIT_E_ARG in the status), the same string tables (same device
+ * bytes, unchanged) and a table of the same capacity.  The statistics are exact either way; a
+ * stale plan only makes more launches take the cold path. */
+#define FIKIT_MEASURE_REUSE_PLAN 1u
+int fikit_measure_dict_ex(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next,
+                          fikit_strtab_t names, fikit_strtab_t sigs, const uint64_t* dict_kid,
+                          const uint32_t* dict_task, uint32_t dict_n, uint32_t flags, const fikit_table_t* tab,
+                          uint32_t* out_row, void* ws, size_t ws_bytes, void* stream, void* ev_start, void* ev_stop);
 /* fikit_measure_dict with fikit_measure_timed's events around the streaming kernel. */
 int fikit_measure_dict_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next,
                              fikit_strtab_t names, fikit_strtab_t sigs, const uint64_t* dict_kid,

@@ -23,7 +23,7 @@ OK, E_ARG, E_RECORD, E_CAPACITY, E_CUDA, E_NAME, E_DICT = 0, -1, -2, -3, -4, -5,
 NO_ROW = 0xFFFFFFFF
 NBINS = 32
 SYMBOLS = ("fikit_ws_bytes", "fikit_table_bytes", "fikit_table_carve", "fikit_identify", "fikit_measure",
-           "fikit_measure_timed", "fikit_measure_dict", "fikit_measure_dict_timed", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_resolve_ex", "fikit_lookup", "fikit_fill",
+           "fikit_measure_timed", "fikit_measure_dict", "fikit_measure_dict_timed", "fikit_measure_dict_ex", "fikit_table_finalize", "fikit_table_means", "fikit_table_predict", "fikit_resolve", "fikit_resolve_ex", "fikit_lookup", "fikit_fill",
            "fikit_simulate_batch", "fikit_simulate_stream_batch",
            "fikit_dict_union", "fikit_table_remap", "fikit_table_bias", "fikit_get_status", "fikit_strerror",
            "fikit_launch_count")
@@ -79,6 +79,8 @@ def lib():
         L.fikit_measure_dict.argtypes = [p, u64, p, StrTabC, StrTabC, p, p, u32, C.POINTER(TableC), p, p, sz, p]
         L.fikit_measure_dict_timed.argtypes = [p, u64, p, StrTabC, StrTabC, p, p, u32, C.POINTER(TableC), p, p, sz,
                                                p, p, p]
+        L.fikit_measure_dict_ex.argtypes = [p, u64, p, StrTabC, StrTabC, p, p, u32, u32, C.POINTER(TableC), p, p, sz,
+                                            p, p, p]
         L.fikit_table_finalize.argtypes = [C.POINTER(TableC), p, u64, p, sz, p]
         L.fikit_table_means.argtypes = [C.POINTER(TableC), p]
         L.fikit_table_predict.argtypes = [C.POINTER(TableC), u32, u32, p]
@@ -265,22 +267,18 @@ def identify(recs, n: int, names: DevStrTab, sigs: DevStrTab, out_kid, ws: Works
 
 
 def measure(recs, n: int, names: DevStrTab, sigs: DevStrTab, table: Table, ws: Workspace, halo=None, out_row=None,
-            stream=None, events=None, dictionary=None):
+            stream=None, events=None, dictionary=None, reuse_plan: bool = False):
     """events: (start, stop) torch.cuda.Event pair recorded around the fused streaming kernel
     (fikit_measure_timed; the events must exist, i.e. have been recorded once).  dictionary:
-    (kid int64 device tensor, task int32 device tensor, n) -> fikit_measure_dict(_timed)."""
+    (kid int64 device tensor, task int32 device tensor, n) -> fikit_measure_dict_ex; reuse_plan:
+    FIKIT_MEASURE_REUSE_PLAN (keep the previous dictionary call's string hashes and hot sets)."""
     if dictionary is not None:
-        dk, dt, dn = dictionary
-        if events is None:
-            _chk(lib().fikit_measure_dict(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), _ptr(dk), _ptr(dt), int(dn),
-                                          C.byref(table.c), _ptr(out_row), ws.ptr(), ws.nbytes, _stream(stream)),
-                 "measure_dict")
-        else:
-            e0, e1 = events
-            _chk(lib().fikit_measure_dict_timed(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), _ptr(dk), _ptr(dt),
-                                                int(dn), C.byref(table.c), _ptr(out_row), ws.ptr(), ws.nbytes,
-                                                _stream(stream), C.c_void_p(e0.cuda_event),
-                                                C.c_void_p(e1.cuda_event)), "measure_dict_timed")
+        dk, dt, dn = dictionary[:3]
+        flags = 1 if reuse_plan else 0  # FIKIT_MEASURE_REUSE_PLAN
+        e0, e1 = (C.c_void_p(events[0].cuda_event), C.c_void_p(events[1].cuda_event)) if events else (None, None)
+        _chk(lib().fikit_measure_dict_ex(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), _ptr(dk), _ptr(dt), int(dn),
+                                         flags, C.byref(table.c), _ptr(out_row), ws.ptr(), ws.nbytes, _stream(stream),
+                                         e0, e1), "measure_dict")
         return
     if events is None:
         _chk(lib().fikit_measure(_ptr(recs), n, _ptr(halo), names.c(), sigs.c(), C.byref(table.c), _ptr(out_row),

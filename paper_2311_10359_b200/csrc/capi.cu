@@ -26,7 +26,7 @@ __global__ void k_fin_sort(const fikit_status_t*, const RawRow*, uint32_t, fikit
 __global__ void k_fin_scatter(const fikit_status_t*, const RawRow*, uint32_t, uint32_t, const FinKey*, fikit_table_t,
                               uint32_t*, const uint32_t*);
 __global__ void k_dict_load(const uint64_t*, const uint32_t*, uint32_t, IndexEntry*, uint32_t, RawRow*,
-                            fikit_status_t*, uint32_t*);
+                            fikit_status_t*, uint32_t*, uint32_t);
 __global__ void k_remap_rows(uint32_t*, uint64_t, const uint32_t*, const uint32_t*);
 __global__ void k_means(fikit_table_t);
 __global__ void k_predict(fikit_table_t, uint32_t, uint32_t);
@@ -247,12 +247,14 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
                         fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws,
                         size_t ws_bytes, void* stream, cudaEvent_t ev0, cudaEvent_t ev1,
                         const uint64_t* dict_kid = nullptr, const uint32_t* dict_task = nullptr,
-                        uint32_t dict_n = 0) {
+                        uint32_t dict_n = 0, uint32_t flags = 0) {
   cudaStream_t s = (cudaStream_t)stream;
   Ws w;
   const bool dict = dict_kid != nullptr;
+  const bool reuse = (flags & FIKIT_MEASURE_REUSE_PLAN) != 0;
   if (n >= (1ull << 32) || (n && (!recs || !aligned(recs, 16))) || !strtab_ok(names) || !strtab_ok(sigs) ||
-      !table_ok(tab) || (dict && (!dict_task || dict_n == 0 || dict_n > tab->capacity)))
+      !table_ok(tab) || (dict && (!dict_task || dict_n == 0 || dict_n > tab->capacity)) ||
+      (flags & ~FIKIT_MEASURE_REUSE_PLAN) || (reuse && !dict))
     return FIKIT_E_ARG;
   if (int r = get_ws(ws, ws_bytes, tab->capacity, names.count, sigs.count, &w, n)) return r;
   const uint32_t cap = tab->capacity;
@@ -265,20 +267,20 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
     z.n[z.k++] = bytes;
   };
   add(w.raw(), sizeof(RawRow) * (size_t)cap);
-  add(w.index(), sizeof(IndexEntry) * (size_t)w.L.slots);
+  if (!reuse) add(w.index(), sizeof(IndexEntry) * (size_t)w.L.slots);  // (dictionary rows only: reusable)
   add(w.tindex(), sizeof(Tuple) * (size_t)w.L.tslots);
-  add(w.samp(), sizeof(SampEntry) * (size_t)kSampSlots);
-  add(w.misc(), 256);  // (dictionary word: none unless k_dict_load sets it)
-  add(w.hot_n(), 4ull * kHotHdr);
+  if (!reuse) add(w.samp(), sizeof(SampEntry) * (size_t)kSampSlots);  // (a reused plan keeps its
+  add(w.misc(), 256);  // (dictionary word: none unless k_dict_load sets it)   hot sets and header)
+  if (!reuse) add(w.hot_n(), 4ull * kHotHdr);
   add(w.cur(), 16ull * kSchedWords);  // cur, act, bstart, btot
   launch_pdl(k_zero, 2 * num_sms(), 256, 0, s, z, w.st());
   if (int r = launched()) return r;
   if (dict) {  // rows fixed in advance: dictionary key j -> row j
     launch_pdl(k_dict_load, (dict_n + 255) / 256, 256, 0, s, dict_kid, dict_task, dict_n, w.index(), w.L.slots, w.raw(),
-                                                      w.st(), w.misc());
+                                                      w.st(), w.misc(), reuse ? 1u : 0u);
     if (int r = launched()) return r;
   }
-  if (n == 0) return hash_strtabs(w, names, sigs, s);
+  if (n == 0) return reuse ? FIKIT_OK : hash_strtabs(w, names, sigs, s);
   // persistent k_measure: one CTA per SM, fewer if there are not enough 64-launch warp-tiles
   const uint32_t ntiles = (uint32_t)((n + kTileLaunches - 1) / kTileLaunches);
   const uint32_t ngroups = (ntiles + kGroupTiles - 1) / kGroupTiles;
@@ -304,12 +306,13 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pa.grp_bucket = w.grp_bucket();
   pa.blkcnt = w.blkcnt();
   pa.ngroups = ngroups;
-  uint32_t sb = (ngroups + 2047) / 2048;  // group blocks: ~2k groups (512k launches) each
+  uint32_t sb = (ngroups + 511) / 512;  // group blocks: <= 512 groups (128k launches) each, <= 160
   sb = sb < 1 ? 1 : sb > kSortBlocks ? kSortBlocks : sb;
   pa.sb = sb;
   const uint64_t nstr = (uint64_t)names.count + sigs.count;
-  pa.nb_hash = (uint32_t)((nstr + kPrepThreads / 32 - 1) / (kPrepThreads / 32));
-  pa.nb_samp = (uint32_t)((pa.n_samples + 2 * kPrepThreads - 1) / (2 * kPrepThreads));  // <= 2 samples per thread
+  // (a reused plan: the string hashes and the hot sets of the previous call; only the tile groups)
+  pa.nb_hash = reuse ? 0u : (uint32_t)((nstr + kPrepThreads / 32 - 1) / (kPrepThreads / 32));
+  pa.nb_samp = reuse ? 0u : (uint32_t)((pa.n_samples + 2 * kPrepThreads - 1) / (2 * kPrepThreads));  // <= 2 per thread
   launch_pdl(k_prep, pa.nb_hash + pa.nb_samp + pa.sb, kPrepThreads, 0, s, pa);
   if (int r = launched()) return r;
   // 3. k_plan: hot sets + schedule mode | the groups' counting-sort scatter, bucket ranges, first buckets
@@ -325,6 +328,8 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pl.row_tuple = w.row_tuple();
   pl.cap = cap;
   pl.dict = dict ? 1u : 0u;
+  pl.hot_blocks = reuse ? 0u : kBuckets + 1;
+  pl.dict_hash = reinterpret_cast<const unsigned long long*>(w.misc() + kMiscDictHash);
   pl.hot_all = w.hot();
   pl.hot_hdr = w.hot_n();
   pl.grp_bucket = w.grp_bucket();
@@ -336,7 +341,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pl.bstart = w.bstart();
   pl.btot = w.btot();
   pl.first = w.first();
-  launch_pdl(k_plan, kBuckets + 1 + sb, 1024, 0, s, pl);
+  launch_pdl(k_plan, pl.hot_blocks + sb, 1024, 0, s, pl);
   if (int r = launched()) return r;
   // 4. the streaming kernel
   const size_t smem = measure_smem_bytes();
@@ -377,6 +382,15 @@ int fikit_measure_dict(const fikit_record_t* recs, uint64_t n, const fikit_recor
   if (!dict_kid) return FIKIT_E_ARG;
   return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, nullptr, nullptr, dict_kid,
                       dict_task, dict_n);
+}
+
+int fikit_measure_dict_ex(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
+                          fikit_strtab_t sigs, const uint64_t* dict_kid, const uint32_t* dict_task, uint32_t dict_n,
+                          uint32_t flags, const fikit_table_t* tab, uint32_t* out_row, void* ws, size_t ws_bytes,
+                          void* stream, void* ev_start, void* ev_stop) {
+  if (!dict_kid) return FIKIT_E_ARG;
+  return measure_impl(recs, n, halo, names, sigs, tab, out_row, ws, ws_bytes, stream, (cudaEvent_t)ev_start,
+                      (cudaEvent_t)ev_stop, dict_kid, dict_task, dict_n, flags);
 }
 
 int fikit_measure_dict_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo,

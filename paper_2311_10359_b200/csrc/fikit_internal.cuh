@@ -81,6 +81,7 @@ constexpr uint32_t kCovTask = kBuckets + 1;  // samples whose row is in its task
 constexpr uint32_t kCovGlobal = kBuckets + 2;  // samples whose row is in the global hot set
 constexpr uint32_t kCovTotal = kBuckets + 3;  // samples with a row
 constexpr uint32_t kSampN = kBuckets + 4;  // distinct identities in the launch sample
+constexpr uint32_t kPlanStamp = kBuckets + 6;  // (u64, words 70-71) dictionary hash the hot sets were built on
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
 constexpr uint32_t kFinGroup = 256;     // fikit_table_finalize: keys per sorted group (a warp's)
@@ -206,6 +207,8 @@ struct PlanArgs {
   uint32_t* btot;
   uint32_t* first;
   uint32_t dict;  // dictionary mode: rows are never inserted
+  uint32_t hot_blocks;  // kBuckets + 1 (choose the hot sets) or 0 (reused: the plan of the previous call)
+  const unsigned long long* dict_hash;  // this call's dictionary hash (k_dict_load)
 };
 
 // task bucket: xor-fold of the task id's 6-bit digits -- one-to-one for ids < 64 (a node's
@@ -223,7 +226,8 @@ __host__ __device__ __forceinline__ bool use_task_buckets(const uint32_t* hdr) {
 }
 
 // misc counters (u32 words at ws + misc)
-enum MiscWord { kMiscDict = 0 };  // dictionary mode of the last measure call: dict_n + 1, 0 = none
+enum MiscWord { kMiscDict = 0, kMiscDictHash = 2 };  // dictionary mode of the last measure call: dict_n + 1,
+                                                     // 0 = none; words 2-3: the dictionary's hash (u64)
 
 // Programmatic dependent launch (the C-ABI launches the kernels of a call with
 // cudaLaunchAttributeProgrammaticStreamSerialization): a kernel's CTAs may be scheduled while the

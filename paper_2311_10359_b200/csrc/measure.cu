@@ -90,12 +90,21 @@ __global__ void k_zero(ZeroList z, fikit_status_t* st) {
 // k_zero); a key not strictly above its predecessor flags E_ARG.  Thread 0 sets the row counter
 // to dict_n and the workspace's dictionary word (read by finalize).
 __global__ void k_dict_load(const uint64_t* __restrict__ dkid, const uint32_t* __restrict__ dtask, uint32_t K,
-                            IndexEntry* idx, uint32_t slots, RawRow* raw, fikit_status_t* st, uint32_t* misc) {
+                            IndexEntry* idx, uint32_t slots, RawRow* raw, fikit_status_t* st, uint32_t* misc,
+                            uint32_t keep_index) {
   pdl_entry();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j == 0) {
     st->n_rows_needed = K;
     misc[kMiscDict] = K + 1;
+  }
+  {  // the dictionary's hash (XOR of per-key mixes with their positions): a reused plan must match
+     // it.  Warp-reduced first: one 64-bit atomic per warp, not per key.
+    const uint64_t x = j < K ? mix64(dkid[j] ^ (0x9E3779B97F4A7C15ULL * (uint64_t)(dtask[j] + 1)) ^ ((uint64_t)j << 40))
+                             : 0ull;
+    const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)x), hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(x >> 32));
+    if ((threadIdx.x & 31) == 0 && (lo | hi))
+      atomicXor(reinterpret_cast<unsigned long long*>(misc + kMiscDictHash), ((unsigned long long)hi << 32) | lo);
   }
   if (j >= K) return;
   const uint64_t kid = dkid[j];
@@ -107,6 +116,7 @@ __global__ void k_dict_load(const uint64_t* __restrict__ dkid, const uint32_t* _
   }
   raw[j].kid = kid;
   raw[j].task = task;
+  if (keep_index) return;  // (a reused plan: the index already maps this dictionary; the hash checks it)
   uint32_t h = key_hash(kid, task) & (slots - 1);
   for (uint32_t probe = 0; probe < slots; probe++, h = (h + 1) & (slots - 1)) {
     if (atomicCAS(&idx[h].state, 0u, kBusy) == 0u) {
@@ -745,11 +755,19 @@ __global__ void __launch_bounds__(1024) k_plan(PlanArgs a) {
   __shared__ __align__(16) unsigned char sm[(4096 + 32 + 8) * 4 > (2 * 16 + 2 + 32) * kBuckets * 4
                                                 ? (4096 + 32 + 8) * 4
                                                 : (2 * 16 + 2 + 32) * kBuckets * 4];
-  if (blockIdx.x <= kBuckets) {
+  unsigned long long* stamp = reinterpret_cast<unsigned long long*>(a.hot_hdr + kPlanStamp);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.hot_blocks) {  // a new plan: stamp it with this call's dictionary (0: no dictionary)
+      *stamp = a.dict ? *a.dict_hash : 0ull;
+    } else if (*stamp == 0ull || *stamp != *a.dict_hash) {  // reused plan of another dictionary
+      atomicOr(&a.st->flags, kStatusArg);
+    }
+  }
+  if (blockIdx.x < a.hot_blocks) {
     plan_hot(a, blockIdx.x, sm);
   } else {
     FK_TR(if (threadIdx.x == 0) { FK_TQ(0); g_trace_pre[(1024 + blockIdx.x) * 8 + 7] = 11; })
-    plan_scatter(a, blockIdx.x - (kBuckets + 1), sm);
+    plan_scatter(a, blockIdx.x - a.hot_blocks, sm);
     FK_TR(if (threadIdx.x == 0) FK_TQ(4);)
   }
 }

@@ -39,7 +39,8 @@ def oracle_keys(tab):
     return [(int(tab.task_id[r]), int(tab.kernel_id[r])) for r in range(tab.n_rows)]
 
 
-def run_dict(fk, recs, names, sigs, keys, cap, halo=None, want_rows=False):
+def run_dict(fk, recs, names, sigs, keys, cap, halo=None, want_rows=False, ws=None, strtabs=None, reuse=False,
+             dictionary=None):
     import torch
 
     from paper_2311_10359_b200 import (Table, Workspace, measure, records_to_device, strtab_to_device,
@@ -48,11 +49,13 @@ def run_dict(fk, recs, names, sigs, keys, cap, halo=None, want_rows=False):
     n = recs.shape[0]
     d_recs = records_to_device(recs) if n else torch.zeros(48, dtype=torch.uint8, device="cuda")
     t = Table(cap)
-    ws = Workspace(cap, max(1, names.count), max(1, sigs.count), n_records=n)
+    if ws is None:
+        ws = Workspace(cap, max(1, names.count), max(1, sigs.count), n_records=n)
     rows = torch.empty(max(1, n), dtype=torch.int32, device="cuda") if want_rows else None
     h = records_to_device(halo.reshape(1)) if halo is not None else None
-    measure(d_recs, n, strtab_to_device(names), strtab_to_device(sigs), t, ws, halo=h, out_row=rows,
-            dictionary=dict_tensors(keys))
+    dn, ds = strtabs if strtabs is not None else (strtab_to_device(names), strtab_to_device(sigs))
+    measure(d_recs, n, dn, ds, t, ws, halo=h, out_row=rows,
+            dictionary=dictionary if dictionary is not None else dict_tensors(keys), reuse_plan=reuse)
     st = fk.get_status(ws)
     table_finalize(t, ws, out_row=rows, n=n)
     return t, st, rows
@@ -152,3 +155,36 @@ def test_dict_merge_one_gpu(fk, orc, P):
     fk.table_bias(out)
     fk.table_means(out)
     check_dict_table(out.to_numpy(), keys, ref)
+
+
+def test_measure_dict_reuse_plan(fk, orc):
+    """FIKIT_MEASURE_REUSE_PLAN: a second trace of the same services measured with the first
+    call's hot sets and string hashes gives the oracle's table for the second trace; a
+    different dictionary is rejected (E_ARG)."""
+    from paper_2311_10359_b200 import Workspace, strtab_to_device
+
+    cfg = F.zipf_trace(n_runs=3000, threads=8)
+    tr = cfg.trace
+    a, b = tr.records[: 256 * 1500], tr.records[256 * 1500:]
+    ref_all, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=8192)
+    keys = oracle_keys(ref_all)
+    ref_b, _, _ = orc.measure(b, tr.names, tr.sigs, capacity=8192)
+    ws = Workspace(8192, tr.names.count, tr.sigs.count, n_records=tr.records.shape[0])
+    st_tabs = (strtab_to_device(tr.names), strtab_to_device(tr.sigs))
+    dic = dict_tensors(keys)
+    _, st, _ = run_dict(fk, a, tr.names, tr.sigs, keys, 8192, ws=ws, strtabs=st_tabs, dictionary=dic)
+    assert st["code"] == 0
+    t, st, _ = run_dict(fk, b, tr.names, tr.sigs, keys, 8192, ws=ws, strtabs=st_tabs, dictionary=dic, reuse=True)
+    assert st["code"] == 0, st
+    check_dict_table(t.to_numpy(), keys, ref_b)
+    # a plan built on another dictionary
+    other = keys[:-1]
+    _, st, _ = run_dict(fk, b[: 256 * 10], tr.names, tr.sigs, other, 8192, ws=ws, strtabs=st_tabs, reuse=True)
+    assert st["code"] == fk.E_ARG
+    # reuse without a dictionary: a host-side argument error
+    import ctypes as C
+
+    t2 = fk.Table(8192)
+    rc = fk.lib().fikit_measure_dict_ex(None, 0, None, st_tabs[0].c(), st_tabs[1].c(), None, None, 0, 1,
+                                        C.byref(t2.c), None, ws.ptr(), ws.nbytes, None, None, None)
+    assert rc == fk.E_ARG
