@@ -25,3 +25,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 echo "launches rc=$?"
 TAG=rp_kmeasure KREGEX="k_measure" SKIP=1 COUNT=1 ARGS="--steps 2 --warmup 1 --no-configs2" bash scripts/ncu_full.sh
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/rp_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/rp_smoke.log
+# the replay kernels' warp-instructions per scenario (profiles/replay_inst.json, bench.py's replay roofline)
+for wl in zipf bert_vgg sweep; do
+  timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum -k regex:k_simulate --csv \
+    --log-file gpurun_out/replay_inst_$wl.csv python bench.py --workload $wl --steps 1 --warmup 1 --no-e2e \
+    --no-cpu-baseline --no-configs2 > /dev/null 2>&1
+  echo "replay_inst $wl rc=$?"
+done
