@@ -311,6 +311,8 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   pa.sb = sb;
   const uint64_t nstr = (uint64_t)names.count + sigs.count;
   // (a reused plan: the string hashes and the hot sets of the previous call; only the tile groups)
+  pa.hot_hdr = w.hot_n();
+  pa.reused_plan = reuse ? 1u : 0u;
   pa.nb_hash = reuse ? 0u : (uint32_t)((nstr + kPrepThreads / 32 - 1) / (kPrepThreads / 32));
   pa.nb_samp = reuse ? 0u : (uint32_t)((pa.n_samples + 2 * kPrepThreads - 1) / (2 * kPrepThreads));  // <= 2 per thread
   launch_pdl(k_prep, pa.nb_hash + pa.nb_samp + pa.sb, kPrepThreads, 0, s, pa);

@@ -180,6 +180,8 @@ struct PrepArgs {
   uint8_t* grp_bucket;
   uint32_t* blkcnt;
   uint32_t ngroups, sb;     // tile groups, group-role blocks
+  const uint32_t* hot_hdr;  // the hot-set header (a reused plan's schedule mode)
+  uint32_t reused_plan;     // FIKIT_MEASURE_REUSE_PLAN
   uint32_t nb_hash, nb_samp;  // block ranges: [0, nb_hash) hash, then nb_samp sample blocks, then sb group blocks
 };
 constexpr int kPrepThreads = 256;

@@ -410,6 +410,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(PrepArgs a) {
   } else if (b < a.nb_hash + a.nb_samp) {
     prep_sample(a, b - a.nb_hash, a.nb_samp, sm);
   } else {
+    // a reused plan in address-order mode needs no task buckets (k_measure sweeps the tiles in order)
+    if (a.reused_plan && !use_task_buckets(a.hot_hdr)) return;
     prep_groups(a, b - a.nb_hash - a.nb_samp, reinterpret_cast<uint32_t*>(sm));
   }
 }
@@ -767,6 +769,7 @@ __global__ void __launch_bounds__(1024) k_plan(PlanArgs a) {
     plan_hot(a, blockIdx.x, sm);
   } else {
     FK_TR(if (threadIdx.x == 0) { FK_TQ(0); g_trace_pre[(1024 + blockIdx.x) * 8 + 7] = 11; })
+    if (a.hot_blocks == 0 && !use_task_buckets(a.hot_hdr)) return;  // (a reused address-order plan)
     plan_scatter(a, blockIdx.x - a.hot_blocks, sm);
     FK_TR(if (threadIdx.x == 0) FK_TQ(4);)
   }

@@ -157,15 +157,22 @@ def test_dict_merge_one_gpu(fk, orc, P):
     check_dict_table(out.to_numpy(), keys, ref)
 
 
-def test_measure_dict_reuse_plan(fk, orc):
+@pytest.mark.parametrize("kind", ["zipf", "resnet"])
+def test_measure_dict_reuse_plan(fk, orc, kind):
     """FIKIT_MEASURE_REUSE_PLAN: a second trace of the same services measured with the first
-    call's hot sets and string hashes gives the oracle's table for the second trace; a
+    call's hot sets and string hashes gives the oracle's table for the second trace (Zipf:
+    task-bucket schedule; ResNet-like: address order, the schedule kernels exit at once); a
     different dictionary is rejected (E_ARG)."""
     from paper_2311_10359_b200 import Workspace, strtab_to_device
 
-    cfg = F.zipf_trace(n_runs=3000, threads=8)
+    if kind == "zipf":
+        cfg = F.zipf_trace(n_runs=3000, threads=8)
+        run = 256
+    else:
+        cfg = F.resnet_trace(n_runs=3000)
+        run = 300
     tr = cfg.trace
-    a, b = tr.records[: 256 * 1500], tr.records[256 * 1500:]
+    a, b = tr.records[: run * 1500], tr.records[run * 1500:]
     ref_all, _, _ = orc.measure(tr.records, tr.names, tr.sigs, capacity=8192)
     keys = oracle_keys(ref_all)
     ref_b, _, _ = orc.measure(b, tr.names, tr.sigs, capacity=8192)
@@ -179,7 +186,7 @@ def test_measure_dict_reuse_plan(fk, orc):
     check_dict_table(t.to_numpy(), keys, ref_b)
     # a plan built on another dictionary
     other = keys[:-1]
-    _, st, _ = run_dict(fk, b[: 256 * 10], tr.names, tr.sigs, other, 8192, ws=ws, strtabs=st_tabs, reuse=True)
+    _, st, _ = run_dict(fk, b[: run * 10], tr.names, tr.sigs, other, 8192, ws=ws, strtabs=st_tabs, reuse=True)
     assert st["code"] == fk.E_ARG
     # reuse without a dictionary: a host-side argument error
     import ctypes as C
@@ -188,3 +195,5 @@ def test_measure_dict_reuse_plan(fk, orc):
     rc = fk.lib().fikit_measure_dict_ex(None, 0, None, st_tabs[0].c(), st_tabs[1].c(), None, None, 0, 1,
                                         C.byref(t2.c), None, ws.ptr(), ws.nbytes, None, None, None)
     assert rc == fk.E_ARG
+    st = fk.get_status(ws)  # (the reused plan's schedule mode is the one the kind exercises)
+    assert st["schedule"] == (1 if kind == "zipf" else 0) or st["code"] != 0
