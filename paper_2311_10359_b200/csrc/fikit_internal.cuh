@@ -231,19 +231,21 @@ __host__ __device__ __forceinline__ bool use_task_buckets(const uint32_t* hdr) {
 enum MiscWord { kMiscDict = 0, kMiscDictHash = 2 };  // dictionary mode of the last measure call: dict_n + 1,
                                                      // 0 = none; words 2-3: the dictionary's hash (u64)
 
-// Programmatic dependent launch (the C-ABI launches the kernels of a call with
-// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel's CTAs may be scheduled while the
-// previous kernel of the stream finishes; griddepcontrol.wait (first statement of every such
-// kernel, before any global memory access) blocks until that grid has completed and its writes
-// are visible, so only launch latency overlaps.  launch_dependents lets the next kernel's launch
-// begin as soon as every CTA of this one has started.  Both are no-ops without the attribute.
+// Programmatic dependent launch hooks (first statement of every kernel of a call): with
+// cudaLaunchAttributeProgrammaticStreamSerialization a kernel's CTAs could be scheduled while the
+// previous kernel finishes, griddepcontrol.wait then blocking until its writes are visible.  The
+// C-ABI launches without the attribute (see launch_pdl: it measured slower), so both are no-ops;
+// they keep every kernel correct should a caller launch them programmatically.
 __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
-// Launch with programmatic stream serialization (the kernel's first statement is pdl_entry():
-// only the launch latency overlaps the previous kernel of the stream).
+// Kernel launch helper.  Programmatic dependent launch (the attribute
+// cudaLaunchAttributeProgrammaticStreamSerialization, with griddepcontrol.wait as every kernel's
+// first statement) was measured and left off: the early-launched CTAs sat on SM resources while
+// the previous kernel finished, and the measure call got 1-7 % slower (interleaved A/B,
+// profiles/r02/README.md).  Without the attribute pdl_entry() is a no-op.
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -251,11 +253,8 @@ inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
   (void)cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);  // (errors surface in launched())
 }
 
