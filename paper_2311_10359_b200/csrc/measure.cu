@@ -798,7 +798,9 @@ struct Smem {
   // slot -> identity in 5 words: name | sig << 16, grid_x, grid_y | grid_z << 16,
   // block_x | block_y << 16, block_z | task << 16 (one 16-B + one 4-B load verify).  Only
   // identities with name, sig, task < 2^16 are kept hot; the others always take the cold path.
-  uint4 tq[kHotMax + 1];  // (+1: the spare slot speculative verification reads without a tag match)
+  // Indexed by slot + 1 (the tag's low bits): entry 0 is never admitted, so the speculative
+  // verification of a launch without a matching tag reads it without a race.
+  uint4 tq[kHotMax + 1];
   uint32_t tq4[kHotMax + 1];
   // Odd row strides (33 and 9 words) spread the slots of a warp over all 32 banks.
   uint32_t hist[kHotMax][2 * kBins + 1];  // 64 u32 bins (32 duration, 32 gap) (+1 pad)
@@ -965,7 +967,11 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // load the hot set of a task bucket into the shared dictionary, zero the statistics
   auto load_hot_set = [&](uint32_t bkt) {
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
-    if (tid == 0) S.hot_n = min(hot_n_all[bkt], kHotMax);
+    if (tid == 0) {
+      S.hot_n = min(hot_n_all[bkt], kHotMax);
+      S.tq[0] = make_uint4(0u, 0u, 0u, 0u);
+      S.tq4[0] = 0u;
+    }
     for (int i = tid; i < (int)(mk::TAG_Q * mk::TAG_W); i += mk::THREADS) S.tagw[i] = 0u;
     for (int i = tid; i < kHotMax * (2 * kBins + 1); i += mk::THREADS) (&S.hist[0][0])[i] = 0;
     for (int i = tid; i < kHotMax * 5; i += mk::THREADS) (&S.st[0][0])[i] = 0u;
@@ -976,8 +982,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       Tuple t = hot[e];
       S.grow[e] = t.row;
       if (((t.w[0] | t.w[1] | t.w[6]) >> 16) == 0u) {  // compressible: may be hot
-        S.tq[e] = make_uint4(t.w[0] | (t.w[1] << 16), t.w[2], t.w[3], t.w[4]);
-        S.tq4[e] = t.w[5] | (t.w[6] << 16);
+        S.tq[e + 1] = make_uint4(t.w[0] | (t.w[1] << 16), t.w[2], t.w[3], t.w[4]);
+        S.tq4[e + 1] = t.w[5] | (t.w[6] << 16);
         mk::tag_insert(S, tuple_hash(t.w), e);
       }
     }
@@ -1101,8 +1107,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         const uint32_t e = atomicAdd(&S.hot_n, 1u);
         if (e < kHotMax) {
           S.grow[e] = row;
-          S.tq[e] = make_uint4(key[0] | (key[1] << 16), key[2], key[3], key[4]);
-          S.tq4[e] = key[5] | (key[6] << 16);
+          S.tq[e + 1] = make_uint4(key[0] | (key[1] << 16), key[2], key[3], key[4]);
+          S.tq4[e + 1] = key[5] | (key[6] << 16);
           __threadfence_block();
           mk::tag_insert(S, tuple_hash(key), e);
         }
@@ -1172,9 +1178,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     // every loaded word is consumed here, so the shared loads have completed
     asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
   };
-  auto verify = [&](uint32_t e, const Rec& R) -> bool {  // branch-free: both loads in flight
-    const uint4 a = S.tq[e];
-    const uint32_t b = S.tq4[e];
+  auto verify = [&](uint32_t c, const Rec& R) -> bool {  // c = slot + 1; branch-free: both loads in flight
+    const uint4 a = S.tq[c];
+    const uint32_t b = S.tq4[c];
     return ((a.x ^ R.ck0) | (a.y ^ R.key[2]) | (a.z ^ R.key[3]) | (a.w ^ R.key[4]) | (b ^ R.ck4)) == 0u;
   };
   // full lookup (rare: a full home bucket without the key, or a 20-bit tag collision)
@@ -1186,7 +1192,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < (int)mk::TAG_W; i++) {
         if (v[i] == 0u) return -1;  // end of the filled prefix: absent
-        if ((v[i] ^ hb) < 0x800u && verify((v[i] & 0x7FFu) - 1, R)) return (int)(v[i] & 0x7FFu) - 1;
+        if ((v[i] ^ hb) < 0x800u && verify(v[i] & 0x7FFu, R)) return (int)(v[i] & 0x7FFu) - 1;
       }
     }
   };
@@ -1331,14 +1337,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         uint32_t cA = mk::bucket_match(tA, mk::tag_bits(A.hk)), cB = mk::bucket_match(tB, mk::tag_bits(B.hk));
         const bool fullA = mk::bucket_full(tA), fullB = mk::bucket_full(tB);
         // speculative verification (both loads in flight before the tag compare resolves): without
-        // a matching tag the read goes to the spare slot kHotMax, which is never admitted (no race
-        // with an admission writing a real slot)
-        const uint32_t eA = cA ? cA - 1 : kHotMax, eB = cB ? cB - 1 : kHotMax;
-        const bool vA = verify(eA, A) & (cA != 0u);
-        const bool vB = verify(eB, B) & (cB != 0u);
+        // a matching tag (c = 0) the read goes to identity entry 0, which no admission writes
+        const bool vA = verify(cA, A) & (cA != 0u);
+        const bool vB = verify(cB, B) & (cB != 0u);
         int sA = -1, sB = -1;
-        if (A.valid && A.cmp) sA = vA ? (int)eA : ((cA != 0u || fullA) ? probe_slow(A) : -1);
-        if (B.valid && B.cmp) sB = vB ? (int)eB : ((cB != 0u || fullB) ? probe_slow(B) : -1);
+        if (A.valid && A.cmp) sA = vA ? (int)cA - 1 : ((cA != 0u || fullA) ? probe_slow(A) : -1);
+        if (B.valid && B.cmp) sB = vB ? (int)cB - 1 : ((cB != 0u || fullB) ? probe_slow(B) : -1);
         if (sA >= 0) update(A, sA);
         if (sB >= 0) update(B, sB);
         if (A.live && !A.valid) flag_record(st, A.gi);
