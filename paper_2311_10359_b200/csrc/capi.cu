@@ -19,7 +19,7 @@ __global__ void k_plan(PlanArgs);
 __global__ void k_measure(const fikit_record_t*, uint64_t, const fikit_record_t*, const uint64_t*, const uint64_t*,
                           uint32_t, uint32_t, IndexEntry*, uint32_t, Tuple*, uint32_t, fikit_status_t*, RawTab, Tuple*,
                           const Tuple*, const uint32_t*, uint32_t*, uint32_t*, const uint32_t*, const uint32_t*,
-                          const uint32_t*, const uint32_t*, uint32_t, uint32_t*, uint32_t);
+                          const uint32_t*, const uint32_t*, const uint8_t*, uint32_t, uint32_t*, uint32_t);
 size_t measure_smem_bytes();
 int measure_threads();
 __global__ void k_fin_sort(const fikit_status_t*, const RawRow*, uint32_t, fikit_table_t, FinKey*, const uint32_t*);
@@ -359,7 +359,7 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
   launch_pdl(k_measure, grid, measure_threads(), smem, s, 
       recs, n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, w.index(), w.L.slots, w.tindex(),
       w.L.tslots, w.st(), RawTab{w.raw(), cap}, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.act(), w.bstart(),
-      w.btot(), w.first(), w.order(), ntiles, out_row, dict ? 1u : 0u);
+      w.btot(), w.first(), w.order(), w.grp_bucket(), ntiles, out_row, dict ? 1u : 0u);
   if (int r = launched()) return r;
   if (ev1 && cudaEventRecord(ev1, s) != cudaSuccess) return FIKIT_E_CUDA;
   return FIKIT_OK;

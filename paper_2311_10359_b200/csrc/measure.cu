@@ -946,7 +946,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
               RawTab tab, Tuple* row_tuple, const Tuple* __restrict__ hot_all,
               const uint32_t* __restrict__ hot_n_all, uint32_t* cur, uint32_t* act, const uint32_t* __restrict__ bstart,
               const uint32_t* __restrict__ btot, const uint32_t* __restrict__ first,
-              const uint32_t* __restrict__ order, uint32_t ntiles, uint32_t* __restrict__ out_row, uint32_t dict) {
+              const uint32_t* __restrict__ order, const uint8_t* __restrict__ grp_bucket, uint32_t ntiles,
+              uint32_t* __restrict__ out_row, uint32_t dict) {
   pdl_entry();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   mk::Smem& S = *reinterpret_cast<mk::Smem*>(smem_raw);
@@ -1015,9 +1016,17 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   uint32_t kk = 0;
   uint32_t sfirst = 0;  // (all lanes) first launch of the tile in the stage
   const bool by_task = use_task_buckets(hot_n_all);  // else sorted position = tile
-  // tile positions of bucket b: [base_of(b), base_of(b) + len_of(b))
+  // tile positions of bucket b: [base_of(b), base_of(b) + len_of(b)).  A bucket's groups keep
+  // address order, so the last (partial) group is the last of its bucket: that bucket's length
+  // stops at the last tile and every position maps to a real tile.
+  // (Read when needed: called once per phase and by the bucket picks, nothing kept in registers.)
   auto len_of = [&](uint32_t b) -> uint32_t {
-    return by_task ? (b < kBuckets ? kGroupTiles * btot[b] : 0u) : (b == kGlobalSet ? ntiles : 0u);
+    if (!by_task) return b == kGlobalSet ? ntiles : 0u;
+    const uint32_t nt = b < kBuckets ? btot[b] : 0u;
+    if (nt == 0u) return 0u;
+    const uint32_t ng = (ntiles + kGroupTiles - 1) / kGroupTiles;  // (a non-empty bucket: ng >= 1)
+    const uint32_t miss = (uint32_t)__ldg(grp_bucket + ng - 1) == b ? ng * kGroupTiles - ntiles : 0u;
+    return kGroupTiles * nt - miss;
   };
   uint32_t cb = kNoBucket, cb_end = 0, cb_base = 0;  // the CTA's current bucket, its length and base
   if (blockIdx.x == 0 && tid == 0) {
@@ -1051,18 +1060,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     pc = q_pos++;
   };
   auto tile_of_claim = [&]() {  // lane 0: position pc -> tile
-    for (;;) {
-      if (pc == kNone || !by_task) {
-        tn = pc;
-        return;
-      }
+    tn = pc;
+    if (by_task && pc != kNone) {
       const uint32_t p = cb_base + pc;
-      const uint32_t t = __ldg(order + (p / kGroupTiles)) * kGroupTiles + p % kGroupTiles;
-      if (t < ntiles) {
-        tn = t;
-        return;
-      }
-      claim();  // a missing tile of the last (partial) group: the next position
+      tn = __ldg(order + p / kGroupTiles) * kGroupTiles + p % kGroupTiles;
     }
   };
   // 1-D TMA of a tile (+ the next launch) into the warp's stage (lane 0)

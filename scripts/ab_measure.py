@@ -30,7 +30,7 @@ def build(specs):
         objs = []
         for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
             o = os.path.join(d, f + ".o")
-            subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+            subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
                                    "-std=c++17", "-Xcompiler", "-fPIC", "-c",
                                    os.path.join(src, "paper_2311_10359_b200", "csrc", f), "-o", o])
             objs.append(o)
