@@ -828,6 +828,19 @@ __device__ __forceinline__ void red_shared_min(uint32_t saddr, uint32_t v) {
 __device__ __forceinline__ void red_shared_max(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
+// predicated forms (no branch, no reconvergence point): the reduction happens where p holds
+__device__ __forceinline__ void red_shared_add_if(bool p, uint32_t saddr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], %2;\n\t}" ::"r"((uint32_t)p),
+               "r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_shared_min_if(bool p, uint32_t saddr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.min.u32 [%1], %2;\n\t}" ::"r"((uint32_t)p),
+               "r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_shared_max_if(bool p, uint32_t saddr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.max.u32 [%1], %2;\n\t}" ::"r"((uint32_t)p),
+               "r"(saddr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -838,10 +851,10 @@ __device__ __forceinline__ void red_max_u64(uint64_t* p, uint64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// one duration (j = 0) or gap (j = 1) value of a hot row.  Histogram and split sums are
-// fire-and-forget shared reductions; min/max are read first (a broadcast when several lanes
-// hit the same row) and reduced only when the value improves them.  Values >= 2^32 ns
-// (4.3 s, rare) go straight to the table.
+// one duration (j = 0) or gap (j = 1, on: the launch has a gap) value of a hot row, without
+// branches for values < 2^32.  Histogram and split sums are fire-and-forget shared reductions;
+// min/max are read first (a broadcast when several lanes hit the same row) and reduced only when
+// the value improves them.  Values >= 2^32 ns (4.3 s, rare) go straight to the table.
 __device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
@@ -852,26 +865,28 @@ __device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) 
 // The sum of values < 2^32 is kept mod 2^32 with a carry counter: the add returns the old
 // word and a wrap (old + v < old, exact: the atomic serializes) adds one carry.  Returns the
 // old word (the caller checks the carry after its other reductions, off the critical path).
+// The split sum gets a (v, or 0 when off or >= 2^32: every lane adds, the old word is returned
+// for the carry check, which the caller makes after its other reductions).
 template <class RowOf>  // row_of(): the slot's table row, read only on the rare >= 2^32 path
 __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const RawTab& tab,
-                                            RowOf row_of, int j, uint64_t v, uint32_t mn, uint32_t mx) {
-  if ((v >> 32) == 0) {
-    const uint32_t v32 = (uint32_t)v;
-    const uint32_t b = min(32u - (uint32_t)__clz(v32), 31u) + 32u * j;  // bin_of for v < 2^32
-    const uint32_t old = atom_shared_add(st_e + 8u * j, v32);
-    red_shared_add(hist_e + 4u * b, 1u);
-    if (v32 < mn) red_shared_min(mm_e + 8u * j, v32);
-    if (v32 > mx) red_shared_max(mm_e + 8u * j + 4u, v32);
-    return old;
-  } else {  // rare: a value >= 2^32 ns
-    const int b = bin_of(v) + 32 * j;
-    red_shared_add(hist_e + 4u * (uint32_t)b, 1u);
+                                            RowOf row_of, int j, uint64_t v, bool on, uint32_t mn, uint32_t mx,
+                                            uint32_t& a) {
+  const bool small = (v >> 32) == 0;
+  const uint32_t v32 = (uint32_t)v;
+  const uint32_t b = (small ? min(32u - (uint32_t)__clz(v32), 31u) : 31u) + 32u * j;  // bin_of(v)
+  const bool son = on && small;
+  a = son ? v32 : 0u;
+  const uint32_t old = atom_shared_add(st_e + 8u * j, a);
+  red_shared_add_if(on, hist_e + 4u * b, 1u);
+  red_shared_min_if(son && v32 < mn, mm_e + 8u * j, v32);
+  red_shared_max_if(son && v32 > mx, mm_e + 8u * j + 4u, v32);
+  if (on && !small) {  // rare: a value >= 2^32 ns
     const uint32_t row = row_of();
     red_add_u64(tab.rows[row].sums + 2 * j + 1, v);
     red_max_u64(tab.rows[row].ext + 2 * j, v);
     red_max_u64(tab.rows[row].ext + 2 * j + 1, ~v);
-    return 0u;  // (v >> 32 != 0: the low word 0 never wraps the sum)
   }
+  return old;
 }
 
 __device__ __forceinline__ void cold_add(const RawTab& tab, uint32_t row, int j, uint64_t v) {
@@ -912,6 +927,19 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 
 namespace mk {
 __device__ __forceinline__ uint32_t tag_bits(uint32_t h) { return (h & TAG_HB) | 0x80000000u; }
+// hash of a hot identity's five compressed words (tq, tq4 below): 5 multiply rounds and a short
+// finaliser (the bucket takes the low 11 bits, the tag bits 11..30); collisions only cost a probe
+__device__ __forceinline__ uint32_t hot_hash(uint32_t c0, uint32_t k2, uint32_t k3, uint32_t k4, uint32_t c4) {
+  uint32_t h = c0 * 0x9E3779B1u;
+  h = (h ^ k2) * 0x85EBCA77u;
+  h = (h ^ k3) * 0xC2B2AE3Du;
+  h = (h ^ k4) * 0x27D4EB2Fu;
+  h = (h ^ c4) * 0x165667B1u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  return h;
+}
 // slot + 1 of the first tag of bucket t whose hash bits are hb's, 0 if none (an empty tag never
 // matches: hb has bit 31 set)
 __device__ __forceinline__ uint32_t bucket_match(const uint4 t, uint32_t hb) {
@@ -983,9 +1011,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       Tuple t = hot[e];
       S.grow[e] = t.row;
       if (((t.w[0] | t.w[1] | t.w[6]) >> 16) == 0u) {  // compressible: may be hot
-        S.tq[e + 1] = make_uint4(t.w[0] | (t.w[1] << 16), t.w[2], t.w[3], t.w[4]);
-        S.tq4[e + 1] = t.w[5] | (t.w[6] << 16);
-        mk::tag_insert(S, tuple_hash(t.w), e);
+        const uint32_t c0 = t.w[0] | (t.w[1] << 16), c4 = t.w[5] | (t.w[6] << 16);
+        S.tq[e + 1] = make_uint4(c0, t.w[2], t.w[3], t.w[4]);
+        S.tq4[e + 1] = c4;
+        mk::tag_insert(S, mk::hot_hash(c0, t.w[2], t.w[3], t.w[4], c4), e);
       }
     }
     __syncthreads();
@@ -1111,7 +1140,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
           S.tq[e + 1] = make_uint4(key[0] | (key[1] << 16), key[2], key[3], key[4]);
           S.tq4[e + 1] = key[5] | (key[6] << 16);
           __threadfence_block();
-          mk::tag_insert(S, tuple_hash(key), e);
+          mk::tag_insert(S, mk::hot_hash(key[0] | (key[1] << 16), key[2], key[3], key[4], key[5] | (key[6] << 16)), e);
         }
       }
     }
@@ -1133,10 +1162,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     const uint32_t cnt = n32 > first ? min((uint32_t)mk::TILE, n32 - first) : 0u;
     const uint4* rp = S.ring[warp] + (h * mk::TILE + lane) * 3;
     R.live = (uint32_t)lane < cnt;
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0;
-    if (R.live) {
+    uint4 r0, r1, r2;
+    {
       // one 16-B shared load per quarter record (the compiler splits rp[0] into two 8-B loads,
-      // which cost as many wavefronts each at this 48-B stride)
+      // which cost as many wavefronts each at this 48-B stride).  Every lane loads (the stage
+      // holds 65 records, so the address is in bounds): a lane past the end reads a stale
+      // record and every use of it is masked by R.live.
       const uint32_t a = smem_u32(rp);
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w) : "r"(a));
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -1175,7 +1206,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     R.ck0 = w[4] | (w[5] << 16);
     R.ck4 = (w[9] & 0xFFFFu) | (w[11] << 16);
     R.cmp = ((w[4] | w[5] | w[11]) >> 16) == 0u;
-    R.hk = tuple_hash(R.key);
+    R.hk = mk::hot_hash(R.ck0, R.key[2], R.key[3], R.key[4], R.ck4);
     // every loaded word is consumed here, so the shared loads have completed
     asm volatile("" ::"r"(R.hk), "l"(R.d), "l"(R.g), "r"((uint32_t)R.gap), "r"((uint32_t)R.valid), "r"(R.gi));
   };
@@ -1206,12 +1237,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     uint4 mm;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "r"(mm_e));
-    const uint32_t od = hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, mm.x, mm.y);
-    const uint32_t og = R.gap ? hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, mm.z, mm.w) : 0u;
+    uint32_t ad, ag;
+    const uint32_t od = hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, true, mm.x, mm.y, ad);
+    const uint32_t og = hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, R.gap, mm.z, mm.w, ag);
     if (out_row) out_row[R.gi] = row();
-    // carries of the two sums (old + v wrapped past 2^32)
-    if ((R.d >> 32) == 0 && od + (uint32_t)R.d < od) red_shared_add(st_e + 4u, 1u);
-    if (R.gap && (R.g >> 32) == 0 && og + (uint32_t)R.g < og) red_shared_add(st_e + 12u, 1u);
+    // carries of the two sums (old + a wrapped past 2^32)
+    red_shared_add_if(od + ad < od, st_e + 4u, 1u);
+    red_shared_add_if(og + ag < og, st_e + 12u, 1u);
   };
   // compact this tile's cold launches behind the pending ones; resolve when a batch is full
   auto compact = [&](const Rec& R, bool cold) {
