@@ -364,14 +364,14 @@ struct DigestBatch {
   }
 };
 
-// LP pool of at most 64 requests in registers: lane l holds sorted positions l and 32 + l
+// LP pool of at most 64 requests in registers: lane l holds sorted positions 2l and 2l + 1
 // (key order = BestPrioFit's preference order, as in make_sorted_pool), and, by request index,
-// the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^50.
+// the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^22.
 struct RegPool {
   static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
-  // at sorted positions lane, 32 + lane: q << 6 | request index (q < 2^22 ns; 0xFFFFFFFF: an
+  // at sorted positions 2 lane, 2 lane + 1: q << 6 | request index (q < 2^22 ns; 0xFFFFFFFF: an
   // ineligible position), and the request's LP duration (< 2^32 ns), so a pick is one ballot on
-  // the packed word and two independent shuffles (no duration lookup by index after it)
+  // the packed words and two independent shuffles (no duration lookup by index after it)
   uint32_t pk0, pk1;
   uint32_t es0, es1;
   bool a0, a1;        // alive and eligible there
@@ -380,24 +380,26 @@ struct RegPool {
   uint64_t alive;     // alive requests by index (warp-uniform)
   uint32_t ek;        // the last pick's duration
 
-  __device__ __forceinline__ uint64_t min_q() const {
+  // smallest alive eligible q, 0xFFFFFFFF if none
+  __device__ __forceinline__ uint32_t min_q32() const {
     const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? pk0 : 0xFFFFFFFFu, a1 ? pk1 : 0xFFFFFFFFu));
-    return v == 0xFFFFFFFFu ? ~0ull : (uint64_t)(v >> 6);
+    return v == 0xFFFFFFFFu ? v : v >> 6;
   }
   // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
   // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
-  __device__ __forceinline__ int pick(uint64_t R, int lane, uint64_t& qk) {
-    const uint32_t Rc = R >= (1ull << 22) ? 0xFFFFFFFFu : ((uint32_t)R << 6) | 63u;
-    uint32_t b = __ballot_sync(0xffffffffu, a0 && pk0 <= Rc);
-    const bool hi = b == 0;
-    if (hi) b = __ballot_sync(0xffffffffu, a1 && pk1 <= Rc);
+  // Position 2 lane precedes 2 lane + 1, so the first lane with a fitting position holds the
+  // first one: one ballot, and each lane offers its own first fitting entry to the shuffles.
+  __device__ __forceinline__ int pick32(uint32_t R, int lane, uint32_t& qk) {
+    const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFFu : (R << 6) | 63u;
+    const bool f0 = a0 && pk0 <= Rc, f1 = a1 && pk1 <= Rc;
+    const uint32_t b = __ballot_sync(0xffffffffu, f0 || f1);
     if (!b) return -1;
     const int src = __ffs(b) - 1;
-    const uint32_t w = __shfl_sync(0xffffffffu, hi ? pk1 : pk0, src);
-    ek = __shfl_sync(0xffffffffu, hi ? es1 : es0, src);
+    const uint32_t w = __shfl_sync(0xffffffffu, f0 ? pk0 : pk1, src);
+    ek = __shfl_sync(0xffffffffu, f0 ? es0 : es1, src);
     qk = w >> 6;
     if (lane == src) {
-      if (hi) a1 = false; else a0 = false;
+      if (f0) a0 = false; else a1 = false;
     }
     return (int)(w & 63u);
   }
@@ -489,6 +491,13 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
   if (!__all_sync(0xffffffffu, ok)) return 1;
   if (!__all_sync(0xffffffffu, small)) return 2;
   reg_bitonic64_u32(f0, f1, lane);
+  {  // sorted positions lane, 32 + lane -> 2 lane, 2 lane + 1
+    const int s0 = (2 * lane) & 31, s1 = (2 * lane + 1) & 31;
+    const uint32_t x0 = __shfl_sync(0xffffffffu, f0, s0), y0 = __shfl_sync(0xffffffffu, f1, s0);
+    const uint32_t x1 = __shfl_sync(0xffffffffu, f0, s1), y1 = __shfl_sync(0xffffffffu, f1, s1);
+    f0 = lane < 16 ? x0 : y0;
+    f1 = lane < 16 ? x1 : y1;
+  }
   P.a0 = f0 != 0xFFFFFFFFu;
   P.a1 = f1 != 0xFFFFFFFFu;
   P.pk0 = P.a0 ? ((kQ22 - ((f0 >> 6) & kQ22)) << 6) | (f0 & 63u) : 0xFFFFFFFFu;
@@ -653,6 +662,41 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
   return replay_hp_core([&]() { return qmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane);
 }
 
+// The same loop on the register pool, with the idle time R and qmin in 32 bits: every eligible
+// q < 2^22 there, so R saturated at 2^32 - 1 takes every fit decision R does (after at most 64
+// picks, a saturated R is still >= 2^32 - 1 - 2^28 > any q, and so is the exact one).
+__device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& tab, uint32_t K,
+                                               const uint32_t* __restrict__ hp_row,
+                                               const uint64_t* __restrict__ hp_dur,
+                                               const uint64_t* __restrict__ hp_gap, const fikit_scenario_t& c,
+                                               const fikit_fill_params_t& prm, bool sched, int32_t* fill_gap,
+                                               uint64_t* lp_start, uint64_t so, DigestBatch& dig, int lane) {
+  uint32_t qmin = P.min_q32();  // 0xFFFFFFFF: no alive eligible request
+  auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R64, HpOut& o) -> uint64_t {
+    uint32_t R = R64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R64;
+    for (;;) {
+      if (prm.feedback && t >= r) break;
+      if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
+      uint32_t qk;
+      const int k = P.pick32(R, lane, qk);  // Alg. 2
+      if (k < 0) break;
+      const uint64_t e = P.ek;
+      if (sched && lane == 0) {
+        fill_gap[so + k] = (int32_t)i;
+        lp_start[so + k] = t;
+      }
+      P.record((uint32_t)k, (int32_t)i, t, lane, dig);
+      R -= qk;
+      t += e;
+      if (qk == qmin) qmin = P.min_q32();
+      o.lp_end = t;  // fills run in time order: the last one ends last
+    }
+    return t;
+  };
+  return replay_hp_core([&]() { return qmin == 0xFFFFFFFFu ? ~0ull : (uint64_t)qmin; }, fill, tab, K, hp_row,
+                        hp_dur, hp_gap, c, prm, lane);
+}
+
 // tail (R22): the requests still queued run after the HP end in Q1..Q9 order, FIFO within a
 // queue; sel(k) / dur(k) / level presence come from the pool representation
 template <class Sel, class Dur>
@@ -786,8 +830,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 war
     const uint64_t so = sched ? sched_off[s] : 0;
     DigestBatch db;
     P.fg0 = P.fg1 = -1;
-    HpOut o = replay_hp(P, [&]() { return P.min_q(); }, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched, fill_gap,
-                        lp_start, so, db, lane);
+    HpOut o = replay_hp_reg(P, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched, fill_gap, lp_start, so, db, lane);
     {  // fills: the requests with a gap index, summed from their owning lanes
       const bool f0 = P.fg0 >= 0 && (uint32_t)lane < m, f1 = P.fg1 >= 0 && 32u + (uint32_t)lane < m;
       o.n_fills = __popc(__ballot_sync(0xffffffffu, f0)) + __popc(__ballot_sync(0xffffffffu, f1));
