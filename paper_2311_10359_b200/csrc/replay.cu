@@ -364,44 +364,42 @@ struct DigestBatch {
   }
 };
 
-// LP pool of at most 64 requests in registers: lane l holds sorted positions 2l and 2l + 1
-// (key order = BestPrioFit's preference order, as in make_sorted_pool), and, by request index,
-// the level and LP duration of requests l and 32 + l.  Requires every eligible q < 2^22.
+// LP pool of at most 64 requests in registers, by request index: lane l holds requests l and
+// 32 + l.  Requires every eligible q < 2^22 ns and every LP duration < 2^32 ns.
+// BestPrioFit (Alg. 2) is one warp argmin: the strict total order (level asc, q desc, index asc)
+// of R14-R16 is the order of the 32-bit key  level << 28 | (2^22 - 1 - q) << 6 | index, so the
+// best fitting request is the REDUX minimum of the keys of the alive eligible requests with
+// q <= R (no sort, no per-scenario setup beyond the loads).
+constexpr uint32_t kQ22 = (1u << 22) - 1;
 struct RegPool {
   static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
-  // at sorted positions 2 lane, 2 lane + 1: q << 6 | request index (q < 2^22 ns; 0xFFFFFFFF: an
-  // ineligible position), and the request's LP duration (< 2^32 ns), so a pick is one ballot on
-  // the packed words and two independent shuffles (no duration lookup by index after it)
-  uint32_t pk0, pk1;
-  uint32_t es0, es1;
-  bool a0, a1;        // alive and eligible there
+  uint32_t key0, key1;  // the order key of requests lane, 32 + lane (0xFFFFFFFF: ineligible)
+  uint32_t pq0, pq1;    // q << 6 | index (0xFFFFFFFF: ineligible): q <= R <=> pq <= R << 6 | 63
+  bool a0, a1;          // alive and eligible
   uint32_t dur0, dur1;  // LP duration of requests lane, 32 + lane (< 2^32 ns)
   uint32_t lvl0, lvl1;  // level of requests lane, 32 + lane
-  uint64_t alive;     // alive requests by index (warp-uniform)
-  uint32_t ek;        // the last pick's duration
+  uint64_t alive;       // alive requests by index (warp-uniform)
+  uint32_t ek;          // the last pick's duration
 
   // smallest alive eligible q, 0xFFFFFFFF if none
   __device__ __forceinline__ uint32_t min_q32() const {
-    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? pk0 : 0xFFFFFFFFu, a1 ? pk1 : 0xFFFFFFFFu));
+    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? pq0 : 0xFFFFFFFFu, a1 ? pq1 : 0xFFFFFFFFu));
     return v == 0xFFFFFFFFu ? v : v >> 6;
   }
-  // Alg. 2: first alive sorted position with q <= R; dequeued.  Returns the index or -1.
+  // Alg. 2: the best alive eligible request with q <= R, dequeued.  Returns its index or -1.
   // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
-  // Position 2 lane precedes 2 lane + 1, so the first lane with a fitting position holds the
-  // first one: one ballot, and each lane offers its own first fitting entry to the shuffles.
   __device__ __forceinline__ int pick32(uint32_t R, int lane, uint32_t& qk) {
     const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFFu : (R << 6) | 63u;
-    const bool f0 = a0 && pk0 <= Rc, f1 = a1 && pk1 <= Rc;
-    const uint32_t b = __ballot_sync(0xffffffffu, f0 || f1);
-    if (!b) return -1;
-    const int src = __ffs(b) - 1;
-    const uint32_t w = __shfl_sync(0xffffffffu, f0 ? pk0 : pk1, src);
-    ek = __shfl_sync(0xffffffffu, f0 ? es0 : es1, src);
-    qk = w >> 6;
-    if (lane == src) {
-      if (f0) a0 = false; else a1 = false;
+    const uint32_t c0 = (a0 && pq0 <= Rc) ? key0 : 0xFFFFFFFFu, c1 = (a1 && pq1 <= Rc) ? key1 : 0xFFFFFFFFu;
+    const uint32_t best = __reduce_min_sync(0xffffffffu, min(c0, c1));
+    if (best == 0xFFFFFFFFu) return -1;
+    const uint32_t k = best & 63u;
+    qk = kQ22 - ((best >> 6) & kQ22);
+    ek = __shfl_sync(0xffffffffu, k < 32u ? dur0 : dur1, (int)(k & 31u));
+    if ((uint32_t)lane == (k & 31u)) {
+      if (k < 32u) a0 = false; else a1 = false;
     }
-    return (int)(w & 63u);
+    return (int)k;
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t) const { return ek; }  // (of the last pick)
   // the schedule of request kk (gap, start), kept by its owning lane for the digest at the end
@@ -418,51 +416,22 @@ struct RegPool {
       }
     }
   }
-  // requests dequeued by fills, by index (pk = 0xFFFFFFFF: an ineligible position)
+  // requests dequeued by fills, by index
   __device__ __forceinline__ uint64_t picked_mask() const {
-    uint32_t lo = 0, hi = 0;
-    const uint32_t k0 = pk0 & 63u, k1 = pk1 & 63u;
-    if (pk0 != 0xFFFFFFFFu && !a0) (k0 < 32 ? lo : hi) |= 1u << (k0 & 31u);
-    if (pk1 != 0xFFFFFFFFu && !a1) (k1 < 32 ? lo : hi) |= 1u << (k1 & 31u);
-    lo = __reduce_or_sync(0xffffffffu, lo);
-    hi = __reduce_or_sync(0xffffffffu, hi);
+    const uint32_t lo = __ballot_sync(0xffffffffu, pq0 != 0xFFFFFFFFu && !a0);
+    const uint32_t hi = __ballot_sync(0xffffffffu, pq1 != 0xFFFFFFFFu && !a1);
     return ((uint64_t)hi << 32) | lo;
   }
 };
 
-// register bitonic sort of 64 32-bit keys (lane holds positions lane (e0) and 32 + lane (e1)),
-// ascending: one SHFL and one min/max instruction per element and stage
-__device__ __forceinline__ void reg_bitonic64_u32(uint32_t& e0, uint32_t& e1, int lane) {
-#pragma unroll
-  for (uint32_t k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      if (j == 32) {
-        const uint32_t lo = min(e0, e1), hi = max(e0, e1);
-        e0 = lo;
-        e1 = hi;
-      } else {
-        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, j), o1 = __shfl_xor_sync(0xffffffffu, e1, j);
-        const bool lower = ((uint32_t)lane & j) == 0;
-        const bool asc0 = ((uint32_t)lane & k) == 0, asc1 = ((32u + (uint32_t)lane) & k) == 0;
-        e0 = (asc0 == lower) ? min(e0, o0) : max(e0, o0);
-        e1 = (asc1 == lower) ? min(e1, o1) : max(e1, o1);
-      }
-    }
-  }
-}
-constexpr uint32_t kQ22 = (1u << 22) - 1;  // 32-bit keys: level << 28 | (kQ22 - q) << 6 | index
-
-// load and sort a pool of m <= 64 requests into registers.  Returns 0 ok, 1 invalid level
-// (flagged), 2 fast path not applicable (some eligible q >= 2^50).
+// load a pool of m <= 64 requests into registers.  Returns 0 ok, 1 invalid level (flagged),
+// 2 the register pool does not apply (some eligible q >= 2^22 or duration >= 2^32: pass 2).
 __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t K, const uint32_t* __restrict__ row,
                                              const uint8_t* __restrict__ level, const uint64_t* __restrict__ dur,
                                              uint64_t off, uint32_t m, int lane, fikit_status_t* st, RegPool& P) {
-  // the register pool is 32-bit: every eligible q < 2^22 ns (4.2 ms) and every e < 2^32 ns;
-  // any other scenario goes to pass 2
   bool ok = true, small = true;
-  auto one = [&](uint32_t kk, uint32_t& key, uint32_t& d, uint32_t& lv) {
-    key = 0xFFFFFFFFu;
+  auto one = [&](uint32_t kk, uint32_t& key, uint32_t& pq, uint32_t& d, uint32_t& lv) {
+    key = pq = 0xFFFFFFFFu;
     d = 0;
     lv = 0;
     if (kk < m) {
@@ -480,35 +449,18 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
       if (el) {
         const uint64_t q = __ldg(tab.mean + (size_t)r * 2);  // SK of the request's ID
         if (q > kQ22) small = false;
-        // BestPrioFit's order (level asc, q desc, index asc) as one 32-bit key
-        key = ((L & 0xFu) << 28) | ((kQ22 - (uint32_t)(q & kQ22)) << 6) | kk;
+        const uint32_t q22 = (uint32_t)(q & kQ22);
+        key = ((L & 0xFu) << 28) | ((kQ22 - q22) << 6) | kk;
+        pq = (q22 << 6) | kk;
       }
     }
   };
-  uint32_t f0, f1;
-  one((uint32_t)lane, f0, P.dur0, P.lvl0);
-  one(32u + (uint32_t)lane, f1, P.dur1, P.lvl1);
+  one((uint32_t)lane, P.key0, P.pq0, P.dur0, P.lvl0);
+  one(32u + (uint32_t)lane, P.key1, P.pq1, P.dur1, P.lvl1);
   if (!__all_sync(0xffffffffu, ok)) return 1;
   if (!__all_sync(0xffffffffu, small)) return 2;
-  reg_bitonic64_u32(f0, f1, lane);
-  {  // sorted positions lane, 32 + lane -> 2 lane, 2 lane + 1
-    const int s0 = (2 * lane) & 31, s1 = (2 * lane + 1) & 31;
-    const uint32_t x0 = __shfl_sync(0xffffffffu, f0, s0), y0 = __shfl_sync(0xffffffffu, f1, s0);
-    const uint32_t x1 = __shfl_sync(0xffffffffu, f0, s1), y1 = __shfl_sync(0xffffffffu, f1, s1);
-    f0 = lane < 16 ? x0 : y0;
-    f1 = lane < 16 ? x1 : y1;
-  }
-  P.a0 = f0 != 0xFFFFFFFFu;
-  P.a1 = f1 != 0xFFFFFFFFu;
-  P.pk0 = P.a0 ? ((kQ22 - ((f0 >> 6) & kQ22)) << 6) | (f0 & 63u) : 0xFFFFFFFFu;
-  P.pk1 = P.a1 ? ((kQ22 - ((f1 >> 6) & kQ22)) << 6) | (f1 & 63u) : 0xFFFFFFFFu;
-  {  // durations to the sorted positions (request k is held by lane k % 32)
-    const uint32_t k0 = f0 & 31u, k1 = f1 & 31u;
-    const uint32_t x0 = __shfl_sync(0xffffffffu, P.dur0, k0), y0 = __shfl_sync(0xffffffffu, P.dur1, k0);
-    const uint32_t x1 = __shfl_sync(0xffffffffu, P.dur0, k1), y1 = __shfl_sync(0xffffffffu, P.dur1, k1);
-    P.es0 = (f0 & 32u) ? y0 : x0;
-    P.es1 = (f1 & 32u) ? y1 : x1;
-  }
+  P.a0 = P.pq0 != 0xFFFFFFFFu;
+  P.a1 = P.pq1 != 0xFFFFFFFFu;
   P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
   return 0;
 }
