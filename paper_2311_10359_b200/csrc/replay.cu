@@ -373,9 +373,11 @@ struct DigestBatch {
 constexpr uint32_t kQ22 = (1u << 22) - 1;
 struct RegPool {
   static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
-  uint32_t key0, key1;  // the order key of requests lane, 32 + lane (0xFFFFFFFF: ineligible)
-  uint32_t pq0, pq1;    // q << 6 | index (0xFFFFFFFF: ineligible): q <= R <=> pq <= R << 6 | 63
-  bool a0, a1;          // alive and eligible
+  // the order key and q << 6 | index of requests lane, 32 + lane while they are alive and
+  // eligible (both 0xFFFFFFFF otherwise): q <= R <=> pq <= R << 6 | 63
+  uint32_t key0, key1;
+  uint32_t pq0, pq1;
+  uint64_t elig;        // eligible requests by index (warp-uniform)
   uint32_t dur0, dur1;  // LP duration of requests lane, 32 + lane (< 2^32 ns)
   uint32_t lvl0, lvl1;  // level of requests lane, 32 + lane
   uint64_t alive;       // alive requests by index (warp-uniform)
@@ -383,21 +385,21 @@ struct RegPool {
 
   // smallest alive eligible q, 0xFFFFFFFF if none
   __device__ __forceinline__ uint32_t min_q32() const {
-    const uint32_t v = __reduce_min_sync(0xffffffffu, min(a0 ? pq0 : 0xFFFFFFFFu, a1 ? pq1 : 0xFFFFFFFFu));
+    const uint32_t v = __reduce_min_sync(0xffffffffu, min(pq0, pq1));
     return v == 0xFFFFFFFFu ? v : v >> 6;
   }
   // Alg. 2: the best alive eligible request with q <= R, dequeued.  Returns its index or -1.
   // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
   __device__ __forceinline__ int pick32(uint32_t R, int lane, uint32_t& qk) {
     const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFFu : (R << 6) | 63u;
-    const uint32_t c0 = (a0 && pq0 <= Rc) ? key0 : 0xFFFFFFFFu, c1 = (a1 && pq1 <= Rc) ? key1 : 0xFFFFFFFFu;
+    const uint32_t c0 = pq0 <= Rc ? key0 : 0xFFFFFFFFu, c1 = pq1 <= Rc ? key1 : 0xFFFFFFFFu;
     const uint32_t best = __reduce_min_sync(0xffffffffu, min(c0, c1));
     if (best == 0xFFFFFFFFu) return -1;
     const uint32_t k = best & 63u;
     qk = kQ22 - ((best >> 6) & kQ22);
     ek = __shfl_sync(0xffffffffu, k < 32u ? dur0 : dur1, (int)(k & 31u));
     if ((uint32_t)lane == (k & 31u)) {
-      if (k < 32u) a0 = false; else a1 = false;
+      if (k < 32u) key0 = pq0 = 0xFFFFFFFFu; else key1 = pq1 = 0xFFFFFFFFu;
     }
     return (int)k;
   }
@@ -418,9 +420,9 @@ struct RegPool {
   }
   // requests dequeued by fills, by index
   __device__ __forceinline__ uint64_t picked_mask() const {
-    const uint32_t lo = __ballot_sync(0xffffffffu, pq0 != 0xFFFFFFFFu && !a0);
-    const uint32_t hi = __ballot_sync(0xffffffffu, pq1 != 0xFFFFFFFFu && !a1);
-    return ((uint64_t)hi << 32) | lo;
+    const uint32_t lo = __ballot_sync(0xffffffffu, pq0 == 0xFFFFFFFFu);
+    const uint32_t hi = __ballot_sync(0xffffffffu, pq1 == 0xFFFFFFFFu);
+    return elig & (((uint64_t)hi << 32) | lo);
   }
 };
 
@@ -459,8 +461,8 @@ __device__ __forceinline__ int load_reg_pool(const fikit_table_t& tab, uint32_t 
   one(32u + (uint32_t)lane, P.key1, P.pq1, P.dur1, P.lvl1);
   if (!__all_sync(0xffffffffu, ok)) return 1;
   if (!__all_sync(0xffffffffu, small)) return 2;
-  P.a0 = P.pq0 != 0xFFFFFFFFu;
-  P.a1 = P.pq1 != 0xFFFFFFFFu;
+  P.elig = ((uint64_t)__ballot_sync(0xffffffffu, P.pq1 != 0xFFFFFFFFu) << 32) |
+           __ballot_sync(0xffffffffu, P.pq0 != 0xFFFFFFFFu);
   P.alive = m >= 64 ? ~0ull : ((1ull << m) - 1);
   return 0;
 }
@@ -626,8 +628,10 @@ __device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& 
   uint32_t qmin = P.min_q32();  // 0xFFFFFFFF: no alive eligible request
   auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R64, HpOut& o) -> uint64_t {
     uint32_t R = R64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R64;
+    const uint64_t r_stop = prm.feedback ? r : ~0ull;  // (without feedback t never reaches it)
+    bool any = false;
     for (;;) {
-      if (prm.feedback && t >= r) break;
+      if (t >= r_stop) break;
       if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
       uint32_t qk;
       const int k = P.pick32(R, lane, qk);  // Alg. 2
@@ -640,9 +644,10 @@ __device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& 
       P.record((uint32_t)k, (int32_t)i, t, lane, dig);
       R -= qk;
       t += e;
+      any = true;
       if (qk == qmin) qmin = P.min_q32();
-      o.lp_end = t;  // fills run in time order: the last one ends last
     }
+    if (any) o.lp_end = t;  // fills run in time order: the last one ends last
     return t;
   };
   return replay_hp_core([&]() { return qmin == 0xFFFFFFFFu ? ~0ull : (uint64_t)qmin; }, fill, tab, K, hp_row,
