@@ -404,20 +404,15 @@ struct RegPool {
     return (int)k;
   }
   __device__ __forceinline__ uint64_t dur_of(uint32_t) const { return ek; }  // (of the last pick)
-  // the schedule of request kk (gap, start), kept by its owning lane for the digest at the end
+  // the schedule of a filled request kk (gap, start): lane 0 logs it in the warp's shared slot
+  // kk (one store, no per-lane selects); the owning lanes read it back for the digest at the end
+  uint4* log;
+  __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch&) {
+    if (lane == 0) log[kk] = make_uint4((uint32_t)g, (uint32_t)t, (uint32_t)(t >> 32), 0u);
+  }
+  // the tail start of requests lane, 32 + lane (set by replay_tail_reg; fg = -1 there)
   int32_t fg0, fg1;
   uint64_t st0, st1;
-  __device__ __forceinline__ void record(uint32_t kk, int32_t g, uint64_t t, int lane, DigestBatch&) {
-    if (lane == (int)(kk & 31u)) {
-      if (kk < 32) {
-        fg0 = g;
-        st0 = t;
-      } else {
-        fg1 = g;
-        st1 = t;
-      }
-    }
-  }
   // requests dequeued by fills, by index
   __device__ __forceinline__ uint64_t picked_mask() const {
     const uint32_t lo = __ballot_sync(0xffffffffu, pq0 == 0xFFFFFFFFu);
@@ -774,11 +769,13 @@ __global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 war
   const uint32_t nw = gridDim.x * kRegWarps;
   uint32_t s = blockIdx.x * kRegWarps + w;  // first scenario: static; later ones claimed
   uint32_t nxt = 0;
+  __shared__ uint4 s_log[kRegWarps][64];  // per warp: (gap, start) of each filled request
   for (; s < S; s = nw + __shfl_sync(0xffffffffu, nxt, 0)) {
     if (lane == 0) nxt = atomicAdd(ctr, 1u);  // claim the next one now, use it after this one
     const fikit_scenario_t c = sc[s];
     const uint32_t m = c.lp_len;
     RegPool P;
+    P.log = s_log[w];
     const int rc = m <= 64 ? load_reg_pool(tab, K, lp_row, lp_level, lp_dur, c.lp_off, m, lane, st, P) : 2;
     if (rc != 0) {  // invalid level (flagged; pass 2 flags it again) or not for this pass
       if (lane == 0) out[s].n_tail = kDeferred;
@@ -788,15 +785,16 @@ __global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 war
     DigestBatch db;
     P.fg0 = P.fg1 = -1;
     HpOut o = replay_hp_reg(P, tab, K, hp_row, hp_dur, hp_gap, c, prm, sched, fill_gap, lp_start, so, db, lane);
-    {  // fills: the requests with a gap index, summed from their owning lanes
-      const bool f0 = P.fg0 >= 0 && (uint32_t)lane < m, f1 = P.fg1 >= 0 && 32u + (uint32_t)lane < m;
-      o.n_fills = __popc(__ballot_sync(0xffffffffu, f0)) + __popc(__ballot_sync(0xffffffffu, f1));
+    const uint64_t picked = P.picked_mask();
+    const bool f0 = (picked >> lane) & 1ull, f1 = (picked >> (32 + lane)) & 1ull;
+    {  // fills: the picked requests, summed from their owning lanes
+      o.n_fills = __popc((uint32_t)picked) + __popc((uint32_t)(picked >> 32));
       uint64_t fw = (f0 ? (uint64_t)P.dur0 : 0ull) + (f1 ? (uint64_t)P.dur1 : 0ull);
 #pragma unroll
       for (int off2 = 16; off2; off2 >>= 1) fw += __shfl_xor_sync(0xffffffffu, fw, off2);
       o.fill_work = fw;
     }
-    P.alive &= ~P.picked_mask();
+    P.alive &= ~picked;
     uint32_t lv = 0;  // levels still queued
     if ((P.alive >> lane) & 1ull) lv |= 1u << P.lvl0;
     if ((P.alive >> (32 + lane)) & 1ull) lv |= 1u << P.lvl1;
@@ -807,7 +805,19 @@ __global__ void __launch_bounds__(kRegWarps * 32, 2)  // <= 64 registers: 32 war
         [&](uint32_t k, uint32_t L) { return ((P.alive >> k) & 1ull) && (k < 32 ? P.lvl0 : P.lvl1) == L; },
         [&](uint32_t k) { return k < 32 ? P.dur0 : P.dur1; }, sched, fill_gap, lp_start, so, P, n_tail, lane);
     // every request ran (fill or tail): its digest term from its owning lane
+    __syncwarp();  // (lane 0's log stores -> the owning lanes)
     uint64_t dig = 0;
+    if (f0) {
+      const uint4 x = P.log[lane];
+      P.fg0 = (int32_t)x.x;
+      P.st0 = (uint64_t)x.y | ((uint64_t)x.z << 32);
+    }
+    if (f1) {
+      const uint4 x = P.log[32 + lane];
+      P.fg1 = (int32_t)x.x;
+      P.st1 = (uint64_t)x.y | ((uint64_t)x.z << 32);
+    }
+    __syncwarp();  // (the reads, before the next scenario's stores)
     if ((uint32_t)lane < m) dig += digest_term((uint32_t)lane, P.fg0, P.st0);
     if (32u + (uint32_t)lane < m) dig += digest_term(32u + (uint32_t)lane, P.fg1, P.st1);
     write_result(out, s, o, t, m, n_tail, db, dig, lane);
