@@ -504,6 +504,14 @@ __device__ __forceinline__ uint64_t warp_inclusive_scan(uint64_t v, int lane) {
   return x;
 }
 
+// warp sum of u64 values (all lanes): one REDUX when every value is < 2^27 (the common case)
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+  if (__all_sync(0xffffffffu, v < (1ull << 27))) return __reduce_add_sync(0xffffffffu, (uint32_t)v);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
 struct HpOut {
   uint64_t t, hp_delay, fill_work, lp_end;
   uint32_t n_fills;
@@ -514,7 +522,9 @@ struct HpOut {
 // open (p >= tau, p >= qmin, and with feedback a' > 0) need the serial Alg. 1 loop, so each
 // chunk of 32 HP kernels is advanced by a prefix sum and visits just its open gates.  The next
 // chunk's inputs are loaded while this one is processed.
-template <class GateMin, class Fill>
+// kLazyScan: a chunk without an open gate advances t by its REDUX total, skipping the prefix
+// scan (off for the STREAM model: its larger fill then spills)
+template <bool kLazyScan = true, class GateMin, class Fill>
 __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, const fikit_table_t& tab, uint32_t K,
                                                 const uint32_t* __restrict__ hp_row,
                                                 const uint64_t* __restrict__ hp_dur,
@@ -548,9 +558,13 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
     const uint64_t p_l = (valid && r_l < K) ? ((__ldg(tab.mean + (size_t)r_l * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
     if (base + 32 < nh) ld(base + 32, dn, gn, rn);
     const uint64_t x_l = d_l + a_l;
-    const uint64_t X = warp_inclusive_scan(x_l, lane);  // prefix over the chunk
     const bool gate = valid && !last && p_l >= prm.threshold_ns && (!prm.feedback || a_l > 0);
     uint32_t gmask = __ballot_sync(0xffffffffu, gate && p_l >= gate_min());
+    if (kLazyScan && !gmask) {  // no gate opens in this chunk (the common case): only its total advances t
+      t += warp_sum_u64(x_l);
+      continue;
+    }
+    const uint64_t X = warp_inclusive_scan(x_l, lane);  // prefix over the chunk
     const uint64_t T0 = t;
     uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
     while (gmask) {
@@ -1128,7 +1142,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 5)  // <= 102 registers: 20
       lp_end = max(lp_end, t);
     }
     if (prm.feedback) gmin = heads_min();
-    HpOut o = replay_hp_core([&]() { return gmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane,
+    HpOut o = replay_hp_core<false>([&]() { return gmin; }, fill, tab, K, hp_row, hp_dur, hp_gap, c, prm, lane,
                              t > Ta ? t : Ta);
     // tail (R31)
     t = o.t;
