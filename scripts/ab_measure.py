@@ -17,7 +17,9 @@ sys.path.insert(0, ROOT)
 
 def build(specs):
     for spec in specs:
+        # name=rev[+DEFINE[+DEFINE...]]; rev "." = the working tree
         name, rev = spec.split("=")
+        rev, *defs = rev.split("+")
         d = os.path.join(AB, name)
         src = os.path.join(d, "src")
         os.makedirs(os.path.join(src, "paper_2311_10359_b200", "csrc"), exist_ok=True)
@@ -25,13 +27,14 @@ def build(specs):
         files = ["paper_2311_10359_b200/csrc/" + f for f in
                  ("measure.cu", "finalize.cu", "replay.cu", "capi.cu", "fikit_internal.cuh")] + ["include/fikit.h"]
         for f in files:
-            data = subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:{f}"])
+            data = (open(os.path.join(ROOT, f), "rb").read() if rev == "." else
+                    subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:{f}"]))
             open(os.path.join(src, f), "wb").write(data)
         objs = []
         for f in ("measure.cu", "finalize.cu", "replay.cu", "capi.cu"):
             o = os.path.join(d, f + ".o")
             subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
-                                   "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+                                   "-std=c++17", "-Xcompiler", "-fPIC", *[f"-D{x}" for x in defs], "-c",
                                    os.path.join(src, "paper_2311_10359_b200", "csrc", f), "-o", o])
             objs.append(o)
         subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
@@ -70,6 +73,8 @@ def run(records, workload="zipf"):
                                           C.POINTER(fk.TableC), C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                           C.c_void_p, C.c_void_p]
         L.fikit_get_status.argtypes = [C.c_void_p, C.POINTER(fk.StatusC), C.c_void_p]
+        L.fikit_table_finalize.argtypes = [C.POINTER(fk.TableC), C.c_void_p, C.c_uint64, C.c_void_p, C.c_size_t,
+                                           C.c_void_p]
         cap = 8192
         wsb = L.fikit_ws_bytes(cap, names.count, sigs.count, n)
         ws = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
@@ -95,6 +100,11 @@ def run(records, workload="zipf"):
         st = fk.StatusC()
         v[1].fikit_get_status(C.c_void_p(v[3]), C.byref(st), stream)
         out[v[0]] = {"ms": [], "kernel_ms": [], "status": st.code, "rows": st.n_rows_needed}
+        # the finalized table must be identical across variants (bytes of the whole table block)
+        v[1].fikit_table_finalize(C.byref(v[6]), None, 0, C.c_void_p(v[3]), v[4], stream)
+        torch.cuda.synchronize()
+        blk = v[5].cpu().numpy()
+        out[v[0]]["table_equal_first"] = bool(np.array_equal(blk, variants[0][5].cpu().numpy()))
     if os.environ.get("AB_ONCE"):  # for an ncu launch list: 3 calls each only
         return out
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

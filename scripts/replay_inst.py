@@ -30,7 +30,7 @@ for spec in sys.argv[1:]:
     last = [launches[i] for i in ids[-2:]]
     inst = sum(x["smsp__inst_executed.sum"] for x in last)
     out[wl] = {"warp_inst_per_scenario": inst / int(S), "kernels": [x["kernel"] for x in last],
-               "ncu_us": [x.get("gpu__time_duration.sum") for x in last],
+               "ncu_ns": [x.get("gpu__time_duration.sum") for x in last],
                "source": f"ncu smsp__inst_executed.sum, {os.path.basename(path)} (last step's replay launches)"}
     print(wl, out[wl])
 json.dump(out, open(out_p, "w"), indent=1)
