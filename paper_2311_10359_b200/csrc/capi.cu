@@ -417,10 +417,10 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
   // rows per scatter block: one wave of <= num_sms() blocks, at least 64 rows each
   uint32_t R = (cap + num_sms() - 1) / num_sms();
   R = R < 64 ? 64 : R > 4096 ? 4096 : (R + 31) / 32 * 32;
-  const size_t fsm = sizeof(FinKey) * (kFinChunk + (size_t)R) + 4ull * R;  // chunk + row keys + ranks
+  const size_t fsm = (sizeof(FinKey) + 4) * (size_t)R;  // row keys + ranks
   if (dev_prop(kPropFinAttr, [&](int) {
         return cudaFuncSetAttribute(k_fin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(sizeof(FinKey) * (kFinChunk + 4096) + 4 * 4096)) == cudaSuccess
+                                    (int)((sizeof(FinKey) + 4) * 4096)) == cudaSuccess
                    ? 1
                    : -1;
       }) < 0)

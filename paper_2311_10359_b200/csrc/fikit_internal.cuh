@@ -85,7 +85,6 @@ constexpr uint32_t kPlanStamp = kBuckets + 6;  // (u64, words 70-71) dictionary 
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
 constexpr uint32_t kFinGroup = 256;     // fikit_table_finalize: keys per sorted group (a warp's)
-constexpr uint32_t kFinChunk = 8192;    // ... sorted keys staged in shared memory at a time (128 KB)
 struct FinKey {                          // a sorted key of finalize's groups (workspace)
   unsigned long long kid;
   uint32_t task, pad;

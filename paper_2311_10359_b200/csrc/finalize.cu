@@ -21,8 +21,10 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
 //   k_fin_sort     one 128-thread block per group of kFinGroup = 256 keys: a shared-memory bitonic
 //                  sort (one compare-exchange per thread and stage), the sorted group to the workspace.
 //   k_fin_scatter  block b owns rows [b R, (b + 1) R): a row's rank is the sum over the sorted
-//                  groups of the keys below it (the groups staged in shared memory 8192 keys at a
-//                  time, one 8-step binary search per row and group); then the block writes its
+//                  groups of the keys below it (one branch-free 9-step binary search per row and
+//                  group in the L2-resident sorted keys, four groups interleaved per thread; staging
+//                  every group in each block's shared memory had cost more than the searches, and
+//                  the search loop 4 M warp-instructions per 8192 rows); then the block writes its
 //                  rows into the caller's table at their ranks, a warp per half row (32 histogram
 //                  bins: the count is their sum), with the sums, extremes and
 //                  SK_j / SG_j (R8).
@@ -76,47 +78,47 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
                                                      uint32_t* __restrict__ rank, const uint32_t* __restrict__ misc) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char fin_sm[];
-  FinKey* gk = reinterpret_cast<FinKey*>(fin_sm);              // [kFinChunk]
-  FinKey* rk = gk + kFinChunk;                                 // [R] this block's row keys
+  FinKey* rk = reinterpret_cast<FinKey*>(fin_sm);              // [R] this block's row keys
   uint32_t* srank = reinterpret_cast<uint32_t*>(rk + R);       // [R]
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
   const uint32_t r0 = blockIdx.x * R;
   if (r0 >= K) return;
   const uint32_t nr = min(R, K - r0), tid = threadIdx.x;
+  const bool dict = misc[kMiscDict] != 0u;  // dictionary mode: rank = row
   for (uint32_t i = tid; i < nr; i += blockDim.x) {
-    srank[i] = 0;
+    srank[i] = dict ? r0 + i : 0u;
     rk[i] = FinKey{raw[r0 + i].kid, raw[r0 + i].task, 0u};
   }
-  const bool dict = misc[kMiscDict] != 0u;  // dictionary mode: rank = row
-  if (dict)
-    for (uint32_t i = tid; i < nr; i += blockDim.x) srank[i] = r0 + i;
-  for (uint32_t c0 = 0; c0 < (dict ? 0u : K); c0 += kFinChunk) {
-    const uint32_t mc = min(kFinChunk, K - c0);
-    __syncthreads();  // (the previous chunk's searches are done)
-    for (uint32_t i = tid; i < mc; i += blockDim.x) {
-      const uint32_t d = smem_u32(gk + i);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(skeys + c0 + i) : "memory");
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    const uint32_t ng = (mc + kFinGroup - 1) / kFinGroup;
-    // consecutive lanes take consecutive rows of ONE group (a lane per group would put the whole
-    // warp's probes 4 KB apart: one bank, 32-way conflicts)
-    for (uint32_t it = tid; it < nr * ng; it += blockDim.x) {
-      const uint32_t g = it / nr, i = it - g * nr;
-      const FinKey* grp = gk + g * kFinGroup;
-      const uint32_t m = min(kFinGroup, mc - g * kFinGroup);
-      const uint64_t mk = rk[i].kid;
-      const uint32_t mt = rk[i].task;
-      uint32_t lo = 0, hi = m;  // keys of group g below (mt, mk)
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (fin_less(grp[mid].task, grp[mid].kid, mt, mk))
-          lo = mid + 1;
-        else
-          hi = mid;
+  __syncthreads();
+  if (!dict) {
+    // rank = the keys below the row's in every sorted group: Q threads per row, each a share of the
+    // groups, four groups' branch-free binary searches interleaved (9 steps each: 16-B loads of the
+    // L2-resident sorted keys; positions past a partial last group read as +infinity)
+    const uint32_t ng = (K + kFinGroup - 1) / kFinGroup;
+    const uint32_t Q = max(1u, (uint32_t)blockDim.x / nr);
+    for (uint32_t it = tid; it < nr * Q; it += blockDim.x) {
+      const uint32_t i = it / Q, q = it - i * Q;
+      const uint64_t xk = rk[i].kid;
+      const uint32_t xt = rk[i].task;
+      uint32_t below = 0;
+      for (uint32_t g0 = q * 4; g0 < ng; g0 += Q * 4) {
+        uint32_t lo[4] = {0u, 0u, 0u, 0u}, m[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) m[u] = g0 + u < ng ? min(kFinGroup, K - (g0 + u) * kFinGroup) : 0u;
+#pragma unroll
+        for (uint32_t half = kFinGroup; half; half >>= 1) {  // (9 steps: 257 possible counts)
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const uint32_t idx = lo[u] + half - 1;
+            if (idx < m[u]) {
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(skeys + (size_t)(g0 + u) * kFinGroup + idx));
+              if (fin_less(v.z, ((uint64_t)v.y << 32) | v.x, xt, xk)) lo[u] += half;
+            }
+          }
+        }
+        below += lo[0] + lo[1] + lo[2] + lo[3];
       }
-      if (lo) atomicAdd(&srank[i], lo);
+      if (below) atomicAdd(&srank[i], below);
     }
   }
   __syncthreads();

@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 def build(specs):
     for spec in specs:
         # name=rev[+DEFINE[+DEFINE...]]; rev "." = the working tree
-        name, rev = spec.split("=")
+        name, rev = spec.split("=", 1)
         rev, *defs = rev.split("+")
         d = os.path.join(AB, name)
         src = os.path.join(d, "src")
@@ -118,7 +118,20 @@ def run(records, workload="zipf"):
             torch.cuda.synchronize()
             out[v[0]]["ms"].append(e0.elapsed_time(e1) / 10)
             out[v[0]]["kernel_ms"].append(k0.elapsed_time(k1))  # (the last call's k_measure)
+    # fikit_table_finalize alone (re-runnable: it reads the workspace's measured rows), interleaved
+    for v in variants:
+        call(v)
+        out[v[0]]["fin_ms"] = []
+    for rep in range(7):
+        for v in variants:
+            e0.record()
+            for _ in range(20):
+                v[1].fikit_table_finalize(C.byref(v[6]), None, 0, C.c_void_p(v[3]), v[4], stream)
+            e1.record()
+            torch.cuda.synchronize()
+            out[v[0]]["fin_ms"].append(e0.elapsed_time(e1) / 20)
     for name, r in out.items():
+        r["fin_ms"] = min(r["fin_ms"])
         r["ms"], r["kernel_ms"] = min(r["ms"]), float(np.median(r["kernel_ms"]))
         r["GBps_call"] = 48 * n / r["ms"] / 1e6
         r["GBps_kernel"] = 48 * n / r["kernel_ms"] / 1e6
