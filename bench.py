@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-configs2", action="store_true",
                     help="skip the configs[2] (BERT/VGG 100k-scenario replay) leg of the default line")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every timed step's calls directly instead of replaying a CUDA graph of them")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -555,12 +557,18 @@ def main():
     stage_ms = np.zeros(4)
 
     # k_measure alone, live in every timed step: one event pair per step (fikit_measure_timed)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # (external: inside a captured step graph they are event-record nodes that time every replay)
+    kev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in range(args.steps)]
     for a, b in kev:  # (torch creates the CUDA events on first record)
         a.record(stream)
         b.record(stream)
     # the replay call alone (fikit_simulate_batch: its two kernels), live in every timed step
-    rev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    rev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in range(args.steps)]
+    for a, b in rev:
+        a.record(stream)
+        b.record(stream)
 
     # dictionary mode (repeated services keep their kernel IDs): the first
     # warm-up step measures and merges with the general path; its (merged) table's keys become the
@@ -633,6 +641,24 @@ def main():
     sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)] \
         if flush is not None else None
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # 1 GPU: every timed step is the replay of a CUDA graph captured from the same calls (one graph per
+    # step: each holds its own k_measure / replay event pairs).  The library's launch counter counts
+    # at capture, so the step's launches are counted there.  (N > 1 keeps direct launches: its
+    # merge runs torch.distributed collectives between the calls.)
+    graphs = None
+    launches_per_graph = 0
+    if world == 1 and not args.no_graph:
+        graphs = []
+        for i in range(args.steps):
+            g = torch.cuda.CUDAGraph()
+            l0 = fk.launch_count()
+            with torch.cuda.graph(g):
+                step(False, kev[i], spair=rev[i] if p.replay else None)
+            launches_per_graph = fk.launch_count() - l0
+            graphs.append(g)
+        for g in graphs[:2]:  # (first replays upload the graph; their results are the same step's)
+            g.replay()
+        torch.cuda.synchronize()
     launches0 = fk.launch_count()
     with ClockSampler(dev_index) as clk:
         if world > 1:
@@ -643,7 +669,10 @@ def main():
             if flush is not None:
                 flush.zero_()
                 sev[i][0].record(stream)
-            step(False, kev[i], spair=rev[i] if p.replay else None)
+            if graphs is not None:
+                graphs[i].replay()
+            else:
+                step(False, kev[i], spair=rev[i] if p.replay else None)
             if flush is not None:
                 sev[i][1].record(stream)
         t1.record(stream)
@@ -654,7 +683,7 @@ def main():
     l2_note = (f"inputs ({in_bytes / 1e6:.0f} MB) larger than 2x the 126 MB L2: steps back to back, no flush"
                if flush is None else f"inputs ({in_bytes / 1e6:.1f} MB) fit the L2: a {L2_FLUSH_BYTES >> 20} MB "
                f"write flushes L2 before every step (outside the step's event pair)")
-    launches = fk.launch_count() - launches0
+    launches = fk.launch_count() - launches0 + (launches_per_graph * args.steps if graphs is not None else 0)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -697,6 +726,8 @@ def main():
                                  + ("; plan reused" if plan_ready[0] else "") + ")"
                                  if dict_state is not None else "none (1 GPU)"),
                        "l2": l2_note,
+                       "launch": (f"CUDA graph per step ({launches_per_graph} libfikit kernels, captured after warm-up)"
+                                  if graphs is not None else "direct launches"),
                        "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},
             "scenarios_per_s": (S_total / (ms * 1e-3)) if S_total else None,
             "stages_ms": {"measure": stage_ms[0], "finalize+merge": stage_ms[1], "resolve+replay": stage_ms[2]},

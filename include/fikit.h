@@ -25,6 +25,9 @@
  *    opt-in), computed idempotently and published atomically, and (b) the
  *    launch counter (fikit_launch_count).  Calls on different streams (or
  *    devices, or host threads) with distinct workspaces may run concurrently.
+ *    No call synchronises the host or allocates, so a sequence of calls can
+ *    be captured into a CUDA graph (cudaStreamBeginCapture) and replayed; the
+ *    launch counter counts launches at capture, not at replay.
  *  - The return value is a HOST status checked before any launch:
  *    FIKIT_OK, FIKIT_E_ARG (null / misaligned pointer, n >= 2^32, workspace
  *    too small) or FIKIT_E_CUDA (launch failure).
@@ -223,7 +226,9 @@ int fikit_table_finalize(const fikit_table_t* tab, uint32_t* out_row, uint64_t n
 
 /* fikit_measure, instrumented: ev_start / ev_stop (cudaEvent_t, created by the caller, may
  * be null) are recorded on `stream` just before and after the fused streaming kernel
- * (k_measure), so a benchmark can time the dominant kernel alone inside a live step. */
+ * (k_measure), so a benchmark can time the dominant kernel alone inside a live step.  Inside a
+ * stream capture they are recorded as external event nodes (cudaEventRecordExternal), so they
+ * time the kernel on every replay of the captured graph. */
 int fikit_measure_timed(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo_next,
                         fikit_strtab_t names, fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row,
                         void* ws, size_t ws_bytes, void* stream, void* ev_start, void* ev_stop);

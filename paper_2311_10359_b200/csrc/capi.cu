@@ -243,6 +243,16 @@ int fikit_identify(const fikit_record_t* recs, uint64_t n, fikit_strtab_t names,
   return launched();
 }
 
+// the caller's timing events: inside a stream capture they become external event-record nodes, so
+// they still time the kernel on every replay of the graph (a plain record there is only an
+// internal dependency)
+static bool record_ev(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) return false;
+  return (cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                              : cudaEventRecord(ev, s)) == cudaSuccess;
+}
+
 static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_record_t* halo, fikit_strtab_t names,
                         fikit_strtab_t sigs, const fikit_table_t* tab, uint32_t* out_row, void* ws,
                         size_t ws_bytes, void* stream, cudaEvent_t ev0, cudaEvent_t ev1,
@@ -355,13 +365,13 @@ static int measure_impl(const fikit_record_t* recs, uint64_t n, const fikit_reco
                    : -1;
       }) < 0)
     return FIKIT_E_CUDA;
-  if (ev0 && cudaEventRecord(ev0, s) != cudaSuccess) return FIKIT_E_CUDA;
+  if (ev0 && !record_ev(ev0, s)) return FIKIT_E_CUDA;
   launch_pdl(k_measure, grid, measure_threads(), smem, s, 
       recs, n, halo, w.name_hash(), w.sig_hash(), names.count, sigs.count, w.index(), w.L.slots, w.tindex(),
       w.L.tslots, w.st(), RawTab{w.raw(), cap}, w.row_tuple(), w.hot(), w.hot_n(), w.cur(), w.act(), w.bstart(),
       w.btot(), w.first(), w.order(), w.grp_bucket(), ntiles, out_row, dict ? 1u : 0u);
   if (int r = launched()) return r;
-  if (ev1 && cudaEventRecord(ev1, s) != cudaSuccess) return FIKIT_E_CUDA;
+  if (ev1 && !record_ev(ev1, s)) return FIKIT_E_CUDA;
   return FIKIT_OK;
 }
 
