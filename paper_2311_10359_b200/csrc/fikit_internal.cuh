@@ -84,7 +84,7 @@ constexpr uint32_t kSampN = kBuckets + 4;  // distinct identities in the launch 
 constexpr uint32_t kPlanStamp = kBuckets + 6;  // (u64, words 70-71) dictionary hash the hot sets were built on
 constexpr uint32_t kHotHdr = kBuckets + 8;
 constexpr uint32_t kTileLaunches = 64;  // launches per warp-tile of the measure kernel (one TMA)
-constexpr uint32_t kFinGroup = 256;     // fikit_table_finalize: keys per sorted group (a warp's)
+constexpr uint32_t kFinGroup = 2048;    // fikit_table_finalize: keys per sorted group (one 1024-thread block's)
 struct FinKey {                          // a sorted key of finalize's groups (workspace)
   unsigned long long kid;
   uint32_t task, pad;

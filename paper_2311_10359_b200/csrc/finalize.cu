@@ -18,10 +18,11 @@ __device__ __forceinline__ uint64_t mean_half_up(uint64_t sum, uint64_t cnt) {
 
 // fikit_table_finalize in two launches.  The canonical row of measured row r (R11) is its rank
 // among the K distinct (task, kernel ID) keys.
-//   k_fin_sort     one 128-thread block per group of kFinGroup = 256 keys: a shared-memory bitonic
-//                  sort (one compare-exchange per thread and stage), the sorted group to the workspace.
+//   k_fin_sort     one block per group of G keys (G = 256 for tables of <= 8192 rows, else kFinGroup =
+//                  2048): a shared-memory bitonic sort (G / 2 threads, one compare-exchange per thread
+//                  and stage), the sorted group to the workspace.
 //   k_fin_scatter  block b owns rows [b R, (b + 1) R): a row's rank is the sum over the sorted
-//                  groups of the keys below it (one branch-free 9-step binary search per row and
+//                  groups of the keys below it (one branch-free (log2 G + 1)-step binary search per row and
 //                  group in the L2-resident sorted keys, four groups interleaved per thread; staging
 //                  every group in each block's shared memory had cost more than the searches, and
 //                  the search loop 4 M warp-instructions per 8192 rows); then the block writes its
@@ -33,21 +34,21 @@ __device__ __forceinline__ bool fin_less(uint32_t ta, uint64_t ka, uint32_t tb, 
   return (ta < tb) | ((ta == tb) & (ka < kb));  // (branch-free: the sort network selects, never branches)
 }
 
-__global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t* __restrict__ st,
-                                                            const RawRow* __restrict__ raw, uint32_t cap,
-                                                            fikit_table_t tab, FinKey* __restrict__ skeys,
-                                                            const uint32_t* __restrict__ misc) {
+template <uint32_t G>  // keys per sorted group (256 up to 8192 rows, kFinGroup above)
+__device__ __forceinline__ void fin_sort_body(const fikit_status_t* __restrict__ st, const RawRow* __restrict__ raw,
+                                              uint32_t cap, fikit_table_t tab, FinKey* __restrict__ skeys,
+                                              const uint32_t* __restrict__ misc) {
   pdl_entry();
-  __shared__ uint64_t sk[kFinGroup];
-  __shared__ uint32_t stk[kFinGroup];
+  __shared__ uint64_t sk[G];
+  __shared__ uint32_t stk[G];
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0) *tab.n_rows = K;
   if (misc[kMiscDict]) return;  // dictionary mode: the rows are already canonical
-  const uint32_t g0 = blockIdx.x * kFinGroup;
+  const uint32_t g0 = blockIdx.x * G;
   if (g0 >= K) return;
-  const uint32_t m = min(kFinGroup, K - g0);
-  for (uint32_t i = tid; i < kFinGroup; i += blockDim.x) {
+  const uint32_t m = min(G, K - g0);
+  for (uint32_t i = tid; i < G; i += blockDim.x) {
     const bool in = i < m;
     sk[i] = in ? raw[g0 + i].kid : ~0ull;  // padding sorts last
     stk[i] = in ? raw[g0 + i].task : 0xFFFFFFFFu;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t
   __syncthreads();
   // bitonic network: one compare-exchange per thread and stage (branch-free selects)
 #pragma unroll
-  for (uint32_t kk = 2; kk <= kFinGroup; kk <<= 1)
+  for (uint32_t kk = 2; kk <= G; kk <<= 1)
 #pragma unroll
     for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
       const uint32_t a = ((tid & ~(j - 1)) << 1) | (tid & (j - 1)), b = a + j;
@@ -71,10 +72,21 @@ __global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t
     }
   for (uint32_t i = tid; i < m; i += blockDim.x) skeys[g0 + i] = FinKey{sk[i], stk[i], 0u};
 }
+__global__ void __launch_bounds__(128) k_fin_sort256(const fikit_status_t* __restrict__ st,
+                                                   const RawRow* __restrict__ raw, uint32_t cap, fikit_table_t tab,
+                                                   FinKey* __restrict__ skeys, const uint32_t* __restrict__ misc) {
+  fin_sort_body<256>(st, raw, cap, tab, skeys, misc);
+}
+__global__ void __launch_bounds__(kFinGroup / 2) k_fin_sort(const fikit_status_t* __restrict__ st,
+                                                            const RawRow* __restrict__ raw, uint32_t cap,
+                                                            fikit_table_t tab, FinKey* __restrict__ skeys,
+                                                            const uint32_t* __restrict__ misc) {
+  fin_sort_body<kFinGroup>(st, raw, cap, tab, skeys, misc);
+}
 
 __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __restrict__ st,
                                                      const RawRow* __restrict__ raw, uint32_t cap, uint32_t R,
-                                                     const FinKey* __restrict__ skeys, fikit_table_t tab,
+                                                     const FinKey* __restrict__ skeys, uint32_t G, fikit_table_t tab,
                                                      uint32_t* __restrict__ rank, const uint32_t* __restrict__ misc) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char fin_sm[];
@@ -92,9 +104,9 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
   __syncthreads();
   if (!dict) {
     // rank = the keys below the row's in every sorted group: Q threads per row, each a share of the
-    // groups, four groups' branch-free binary searches interleaved (9 steps each: 16-B loads of the
+    // groups, four groups' branch-free binary searches interleaved (log2 G + 1 steps each: 16-B loads of the
     // L2-resident sorted keys; positions past a partial last group read as +infinity)
-    const uint32_t ng = (K + kFinGroup - 1) / kFinGroup;
+    const uint32_t ng = (K + G - 1) / G;
     const uint32_t Q = max(1u, (uint32_t)blockDim.x / nr);
     for (uint32_t it = tid; it < nr * Q; it += blockDim.x) {
       const uint32_t i = it / Q, q = it - i * Q;
@@ -104,14 +116,14 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
       for (uint32_t g0 = q * 4; g0 < ng; g0 += Q * 4) {
         uint32_t lo[4] = {0u, 0u, 0u, 0u}, m[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) m[u] = g0 + u < ng ? min(kFinGroup, K - (g0 + u) * kFinGroup) : 0u;
+        for (int u = 0; u < 4; u++) m[u] = g0 + u < ng ? min(G, K - (g0 + u) * G) : 0u;
 #pragma unroll
-        for (uint32_t half = kFinGroup; half; half >>= 1) {  // (9 steps: 257 possible counts)
+        for (uint32_t half = G; half; half >>= 1) {  // (log2 G + 1 steps: G + 1 possible counts)
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const uint32_t idx = lo[u] + half - 1;
             if (idx < m[u]) {
-              const uint4 v = __ldg(reinterpret_cast<const uint4*>(skeys + (size_t)(g0 + u) * kFinGroup + idx));
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(skeys + (size_t)(g0 + u) * G + idx));
               if (fin_less(v.z, ((uint64_t)v.y << 32) | v.x, xt, xk)) lo[u] += half;
             }
           }
