@@ -1111,6 +1111,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   uint32_t nsz = kClaim;                       // lane 0: size of the next range
   auto claim = [&]() {   // lane 0
     pc = kNone;
+#ifndef FIKIT_ADDR_DYNAMIC
+    if (!by_task) {  // address order: the warp's static share [q_pos, q_end) (no claims, no tail skew)
+      if (q_pos < q_end) pc = q_pos++;
+      return;
+    }
+#endif
     if (q_pos >= q_end) {
       if (nx == kNone || nx >= cb_end) return;  // drained (claims are monotone)
       q_pos = nx;
@@ -1345,6 +1351,17 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     cb_base = by_task ? kGroupTiles * bstart[cb] : 0u;
     q_pos = q_end = 0;
     nsz = 1u;  // (the first range: one tile, the pipeline then sizes the next from its position)
+#ifndef FIKIT_ADDR_DYNAMIC
+    if (!by_task) {
+      // Address order: every warp of the grid takes a static contiguous share of the tiles (+-1
+      // tile).  Claiming from one counter shared by all 3552 warps needed multi-tile claims to keep
+      // the atomic rate down, and a warp holding a multi-tile claim at the end kept its CTA ~13 us
+      // past the others (ResNet-like 3M: phase tail 13 us of a 48 us kernel).
+      const uint64_t gw = (uint64_t)blockIdx.x * mk::WARPS + (uint64_t)warp, W = (uint64_t)gridDim.x * mk::WARPS;
+      q_pos = (uint32_t)((uint64_t)ntiles * gw / W);
+      q_end = (uint32_t)((uint64_t)ntiles * (gw + 1) / W);
+    } else
+#endif
     if (lane == 0) nx = atomicAdd(cur + cb, 1u);
     // prime the pipeline: the first tile's TMA, the second tile's order[] load, a third claim
     bool staged = false;  // (all lanes) a tile is in flight to the stage
@@ -1418,6 +1435,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
     flush_hot_set_ext();
     if (tid == 0) atomicSub(act + cb, 1u);  // every claim of cb is done
+#ifndef FIKIT_ADDR_DYNAMIC
+    if (!by_task) break;  // (address order: the static shares cover every tile)
+#endif
     cb = pick_bucket();  // (its barriers also keep the shared rows until every warp is done)
     FK_TR(if (tid == 0) FK_TR_ADD(7, gtime() - tr_t0);)
   }

@@ -89,4 +89,10 @@ for arg in sys.argv[2:] or ["12500000"]:
                         f"{us(np.median(r[:, 3] - r[:, 2]))} resolve {us(np.median(r[:, 4] - r[:, 3]))}"
                         f" (max {us((r[:, 4] - r[:, 3]).max())})")
             print(msg)
+            if role == 10:  # the slowest hot blocks (block 64 = the global set): start, hist+T, choose, resolve
+                idx = np.where(qb[:, 7] == role)[0]
+                slow = idx[np.argsort(qb[idx, 4])[-4:]]
+                print("     slowest hot blocks (block: end, hist+T, choose, resolve us): " + "; ".join(
+                    f"{b}: {us(qb[b, 4] - base)}, {us(qb[b, 2] - qb[b, 0])}, {us(qb[b, 3] - qb[b, 2])}, "
+                    f"{us(qb[b, 4] - qb[b, 3])}" for b in slow))
     print(f"   k_measure entry at {us(t0 - base)} us after the first k_prep block started")
