@@ -558,13 +558,18 @@ __device__ __forceinline__ HpOut replay_hp_core(GateMin gate_min, Fill fill, con
     const uint64_t p_l = (valid && r_l < K) ? ((__ldg(tab.mean + (size_t)r_l * 2 + 1) * scale) >> 16) : 0;  // SG (Alg.1 3-5, R12)
     if (base + 32 < nh) ld(base + 32, dn, gn, rn);
     const uint64_t x_l = d_l + a_l;
+    // prefix over the chunk: issued before the gate ballot when it is always needed (no lazy path), so
+    // it overlaps the SG load the ballot waits on (after the ballot it cost the STREAM model's
+    // exclusive arm, whose gates never open, 11 %: ratio workload 5.00 -> 5.57 ms)
+    uint64_t X = 0;
+    if constexpr (!kLazyScan) X = warp_inclusive_scan(x_l, lane);
     const bool gate = valid && !last && p_l >= prm.threshold_ns && (!prm.feedback || a_l > 0);
     uint32_t gmask = __ballot_sync(0xffffffffu, gate && p_l >= gate_min());
     if (kLazyScan && !gmask) {  // no gate opens in this chunk (the common case): only its total advances t
       t += warp_sum_u64(x_l);
       continue;
     }
-    const uint64_t X = warp_inclusive_scan(x_l, lane);  // prefix over the chunk
+    if constexpr (kLazyScan) X = warp_inclusive_scan(x_l, lane);
     const uint64_t T0 = t;
     uint64_t shift = 0;  // delays imposed by fills earlier in this chunk
     while (gmask) {

@@ -60,6 +60,11 @@ class Pipeline:
         dev = self.device
         nh, nl = int(rp.hp_records.shape[0]), int(rp.lp_records.shape[0])
         S = int(rp.scenarios.shape[0])
+        # HP and LP launches resolved by ONE fikit_resolve call over their concatenation (one launch
+        # instead of two) when that is exact: the last HP launch then has a next launch, so its
+        # gap must stay 0 -- a different (task, run) than the first LP launch guarantees it (R5)
+        both = (nh > 0 and nl > 0 and (int(rp.hp_records["task_id"][-1]) != int(rp.lp_records["task_id"][0])
+                                        or int(rp.hp_records["run_id"][-1]) != int(rp.lp_records["run_id"][0])))
         r = {
             "nh": nh, "nl": nl, "S": S, "threshold_ns": int(rp.threshold_ns), "feedback": int(rp.feedback),
             "hp_recs": records_to_device(rp.hp_records, dev) if nh else torch.zeros(48, dtype=torch.uint8,
@@ -78,6 +83,14 @@ class Pipeline:
             "lp_gap": torch.empty(max(1, nl), dtype=torch.int64, device=dev),
             "out": torch.empty(max(1, S) * 48, dtype=torch.uint8, device=dev),
         }
+        if both:  # one buffer per quantity, the HP / LP arrays are views of it
+            recs = records_to_device(np.concatenate([rp.hp_records, rp.lp_records]), dev)
+            r["recs_both"] = recs
+            r["hp_recs"], r["lp_recs"] = recs[: 48 * nh], recs[48 * nh:]
+            for k, dt in (("row", torch.int32), ("dur", torch.int64), ("gap", torch.int64)):
+                t = torch.empty(nh + nl, dtype=dt, device=dev)
+                r[k + "_both"] = t
+                r["hp_" + k], r["lp_" + k] = t[:nh], t[nh:]
         if want_schedule and S:
             m = rp.scenarios["lp_len"].astype(np.uint64)
             so = np.zeros(S, dtype=np.uint64)
@@ -106,12 +119,17 @@ class Pipeline:
         if self.predictor is not None:
             table_predict(tab, *self.predictor, stream=stream)
         # (the measure call on this workspace hashed these string tables: no re-hashing)
-        resolve(r["hp_recs"], r["nh"], self.names, self.sigs, tab, r["hp_row"], r["hp_dur"], r["hp_gap"],
-                self.ws, stream=stream, reuse_hashes=self.measured)
-        self._chk("resolve(hp)", stream)
-        resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
-                self.ws, stream=stream, reuse_hashes=True)
-        self._chk("resolve(lp)", stream)
+        if "recs_both" in r:
+            resolve(r["recs_both"], r["nh"] + r["nl"], self.names, self.sigs, tab, r["row_both"], r["dur_both"],
+                    r["gap_both"], self.ws, stream=stream, reuse_hashes=self.measured)
+            self._chk("resolve(hp + lp)", stream)
+        else:
+            resolve(r["hp_recs"], r["nh"], self.names, self.sigs, tab, r["hp_row"], r["hp_dur"], r["hp_gap"],
+                    self.ws, stream=stream, reuse_hashes=self.measured)
+            self._chk("resolve(hp)", stream)
+            resolve(r["lp_recs"], r["nl"], self.names, self.sigs, tab, r["lp_row"], r["lp_dur"], r["lp_gap"],
+                    self.ws, stream=stream, reuse_hashes=True)
+            self._chk("resolve(lp)", stream)
         if sim_events is not None:
             sim_events[0].record(stream)
         self._simulate(tab, r["out"], r["threshold_ns"], True, stream)

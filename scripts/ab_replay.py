@@ -43,6 +43,9 @@ VARIANTS = {
     "w4b8": [reg_cfg(4, 8)],  # 32 warps per SM, up to 64 registers
     "w8b4": [reg_cfg(8, 4)],
     "w16b2": [reg_cfg(16, 2)],
+    # the POOL models' HP chunk walk without the lazy (REDUX-total) path: the prefix scan every chunk
+    "eager": [lambda r, h: (sub(r, "template <bool kLazyScan = true, class GateMin, class Fill>",
+                                "template <bool kLazyScan = false, class GateMin, class Fill>"), h)],
 }
 
 
