@@ -1025,11 +1025,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto load_hot_set = [&](uint32_t bkt) {
     const Tuple* hot = hot_all + (size_t)bkt * kHotMax;
     if (tid == 0) {
-#ifdef FIKIT_NO_PRELOAD
-      S.hot_n = 0;
-#else
       S.hot_n = min(hot_n_all[bkt], kHotMax);
-#endif
       S.tq[0] = make_uint4(0u, 0u, 0u, 0u);
       S.tq4[0] = 0u;
     }
