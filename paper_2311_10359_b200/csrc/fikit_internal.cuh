@@ -5,6 +5,23 @@
 
 #include "../../include/fikit.h"
 
+// FK_CHECK: device-side invariant checks of the checked diagnosis build (nvcc -DFIKIT_CHECKS,
+// tests/test_gpu_checked.py: the parity cases rerun on it; a failed check prints and traps, which
+// fails the call).  The product build compiles none of them.
+#ifdef FIKIT_CHECKS
+#include <cstdio>
+#define FK_CHECK(c)                                                                    \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("FIKIT_CHECK failed: %s (%s:%d, block %d thread %d)\n", #c, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                       \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define FK_CHECK(c) ((void)0)
+#endif
+
 namespace fikit {
 
 constexpr uint32_t kStatusArg = 1u, kStatusName = 2u, kStatusRecord = 4u, kStatusCapacity = 8u, kStatusDict = 16u;

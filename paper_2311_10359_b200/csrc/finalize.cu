@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
       const uint32_t h = h0 + u;
       if (h >= nh) break;
       const uint32_t j = h & 1;
+      FK_CHECK(d[u] < K);
       tab.hist[(size_t)d[u] * 64 + 32 * j + lane] = bin[u];
       // row counts < 2^32 (a call measures < 2^32 launches)
       const uint64_t c = __reduce_add_sync(0xffffffffu, bin[u]);

@@ -736,6 +736,7 @@ __device__ __forceinline__ void plan_scatter(const PlanArgs& a, uint32_t k, unsi
     if (b < kBuckets) {
       uint32_t pos = cur[b] + rank;
       for (uint32_t v = 0; v < warp; v++) pos += wcnt[v * kBuckets + b];
+      FK_CHECK(pos < a.ngroups && t < a.ngroups);
       a.order[pos] = t;
     }
     __syncthreads();
@@ -1127,10 +1128,12 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     if (by_task && pc != kNone) {
       const uint32_t p = cb_base + pc;
       tn = __ldg(order + p / kGroupTiles) * kGroupTiles + p % kGroupTiles;
+      FK_CHECK(pc < cb_end && tn < ntiles);
     }
   };
   // 1-D TMA of a tile (+ the next launch) into the warp's stage (lane 0)
   auto issue = [&](uint32_t first) {
+    FK_CHECK(first < n32 && (first & (mk::CH - 1)) == 0u);
     const uint32_t cnt = min((uint32_t)mk::CH + 1, n32 - first);
     mbar_arrive_expect_tx(&S.full[warp], cnt * 48);
     bulk_g2s(S.ring[warp], recs + first, cnt * 48, &S.full[warp]);
@@ -1160,6 +1163,7 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         cold_add(tab, row, 0, pd);
         if (pk5 >> 16) cold_add(tab, row, 1, pg);
       }
+      FK_CHECK(pgi < n32);
       if (out_row) out_row[pgi] = row;
       // admit the row to the shared dictionary while it has room (one lane per distinct row):
       // this CTA's later launches of it are hot.  mk::admit reserves the tag first, so two warps
@@ -1258,7 +1262,9 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     }
   };
   auto update = [&](const Rec& R, int slot) {
+    FK_CHECK(slot >= 0 && (uint32_t)slot < min(S.hot_n, kHotMax));
     const uint32_t rowv = S.grow[slot];  // (loading it here schedules better than on demand)
+    FK_CHECK(rowv < tab.capacity);
     auto row = [&]() { return rowv; };
     const uint32_t hist_e = s_hist + (uint32_t)slot * ((2 * kBins + 1) * 4);
     const uint32_t st_e = s_st + (uint32_t)slot * 20u;

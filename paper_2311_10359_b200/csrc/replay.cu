@@ -246,6 +246,7 @@ __device__ __forceinline__ uint64_t sorted_min_q(uint32_t CM, uint32_t nch, int 
 // and its q; dequeues it (alive bit cleared in both views).
 // ek: the pick's actual duration, its global load issued as soon as the index is known (the
 // dequeue bookkeeping below overlaps its latency)
+__device__ __forceinline__ bool qk_fits(uint64_t q, uint64_t R) { return q <= R; }  // (FK_CHECK: R14)
 __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, uint32_t m, uint32_t& A,
                                          uint32_t& CM, uint32_t nch, uint64_t R, int lane, uint64_t& qk,
                                          const uint64_t* __restrict__ dur, uint64_t& ek, bool epack = false) {
@@ -255,6 +256,7 @@ __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, 
     if (p < 0) return -1;
     const uint64_t x = q[p];  // q << 32 | [e << 10 |] index
     k = (int)(x & 1023u);
+    FK_CHECK((uint32_t)p < m && (uint32_t)k < m && qk_fits(x >> 32, R));
     ek = epack ? ((x >> 10) & 0x3FFFFFull) : __ldg(dur + k);
     qk = x >> 32;
     if (lane == (p >> 5)) A &= ~(1u << (p & 31));
@@ -396,6 +398,7 @@ struct RegPool {
     const uint32_t best = __reduce_min_sync(0xffffffffu, min(c0, c1));
     if (best == 0xFFFFFFFFu) return -1;
     const uint32_t k = best & 63u;
+    FK_CHECK((uint32_t)lane != (k & 31u) || (k < 32u ? pq0 : pq1) != 0xFFFFFFFFu);  // (alive when picked)
     qk = kQ22 - ((best >> 6) & kQ22);
     ek = __shfl_sync(0xffffffffu, k < 32u ? dur0 : dur1, (int)(k & 31u));
     if ((uint32_t)lane == (k & 31u)) {
