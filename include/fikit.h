@@ -25,9 +25,11 @@
  *    opt-in), computed idempotently and published atomically, and (b) the
  *    launch counter (fikit_launch_count).  Calls on different streams (or
  *    devices, or host threads) with distinct workspaces may run concurrently.
- *    No call synchronises the host or allocates, so a sequence of calls can
- *    be captured into a CUDA graph (cudaStreamBeginCapture) and replayed; the
- *    launch counter counts launches at capture, not at replay.
+ *    No call allocates, and none but fikit_get_status (which copies the
+ *    status back and synchronises the stream) synchronises the host, so a
+ *    sequence of the other calls can be captured into a CUDA graph
+ *    (cudaStreamBeginCapture) and replayed; the launch counter counts
+ *    launches at capture, not at replay.
  *  - The return value is a HOST status checked before any launch:
  *    FIKIT_OK, FIKIT_E_ARG (null / misaligned pointer, n >= 2^32, workspace
  *    too small) or FIKIT_E_CUDA (launch failure).
