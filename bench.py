@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every timed step's calls directly instead of replaying a CUDA graph of them")
+    ap.add_argument("--graph-multi", action="store_true",
+                    help="N > 1: replay two CUDA graphs per step around the merge (untested with NCCL: off by "
+                         "default; with gloo on one GPU it measured slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -578,9 +581,8 @@ def main():
     dict_state = None
     plan_ready = [False]  # the workspace holds a dictionary call's plan (FIKIT_MEASURE_REUSE_PLAN)
 
-    def step(timed, kpair=None, checked=False, spair=None):
-        # checked (first warm-up step): the workspace status after EVERY call (each validating
-        # call resets it, so one check at the end would only see the last call)
+    # a step = part A (measure + finalize), the N > 1 merge (collectives), part B (resolve + replay)
+    def part_a(kpair=None, checked=False, timed=False):
         if timed:
             ev[0].record(stream)
         fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair, dictionary=dict_state,
@@ -592,6 +594,18 @@ def main():
         if timed:
             ev[1].record(stream)
         fk.table_finalize(p.table, p.ws)
+        return st
+
+    def part_b(tab, spair=None, checked=False):
+        if p.replay:
+            p.checked = checked
+            p.run_replay(table=tab, sim_events=spair)  # (checked: after each resolve and replay call)
+            p.checked = False
+
+    def step(timed, kpair=None, checked=False, spair=None):
+        # checked (first warm-up step): the workspace status after EVERY call (each validating
+        # call resets it, so one check at the end would only see the last call)
+        st = part_a(kpair, checked, timed)
         tab = p.table
         if world > 1 and dict_state is not None:
             merge_tables_dict(p.table, ops)
@@ -604,13 +618,16 @@ def main():
             tab = dense
         if timed:
             ev[2].record(stream)
-        if p.replay:
-            p.checked = checked
-            p.run_replay(table=tab, sim_events=spair)  # (checked: after each resolve and replay call)
-            p.checked = False
+        part_b(tab, spair, checked)
         if timed:
             ev[3].record(stream)
         return st
+
+    def step_merge():  # the N > 1 merge of a graph-replayed step (direct collectives)
+        if dict_state is not None:
+            merge_tables_dict(p.table, ops)
+        else:
+            merge_tables(p.table, dense, ops)
 
     st = None
     for i in range(args.warmup):
@@ -641,23 +658,37 @@ def main():
     sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)] \
         if flush is not None else None
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # 1 GPU: every timed step is the replay of a CUDA graph captured from the same calls (one graph per
-    # step: each holds its own k_measure / replay event pairs).  The library's launch counter counts
-    # at capture, so the step's launches are counted there.  (N > 1 keeps direct launches: its
-    # merge runs torch.distributed collectives between the calls.)
+    # Every timed 1-GPU step replays a CUDA graph captured from the same calls (one per step: each
+    # holds its own k_measure / replay event pairs).  N > 1 with --graph-multi: part A (measure +
+    # finalize) and part B (resolve + replay) are two graphs and the merge's torch.distributed
+    # collectives run between them, outside any graph; by default N > 1 launches directly.  The
+    # library's launch counter counts at capture, so the step's launches are counted there.
     graphs = None
     launches_per_graph = 0
-    if world == 1 and not args.no_graph:
+    merged_tab = dense if (world > 1 and dict_state is None) else p.table  # (the table part B replays against)
+    if not args.no_graph and (world == 1 or args.graph_multi):
         graphs = []
         for i in range(args.steps):
-            g = torch.cuda.CUDAGraph()
             l0 = fk.launch_count()
-            with torch.cuda.graph(g):
-                step(False, kev[i], spair=rev[i] if p.replay else None)
+            ga = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga):
+                if world == 1:
+                    step(False, kev[i], spair=rev[i] if p.replay else None)
+                else:
+                    part_a(kev[i])
+            gb = None
+            if world > 1 and p.replay:
+                gb = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gb):
+                    part_b(merged_tab, rev[i])
             launches_per_graph = fk.launch_count() - l0
-            graphs.append(g)
-        for g in graphs[:2]:  # (first replays upload the graph; their results are the same step's)
-            g.replay()
+            graphs.append((ga, gb))
+        for ga, gb in graphs[:2]:  # (first replays upload the graphs)
+            ga.replay()
+            if world > 1:
+                step_merge()
+            if gb is not None:
+                gb.replay()
         torch.cuda.synchronize()
     launches0 = fk.launch_count()
     with ClockSampler(dev_index) as clk:
@@ -670,7 +701,11 @@ def main():
                 flush.zero_()
                 sev[i][0].record(stream)
             if graphs is not None:
-                graphs[i].replay()
+                graphs[i][0].replay()
+                if world > 1:
+                    step_merge()
+                if graphs[i][1] is not None:
+                    graphs[i][1].replay()
             else:
                 step(False, kev[i], spair=rev[i] if p.replay else None)
             if flush is not None:
@@ -726,7 +761,10 @@ def main():
                                  + ("; plan reused" if plan_ready[0] else "") + ")"
                                  if dict_state is not None else "none (1 GPU)"),
                        "l2": l2_note,
-                       "launch": (f"CUDA graph per step ({launches_per_graph} libfikit kernels, captured after warm-up)"
+                       "launch": ((f"CUDA graph per step ({launches_per_graph} libfikit kernels, captured after warm-up)"
+                                   if world == 1 else
+                                   f"two CUDA graphs per step (measure + finalize; resolve + replay: {launches_per_graph} "
+                                   f"libfikit kernels, captured after warm-up) around the merge's collectives")
                                   if graphs is not None else "direct launches"),
                        "parallelism": f"dp{world} (record shards + halo, NCCL table merge)" if world > 1 else "1 GPU"},
             "scenarios_per_s": (S_total / (ms * 1e-3)) if S_total else None,
