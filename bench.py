@@ -556,7 +556,9 @@ def main():
     dense = fk.Table(wl["cap"]) if world > 1 else None
     ops = LibOps(fk.Workspace(1, 1, 1, extra=64 * world * wl["cap"] + (1 << 20))) if world > 1 else None
     S_local = p.replay["S"] if p.replay else 0
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(5)]  # (stage events)
+    for e in ev:
+        e.record(stream)
     stage_ms = np.zeros(4)
 
     # k_measure alone, live in every timed step: one event pair per step (fikit_measure_timed)
@@ -584,7 +586,7 @@ def main():
     # a step = part A (measure + finalize), the N > 1 merge (collectives), part B (resolve + replay)
     def part_a(kpair=None, checked=False, timed=False):
         if timed:
-            ev[0].record(stream)
+            ev[0].record()  # (current stream: the capture stream inside a graph)
         fk.measure(p.recs, p.n, p.names, p.sigs, p.table, p.ws, halo=p.halo, events=kpair, dictionary=dict_state,
                    reuse_plan=dict_state is not None and plan_ready[0])
         if dict_state is not None:
@@ -592,7 +594,7 @@ def main():
         p.measured = True  # (the workspace holds the string hashes: resolve reuses them)
         st = fk.check(p.ws, "bench warm-up: measure") if checked else None
         if timed:
-            ev[1].record(stream)
+            ev[1].record()
         fk.table_finalize(p.table, p.ws)
         return st
 
@@ -617,10 +619,10 @@ def main():
                 fk.check(ops.ws, "bench warm-up: merge")
             tab = dense
         if timed:
-            ev[2].record(stream)
+            ev[2].record()
         part_b(tab, spair, checked)
         if timed:
-            ev[3].record(stream)
+            ev[3].record()
         return st
 
     def step_merge():  # the N > 1 merge of a graph-replayed step (direct collectives)
@@ -639,10 +641,22 @@ def main():
             dict_state = (src.kernel_id[:K].clone(), src.task_id[:K].clone(), K)
             dense = None if world > 1 else dense
     torch.cuda.synchronize()
-    # per-stage breakdown on separately timed steps (events between launches)
+    # per-stage breakdown on separately timed steps (events between the calls), launched the way the
+    # timed steps are: a CUDA graph of the step with the stage events as external event nodes (1 GPU),
+    # else direct launches
     n_stage = min(20, args.steps)
+    stage_graph = None
+    if world == 1 and not args.no_graph:
+        stage_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(stage_graph):
+            step(True)
+        stage_graph.replay()
+        torch.cuda.synchronize()
     for _ in range(n_stage):
-        step(True)
+        if stage_graph is not None:
+            stage_graph.replay()
+        else:
+            step(True)
         torch.cuda.synchronize()
         stage_ms += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]), 0]
     stage_ms /= n_stage
