@@ -5,6 +5,8 @@
 # halo), random replays (register and shared-memory pools, m up to 1025), fill, STREAM / Case A
 # replay, predictors, the one-GPU sharded merge, lookup, empty inputs.  Every case still checks
 # its outputs against the oracle under the tool.  Logs: gpurun_out/sanitize_<tool>.log
+# (compute-sanitizer has since been closed on the GPU pool; tests/test_gpu_checked.py reruns these
+# cases on the checked build, -DFIKIT_CHECKS, instead.)
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
