@@ -16,6 +16,8 @@
 //                    L2 reductions).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fikit_internal.cuh"
 
 namespace fikit {
@@ -868,20 +870,22 @@ __device__ __forceinline__ uint32_t atom_shared_add(uint32_t saddr, uint32_t v) 
 // old word (the caller checks the carry after its other reductions, off the critical path).
 // The split sum gets a (v, or 0 when off or >= 2^32: every lane adds, the old word is returned
 // for the carry check, which the caller makes after its other reductions).
-template <class RowOf>  // row_of(): the slot's table row, read only on the rare >= 2^32 path
+// kSmall: the caller checked v < 2^32 for the whole warp (no per-value check, no >= 2^32 path).
+template <bool kSmall, class RowOf>  // row_of(): the slot's table row, read only on the rare >= 2^32 path
 __device__ __forceinline__ uint32_t hot_add(uint32_t hist_e, uint32_t st_e, uint32_t mm_e, const RawTab& tab,
                                             RowOf row_of, int j, uint64_t v, bool on, uint32_t mn, uint32_t mx,
                                             uint32_t& a) {
-  const bool small = (v >> 32) == 0;
+  const bool small = kSmall || (v >> 32) == 0;
   const uint32_t v32 = (uint32_t)v;
-  const uint32_t b = (small ? min(32u - (uint32_t)__clz(v32), 31u) : 31u) + 32u * j;  // bin_of(v)
+  // bin_of(v) = min(bit_length(v), 31)
+  const uint32_t b = (small ? 32u - (uint32_t)__clz(min(v32, 0x7FFFFFFFu)) : 31u) + 32u * j;
   const bool son = on && small;
   a = son ? v32 : 0u;
   const uint32_t old = atom_shared_add(st_e + 8u * j, a);
   red_shared_add_if(on, hist_e + 4u * b, 1u);
   red_shared_min_if(son && v32 < mn, mm_e + 8u * j, v32);
   red_shared_max_if(son && v32 > mx, mm_e + 8u * j + 4u, v32);
-  if (on && !small) {  // rare: a value >= 2^32 ns
+  if (!kSmall && on && !small) {  // rare: a value >= 2^32 ns
     const uint32_t row = row_of();
     red_add_u64(tab.rows[row].sums + 2 * j + 1, v);
     red_max_u64(tab.rows[row].ext + 2 * j, v);
@@ -1261,7 +1265,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
       }
     }
   };
-  auto update = [&](const Rec& R, int slot) {
+  auto update = [&](const Rec& R, int slot, auto small_tile) {
+    constexpr bool kSmall = decltype(small_tile)::value;
     FK_CHECK(slot >= 0 && (uint32_t)slot < min(S.hot_n, kHotMax));
     const uint32_t rowv = S.grow[slot];  // (loading it here schedules better than on demand)
     FK_CHECK(rowv < tab.capacity);
@@ -1273,8 +1278,8 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(mm.x), "=r"(mm.y), "=r"(mm.z), "=r"(mm.w) : "r"(mm_e));
     uint32_t ad, ag;
-    const uint32_t od = hot_add(hist_e, st_e, mm_e, tab, row, 0, R.d, true, mm.x, mm.y, ad);
-    const uint32_t og = hot_add(hist_e, st_e, mm_e, tab, row, 1, R.g, R.gap, mm.z, mm.w, ag);
+    const uint32_t od = hot_add<kSmall>(hist_e, st_e, mm_e, tab, row, 0, R.d, true, mm.x, mm.y, ad);
+    const uint32_t og = hot_add<kSmall>(hist_e, st_e, mm_e, tab, row, 1, R.g, R.gap, mm.z, mm.w, ag);
     if (out_row) out_row[R.gi] = row();
     // carries of the two sums (old + a wrapped past 2^32)
     red_shared_add_if(od + ad < od, st_e + 4u, 1u);
@@ -1422,8 +1427,16 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         int sA = -1, sB = -1;
         if (A.valid && A.cmp) sA = vA ? (int)cA - 1 : ((cA != 0u || fullA) ? probe_slow(A) : -1);
         if (B.valid && B.cmp) sB = vB ? (int)cB - 1 : ((cB != 0u || fullB) ? probe_slow(B) : -1);
-        if (sA >= 0) update(A, sA);
-        if (sB >= 0) update(B, sB);
+        // every value the warp adds < 2^32 ns (all but pathological traces): the update without the
+        // per-value >= 2^32 checks and path
+        const uint64_t big = (sA >= 0 ? (A.d | (A.gap ? A.g : 0ull)) : 0ull) | (sB >= 0 ? (B.d | (B.gap ? B.g : 0ull)) : 0ull);
+        if (__all_sync(0xffffffffu, (big >> 32) == 0ull)) {
+          if (sA >= 0) update(A, sA, std::true_type{});
+          if (sB >= 0) update(B, sB, std::true_type{});
+        } else {
+          if (sA >= 0) update(A, sA, std::false_type{});
+          if (sB >= 0) update(B, sB, std::false_type{});
+        }
         if (A.live && !A.valid) flag_record(st, A.gi);
         if (B.live && !B.valid) flag_record(st, B.gi);
         compact(A, A.valid && sA < 0);
