@@ -1194,11 +1194,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   // read this lane's launch of half h of the stage's tile and the next launch's start/run/task
   // (lane + 1 by shuffle; lane 31 from the record after the half; the halo after the last
   // launch), validate, and compute K, G and the identity hash
-  auto load_half = [&](int h, Rec& R) {
+  // kFull: the whole tile and the launch after it exist (sfirst + 64 < n, warp-uniform): every lane
+  // is live and has a next launch (no per-lane range checks, no halo)
+  auto load_half = [&](int h, Rec& R, auto full_tile) {
+    constexpr bool kFull = decltype(full_tile)::value;
     const uint32_t first = sfirst + h * mk::TILE;
-    const uint32_t cnt = n32 > first ? min((uint32_t)mk::TILE, n32 - first) : 0u;
+    const uint32_t cnt = kFull ? (uint32_t)mk::TILE : n32 > first ? min((uint32_t)mk::TILE, n32 - first) : 0u;
     const uint4* rp = S.ring[warp] + (h * mk::TILE + lane) * 3;
-    R.live = (uint32_t)lane < cnt;
+    R.live = kFull || (uint32_t)lane < cnt;
     uint4 r0, r1, r2;
     {
       // one 16-B shared load per quarter record (the compiler splits rp[0] into two 8-B loads,
@@ -1216,14 +1219,14 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
     uint32_t nrun = __shfl_down_sync(0xffffffffu, r2.z, 1);
     uint32_t ntask = __shfl_down_sync(0xffffffffu, r2.w, 1);
     R.gi = first + lane;
-    bool has_next = R.gi + 1 < n32;
+    bool has_next = kFull || R.gi + 1 < n32;
     if (lane == 31 && R.live && has_next) {
       const uint4 x = rp[3], y = rp[5];
       nstart = (uint64_t)x.x | ((uint64_t)x.y << 32);
       nrun = y.z;
       ntask = y.w;
     }
-    if (!has_next && halo != nullptr && R.live) {
+    if (!kFull && !has_next && halo != nullptr && R.live) {
       nstart = halo->start_ns;
       nrun = halo->run_id;
       ntask = halo->task_id;
@@ -1400,8 +1403,13 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
         mbar_wait_s(s_full + 8u * warp, kk & 1u);
         kk++;
         FK_TR(tr_tiles++;)
-        load_half(0, A);
-        load_half(1, B);
+        if (sfirst + (uint32_t)mk::CH < n32) {  // (every tile but the trace's last)
+          load_half(0, A, std::true_type{});
+          load_half(1, B, std::true_type{});
+        } else {
+          load_half(0, A, std::false_type{});
+          load_half(1, B, std::false_type{});
+        }
         // order the stage reads (generic proxy) before the TMA overwrite (async proxy), refill early
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
