@@ -93,6 +93,10 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const fikit_status_t* __res
   FinKey* rk = reinterpret_cast<FinKey*>(fin_sm);              // [R] this block's row keys
   uint32_t* srank = reinterpret_cast<uint32_t*>(rk + R);       // [R]
   const uint32_t K = (uint32_t)umin64(st->n_rows_needed, cap);
+  // rows per block for this K (R_max: the shared arrays' size, >= cap / gridDim): K spread over the
+  // grid (one block per SM), at least 16 rows per block
+  const uint32_t R_max = R;
+  R = min(R_max, max(16u, ((K + gridDim.x - 1) / gridDim.x + 15u) & ~15u));
   const uint32_t r0 = blockIdx.x * R;
   if (r0 >= K) return;
   const uint32_t nr = min(R, K - r0), tid = threadIdx.x;
