@@ -932,14 +932,11 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 
 namespace mk {
 __device__ __forceinline__ uint32_t tag_bits(uint32_t h) { return (h & TAG_HB) | 0x80000000u; }
-// hash of a hot identity's five compressed words (tq, tq4 below): 5 multiply rounds and a short
+// hash of a hot identity's five compressed words (tq, tq4 below): five multiply-adds and a short
 // finaliser (the bucket takes the low 11 bits, the tag bits 11..30); collisions only cost a probe
 __device__ __forceinline__ uint32_t hot_hash(uint32_t c0, uint32_t k2, uint32_t k3, uint32_t k4, uint32_t c4) {
-  uint32_t h = c0 * 0x9E3779B1u;
-  h = (h ^ k2) * 0x85EBCA77u;
-  h = (h ^ k3) * 0xC2B2AE3Du;
-  h = (h ^ k4) * 0x27D4EB2Fu;
-  h = (h ^ c4) * 0x165667B1u;
+  // a sum of odd-constant products (one IMAD each) and a short finaliser
+  uint32_t h = c0 * 0x9E3779B1u + k2 * 0x85EBCA77u + k3 * 0xC2B2AE3Du + k4 * 0x27D4EB2Fu + c4 * 0x165667B1u;
   h ^= h >> 15;
   h *= 0x2C1B3C6Du;
   h ^= h >> 12;
