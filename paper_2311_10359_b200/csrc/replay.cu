@@ -375,8 +375,9 @@ struct DigestBatch {
 constexpr uint32_t kQ22 = (1u << 22) - 1;
 struct RegPool {
   static constexpr bool kOwnerStats = true;  // fill_work / n_fills from the owning lanes at the end
-  // the order key and q << 6 | index of requests lane, 32 + lane while they are alive and
-  // eligible (both 0xFFFFFFFF otherwise): q <= R <=> pq <= R << 6 | 63
+  // the order key and q << 6 | index of requests lane, 32 + lane (both 0xFFFFFFFF if not
+  // eligible; a dequeue sets pq alone to 0xFFFFFFFF, which no Rc <= 0xFFFFFFFE admits):
+  // q <= R <=> pq <= R << 6 | 63
   uint32_t key0, key1;
   uint32_t pq0, pq1;
   uint64_t elig;        // eligible requests by index (warp-uniform)
@@ -393,7 +394,7 @@ struct RegPool {
   // Alg. 2: the best alive eligible request with q <= R, dequeued.  Returns its index or -1.
   // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
   __device__ __forceinline__ int pick32(uint32_t R, int lane, uint32_t& qk) {
-    const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFFu : (R << 6) | 63u;
+    const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFEu : (R << 6) | 63u;  // (a cleared pq never fits)
     const uint32_t c0 = pq0 <= Rc ? key0 : 0xFFFFFFFFu, c1 = pq1 <= Rc ? key1 : 0xFFFFFFFFu;
     const uint32_t best = __reduce_min_sync(0xffffffffu, min(c0, c1));
     if (best == 0xFFFFFFFFu) return -1;
@@ -402,7 +403,7 @@ struct RegPool {
     qk = kQ22 - ((best >> 6) & kQ22);
     ek = __shfl_sync(0xffffffffu, k < 32u ? dur0 : dur1, (int)(k & 31u));
     if ((uint32_t)lane == (k & 31u)) {
-      if (k < 32u) key0 = pq0 = 0xFFFFFFFFu; else key1 = pq1 = 0xFFFFFFFFu;
+      if (k < 32u) pq0 = 0xFFFFFFFFu; else pq1 = 0xFFFFFFFFu;  // (dequeued: only pq is cleared)
     }
     return (int)k;
   }

@@ -43,6 +43,12 @@ VARIANTS = {
     "w4b8": [reg_cfg(4, 8)],  # 32 warps per SM, up to 64 registers
     "w8b4": [reg_cfg(8, 4)],
     "w16b2": [reg_cfg(16, 2)],
+    # register pool: a dequeue clears only pq (Rc capped at 0xFFFFFFFE, so a cleared pq never fits)
+    "deq": [lambda r, h: (sub(sub(r,
+        "const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFFu : (R << 6) | 63u;",
+        "const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFEu : (R << 6) | 63u;"),
+        "if (k < 32u) key0 = pq0 = 0xFFFFFFFFu; else key1 = pq1 = 0xFFFFFFFFu;",
+        "if (k < 32u) pq0 = 0xFFFFFFFFu; else pq1 = 0xFFFFFFFFu;"), h)],
     # the POOL models' HP chunk walk without the lazy (REDUX-total) path: the prefix scan every chunk
     "eager": [lambda r, h: (sub(r, "template <bool kLazyScan = true, class GateMin, class Fill>",
                                 "template <bool kLazyScan = false, class GateMin, class Fill>"), h)],
