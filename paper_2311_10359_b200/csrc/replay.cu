@@ -391,13 +391,15 @@ struct RegPool {
     const uint32_t v = __reduce_min_sync(0xffffffffu, min(pq0, pq1));
     return v == 0xFFFFFFFFu ? v : v >> 6;
   }
-  // Alg. 2: the best alive eligible request with q <= R, dequeued.  Returns its index or -1.
+  // Alg. 2: the best alive eligible request with q <= R, dequeued; returns its index.  The caller
+  // guarantees one fits (R >= qmin, the exact smallest alive eligible q), so there is no "none"
+  // branch here or after the call (3.7 % of the replay).
   // q <= R  <=>  q << 6 | k <= R << 6 | 63  (k < 64), and every q < 2^22 fits an R >= 2^22.
   __device__ __forceinline__ int pick32(uint32_t R, int lane, uint32_t& qk) {
     const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFEu : (R << 6) | 63u;  // (a cleared pq never fits)
     const uint32_t c0 = pq0 <= Rc ? key0 : 0xFFFFFFFFu, c1 = pq1 <= Rc ? key1 : 0xFFFFFFFFu;
     const uint32_t best = __reduce_min_sync(0xffffffffu, min(c0, c1));
-    if (best == 0xFFFFFFFFu) return -1;
+    FK_CHECK(best != 0xFFFFFFFFu);
     const uint32_t k = best & 63u;
     FK_CHECK((uint32_t)lane != (k & 31u) || (k < 32u ? pq0 : pq1) != 0xFFFFFFFFu);  // (alive when picked)
     qk = kQ22 - ((best >> 6) & kQ22);
@@ -652,8 +654,7 @@ __device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& 
       if (t >= r_stop) break;
       if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
       uint32_t qk;
-      const int k = P.pick32(R, lane, qk);  // Alg. 2
-      if (k < 0) break;
+      const int k = P.pick32(R, lane, qk);  // Alg. 2 (R >= qmin: one fits)
       const uint64_t e = P.ek;
       if (sched && lane == 0) {
         fill_gap[so + k] = (int32_t)i;

@@ -49,6 +49,12 @@ VARIANTS = {
         "const uint32_t Rc = R >= (1u << 22) ? 0xFFFFFFFEu : (R << 6) | 63u;"),
         "if (k < 32u) key0 = pq0 = 0xFFFFFFFFu; else key1 = pq1 = 0xFFFFFFFFu;",
         "if (k < 32u) pq0 = 0xFFFFFFFFu; else pq1 = 0xFFFFFFFFu;"), h)],
+    # register pool: no "nothing fits" checks after the pick (the caller's R >= qmin guarantees a fit)
+    "nofitchk": [lambda r, h: (sub(sub(r,
+        "    if (best == 0xFFFFFFFFu) return -1;\n    const uint32_t k = best & 63u;",
+        "    const uint32_t k = best & 63u;"),
+        "      const int k = P.pick32(R, lane, qk);  // Alg. 2\n      if (k < 0) break;",
+        "      const int k = P.pick32(R, lane, qk);  // Alg. 2 (R >= qmin: one fits)"), h)],
     # the POOL models' HP chunk walk without the lazy (REDUX-total) path: the prefix scan every chunk
     "eager": [lambda r, h: (sub(r, "template <bool kLazyScan = true, class GateMin, class Fill>",
                                 "template <bool kLazyScan = false, class GateMin, class Fill>"), h)],
