@@ -228,7 +228,7 @@ __device__ __forceinline__ int sorted_best(const uint64_t* K, uint32_t A, uint32
   // 0xFFFFFFFF then never passes the chunk ballot
   const uint32_t Rc = R >= 0xFFFFFFFFull ? 0xFFFFFFFEu : (uint32_t)R;
   const uint32_t cb = __ballot_sync(0xffffffffu, (uint32_t)lane < nch && CM <= Rc);
-  if (!cb) return -1;
+  FK_CHECK(cb != 0u);  // (the caller's R >= qmin, the exact pool minimum, guarantees a fit)
   const uint32_t c = __ffs(cb) - 1;
   const uint32_t word = __shfl_sync(0xffffffffu, A, c);
   const uint32_t* qh = reinterpret_cast<const uint32_t*>(K) + 1;
@@ -252,8 +252,7 @@ __device__ __forceinline__ int pool_pick(bool fast, uint64_t* q, uint8_t* meta, 
                                          const uint64_t* __restrict__ dur, uint64_t& ek, bool epack = false) {
   int k;
   if (fast) {
-    const int p = sorted_best(q, A, CM, nch, R, lane);
-    if (p < 0) return -1;
+    const int p = sorted_best(q, A, CM, nch, R, lane);  // (always a fit: see sorted_best)
     const uint64_t x = q[p];  // q << 32 | [e << 10 |] index
     k = (int)(x & 1023u);
     FK_CHECK((uint32_t)p < m && (uint32_t)k < m && qk_fits(x >> 32, R));
