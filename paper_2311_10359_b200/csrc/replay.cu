@@ -648,10 +648,10 @@ __device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& 
   auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R64, HpOut& o) -> uint64_t {
     uint32_t R = R64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)R64;
     const uint64_t r_stop = prm.feedback ? r : ~0ull;  // (without feedback t never reaches it)
-    bool any = false;
+    // replay_hp_core visits a gap only when its gate opened against the current qmin (R >= qmin)
+    // and, with feedback, the HP client's next launch is still ahead (a' > 0, t < r): the first
+    // pick needs no check, the loop tests its exits after each fill (2.5 % of the replay)
     for (;;) {
-      if (t >= r_stop) break;
-      if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
       uint32_t qk;
       const int k = P.pick32(R, lane, qk);  // Alg. 2 (R >= qmin: one fits)
       const uint64_t e = P.ek;
@@ -662,10 +662,10 @@ __device__ __forceinline__ HpOut replay_hp_reg(RegPool& P, const fikit_table_t& 
       P.record((uint32_t)k, (int32_t)i, t, lane, dig);
       R -= qk;
       t += e;
-      any = true;
       if (qk == qmin) qmin = P.min_q32();
+      if (t >= r_stop || R < qmin) break;  // feedback stop / no alive eligible request fits
     }
-    if (any) o.lp_end = t;  // fills run in time order: the last one ends last
+    o.lp_end = t;  // fills run in time order: the last one ends last
     return t;
   };
   return replay_hp_core([&]() { return qmin == 0xFFFFFFFFu ? ~0ull : (uint64_t)qmin; }, fill, tab, K, hp_row,
