@@ -609,9 +609,8 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
                                            uint64_t* lp_start, uint64_t so, DigestBatch& dig, int lane) {
   uint64_t qmin = min_q();
   auto fill = [&](uint32_t i, uint64_t t, uint64_t r, uint64_t R, HpOut& o) -> uint64_t {
+    // (a visited gap admits its first pick: see replay_hp_reg; the exits are tested after a fill)
     for (;;) {
-      if (prm.feedback && t >= r) break;
-      if (R < qmin) break;  // no alive eligible request fits: BestPrioFit returns none
       uint64_t qk;
       const int k = P.pick(R, lane, qk);  // Alg. 2
       if (k < 0) break;
@@ -629,6 +628,7 @@ __device__ __forceinline__ HpOut replay_hp(Pool& P, MinQ min_q, const fikit_tabl
         o.n_fills++;
       }
       o.lp_end = t;  // fills run in time order: the last one ends last
+      if ((prm.feedback && t >= r) || R < qmin) break;  // feedback stop / nothing fits
     }
     return t;
   };
