@@ -1268,8 +1268,10 @@ __global__ void __launch_bounds__(mk::THREADS, 1)
   auto update = [&](const Rec& R, int slot, auto small_tile) {
     constexpr bool kSmall = decltype(small_tile)::value;
     FK_CHECK(slot >= 0 && (uint32_t)slot < min(S.hot_n, kHotMax));
-    const uint32_t rowv = S.grow[slot];  // (loading it here schedules better than on demand)
-    FK_CHECK(rowv < tab.capacity);
+    // the slot's table row: needed for out_row and the >= 2^32 path only (a random 4-B shared load
+    // per launch otherwise spent; loading it here schedules better than on demand)
+    const uint32_t rowv = (kSmall && out_row == nullptr) ? 0u : S.grow[slot];
+    FK_CHECK((kSmall && out_row == nullptr) || rowv < tab.capacity);
     auto row = [&]() { return rowv; };
     const uint32_t hist_e = s_hist + (uint32_t)slot * ((2 * kBins + 1) * 4);
     const uint32_t st_e = s_st + (uint32_t)slot * 20u;
